@@ -1,0 +1,368 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 NTT engine (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json config 4, the large-batch throughput config), per GPU and step:
+  * 2^22 Kyber polynomials  (q = 3329,    N = 256, cyclic 8 layers, int16),
+  * 2^21 Dilithium polys    (q = 8380417, N = 256, cyclic 8 layers, int32),
+  each run forward then inverse with the paper's modified-Plantard ("improved")
+  butterfly: n = 16 (32-bit Plantard constant) for Kyber, n = 32 (64-bit) for Dilithium.
+Inputs are seeded uniform [0, q) synthetic data (no dataset is involved: the reference
+benchmarks seeded random polynomials too, bench.hpp:198-230).  The working set
+(4 GiB in + 4 GiB spectra per GPU) is far above the 126 MB L2, so no flush is needed.
+
+Multi-GPU: one process per GPU (torchrun); every rank transforms its own fixed batch
+(weak scaling, no collective on the compute path); the step time is the max over ranks.
+
+--impl reference times the reference's own CPU path (oracle/_ref: ntt_forward_inplace
++ intt_inverse, transform.hpp:228-231,339-343) on the host cores, same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KYBER_Q, DIL_Q = 3329, 8380417
+METRIC = "NTT polys/sec (fwd+inv round trip, modified-Plantard butterfly)"
+UNIT = "polys/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--kyber-log2", type=int, default=22)
+    ap.add_argument("--dil-log2", type=int, default=21)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="NCCL-gather per-rank digests")
+    return ap.parse_args()
+
+
+def workload_config(a, world):
+    return {
+        "workload": (f"config4: per GPU 2^{a.kyber_log2} Kyber (q=3329,N=256,cyclic 8 layers,"
+                     f"improved n=16,int16) + 2^{a.dil_log2} Dilithium (q=8380417,N=256,cyclic"
+                     " 8 layers,improved n=32,int32); step = forward + inverse of both"),
+        "kyber_polys_per_gpu": 1 << a.kyber_log2,
+        "dilithium_polys_per_gpu": 1 << a.dil_log2,
+        "parallelism": f"dp{world} (batch sharding, no collective on the compute path)",
+        "l2": "working set 8 GiB/GPU >> 126 MB L2: no flush needed",
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled DURING the timed region (B200_PROFILING.md clocks line)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (reference code; test-infrastructure libraries under oracle/)
+
+def cpu_reference_rate(n_kyber: int, n_dil: int, threads: int):
+    """Reference round trip (forward_inplace + intt_inverse) on host threads.
+
+    Returns (polys/s, kind, seconds).  Uses oracle/_ref (the unmodified reference) when
+    it was built; otherwise the C restatement (oracle/liboracle.so)."""
+    from oracle.oracle import IMPROVED, Oracle, Reference, reference_available
+
+    o = Oracle()
+    kyb = o.rng(12345, KYBER_Q, n_kyber * 256)
+    dil = o.rng(54321, DIL_Q, n_dil * 256)
+    if reference_available():
+        ref = Reference()
+        # the reference admits `improved` for Kyber at n = 32 (bit-identical outputs to the
+        # engine's n = 16) and for Dilithium via exact-bound params
+        pk = ref.params(KYBER_Q, 256, 32, (IMPROVED,))
+        pd = ref.params(DIL_Q, 256, 32, (IMPROVED,), exact=True)
+        t = pk.time_batch(IMPROVED, 1, kyb, threads) + pd.time_batch(IMPROVED, 1, dil, threads)
+        return (n_kyber + n_dil) / t, "reference", t
+    # fallback: the oracle port, threaded over polynomials
+    from concurrent.futures import ThreadPoolExecutor
+
+    qk = o.params(KYBER_Q, 256, 32, (IMPROVED,))
+    qd = o.params(DIL_Q, 256, 32, (IMPROVED,), exact=True)
+
+    def work(args):
+        P, arr = args
+        P.inverse(IMPROVED, P.forward(IMPROVED, arr))
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        jobs = [(qk, c) for c in np.array_split(kyb.reshape(-1, 256), threads)]
+        jobs += [(qd, c) for c in np.array_split(dil.reshape(-1, 256), threads)]
+        list(ex.map(work, jobs))
+    t = time.perf_counter() - t0
+    return (n_kyber + n_dil) / t, "port", t
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(a, rank, world):
+    if rank != 0:
+        return 0
+    threads = host_threads()
+    per_step_k = max(2, threads * 2048)   # bounded sample per step, 2:1 Kyber:Dilithium
+    per_step_d = max(1, threads * 1024)
+    for _ in range(a.warmup):
+        cpu_reference_rate(per_step_k // 8, per_step_d // 8, threads)
+    total_t, total_polys, kind = 0.0, 0, "reference"
+    for _ in range(a.steps):
+        r, kind, t = cpu_reference_rate(per_step_k, per_step_d, threads)
+        total_t += t
+        total_polys += per_step_k + per_step_d
+    value = total_polys / total_t
+    sample = (f"each step: {per_step_k} Kyber + {per_step_d} Dilithium polys, fwd+inv, "
+              f"{threads} host threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total_t / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (reference Rng, uniform [0,q))",
+        "config": workload_config(a, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# engine arm
+
+def run_engine_arm(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_00675_b200.nttk as nttk
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    nk, nd = 1 << a.kyber_log2, 1 << a.dil_log2
+    Pk = nttk.build_params(KYBER_Q, 256, 16, [nttk.ButterflyKind.improved], exact_bound=True)
+    Pd = nttk.build_params(DIL_Q, 256, 32, [nttk.ButterflyKind.improved], exact_bound=True)
+    IMP = nttk.ButterflyKind.improved
+    assert IMP in Pk.fast_path and IMP in Pd.fast_path
+
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    xk = torch.randint(0, KYBER_Q, (nk, 256), generator=g, device=dev, dtype=torch.int32).to(torch.int16)
+    xd = torch.randint(0, DIL_Q, (nd, 256), generator=g, device=dev, dtype=torch.int32)
+    sk, sd = torch.empty_like(xk), torch.empty_like(xd)
+    ok, od = torch.empty_like(xk), torch.empty_like(xd)
+    stream = torch.cuda.current_stream(dev)
+
+    names = ["kyber_fwd", "kyber_inv", "dil_fwd", "dil_inv"]
+    calls = [lambda: nttk.forward(Pk, IMP, xk, sk), lambda: nttk.inverse(Pk, IMP, sk, ok),
+             lambda: nttk.forward(Pd, IMP, xd, sd), lambda: nttk.inverse(Pd, IMP, sd, od)]
+    # algorithmic HBM bytes per launch: read + write of the coefficient arrays
+    alg_bytes = [nk * 256 * 2 * 2, nk * 256 * 2 * 2, nd * 256 * 4 * 2, nd * 256 * 4 * 2]
+
+    def step(evs=None):
+        for i, c in enumerate(calls):
+            if evs is not None:
+                evs[i][0].record(stream)
+            c()
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness guard on the measured data: round trip must be the identity
+    assert torch.equal(ok, xk) and torch.equal(od, xd), "round trip mismatch"
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in calls]
+           for _ in range(a.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = nttk.launch_count()
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        for k in range(a.steps):
+            step(evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = nttk.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = t0.elapsed_time(t1)
+    per_kernel = [np.mean([evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(a.steps)])
+                  for i in range(len(calls))]
+    tm = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    max_ms = float(tm.item())
+    polys_per_step = (nk + nd) * world
+    value = polys_per_step * a.steps / (max_ms / 1e3)
+
+    # roofline of the dominant kernel
+    dom = int(np.argmax(per_kernel))
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes[dom] / (per_kernel[dom] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "kernel": names[dom],
+                "peak_source": peak_src,
+                "per_kernel_ms": dict(zip(names, [round(x, 4) for x in per_kernel])),
+                "per_kernel_GBps": dict(zip(names, [round(b / (t / 1e3) / 1e9, 1)
+                                                    for b, t in zip(alg_bytes, per_kernel)]))}
+    fwd_rate = (nk + nd) * world / (max(per_kernel[0] + per_kernel[2], 1e-9) / 1e3)
+
+    # end-to-end through the C ABI host entry point (pinned host buffers, copies timed)
+    e2e = None
+    if not a.no_e2e:
+        hk = torch.empty((nk, 256), dtype=torch.int16, pin_memory=True)
+        hd = torch.empty((nd, 256), dtype=torch.int32, pin_memory=True)
+        hk.copy_(xk)
+        hd.copy_(xd)
+        ohk, ohd = torch.empty_like(hk, pin_memory=True), torch.empty_like(hd, pin_memory=True)
+        for _ in range(1):
+            nttk.roundtrip_host(Pk, IMP, hk, None, ohk)
+            nttk.roundtrip_host(Pd, IMP, hd, None, ohd)
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            nttk.roundtrip_host(Pk, IMP, hk, None, ohk)
+            nttk.roundtrip_host(Pd, IMP, hd, None, ohd)
+        dt = torch.tensor([time.perf_counter() - te], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        assert torch.equal(ohk, hk) and torch.equal(ohd, hd), "e2e round trip mismatch"
+        e2e = {"value": polys_per_step * a.e2e_steps / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": nk * 512 + nd * 1024,
+               "d2h_bytes_per_step": nk * 512 + nd * 1024,
+               "path": "nttk_roundtrip_host (C ABI, pinned host buffers, 3-stream pipeline)"}
+
+    digest = None
+    if a.gather and world > 1:  # NCCL only to gather results when asked, outside timing
+        d = torch.stack([sk.view(-1)[:1024].to(torch.int64).sum(), sd.view(-1)[:1024].to(torch.int64).sum()])
+        allv = [torch.empty_like(d) for _ in range(world)]
+        dist.all_gather(allv, d)
+        digest = [v.tolist() for v in allv]
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        threads = host_threads()
+        smp_k, smp_d = threads * 4096, threads * 2048
+        rate, kind, t = cpu_reference_rate(smp_k, smp_d, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"{smp_k} Kyber + {smp_d} Dilithium polys fwd+inv ({t:.1f} s wall)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": max_ms / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32 (int16/int32 storage)",
+            "data": "synthetic uniform [0,q) (torch.randint, seeded)",
+            "config": workload_config(a, world),
+            "fwd_only_polys_per_s": fwd_rate,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+        if digest is not None:
+            line["gathered_digests"] = digest
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        if world > 1 and rank != 0:
+            return 0
+        return run_reference_arm(a, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_engine_arm(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

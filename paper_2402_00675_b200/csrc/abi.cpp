@@ -1,0 +1,524 @@
+// abi.cpp -- the extern "C" boundary of libnttk_gpu.so (include/nttk_gpu.h).
+//
+// Dispatches every entry point to the sm_100a kernels: the specialised N = 256
+// kernels (fast256.cu) when the parameter set qualifies, the any-parameter kernels
+// (generic.cu) otherwise.  No exception crosses this boundary; the reference's
+// contract_violation messages (transform.hpp / params.hpp / reduction.hpp) come back
+// through nttk_last_error() with status 2.  There is no CPU compute path: every
+// transform, product and reduction runs on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/nttk_gpu.h"
+#include "fast256.hpp"
+#include "generic.hpp"
+#include "params.hpp"
+#include "sweep.hpp"
+
+struct nttk_params_s {
+  nttk_b200::HostParams P;
+};
+
+using nttk_b200::HostParams;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(NTTK_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int device_count() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int need_device(const char* who) {
+  if (device_count() <= 0)
+    return fail(NTTK_CUDA, std::string(who) + ": no CUDA device (the engine has no CPU path)");
+  return NTTK_OK;
+}
+
+const char* kind_name(int k) {
+  static const char* names[] = {"ntl", "harvey", "scott", "improved", "smont"};
+  return (k >= 0 && k < 5) ? names[k] : "?";
+}
+
+int check_kind(const HostParams& P, int kind, const char* who) {
+  if (kind < 0 || kind > NTTK_SMONT || !((P.kinds >> kind) & 1u))
+    return fail(NTTK_CONTRACT, std::string(who) + ": kind not built into these params");
+  return NTTK_OK;
+}
+
+// Forward spectrum range per kind (transform.hpp:61-70, plus the extension kinds):
+// values lie in [lo, hi).
+void spectrum_range(const HostParams& P, int kind, int64_t& lo, uint64_t& hi) {
+  lo = 0;
+  switch (kind) {
+    case NTTK_NTL: hi = P.p; break;
+    case NTTK_HARVEY: hi = 2ull * P.p; break;
+    case NTTK_SCOTT: hi = uint64_t(P.N) * P.p; break;
+    case NTTK_IMPROVED: hi = uint64_t(P.layers + 1) * P.p; break;
+    default:  // smont: X + t / X - t growth from [0, p)
+      hi = uint64_t(P.layers + 1) * P.p;
+      lo = -static_cast<int64_t>(P.layers) * static_cast<int64_t>(P.p);
+  }
+}
+
+int check_storage(const HostParams& P, int kind, int elem, const char* who) {
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, std::string(who) + ": elem_bytes must be 2, 4 or 8");
+  if (elem == 8) return NTTK_OK;
+  int64_t lo;
+  uint64_t hi;
+  spectrum_range(P, kind, lo, hi);
+  const bool sgn = kind == NTTK_SMONT;
+  const unsigned bits = 8 * elem;
+  const bool ok = sgn ? (lo >= -(int64_t(1) << (bits - 1)) && hi <= (uint64_t(1) << (bits - 1)))
+                      : hi <= (uint64_t(1) << bits);
+  if (!ok)
+    return fail(NTTK_CONTRACT, std::string(who) + ": elem_bytes=" + std::to_string(elem) +
+                                   " cannot hold the " + kind_name(kind) + " spectrum bound");
+  return NTTK_OK;
+}
+
+bool use_fast(const HostParams& P, int kind) {
+  return ((P.fast_mask >> kind) & 1u) && nttk_b200::fast256_supports(kind, P.layers, P.n_bits);
+}
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+// one transform pass on device buffers
+int run_transform(const HostParams& P, int kind, int dir, const void* in, void* out, size_t batch,
+                  int elem, cudaStream_t st) {
+  cudaError_t e;
+  if (use_fast(P, kind)) {
+    e = nttk_b200::fast256_launch(P, kind, dir, in, out, batch, elem, st);
+    g_launches += batch ? 1 : 0;
+  } else {
+    std::string err;
+    const nttk_b200::DeviceTables* T = P.device_tables(current_device(), err);
+    if (!T) return fail(NTTK_CUDA, err);
+    e = nttk_b200::generic_transform(P, *T, kind, dir, in, out, batch, elem, st);
+    if (batch) g_launches += P.N <= 4096 ? 1 : P.layers + 2;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, dir ? "intt_inverse" : "ntt_forward");
+  return NTTK_OK;
+}
+
+int run_product(const HostParams& P, int kind, const void* l, const void* r, void* out,
+                size_t batch, int elem, cudaStream_t st) {
+  cudaError_t e;
+  if ((P.N >> P.layers) == 2) {
+    std::string err;
+    const nttk_b200::DeviceTables* T = P.device_tables(current_device(), err);
+    if (!T) return fail(NTTK_CUDA, err);
+    e = nttk_b200::generic_basemul(P, T->gamma, kind, l, r, out, batch, elem, st);
+  } else {
+    e = nttk_b200::generic_pointwise(P, kind, l, r, out, batch, elem, st);
+  }
+  if (batch) ++g_launches;
+  if (e != cudaSuccess) return cuda_fail(e, "pointwise_multiply");
+  return NTTK_OK;
+}
+
+// ---- host pipeline: chunked H2D -> kernels -> D2H over three streams ----------
+
+struct Workspace {
+  std::mutex mu;
+  int device = -1;
+  cudaStream_t st[3] = {};
+  void* buf[3][3] = {};
+  size_t cap = 0;  // bytes per buffer
+  unsigned* d_flag = nullptr;
+};
+
+Workspace* workspace(int dev) {
+  static std::mutex m;
+  static std::unique_ptr<Workspace> ws[64];
+  std::lock_guard<std::mutex> lock(m);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!ws[dev]) {
+    auto w = std::make_unique<Workspace>();
+    w->device = dev;
+    for (auto& s : w->st)
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&w->d_flag, sizeof(unsigned)) != cudaSuccess) return nullptr;
+    ws[dev] = std::move(w);
+  }
+  return ws[dev].get();
+}
+
+int ensure_cap(Workspace& W, size_t bytes) {
+  if (W.cap >= bytes) return NTTK_OK;
+  cudaDeviceSynchronize();
+  for (auto& row : W.buf)
+    for (auto& b : row)
+      if (b) {
+        cudaFree(b);
+        b = nullptr;
+      }
+  W.cap = 0;
+  for (auto& row : W.buf)
+    for (auto& b : row) {
+      cudaError_t e = cudaMalloc(&b, bytes);
+      if (e != cudaSuccess) return cuda_fail(e, "workspace");
+    }
+  W.cap = bytes;
+  return NTTK_OK;
+}
+
+constexpr size_t kChunkBytes = size_t(64) << 20;
+
+// compute(stream, dev bufs[3], chunk polys) issues the kernels for one chunk;
+// inputs land in bufs[0..n_in), outputs are read from out_slot[i]
+template <class F>
+int host_pipeline(const HostParams& P, int elem, size_t batch, const std::vector<const void*>& h_in,
+                  const std::vector<std::pair<void*, int>>& h_out, F compute, const char* who,
+                  bool check_input_bound, uint64_t bound) {
+  if (int s = need_device(who)) return s;
+  Workspace* W = workspace(current_device());
+  if (!W) return fail(NTTK_CUDA, std::string(who) + ": workspace setup failed");
+  std::lock_guard<std::mutex> lock(W->mu);
+  const size_t poly_bytes = size_t(P.N) * elem;
+  size_t chunk = std::max<size_t>(1, kChunkBytes / poly_bytes);
+  if (chunk > batch) chunk = batch ? batch : 1;
+  if (int s = ensure_cap(*W, chunk * poly_bytes)) return s;
+  cudaError_t e = cudaMemset(W->d_flag, 0, sizeof(unsigned));
+  if (e != cudaSuccess) return cuda_fail(e, who);
+  size_t k = 0;
+  for (size_t done = 0; done < batch; done += chunk, ++k) {
+    const size_t n = std::min(chunk, batch - done);
+    const int s = static_cast<int>(k % 3);
+    cudaStream_t st = W->st[s];
+    for (size_t i = 0; i < h_in.size(); ++i) {
+      e = cudaMemcpyAsync(W->buf[s][i], static_cast<const char*>(h_in[i]) + done * poly_bytes,
+                          n * poly_bytes, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, who);
+      if (check_input_bound && i == 0) {
+        e = nttk_b200::check_canonical(W->buf[s][0], n * P.N, elem, bound, W->d_flag, st);
+        ++g_launches;
+        if (e != cudaSuccess) return cuda_fail(e, who);
+      }
+    }
+    if (int rc = compute(st, W->buf[s], n)) return rc;
+    for (const auto& o : h_out) {
+      if (!o.first) continue;
+      e = cudaMemcpyAsync(static_cast<char*>(o.first) + done * poly_bytes, W->buf[s][o.second],
+                          n * poly_bytes, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return cuda_fail(e, who);
+    }
+  }
+  for (auto& st : W->st) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, who);
+  }
+  unsigned flag = 0;
+  e = cudaMemcpy(&flag, W->d_flag, sizeof flag, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, who);
+  if (flag) return NTTK_PROPERTY;  // caller turns it into its contract message
+  return NTTK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nttk_last_error(void) { return g_err.c_str(); }
+uint64_t nttk_launch_count(void) { return g_launches.load(); }
+int nttk_device_available(void) { return device_count() > 0 ? 1 : 0; }
+const char* nttk_version(void) { return "nttk-b200 0.1 (sm_100a)"; }
+
+int nttk_build_params(const nttk_params_desc* desc, nttk_params_t* out) {
+  if (!desc || !out) return fail(NTTK_CONTRACT, "build_params: null argument");
+  try {
+    auto h = std::make_unique<nttk_params_s>();
+    std::string err;
+    const int st = nttk_b200::build_params(*desc, h->P, err);
+    if (st != NTTK_OK) return fail(st, err);
+    *out = h.release();
+    return NTTK_OK;
+  } catch (const std::exception& e) {
+    return fail(NTTK_CONTRACT, e.what());
+  }
+}
+
+int nttk_preset(const char* name, nttk_params_t* out) {
+  nttk_params_desc d;
+  std::string err;
+  if (nttk_b200::preset_desc(name ? name : "", d, err) != NTTK_OK) return fail(NTTK_CONTRACT, err);
+  return nttk_build_params(&d, out);
+}
+
+int nttk_params_destroy(nttk_params_t P) {
+  delete P;
+  return NTTK_OK;
+}
+
+int nttk_params_get_info(nttk_params_t h, nttk_params_info* o) {
+  if (!h || !o) return fail(NTTK_CONTRACT, "params_get_info: null argument");
+  const HostParams& P = h->P;
+  o->p = P.p;
+  o->omega = P.omega;
+  o->omega_inv = P.omega_inv;
+  o->n_inv = P.n_inv;
+  o->n_inv_hat = P.n_inv_hat;
+  o->mu = P.ctx.mu;
+  o->N = P.N;
+  o->log2N = P.log2N;
+  o->n_bits = P.n_bits;
+  o->layers = P.layers;
+  o->tree = P.tree;
+  o->kinds_mask = P.kinds;
+  o->scott_L = P.scott_L;
+  o->fast_path = 0;
+  for (int k = 0; k < 5; ++k)
+    if (((P.kinds >> k) & 1u) && use_fast(P, k)) o->fast_path |= 1u << k;
+  return NTTK_OK;
+}
+
+size_t nttk_params_table(nttk_params_t h, const char* name, uint64_t* out, size_t cap) {
+  if (!h || !name) return 0;
+  const HostParams& P = h->P;
+  const std::string n = name;
+  std::vector<uint64_t> tmp;
+  const std::vector<uint64_t>* v = nullptr;
+  if (n == "dif_w") v = &P.dif_w;
+  else if (n == "dif_wq") v = &P.dif_wq;
+  else if (n == "dif_mont") v = &P.dif_mont;
+  else if (n == "ct_plain") v = &P.ct_plain;
+  else if (n == "ct_plantard") v = &P.ct_plantard;
+  else if (n == "ct_mont") v = &P.ct_mont;
+  else if (n == "gs_plain") v = &P.gs_plain;
+  else if (n == "gs_wq") v = &P.gs_wq;
+  else if (n == "gs_mont") v = &P.gs_mont;
+  else if (n == "gs_plantard") v = &P.gs_plantard;
+  else if (n == "gamma") v = &P.gamma;
+  else if (n == "ct_smont" || n == "gs_smont") {
+    for (int64_t x : (n == "ct_smont" ? P.ct_smont : P.gs_smont))
+      tmp.push_back(static_cast<uint64_t>(x));
+    v = &tmp;
+  }
+  if (!v) return 0;
+  if (out) std::memcpy(out, v->data(), std::min(cap, v->size()) * 8);
+  return v->size();
+}
+
+// ---- device entry points ---------------------------------------------------
+
+int nttk_ntt_forward(nttk_params_t h, int kind, const void* d_in, void* d_out, size_t batch,
+                     int elem, void* stream) {
+  if (!h) return fail(NTTK_CONTRACT, "ntt_forward: null params");
+  if (int s = check_kind(h->P, kind, "ntt_forward")) return s;
+  if (int s = check_storage(h->P, kind, elem, "ntt_forward")) return s;
+  if (int s = need_device("ntt_forward")) return s;
+  return run_transform(h->P, kind, 0, d_in, d_out, batch, elem, static_cast<cudaStream_t>(stream));
+}
+
+int nttk_intt_inverse(nttk_params_t h, int kind, const void* d_in, void* d_out, size_t batch,
+                      int elem, void* stream) {
+  if (!h) return fail(NTTK_CONTRACT, "intt_inverse: null params");
+  if (int s = check_kind(h->P, kind, "intt_inverse")) return s;
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, "intt_inverse: elem_bytes must be 2, 4 or 8");
+  if (int s = need_device("intt_inverse")) return s;
+  return run_transform(h->P, kind, 1, d_in, d_out, batch, elem, static_cast<cudaStream_t>(stream));
+}
+
+int nttk_pointwise_multiply(nttk_params_t h, int kind, const void* d_l, const void* d_r,
+                            void* d_out, size_t batch, int elem, void* stream) {
+  if (!h) return fail(NTTK_CONTRACT, "pointwise_multiply: null params");
+  if (int s = check_kind(h->P, kind, "pointwise_multiply")) return s;
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, "pointwise_multiply: elem_bytes must be 2, 4 or 8");
+  if (int s = need_device("pointwise_multiply")) return s;
+  cudaError_t e = nttk_b200::generic_pointwise(h->P, kind, d_l, d_r, d_out, batch, elem,
+                                               static_cast<cudaStream_t>(stream));
+  if (batch) ++g_launches;
+  if (e != cudaSuccess) return cuda_fail(e, "pointwise_multiply");
+  return NTTK_OK;
+}
+
+int nttk_basemul(nttk_params_t h, int kind, const void* d_l, const void* d_r, void* d_out,
+                 size_t batch, int elem, void* stream) {
+  if (!h) return fail(NTTK_CONTRACT, "basemul: null params");
+  if (int s = check_kind(h->P, kind, "basemul")) return s;
+  if ((h->P.N >> h->P.layers) != 2)
+    return fail(NTTK_CONTRACT, "basemul: tree must end in degree-2 factors");
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, "basemul: elem_bytes must be 2, 4 or 8");
+  if (int s = need_device("basemul")) return s;
+  return run_product(h->P, kind, d_l, d_r, d_out, batch, elem, static_cast<cudaStream_t>(stream));
+}
+
+int nttk_polymul(nttk_params_t h, int kind, const void* d_a, const void* d_b, void* d_out,
+                 size_t batch, int elem, void* stream) {
+  if (!h) return fail(NTTK_CONTRACT, "polymul: null params");
+  const HostParams& P = h->P;
+  if (int s = check_kind(P, kind, "polymul")) return s;
+  if (int s = check_storage(P, kind, elem, "polymul")) return s;
+  if (int s = need_device("polymul")) return s;
+  if (!batch) return NTTK_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* tmp = nullptr;
+  const size_t bytes = batch * P.N * size_t(elem);
+  cudaError_t e = cudaMallocAsync(&tmp, bytes, st);
+  if (e != cudaSuccess) return cuda_fail(e, "polymul");
+  int rc = run_transform(P, kind, 0, d_b, tmp, batch, elem, st);
+  if (!rc) rc = run_transform(P, kind, 0, d_a, d_out, batch, elem, st);
+  if (!rc) rc = run_product(P, kind, d_out, tmp, d_out, batch, elem, st);
+  if (!rc) rc = run_transform(P, kind, 1, d_out, d_out, batch, elem, st);
+  cudaFreeAsync(tmp, st);
+  return rc;
+}
+
+// ---- host entry points ----------------------------------------------------------
+
+int nttk_ntt_forward_host(nttk_params_t h, int kind, const void* h_in, void* h_out, size_t batch,
+                          int elem) {
+  if (!h) return fail(NTTK_CONTRACT, "ntt_forward: null params");
+  const HostParams& P = h->P;
+  if (int s = check_kind(P, kind, "ntt_forward")) return s;
+  if (int s = check_storage(P, kind, elem, "ntt_forward")) return s;
+  const int rc = host_pipeline(
+      P, elem, batch, {h_in}, {{h_out, 1}},
+      [&](cudaStream_t st, void** b, size_t n) { return run_transform(P, kind, 0, b[0], b[1], n, elem, st); },
+      "ntt_forward", true, P.p);
+  if (rc == NTTK_PROPERTY) return fail(NTTK_CONTRACT, "ntt_forward: coefficients must be canonical");
+  return rc;
+}
+
+int nttk_intt_inverse_host(nttk_params_t h, int kind, const void* h_in, void* h_out, size_t batch,
+                           int elem) {
+  if (!h) return fail(NTTK_CONTRACT, "intt_inverse: null params");
+  const HostParams& P = h->P;
+  if (int s = check_kind(P, kind, "intt_inverse")) return s;
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, "intt_inverse: elem_bytes must be 2, 4 or 8");
+  return host_pipeline(
+      P, elem, batch, {h_in}, {{h_out, 1}},
+      [&](cudaStream_t st, void** b, size_t n) { return run_transform(P, kind, 1, b[0], b[1], n, elem, st); },
+      "intt_inverse", false, 0);
+}
+
+int nttk_roundtrip_host(nttk_params_t h, int kind, const void* h_in, void* h_spec, void* h_out,
+                        size_t batch, int elem) {
+  if (!h) return fail(NTTK_CONTRACT, "roundtrip: null params");
+  const HostParams& P = h->P;
+  if (int s = check_kind(P, kind, "ntt_forward")) return s;
+  if (int s = check_storage(P, kind, elem, "ntt_forward")) return s;
+  const int rc = host_pipeline(
+      P, elem, batch, {h_in}, {{h_spec, 1}, {h_out, 2}},
+      [&](cudaStream_t st, void** b, size_t n) {
+        int r = run_transform(P, kind, 0, b[0], b[1], n, elem, st);
+        if (!r) r = run_transform(P, kind, 1, b[1], b[2], n, elem, st);
+        return r;
+      },
+      "roundtrip", true, P.p);
+  if (rc == NTTK_PROPERTY) return fail(NTTK_CONTRACT, "ntt_forward: coefficients must be canonical");
+  return rc;
+}
+
+int nttk_pointwise_multiply_host(nttk_params_t h, int kind, const void* h_l, const void* h_r,
+                                 void* h_out, size_t batch, int elem) {
+  if (!h) return fail(NTTK_CONTRACT, "pointwise_multiply: null params");
+  const HostParams& P = h->P;
+  if (int s = check_kind(P, kind, "pointwise_multiply")) return s;
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, "pointwise_multiply: elem_bytes must be 2, 4 or 8");
+  // the improved product consumes a lazy right operand below 2^ell p
+  // (modified_plantard_mul's contract, reduction.hpp:264-273)
+  const bool chk = kind == NTTK_IMPROVED;
+  const uint64_t bound = uint64_t(P.p) << P.log2N;
+  const int rc = host_pipeline(
+      P, elem, batch, {h_r, h_l}, {{h_out, 2}},
+      [&](cudaStream_t st, void** b, size_t n) { return run_product(P, kind, b[1], b[0], b[2], n, elem, st); },
+      "pointwise_multiply", chk, bound);
+  if (rc == NTTK_PROPERTY)
+    return fail(NTTK_CONTRACT, "modified_plantard_mul: T must be < 2^ell * p");
+  return rc;
+}
+
+int nttk_polymul_host(nttk_params_t h, int kind, const void* h_a, const void* h_b, void* h_out,
+                      size_t batch, int elem) {
+  if (!h) return fail(NTTK_CONTRACT, "polymul: null params");
+  const HostParams& P = h->P;
+  if (int s = check_kind(P, kind, "polymul")) return s;
+  if (int s = check_storage(P, kind, elem, "polymul")) return s;
+  const int rc = host_pipeline(
+      P, elem, batch, {h_a, h_b}, {{h_out, 2}},
+      [&](cudaStream_t st, void** b, size_t n) {
+        int r = run_transform(P, kind, 0, b[0], b[0], n, elem, st);
+        if (!r) r = run_transform(P, kind, 0, b[1], b[1], n, elem, st);
+        if (!r) r = run_product(P, kind, b[0], b[1], b[2], n, elem, st);
+        if (!r) r = run_transform(P, kind, 1, b[2], b[2], n, elem, st);
+        return r;
+      },
+      "polymul", true, P.p);
+  if (rc == NTTK_PROPERTY) return fail(NTTK_CONTRACT, "ntt_forward: coefficients must be canonical");
+  return rc;
+}
+
+// ---- reductions -------------------------------------------------------------------
+
+int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, const int64_t* d_A,
+                      size_t na, const int64_t* d_B, size_t nb, int64_t* d_r,
+                      uint64_t* h_checksum, void* stream) {
+  if (variant < NTTK_REDC_MONT || variant > NTTK_REDC_MPLANTARD)
+    return fail(NTTK_CONTRACT, "modmul_sweep: unknown reduction variant");
+  if (n_bits < 2 || n_bits > 32)
+    return fail(NTTK_CONTRACT, "reduction context: word size n must be in [2, 32]");
+  if (p < 3 || !(p & 1)) return fail(NTTK_CONTRACT, "reduction context: p must be odd and >= 3");
+  if (p >= (uint64_t(1) << n_bits)) return fail(NTTK_CONTRACT, "reduction context: p must be < 2^n");
+  if (ell >= n_bits) return fail(NTTK_CONTRACT, "reduction context: ell must be < n");
+  const nttk_b200::Ctx c = nttk_b200::make_ctx(p, n_bits, ell);
+  using nttk_b200::u128;
+  // per-variant context bounds (reduction.hpp:64-77)
+  if (variant == NTTK_REDC_SMONT && !(u128(2) * p < (u128(1) << n_bits)))
+    return fail(NTTK_CONTRACT, "signed_mont_redc: requires 2p < 2^n");
+  if (variant == NTTK_REDC_PLANTARD) {
+    const u128 d = (u128(1) << (n_bits + 1)) - p;
+    if (!(u128(5) * p * p < d * d)) return fail(NTTK_CONTRACT, "plantard_redc: requires p*phi < 2^n");
+  }
+  if (variant == NTTK_REDC_MPLANTARD &&
+      !(ell + 2 < n_bits && u128(p) < (u128(1) << (n_bits - ell - 2))))
+    return fail(NTTK_CONTRACT, "modified_plantard_mul: requires p < 2^{n-ell-2}");
+  if (int s = need_device("modmul_sweep")) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d_sum = nullptr;
+  cudaError_t e = cudaMallocAsync(&d_sum, sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = nttk_b200::sweep_launch(variant, c, d_A, na, d_B, nb, d_r, d_sum, st);
+  ++g_launches;
+  unsigned long long sum = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&sum, d_sum, sizeof sum, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (d_sum) cudaFreeAsync(d_sum, st);
+  if (e != cudaSuccess) return cuda_fail(e, "modmul_sweep");
+  if (h_checksum) *h_checksum = sum;
+  return NTTK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,219 @@
+// arith.cuh -- sm_100a modular arithmetic and butterfly policies (device).
+//
+// Each policy restates one reference butterfly family on the 32-bit integer datapath
+// of Blackwell, bit-exact with the reference's u64 formulas (butterfly.hpp,
+// reduction.hpp) for the parameter ranges the host admits to the fast path
+// (params.cpp fast_eligible):
+//
+//   ImprovedN16 / ImprovedN32   Alg. 10-12 modified Plantard (reduction.hpp:252-258,
+//                               butterfly.hpp:224-243) with n = 16 / n = 32
+//   HarveyN16  / HarveyN32      Alg. 8 Montgomery lazy [0, 2p) (butterfly.hpp:92-106)
+//   SmontN16   / SmontN32       signed Montgomery (reduction.hpp:141-165) in CT/GS form
+//                               (extension)
+//
+// SASS per Plantard multiply (committed census: profiles/sass_census.txt):
+//   n=16: IMAD (h = t * w_hat mu) + IMAD.HI (r = hi32(h p))
+//   n=32: IMAD + IMAD.HI (h_hi + 1) + IMAD.HI (r = hi32((h_hi + 1) p))
+#pragma once
+
+#include <cstdint>
+
+#include "params.hpp"
+
+namespace nttk_b200 {
+
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
+// x mod p, exact for every 32-bit x: q = floor(x m / 2^32) with m = floor((2^32-1)/p)
+// undershoots floor(x/p) by at most one, one min() fixes it.
+__device__ __forceinline__ uint32_t mod_u32(uint32_t x, const FastArgs& A) {
+  const uint32_t r = x - __umulhi(x, A.canon_m) * A.p;
+  return umin32(r, r - A.p);
+}
+// x mod p for x < 2^16: m = ceil(2^32 / p) makes the quotient exact (two IMADs).
+__device__ __forceinline__ uint32_t mod_u16(uint32_t x, const FastArgs& A) {
+  return x - __umulhi(x, A.canon_m16) * A.p;
+}
+// canonical residue of a two's complement 32-bit value
+__device__ __forceinline__ uint32_t mod_s32(uint32_t x, const FastArgs& A) {
+  // x + 2^31 is non-negative; subtract 2^31 mod p afterwards
+  const uint32_t c = mod_u32(x ^ 0x80000000u, A);
+  const uint32_t k = mod_u32(0x80000000u, A);
+  const uint32_t t = c - k;
+  return umin32(t, t + A.p);
+}
+
+// ---------------------------------------------------------------------------
+// Modified Plantard multiply (Alg. 10), twiddle premultiplied by mu.
+//   reference:  h = ((w t) mu) mod 2^{2n};  r = (((h >> n) + 1) p) >> n
+// n = 16: the paper form costs IMAD, SHF, IMAD, SHF.  On a 32-bit datapath the full
+// 2n-bit product h p is one IMAD.HI away, and Prop. 4's exact-quotient identity
+// r = (h p - w t) / 2^{2n} (asserted by reduction_test.cpp:166-170)
+// with 0 <= w t < 2^{2n} gives r = floor(h p / 2^{2n}) = hi32(h p) exactly.
+template <bool PAPER_FORM>
+__device__ __forceinline__ uint32_t mp_n16(uint32_t t, uint32_t wm, uint32_t p) {
+  const uint32_t h = t * wm;
+  if (PAPER_FORM) return (((h >> 16) + 1u) * p) >> 16;
+  return __umulhi(h, p);
+}
+// n = 32: only h_hi = hi32(h) is needed: h_hi + 1 = hi32(lo t) + hi t + 1 (mod 2^32)
+// and r = hi32((h_hi + 1) p) -- three IMADs, no shifts.
+__device__ __forceinline__ uint32_t mp_n32(uint32_t t, uint32_t lo, uint32_t hi, uint32_t p) {
+  const uint32_t a = hi * t + 1u;
+  const uint32_t h1 = mad_hi(lo, t, a);
+  return __umulhi(h1, p);
+}
+
+// ---------------------------------------------------------------------------
+// Policies.  Values live in 32-bit registers (signed kinds: two's complement).
+// fwd(x, y, w): forward butterfly (CT form unless noted); inv(x, y, w, off): GS form.
+
+template <bool PAPER_FORM = false>
+struct ImprovedN16 {
+  using Tw = uint32_t;
+  static constexpr bool kSigned = false;
+  __device__ static Tw tw(const FastArgs& A, int k) { return A.lo[k]; }
+  // Alg. 11 (butterfly.hpp:224-230)
+  __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    const uint32_t r = mp_n16<PAPER_FORM>(y, w, A.p);
+    y = x + A.p - r;
+    x = x + r;
+  }
+  // Alg. 12 (butterfly.hpp:235-243), off = 2^{layer-1} p
+  __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    x = x + y;
+    y = mp_n16<PAPER_FORM>(t, w, A.p);
+  }
+  // final N^{-1} pass (transform.hpp:323-330)
+  __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
+    return mp_n16<PAPER_FORM>(v, A.scale_lo, A.p);
+  }
+};
+
+struct ImprovedN32 {
+  using Tw = uint2;
+  static constexpr bool kSigned = false;
+  __device__ static Tw tw(const FastArgs& A, int k) { return make_uint2(A.lo[k], A.hi[k]); }
+  __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    const uint32_t r = mp_n32(y, w.x, w.y, A.p);
+    y = x + A.p - r;
+    x = x + r;
+  }
+  __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    x = x + y;
+    y = mp_n32(t, w.x, w.y, A.p);
+  }
+  __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
+    return mp_n32(v, A.scale_lo, A.scale_hi, A.p);
+  }
+};
+
+// Montgomery reduction of prod = w t with p^{-1} (harvey_core's Y path,
+// butterfly.hpp:101-105):  r1 + p - ((q p) >> n), q = p^{-1} lo_n(prod) mod 2^n
+template <int N_BITS>
+__device__ __forceinline__ uint32_t harvey_mul(uint32_t t, uint32_t w, const FastArgs& A) {
+  if (N_BITS == 16) {
+    const uint32_t prod = w * t;        // < 4p^2 < 2^32
+    const uint32_t q16 = prod * A.pinv; // (p^{-1} prod mod 2^16) << 16
+    return (prod >> 16) + A.p - __umulhi(q16, A.p);
+  } else {
+    const uint64_t prod = static_cast<uint64_t>(w) * t;  // IMAD.WIDE
+    const uint32_t q = static_cast<uint32_t>(prod) * A.pinv;
+    return static_cast<uint32_t>(prod >> 32) + A.p - __umulhi(q, A.p);
+  }
+}
+
+template <int N_BITS, bool CT_FORWARD>
+struct Harvey {
+  using Tw = uint32_t;
+  static constexpr bool kSigned = false;
+  __device__ static Tw tw(const FastArgs& A, int k) { return A.lo[k]; }
+  __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    if (CT_FORWARD) {
+      // CT-form harvey (extension for the negacyclic tree): all values in [0, 2p)
+      const uint32_t r = harvey_mul<N_BITS>(y, w, A);
+      const uint32_t a = x + r, b = x + A.two_p - r;
+      x = umin32(a, a - A.two_p);
+      y = umin32(b, b - A.two_p);
+    } else {
+      dif(x, y, w, A);
+    }
+  }
+  // harvey_core (butterfly.hpp:92-106): X' = X + Y mod 2p (branchless), Y' lazy
+  __device__ static void dif(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    const uint32_t s = x + y;
+    const uint32_t t = x + A.two_p - y;
+    x = umin32(s, s - A.two_p);
+    y = harvey_mul<N_BITS>(t, w, A);
+  }
+  __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
+    dif(x, y, w, A);
+  }
+  // v in [0, 2p) -> v n^{-1} mod p, canonical (the reference's mul_mod,
+  // transform.hpp:331-335; any exact method is bit-identical)
+  __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
+    const uint32_t r = harvey_mul<N_BITS>(v, A.scale_lo, A);  // (0, 2p)
+    return umin32(r, r - A.p);
+  }
+};
+
+// Signed Montgomery (reduction.hpp:141-165): r = (A - m p) / 2^n, m = centered
+// lo_n(A p^{-1}); A = w y with the premultiplied quotient factor (w p^{-1} mod 2^n).
+template <int N_BITS>
+__device__ __forceinline__ int32_t smont_mul(int32_t y, int32_t w, uint32_t wq,
+                                             const FastArgs& A) {
+  if (N_BITS == 16) {
+    const int32_t a = w * y;                                         // |a| < p 2^15
+    const int32_t m = static_cast<int32_t>(wq * static_cast<uint32_t>(y)) >> 16;  // centered
+    return (a - m * static_cast<int32_t>(A.p)) >> 16;
+  } else {
+    const int64_t a = static_cast<int64_t>(w) * y;
+    const int32_t m = static_cast<int32_t>(wq * static_cast<uint32_t>(y));
+    return static_cast<int32_t>((a - static_cast<int64_t>(m) * A.p) >> 32);
+  }
+}
+
+// signed Barrett a - round(a V / 2^S) p, S = n + 10 (extension; oracle
+// or_signed_barrett)
+template <int N_BITS>
+__device__ __forceinline__ int32_t sbarrett(int32_t a, const FastArgs& A) {
+  if (N_BITS == 16) {
+    const int32_t q = (a * static_cast<int32_t>(A.barrett_v) + (1 << 25)) >> 26;
+    return a - q * static_cast<int32_t>(A.p);
+  } else {
+    const int64_t q = (static_cast<int64_t>(a) * A.barrett_v + (int64_t(1) << 41)) >> 42;
+    return a - static_cast<int32_t>(q) * static_cast<int32_t>(A.p);
+  }
+}
+
+template <int N_BITS>
+struct Smont {
+  using Tw = uint2;  // (w, w p^{-1} mod 2^n [n=16: << 16])
+  static constexpr bool kSigned = true;
+  __device__ static Tw tw(const FastArgs& A, int k) { return make_uint2(A.lo[k], A.hi[k]); }
+  __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    const int32_t t = smont_mul<N_BITS>(static_cast<int32_t>(y), static_cast<int32_t>(w.x), w.y, A);
+    y = static_cast<uint32_t>(static_cast<int32_t>(x) - t);
+    x = static_cast<uint32_t>(static_cast<int32_t>(x) + t);
+  }
+  __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
+    const int32_t xs = static_cast<int32_t>(x), ys = static_cast<int32_t>(y);
+    x = static_cast<uint32_t>(sbarrett<N_BITS>(xs + ys, A));
+    y = static_cast<uint32_t>(smont_mul<N_BITS>(xs - ys, static_cast<int32_t>(w.x), w.y, A));
+  }
+  __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
+    const int32_t r = smont_mul<N_BITS>(static_cast<int32_t>(v), static_cast<int32_t>(A.scale_lo),
+                                        A.scale_hi, A);
+    return static_cast<uint32_t>(r + (r < 0 ? static_cast<int32_t>(A.p) : 0));
+  }
+};
+
+}  // namespace nttk_b200

@@ -1,0 +1,16 @@
+// fast256.hpp -- launcher interface of the N = 256 sm_100a kernels (fast256.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "params.hpp"
+
+namespace nttk_b200 {
+
+bool fast256_supports(int kind, int layers, int n_bits);
+// dir 0 = forward (ntt_forward), 1 = inverse (intt_inverse).  variant 1 selects the
+// paper-form n=16 Plantard tail ((h >> 16) + 1) p >> 16 (SASS census / A-B check).
+cudaError_t fast256_launch(const HostParams& P, int kind, int dir, const void* in, void* out,
+                           size_t batch, int elem_bytes, cudaStream_t st, int variant = 0);
+
+}  // namespace nttk_b200

@@ -1,0 +1,22 @@
+// generic.hpp -- launchers of the any-parameter kernels (generic.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "params.hpp"
+
+namespace nttk_b200 {
+
+cudaError_t generic_transform(const HostParams& P, const DeviceTables& T, int kind, int dir,
+                              const void* in, void* out, size_t batch, int elem_bytes,
+                              cudaStream_t st);
+cudaError_t generic_pointwise(const HostParams& P, int kind, const void* l, const void* r,
+                              void* out, size_t batch, int elem_bytes, cudaStream_t st);
+// d_gamma: N/2 per-pair basemul moduli gamma_k (x^2 - gamma_k), device memory
+cudaError_t generic_basemul(const HostParams& P, const uint64_t* d_gamma, int kind, const void* l,
+                            const void* r, void* out, size_t batch, int elem_bytes,
+                            cudaStream_t st);
+cudaError_t check_canonical(const void* in, size_t n, int elem_bytes, uint64_t p,
+                            unsigned* d_flag, cudaStream_t st);
+
+}  // namespace nttk_b200

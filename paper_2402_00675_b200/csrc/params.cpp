@@ -1,0 +1,428 @@
+// params.cpp -- host-side parameter bundle of the B200 engine.
+//
+// Exact host precompute for one parameter set, the B200 counterpart of
+// build_params (proj/include/nttk/params.hpp:137-268): validation with every fault
+// collected into one message (same fault strings as the reference so callers that
+// grep them keep working), the primitive root, the plain twiddle schedules and their
+// per-kind encodings, plus the device-ready images for the N=256 fast kernels.
+#include "params.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+namespace nttk_b200 {
+
+uint64_t pow_mod(uint64_t b, uint64_t e, uint64_t m) {
+  uint64_t acc = 1 % m;
+  b %= m;
+  for (; e; e >>= 1) {
+    if (e & 1) acc = static_cast<uint64_t>(u128(acc) * b % m);
+    b = static_cast<uint64_t>(u128(b) * b % m);
+  }
+  return acc;
+}
+
+uint64_t bit_reverse(uint64_t x, unsigned bits) {
+  uint64_t r = 0;
+  for (unsigned i = 0; i < bits; ++i, x >>= 1) r = (r << 1) | (x & 1);
+  return r;
+}
+
+// inverse of a modulo m (m up to 2^64 as u128), extended Euclid (crt.hpp:37-57)
+u128 inverse(u128 a, u128 m) {
+  a %= m;
+  i128 r0 = static_cast<i128>(m), r1 = static_cast<i128>(a), t0 = 0, t1 = 1;
+  while (r1 != 0) {
+    const i128 q = r0 / r1;
+    i128 tmp = r0 - q * r1;
+    r0 = r1;
+    r1 = tmp;
+    tmp = t0 - q * t1;
+    t0 = t1;
+    t1 = tmp;
+  }
+  i128 v = t0 % static_cast<i128>(m);
+  if (v < 0) v += static_cast<i128>(m);
+  return static_cast<u128>(v);
+}
+
+// reduction.hpp:80-117
+Ctx make_ctx(uint64_t p, unsigned n, unsigned ell) {
+  Ctx c;
+  c.p = static_cast<uint32_t>(p);
+  c.n_bits = n;
+  c.ell = ell;
+  c.beta = uint64_t(1) << n;
+  c.beta_mask = c.beta - 1;
+  c.r2n_mask = 2 * n == 64 ? ~uint64_t(0) : (uint64_t(1) << (2 * n)) - 1;
+  c.p_inv_beta = static_cast<uint64_t>(inverse(p, u128(1) << n));
+  c.neg_p_inv_beta = (c.beta - c.p_inv_beta) & c.beta_mask;
+  c.mu = static_cast<uint64_t>(inverse(p, u128(1) << (2 * n)));
+  c.beta_mod_p = c.beta % p;
+  c.r2n_mod_p = pow_mod(2, 2 * n, p);
+  return c;
+}
+
+namespace {
+
+unsigned log2_floor(uint64_t x) {
+  unsigned r = 0;
+  while (x >>= 1) ++r;
+  return r;
+}
+
+bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+bool prime(uint64_t x) {
+  if (x < 2) return false;
+  for (uint64_t d = 2; d * d <= x; ++d)
+    if (x % d == 0) return false;
+  return true;
+}
+
+uint64_t to_plantard(uint64_t w, const Ctx& c) {  // reduction.hpp:279-283
+  return (c.p - static_cast<uint64_t>(u128(w) * c.r2n_mod_p % c.p)) % c.p;
+}
+uint64_t to_mont(uint64_t w, const Ctx& c) {  // reduction.hpp:287-291
+  return static_cast<uint64_t>(u128(w) * c.beta_mod_p % c.p);
+}
+int64_t to_smont(uint64_t w, const Ctx& c) {  // centered Montgomery twiddle (extension)
+  const uint64_t m = to_mont(w % c.p, c);
+  return m > c.p / 2 ? static_cast<int64_t>(m) - static_cast<int64_t>(c.p)
+                     : static_cast<int64_t>(m);
+}
+
+uint64_t smallest_root(uint64_t p, uint64_t order) {  // params.hpp:30-43
+  if (order == 1) return 1;
+  for (uint64_t w = 2; w < p; ++w)
+    if (pow_mod(w, order, p) == 1 && pow_mod(w, order / 2, p) != 1) return w;
+  return 0;
+}
+
+void add_fault(std::string& s, const std::string& f) { s += "\n  - " + f; }
+
+// ---- device images for the N=256 fast kernels (fast256.cu) ----
+
+bool fast_eligible(const HostParams& P, int kind) {
+  if (P.N != 256 || P.layers < 5 || !(P.n_bits == 16 || P.n_bits == 32)) return false;
+  const uint64_t p = P.p;
+  switch (kind) {
+    case NTTK_IMPROVED:  // every intermediate < 2^layers p must fit a 32-bit register
+      return (uint64_t(P.layers) + 1) * p < (uint64_t(1) << 32) &&
+             (p << P.layers) < (uint64_t(1) << 32);
+    case NTTK_HARVEY: return 4 * p < (uint64_t(1) << 32);
+    case NTTK_SMONT:  // signed values fit int32; Barrett constant fits 32 bits
+      return (uint64_t(P.layers) + 2) * p < (uint64_t(1) << 31) &&
+             (u128(1) << (P.n_bits + 10)) / p < (u128(1) << 32);
+    default: return false;  // ntl, scott: generic kernel
+  }
+}
+
+void fill_fast(HostParams& P, int kind) {
+  const Ctx& c = P.ctx;
+  const bool n16 = P.n_bits == 16;
+  for (int dir = 0; dir < 2; ++dir) {
+    FastArgs& A = P.fast[kind][dir];
+    A.p = P.p;
+    A.two_p = 2 * P.p;
+    A.layers = P.layers;
+    A.canon_m = static_cast<uint32_t>(0xffffffffull / P.p);
+    A.canon_m16 = static_cast<uint32_t>(((uint64_t(1) << 32) + P.p - 1) / P.p);
+    // K p >= 2^{bits-1} (bits = 16 or 32 storage): lifts two's complement to unsigned
+    {
+      const uint64_t half = n16 ? (uint64_t(1) << 15) : (uint64_t(1) << 31);
+      A.sgn_off = static_cast<uint32_t>((half + P.p - 1) / P.p * P.p);
+    }
+    A.barrett_v = static_cast<uint32_t>(((u128(1) << (P.n_bits + 10)) + (P.p >> 1)) / P.p);
+    const std::vector<uint64_t>* tab = nullptr;
+    switch (kind) {
+      case NTTK_IMPROVED: {
+        tab = dir == 0 ? &P.ct_plantard : &P.gs_plantard;
+        const uint64_t mu = c.mu;  // p^{-1} mod 2^{2n}
+        for (size_t k = 0; k < tab->size(); ++k) {
+          const uint64_t wm = (*tab)[k] * mu & c.r2n_mask;  // w_hat mu mod 2^{2n}
+          A.lo[k] = static_cast<uint32_t>(wm);
+          A.hi[k] = static_cast<uint32_t>(wm >> 32);
+        }
+        const uint64_t sm = P.n_inv_hat * mu & c.r2n_mask;
+        A.scale_lo = static_cast<uint32_t>(sm);
+        A.scale_hi = static_cast<uint32_t>(sm >> 32);
+        break;
+      }
+      case NTTK_HARVEY: {
+        if (dir == 0) tab = P.tree == NTTK_CYCLIC ? &P.dif_mont : &P.ct_mont;
+        else tab = &P.gs_mont;
+        for (size_t k = 0; k < tab->size(); ++k) A.lo[k] = static_cast<uint32_t>((*tab)[k]);
+        A.pinv = n16 ? static_cast<uint32_t>(c.p_inv_beta << 16)
+                     : static_cast<uint32_t>(c.p_inv_beta);
+        A.scale_lo = static_cast<uint32_t>(P.n_inv_mont);
+        break;
+      }
+      case NTTK_SMONT: {
+        const std::vector<int64_t>& st = dir == 0 ? P.ct_smont : P.gs_smont;
+        for (size_t k = 0; k < st.size(); ++k) {
+          const int64_t w = st[k];
+          A.lo[k] = static_cast<uint32_t>(w);
+          // premultiplied Montgomery quotient factor w p^{-1} mod 2^n (n=16: in the
+          // high half so a 32-bit multiply leaves the n-bit product there)
+          const uint64_t wp = static_cast<uint64_t>(w) * c.p_inv_beta & c.beta_mask;
+          A.hi[k] = n16 ? static_cast<uint32_t>(wp << 16) : static_cast<uint32_t>(wp);
+        }
+        const int64_t f = P.n_inv_smont;
+        A.scale_lo = static_cast<uint32_t>(f);
+        const uint64_t fp = static_cast<uint64_t>(f) * c.p_inv_beta & c.beta_mask;
+        A.scale_hi = n16 ? static_cast<uint32_t>(fp << 16) : static_cast<uint32_t>(fp);
+        A.pinv = static_cast<uint32_t>(c.p_inv_beta);
+        break;
+      }
+    }
+  }
+  P.fast_mask |= 1u << kind;
+}
+
+}  // namespace
+
+HostParams::~HostParams() {
+  for (auto& d : dev)
+    if (d.base) cudaFree(d.base);
+}
+
+const DeviceTables* HostParams::device_tables(int device, std::string& err) const {
+  if (device < 0 || device >= 64) {
+    err = "device ordinal out of range";
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu_dev);
+  DeviceTables& D = dev[device];
+  if (D.base) return &D;
+  const std::vector<const std::vector<uint64_t>*> tabs = {
+      &dif_w, &dif_wq, &dif_mont, &ct_plantard, &ct_mont, &gs_plain, &gs_wq, &gs_mont,
+      &gs_plantard};
+  size_t total = 0;
+  for (auto* t : tabs) total += t->size();
+  total += ct_smont.size() + gs_smont.size() + gamma.size();
+  std::vector<uint64_t> host;
+  host.reserve(total);
+  std::vector<size_t> off;
+  for (auto* t : tabs) {
+    off.push_back(host.size());
+    host.insert(host.end(), t->begin(), t->end());
+  }
+  off.push_back(host.size());
+  for (int64_t v : ct_smont) host.push_back(static_cast<uint64_t>(v));
+  off.push_back(host.size());
+  for (int64_t v : gs_smont) host.push_back(static_cast<uint64_t>(v));
+  off.push_back(host.size());
+  host.insert(host.end(), gamma.begin(), gamma.end());
+  uint64_t* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, std::max<size_t>(host.size(), 1) * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(base, host.data(), host.size() * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    err = std::string("device table upload: ") + cudaGetErrorString(e);
+    if (base) cudaFree(base);
+    return nullptr;
+  }
+  D.base = base;
+  D.dif_w = base + off[0];
+  D.dif_wq = base + off[1];
+  D.dif_mont = base + off[2];
+  D.ct_plantard = base + off[3];
+  D.ct_mont = base + off[4];
+  D.gs_w = base + off[5];
+  D.gs_wq = base + off[6];
+  D.gs_mont = base + off[7];
+  D.gs_plantard = base + off[8];
+  D.ct_smont = base + off[9];
+  D.gs_smont = base + off[10];
+  D.gamma = base + off[11];
+  return &D;
+}
+
+int build_params(const nttk_params_desc& d, HostParams& P, std::string& err) {
+  std::string faults = "build_params:";
+  const size_t clean = faults.size();
+  const uint64_t p = d.p;
+  const uint32_t N = d.N, n = d.n_bits, kinds = d.kinds_mask;
+  // structural faults (params.hpp:145-169)
+  if (n < 2 || n > 32) add_fault(faults, "word size n must be in [2, 32]");
+  if (p < 3 || !(p & 1)) add_fault(faults, "p must be odd and >= 3");
+  else if (!prime(p)) add_fault(faults, "p must be prime");
+  if (N < 2 || !pow2(N) || N > (1u << 20)) add_fault(faults, "N must be a power of two in [2, 2^20]");
+  if (!kinds) add_fault(faults, "at least one butterfly kind must be requested");
+  if (kinds & ~0x1fu) add_fault(faults, "unknown butterfly kind");
+  if (d.tree > NTTK_NEGACYCLIC) add_fault(faults, "unknown transform tree");
+  unsigned ell = 0, layers = 0;
+  if (faults.size() == clean) {
+    ell = log2_floor(N);
+    layers = d.layers ? d.layers : ell;
+    if (layers > ell || (d.tree == NTTK_CYCLIC && layers != ell))
+      add_fault(faults, "layers must be log2(N) (cyclic) or <= log2(N) (negacyclic)");
+    const uint64_t order = d.tree == NTTK_CYCLIC ? N : (uint64_t(2) << layers);
+    if ((p - 1) % order != 0)
+      add_fault(faults, "N must divide p - 1 (p=" + std::to_string(p) +
+                            ", N=" + std::to_string(order) + ")");
+    if (ell >= n) add_fault(faults, "word size n must exceed log2(N)");
+    if (p >= (uint64_t(1) << n)) add_fault(faults, "p must be < 2^n");
+  }
+  if (faults.size() != clean) {
+    err = faults;
+    return NTTK_CONTRACT;
+  }
+  P.desc = d;
+  P.p = static_cast<uint32_t>(p);
+  P.N = N;
+  P.log2N = ell;
+  P.n_bits = n;
+  P.tree = d.tree;
+  P.layers = layers;
+  P.kinds = kinds;
+  P.ctx = make_ctx(p, n, ell);
+  const Ctx& c = P.ctx;
+  const uint64_t order = d.tree == NTTK_CYCLIC ? N : (uint64_t(2) << layers);
+  if (d.root) {
+    if (pow_mod(d.root, order, p) != 1 || pow_mod(d.root, order / 2, p) == 1) {
+      err = "build_params:\n  - root does not have the required order";
+      return NTTK_CONTRACT;
+    }
+    P.omega = d.root;
+  } else {
+    P.omega = smallest_root(p, order);
+  }
+  P.omega_inv = static_cast<uint64_t>(inverse(P.omega, p));
+  P.n_inv = static_cast<uint64_t>(
+      inverse((d.tree == NTTK_CYCLIC ? N : (uint64_t(1) << layers)) % p, p));
+
+  // per-kind word-size faults (params.hpp:183-217)
+  auto has = [&](int k) { return (kinds >> k) & 1u; };
+  if (has(NTTK_NTL) && 2 * p >= c.beta)
+    add_fault(faults, "ntl: p=" + std::to_string(p) + " violates 2p < 2^n (n=" +
+                          std::to_string(n) + ")");
+  if (has(NTTK_HARVEY) && 4 * p >= c.beta)
+    add_fault(faults, "harvey: p=" + std::to_string(p) + " violates 4p < 2^n (n=" +
+                          std::to_string(n) + ")");
+  if (has(NTTK_SCOTT) && u128(4) * p >= c.beta)
+    add_fault(faults, "scott: p=" + std::to_string(p) +
+                          " violates 4*N*p < 2^n * L for every L <= N");
+  if (has(NTTK_IMPROVED)) {
+    bool ok;
+    if (d.flags & NTTK_EXACT_BOUND) {
+      // Prop. 4 exact requirement W T < 2^n (2^n - p), W <= p-1,
+      // T <= 2^layers p - 1 (largest lazy operand: inverse merge and final scaling)
+      const uint64_t T = (p << layers) - 1;
+      ok = u128(p - 1) * T < u128(c.beta) * (c.beta - p);
+    } else {
+      ok = ell + 2 < n && u128(p) < (u128(1) << (n - ell - 2));  // reduction.hpp:72-74
+    }
+    if (!ok)
+      add_fault(faults, "improved: p=" + std::to_string(p) + " violates p < 2^{n-ell-2} = " +
+                            std::to_string(n >= ell + 2 ? (uint64_t(1) << (n - ell - 2)) : 0) +
+                            " (n=" + std::to_string(n) + ", ell=" + std::to_string(ell) + ")");
+  }
+  if (has(NTTK_SMONT) && (2 * p >= c.beta || u128(layers + 1) * (p - 1) >= c.beta))
+    add_fault(faults, "smont: p=" + std::to_string(p) + " violates (layers+1)(p-1) < 2^n (n=" +
+                          std::to_string(n) + ")");
+  if (d.tree == NTTK_NEGACYCLIC && (has(NTTK_NTL) || has(NTTK_SCOTT)))
+    add_fault(faults, "ntl/scott are DIF kinds: cyclic tree only");
+  if (faults.size() != clean) {
+    err = faults;
+    return NTTK_CONTRACT;
+  }
+  if (has(NTTK_SCOTT)) {  // butterfly.hpp:157-168
+    for (uint64_t L = 1; L <= N; L *= 2)
+      if (u128(4) * N * p < u128(c.beta) * L) {
+        P.scott_L = static_cast<uint32_t>(L);
+        break;
+      }
+  }
+
+  // plain schedules and their encodings
+  const size_t T = (size_t(1) << layers) - 1;
+  if (d.tree == NTTK_CYCLIC && (has(NTTK_NTL) || has(NTTK_HARVEY) || has(NTTK_SCOTT))) {
+    for (uint64_t len = N / 2; len >= 1; len /= 2) {  // params.hpp:47-58
+      const uint64_t step = N / (2 * len);
+      for (uint64_t j = 0; j < len; ++j) {
+        const uint64_t w = pow_mod(P.omega, j * step, p);
+        P.dif_w.push_back(w);
+        P.dif_wq.push_back(static_cast<uint64_t>((u128(w) << n) / p));
+        P.dif_mont.push_back(to_mont(w, c));
+      }
+    }
+  }
+  for (unsigned s = 1; s <= layers; ++s) {  // forward CT, one twiddle per block
+    for (uint64_t b = 0; b < (uint64_t(1) << (s - 1)); ++b) {
+      uint64_t w;
+      if (d.tree == NTTK_CYCLIC)  // params.hpp:60-72
+        w = pow_mod(P.omega, (uint64_t(N) >> s) * bit_reverse(b, s - 1), p);
+      else  // zeta^{br_L(2^{s-1} + b)}
+        w = pow_mod(P.omega, bit_reverse((uint64_t(1) << (s - 1)) + b, layers), p);
+      P.ct_plain.push_back(w);
+      P.ct_plantard.push_back(to_plantard(w, c));
+      P.ct_mont.push_back(to_mont(w, c));
+      P.ct_smont.push_back(to_smont(w, c));
+    }
+  }
+  for (unsigned s = layers; s >= 1; --s) {  // inverse GS in merge order (params.hpp:74-88)
+    for (uint64_t b = 0; b < (uint64_t(1) << (s - 1)); ++b) {
+      uint64_t e, ord;
+      if (d.tree == NTTK_CYCLIC) {
+        ord = N;
+        e = (uint64_t(N) >> s) * bit_reverse(b, s - 1) % N;
+      } else {
+        ord = uint64_t(2) << layers;
+        e = bit_reverse((uint64_t(1) << (s - 1)) + b, layers) % ord;
+      }
+      const uint64_t w = pow_mod(P.omega, e == 0 ? 0 : ord - e, p);
+      P.gs_plain.push_back(w);
+      P.gs_wq.push_back(static_cast<uint64_t>((u128(w) << n) / p));
+      P.gs_mont.push_back(to_mont(w, c));
+      P.gs_plantard.push_back(to_plantard(w, c));
+      P.gs_smont.push_back(to_smont(w, c));
+    }
+  }
+  (void)T;
+  if ((N >> layers) == 2) {  // degree-2 leaves: x^2 -/+ z_b for last-layer block b
+    const size_t last = (size_t(1) << (layers - 1)) - 1;
+    for (uint32_t k = 0; k < N / 2; ++k) {
+      const uint64_t z = P.ct_plain[last + k / 2];
+      P.gamma.push_back((k & 1) ? (p - z) % p : z);
+    }
+  }
+  if (has(NTTK_IMPROVED)) P.n_inv_hat = to_plantard(P.n_inv, c);  // params.hpp:250
+  P.n_inv_mont = to_mont(P.n_inv, c);
+  P.n_inv_smont = to_smont(P.n_inv, c);
+
+  for (int k : {NTTK_IMPROVED, NTTK_HARVEY, NTTK_SMONT})
+    if (has(k) && fast_eligible(P, k)) fill_fast(P, k);
+  return NTTK_OK;
+}
+
+// params.hpp:273-306
+int preset_desc(const std::string& name, nttk_params_desc& d, std::string& err) {
+  struct Spec {
+    const char* name;
+    uint32_t p, N, n;
+  };
+  static const Spec table[] = {
+      {"kyber256", 7681, 256, 32},     {"kcl256", 7681, 256, 32},
+      {"newhope512", 12289, 512, 32},  {"falcon512", 12289, 512, 32},
+      {"remblem512", 12289, 512, 32},  {"newhope1024", 12289, 1024, 32},
+      {"falcon1024", 12289, 1024, 32}, {"hila5-1024", 12289, 1024, 32},
+      {"toy13", 13, 4, 8},
+  };
+  for (const auto& s : table)
+    if (name == s.name) {
+      std::memset(&d, 0, sizeof d);
+      d.p = s.p;
+      d.N = s.N;
+      d.n_bits = s.n;
+      d.kinds_mask = 0xf;  // all_butterfly_kinds()
+      return NTTK_OK;
+    }
+  std::string known;
+  for (const auto& s : table) known += known.empty() ? s.name : std::string(", ") + s.name;
+  err = "unknown preset '" + name + "' (known: " + known + ")";
+  return NTTK_CONTRACT;
+}
+
+}  // namespace nttk_b200

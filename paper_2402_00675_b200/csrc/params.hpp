@@ -1,0 +1,96 @@
+// params.hpp -- host-side parameter bundle of the B200 engine (internal).
+//
+// B200 counterpart of the reference's NttParams / build_params
+// (proj/include/nttk/params.hpp:107-268) and ReductionContext
+// (reduction.hpp:44-117).  Everything here is exact host integer precompute done once
+// per parameter set; the compute runs in the CUDA kernels of fast256.cu / generic.cu.
+// On top of the reference's encoded tables, the bundle carries the device-ready forms:
+//   * mu-premultiplied Plantard twiddles  w_hat * mu mod 2^{2n}  (the product
+//     (w_hat * t) * mu mod 2^{2n} of reduction.hpp:256 is associative mod 2^{2n}, so
+//     premultiplying is bit-exact and saves one multiply per butterfly);
+//   * per-device copies of every table for the generic kernel (uploaded lazily).
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/nttk_gpu.h"
+
+namespace nttk_b200 {
+
+using u128 = unsigned __int128;
+using i128 = __int128;
+
+// reduction.hpp:44-78
+struct Ctx {
+  uint32_t p = 0;
+  unsigned n_bits = 0, ell = 0;
+  uint64_t beta = 0, beta_mask = 0, r2n_mask = 0;
+  uint64_t p_inv_beta = 0, neg_p_inv_beta = 0, mu = 0;
+  uint64_t beta_mod_p = 0, r2n_mod_p = 0;
+};
+
+// Device copies of the tables used by the generic kernel (u64, reference order).
+struct DeviceTables {
+  uint64_t* base = nullptr;  // one allocation holding every table below
+  const uint64_t *dif_w = nullptr, *dif_wq = nullptr, *dif_mont = nullptr;
+  const uint64_t *ct_plantard = nullptr, *ct_mont = nullptr, *ct_smont = nullptr;
+  const uint64_t *gs_w = nullptr, *gs_wq = nullptr, *gs_mont = nullptr, *gs_plantard = nullptr,
+                 *gs_smont = nullptr;
+  const uint64_t* gamma = nullptr;  // basemul moduli (trees ending in degree-2 factors)
+};
+
+// Kernel-parameter image of one N=256 transform direction for the fast kernels.
+// Passed by value (lives in the constant bank): uniform twiddle reads are free
+// operands of IMAD; lane-dependent ones are loaded once per thread at kernel start.
+struct FastArgs {
+  uint32_t p = 0, two_p = 0;
+  uint32_t pinv = 0;       // harvey/smont: p^{-1} mod 2^n   (n=16: shifted left by 16)
+  uint32_t canon_m = 0;    // floor((2^32 - 1) / p): inverse-input canonicalisation
+  uint32_t canon_m16 = 0;  // ceil(2^32 / p): exact floor(x / p) for x < 2^16
+  uint32_t sgn_off = 0;    // K p >= 2^{bits-1}: lifts signed inputs to unsigned
+  uint32_t scale_lo = 0, scale_hi = 0;  // inverse final multiplier (per kind encoding)
+  uint32_t barrett_v = 0;  // smont signed Barrett constant V (S = n + 10)
+  uint32_t layers = 0;
+  uint32_t lo[256] = {};   // twiddle words in reference table order
+  uint32_t hi[256] = {};   // high words of 64-bit premultiplied Plantard twiddles
+};
+
+struct HostParams {
+  nttk_params_desc desc{};
+  uint32_t p = 0, N = 0, log2N = 0, n_bits = 0, tree = 0, layers = 0, kinds = 0;
+  uint32_t scott_L = 0;
+  uint64_t omega = 0, omega_inv = 0, n_inv = 0, n_inv_hat = 0, n_inv_mont = 0;
+  int64_t n_inv_smont = 0;
+  Ctx ctx;
+  // tables, reference order (params.hpp:47-88, 226-266)
+  std::vector<uint64_t> dif_w, dif_wq, dif_mont;
+  std::vector<uint64_t> ct_plain, ct_plantard, ct_mont;
+  std::vector<int64_t> ct_smont;
+  std::vector<uint64_t> gs_plain, gs_wq, gs_mont, gs_plantard;
+  std::vector<int64_t> gs_smont;
+  // basemul: pair k of a degree-2-leaf tree is a mod (x^2 - gamma[k])
+  std::vector<uint64_t> gamma;
+  // fast-path images, indexed [kind][dir] (dir 0 forward, 1 inverse)
+  uint32_t fast_mask = 0;
+  FastArgs fast[5][2];
+
+  mutable std::mutex mu_dev;
+  mutable DeviceTables dev[64];
+
+  const DeviceTables* device_tables(int device, std::string& err) const;
+  ~HostParams();
+};
+
+int build_params(const nttk_params_desc& d, HostParams& P, std::string& err);
+int preset_desc(const std::string& name, nttk_params_desc& d, std::string& err);
+
+// exact integer helpers shared with the host code
+Ctx make_ctx(uint64_t p, unsigned n_bits, unsigned ell);
+u128 inverse(u128 a, u128 m);
+uint64_t pow_mod(uint64_t b, uint64_t e, uint64_t m);
+uint64_t bit_reverse(uint64_t x, unsigned bits);
+
+}  // namespace nttk_b200

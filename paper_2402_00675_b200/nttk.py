@@ -1,0 +1,474 @@
+"""Python mirror of the reference ``nttk`` interface over the B200 engine's C ABI.
+
+The reference (/root/reference/proj/include/nttk) is a header-only C++20 library whose
+hot path is ``ntt_forward`` / ``intt_inverse`` / ``pointwise_multiply`` /
+``cyclic_convolution_via_ntt`` (transform.hpp:207-379) built on ``build_params``
+(params.hpp:137-268).  This module keeps those names, argument meanings and error
+behaviour (``ContractViolation`` carries the reference's contract_violation message),
+and routes every call through ``libnttk_gpu.so`` (include/nttk_gpu.h) to the sm_100a
+kernels.  There is no CPU fallback: without the built extension or a CUDA device the
+compute calls raise.
+
+Two layers:
+  * reference-shaped host calls on Python lists / numpy arrays (checked, synchronous);
+  * batched device calls on ``torch`` CUDA tensors (asynchronous on the current stream),
+    which is what the benchmark and large workloads use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnttk_gpu.so")
+
+
+class ButterflyKind(enum.IntEnum):
+    """butterfly.hpp:30 plus the signed-Montgomery extension kind."""
+
+    ntl = 0
+    harvey = 1
+    scott = 2
+    improved = 3
+    smont = 4
+
+
+class Ordering(enum.Enum):
+    natural = 0
+    bit_reversed = 1
+
+
+class Tree(enum.IntEnum):
+    cyclic = 0
+    negacyclic = 1
+
+
+class Redc(enum.IntEnum):
+    mont = 0
+    smont = 1
+    plantard = 2
+    modified_plantard = 3
+
+
+class ContractViolation(ValueError):
+    """nttk::contract_violation (int_util.hpp:17-21)."""
+
+
+class PropertyViolation(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def all_butterfly_kinds() -> list[ButterflyKind]:
+    """params.hpp:192-195."""
+    return [ButterflyKind.ntl, ButterflyKind.harvey, ButterflyKind.scott, ButterflyKind.improved]
+
+
+def butterfly_kind_from_string(name: str) -> ButterflyKind:
+    """butterfly.hpp:42-50."""
+    try:
+        return ButterflyKind[name]
+    except KeyError:
+        raise ContractViolation(
+            f'unknown butterfly kind "{name}" (ntl, harvey, scott, improved)') from None
+
+
+# ---------------------------------------------------------------------------
+# library binding
+
+class _Desc(C.Structure):
+    _fields_ = [("p", C.c_uint64), ("N", C.c_uint32), ("n_bits", C.c_uint32),
+                ("kinds_mask", C.c_uint32), ("tree", C.c_uint32), ("layers", C.c_uint32),
+                ("root", C.c_uint64), ("flags", C.c_uint32)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("p", C.c_uint64), ("omega", C.c_uint64), ("omega_inv", C.c_uint64),
+                ("n_inv", C.c_uint64), ("n_inv_hat", C.c_uint64), ("mu", C.c_uint64),
+                ("N", C.c_uint32), ("log2N", C.c_uint32), ("n_bits", C.c_uint32),
+                ("layers", C.c_uint32), ("tree", C.c_uint32), ("kinds_mask", C.c_uint32),
+                ("scott_L", C.c_uint32), ("fast_path", C.c_uint32)]
+
+
+EXPORTS = (
+    "nttk_build_params", "nttk_preset", "nttk_params_destroy", "nttk_params_get_info",
+    "nttk_params_table", "nttk_ntt_forward", "nttk_intt_inverse", "nttk_pointwise_multiply",
+    "nttk_basemul", "nttk_polymul", "nttk_ntt_forward_host", "nttk_intt_inverse_host",
+    "nttk_roundtrip_host", "nttk_pointwise_multiply_host", "nttk_polymul_host",
+    "nttk_modmul_sweep", "nttk_last_error", "nttk_launch_count", "nttk_device_available",
+    "nttk_version",
+)
+
+_lib_handle = None
+
+
+def lib() -> C.CDLL:
+    """Load libnttk_gpu.so; fails loudly when the extension was not built."""
+    global _lib_handle
+    if _lib_handle is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} missing: the CUDA extension is not built (run `make lib` or "
+                "__graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        vp, sz = C.c_void_p, C.c_size_t
+        L.nttk_build_params.argtypes = [C.POINTER(_Desc), C.POINTER(vp)]
+        L.nttk_preset.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.nttk_params_destroy.argtypes = [vp]
+        L.nttk_params_get_info.argtypes = [vp, C.POINTER(_Info)]
+        L.nttk_params_table.restype = sz
+        L.nttk_params_table.argtypes = [vp, C.c_char_p, vp, sz]
+        for f in ("nttk_ntt_forward", "nttk_intt_inverse"):
+            getattr(L, f).argtypes = [vp, C.c_int, vp, vp, sz, C.c_int, vp]
+        for f in ("nttk_pointwise_multiply", "nttk_basemul", "nttk_polymul"):
+            getattr(L, f).argtypes = [vp, C.c_int, vp, vp, vp, sz, C.c_int, vp]
+        for f in ("nttk_ntt_forward_host", "nttk_intt_inverse_host"):
+            getattr(L, f).argtypes = [vp, C.c_int, vp, vp, sz, C.c_int]
+        L.nttk_roundtrip_host.argtypes = [vp, C.c_int, vp, vp, vp, sz, C.c_int]
+        for f in ("nttk_pointwise_multiply_host", "nttk_polymul_host"):
+            getattr(L, f).argtypes = [vp, C.c_int, vp, vp, vp, sz, C.c_int]
+        L.nttk_modmul_sweep.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, vp, sz, vp,
+                                        sz, vp, C.POINTER(C.c_uint64), vp]
+        L.nttk_last_error.restype = C.c_char_p
+        L.nttk_launch_count.restype = C.c_uint64
+        L.nttk_version.restype = C.c_char_p
+        _lib_handle = L
+    return _lib_handle
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().nttk_last_error().decode()
+    if status == 2:
+        raise ContractViolation(msg)
+    if status == 1:
+        raise PropertyViolation(msg)
+    raise CudaError(msg)
+
+
+def device_available() -> bool:
+    return bool(lib().nttk_device_available())
+
+
+def launch_count() -> int:
+    """Kernel launches issued by the engine in this process (bench gpu_launches)."""
+    return int(lib().nttk_launch_count())
+
+
+# ---------------------------------------------------------------------------
+# parameters
+
+class NttParams:
+    """Handle over the engine's parameter bundle (params.hpp:107-128 NttParams)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        info = _Info()
+        _check(lib().nttk_params_get_info(self._h, C.byref(info)))
+        self.p = int(info.p)
+        self.size = int(info.N)
+        self.log2_size = int(info.log2N)
+        self.n_bits = int(info.n_bits)
+        self.omega = int(info.omega)
+        self.omega_inv = int(info.omega_inv)
+        self.n_inv = int(info.n_inv)
+        self.n_inv_hat = int(info.n_inv_hat)
+        self.mu = int(info.mu)
+        self.layers = int(info.layers)
+        self.tree = Tree(info.tree)
+        self.scott_lazy_level = int(info.scott_L)
+        self.kinds = [k for k in ButterflyKind if (info.kinds_mask >> k) & 1]
+        self.fast_path = [k for k in ButterflyKind if (info.fast_path >> k) & 1]
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().nttk_params_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def has(self, kind) -> bool:
+        return ButterflyKind(kind) in self.kinds
+
+    def table(self, name: str) -> np.ndarray:
+        n = lib().nttk_params_table(self._h, name.encode(), None, 0)
+        out = np.zeros(n, dtype=np.uint64)
+        lib().nttk_params_table(self._h, name.encode(), out.ctypes.data, n)
+        return out
+
+    def __repr__(self):
+        return (f"NttParams(p={self.p}, N={self.size}, n={self.n_bits}, tree={self.tree.name}, "
+                f"layers={self.layers}, kinds={[k.name for k in self.kinds]})")
+
+
+def build_params(p: int, N: int, n_bits: int, kinds: Iterable = None, *, tree=Tree.cyclic,
+                 layers: int = 0, root: int = 0, exact_bound: bool = False) -> NttParams:
+    """params.hpp:137-268; ``exact_bound`` admits `improved` under Prop. 4's exact bound."""
+    kinds = all_butterfly_kinds() if kinds is None else list(kinds)
+    mask = 0
+    for k in kinds:
+        mask |= 1 << int(k)
+    d = _Desc(p, N, n_bits, mask, int(tree), layers, root, 1 if exact_bound else 0)
+    h = C.c_void_p()
+    _check(lib().nttk_build_params(C.byref(d), C.byref(h)))
+    return NttParams(h.value)
+
+
+def preset(name: str) -> NttParams:
+    """params.hpp:303-306."""
+    h = C.c_void_p()
+    _check(lib().nttk_preset(name.encode(), C.byref(h)))
+    return NttParams(h.value)
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped host calls
+
+@dataclass
+class Spectrum:
+    """transform.hpp:30-33."""
+
+    values: list = field(default_factory=list)
+    ordering: Ordering = Ordering.bit_reversed
+
+
+_ELEM = {np.dtype(np.uint16): 2, np.dtype(np.int16): 2, np.dtype(np.uint32): 4,
+         np.dtype(np.int32): 4, np.dtype(np.uint64): 8, np.dtype(np.int64): 8}
+
+
+def _as_batch(x, N: int, signed: bool = False) -> np.ndarray:
+    if isinstance(x, np.ndarray) and x.dtype in _ELEM:
+        a = np.ascontiguousarray(x)
+    else:
+        a = np.ascontiguousarray(np.array(list(x) if not isinstance(x, np.ndarray) else x,
+                                          dtype=np.int64 if signed else np.uint64))
+    if a.size % N != 0 or a.size == 0:
+        return None
+    return a.reshape(-1, N)
+
+
+def ntt_forward_batch(f: np.ndarray, P: NttParams, kind) -> np.ndarray:
+    """Batched checked forward on host memory (transform.hpp:207-224 per polynomial)."""
+    a = _as_batch(f, P.size)
+    if a is None:
+        raise ContractViolation("ntt_forward: wrong input length")
+    out = np.empty_like(a)
+    _check(lib().nttk_ntt_forward_host(P.handle, int(kind), a.ctypes.data, out.ctypes.data,
+                                       a.shape[0], a.itemsize))
+    return out
+
+
+def intt_inverse_batch(s: np.ndarray, P: NttParams, kind) -> np.ndarray:
+    """Batched inverse on host memory (transform.hpp:233-343 per polynomial)."""
+    a = _as_batch(s, P.size, signed=ButterflyKind(kind) == ButterflyKind.smont)
+    if a is None:
+        raise ContractViolation("intt_inverse: wrong input length")
+    out = np.empty_like(a)
+    _check(lib().nttk_intt_inverse_host(P.handle, int(kind), a.ctypes.data, out.ctypes.data,
+                                        a.shape[0], a.itemsize))
+    return out
+
+
+def ntt_forward(f: Sequence[int], P: NttParams, kind) -> Spectrum:
+    """transform.hpp:220-224: natural-order canonical input, bit-reversed lazy spectrum."""
+    if not P.has(kind):
+        raise ContractViolation("ntt_forward: kind not built into these params")
+    if len(f) != P.size:
+        raise ContractViolation("ntt_forward: wrong input length")
+    out = ntt_forward_batch(np.asarray(f, dtype=np.uint64), P, kind)
+    vals = out.reshape(-1)
+    if ButterflyKind(kind) == ButterflyKind.smont:
+        vals = vals.view(np.int64)
+    return Spectrum([int(v) for v in vals], Ordering.bit_reversed)
+
+
+def ntt_forward_inplace(a: np.ndarray, P: NttParams, kind) -> None:
+    """transform.hpp:228-231 (benchmark path): no validation beyond the engine's."""
+    out = ntt_forward_batch(a, P, kind)
+    a[...] = out.reshape(a.shape)
+
+
+def intt_inverse(s: Spectrum, P: NttParams, kind) -> list:
+    """transform.hpp:339-343."""
+    if not P.has(kind):
+        raise ContractViolation("intt_inverse: kind not built into these params")
+    if len(s.values) != P.size:
+        raise ContractViolation("intt_inverse: wrong input length")
+    if s.ordering != Ordering.bit_reversed:
+        raise ContractViolation("intt_inverse: spectrum must be in butterfly order")
+    signed = ButterflyKind(kind) == ButterflyKind.smont or any(v < 0 for v in s.values)
+    arr = np.array(s.values, dtype=np.int64 if signed else np.uint64)
+    out = intt_inverse_batch(arr, P, kind)
+    return [int(v) for v in out.reshape(-1)]
+
+
+def pointwise_multiply(lhs: Spectrum, rhs: Spectrum, P: NttParams, kind) -> Spectrum:
+    """transform.hpp:349-370 (canonical output)."""
+    if len(lhs.values) != P.size or len(rhs.values) != P.size:
+        raise ContractViolation("pointwise_multiply: wrong spectrum length")
+    if lhs.ordering != rhs.ordering:
+        raise ContractViolation("pointwise_multiply: mixed orderings")
+    signed = ButterflyKind(kind) == ButterflyKind.smont
+    dt = np.int64 if signed else np.uint64
+    out = pointwise_multiply_batch(np.array(lhs.values, dtype=dt), np.array(rhs.values, dtype=dt),
+                                   P, kind)
+    return Spectrum([int(v) for v in out.reshape(-1)], lhs.ordering)
+
+
+def pointwise_multiply_batch(lhs: np.ndarray, rhs: np.ndarray, P: NttParams, kind) -> np.ndarray:
+    a = _as_batch(lhs, P.size)
+    b = _as_batch(rhs, P.size)
+    if a is None or b is None or a.shape != b.shape or a.dtype != b.dtype:
+        raise ContractViolation("pointwise_multiply: wrong spectrum length")
+    out = np.empty_like(a)
+    _check(lib().nttk_pointwise_multiply_host(P.handle, int(kind), a.ctypes.data, b.ctypes.data,
+                                              out.ctypes.data, a.shape[0], a.itemsize))
+    return out
+
+
+def polymul_batch(x: np.ndarray, y: np.ndarray, P: NttParams, kind) -> np.ndarray:
+    """Batched product via NTT on host memory (cyclic: transform.hpp:372-379)."""
+    a = _as_batch(x, P.size)
+    b = _as_batch(y, P.size)
+    if a is None or b is None or a.shape != b.shape or a.dtype != b.dtype:
+        raise ContractViolation("polymul: size mismatch")
+    out = np.empty_like(a)
+    _check(lib().nttk_polymul_host(P.handle, int(kind), a.ctypes.data, b.ctypes.data,
+                                   out.ctypes.data, a.shape[0], a.itemsize))
+    return out
+
+
+def cyclic_convolution_via_ntt(x: Sequence[int], y: Sequence[int], P: NttParams,
+                               kind=ButterflyKind.improved) -> list:
+    """transform.hpp:372-379."""
+    if len(x) != P.size or len(y) != P.size:
+        raise ContractViolation("ntt_forward: wrong input length")
+    out = polymul_batch(np.asarray(x, dtype=np.uint64), np.asarray(y, dtype=np.uint64), P, kind)
+    return [int(v) for v in out.reshape(-1)]
+
+
+# ---------------------------------------------------------------------------
+# batched device API on torch CUDA tensors
+
+_TORCH_ELEM = None
+
+
+def _torch_elem(t) -> int:
+    global _TORCH_ELEM
+    import torch
+
+    if _TORCH_ELEM is None:
+        _TORCH_ELEM = {torch.int16: 2, torch.uint16: 2, torch.int32: 4, torch.uint32: 4,
+                       torch.int64: 8, torch.uint64: 8}
+    if not t.is_cuda:
+        raise ContractViolation("device API expects CUDA tensors")
+    if not t.is_contiguous():
+        raise ContractViolation("device API expects contiguous tensors")
+    if t.dtype not in _TORCH_ELEM:
+        raise ContractViolation(f"unsupported coefficient dtype {t.dtype}")
+    return _TORCH_ELEM[t.dtype]
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _batch_of(t, N: int) -> int:
+    if t.numel() % N:
+        raise ContractViolation("wrong input length")
+    return t.numel() // N
+
+
+def forward(P: NttParams, kind, x, out=None, stream=None):
+    """Batched ntt_forward on device tensors (natural -> bit-reversed lazy spectrum)."""
+    import torch
+
+    e = _torch_elem(x)
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().nttk_ntt_forward(P.handle, int(kind), x.data_ptr(), out.data_ptr(),
+                                  _batch_of(x, P.size), e, _stream_ptr(stream)))
+    return out
+
+
+def inverse(P: NttParams, kind, x, out=None, stream=None):
+    """Batched intt_inverse on device tensors (canonical natural-order output)."""
+    import torch
+
+    e = _torch_elem(x)
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().nttk_intt_inverse(P.handle, int(kind), x.data_ptr(), out.data_ptr(),
+                                   _batch_of(x, P.size), e, _stream_ptr(stream)))
+    return out
+
+
+def pointwise(P: NttParams, kind, a, b, out=None, stream=None):
+    import torch
+
+    e = _torch_elem(a)
+    out = torch.empty_like(a) if out is None else out
+    _check(lib().nttk_pointwise_multiply(P.handle, int(kind), a.data_ptr(), b.data_ptr(),
+                                         out.data_ptr(), _batch_of(a, P.size), e,
+                                         _stream_ptr(stream)))
+    return out
+
+
+def basemul(P: NttParams, kind, a, b, out=None, stream=None):
+    import torch
+
+    e = _torch_elem(a)
+    out = torch.empty_like(a) if out is None else out
+    _check(lib().nttk_basemul(P.handle, int(kind), a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                              _batch_of(a, P.size), e, _stream_ptr(stream)))
+    return out
+
+
+def polymul(P: NttParams, kind, a, b, out=None, stream=None):
+    import torch
+
+    e = _torch_elem(a)
+    out = torch.empty_like(a) if out is None else out
+    _check(lib().nttk_polymul(P.handle, int(kind), a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                              _batch_of(a, P.size), e, _stream_ptr(stream)))
+    return out
+
+
+def roundtrip_host(P: NttParams, kind, h_in, h_spec, h_out) -> None:
+    """forward + inverse over host memory (numpy or pinned torch CPU tensors)."""
+    def ptr(t):
+        return t.ctypes.data if isinstance(t, np.ndarray) else t.data_ptr()
+
+    def n_elem(t):
+        return t.itemsize if isinstance(t, np.ndarray) else t.element_size()
+
+    n = h_in.size if isinstance(h_in, np.ndarray) else h_in.numel()
+    _check(lib().nttk_roundtrip_host(P.handle, int(kind), ptr(h_in),
+                                     ptr(h_spec) if h_spec is not None else None, ptr(h_out),
+                                     n // P.size, n_elem(h_in)))
+
+
+def modmul_sweep(variant, p: int, n_bits: int, ell: int, A, B, r=None, stream=None) -> int:
+    """Run one reduction over the operand grid (A[i], B[j]) of int64 CUDA tensors.
+
+    Results go to ``r`` (int64, len(A)*len(B), optional); returns the wrapping u64 sum.
+    """
+    s = C.c_uint64()
+    _check(lib().nttk_modmul_sweep(int(variant), p, n_bits, ell, A.data_ptr(), A.numel(),
+                                   B.data_ptr(), B.numel(), r.data_ptr() if r is not None else None,
+                                   C.byref(s), _stream_ptr(stream)))
+    return int(s.value)

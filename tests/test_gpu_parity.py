@@ -1,0 +1,298 @@
+"""GPU parity: the sm_100a engine through its C ABI vs the pinned CPU oracle.
+
+Bit-exact comparisons (integer work) on seeded inputs drawn with the reference's own Rng
+(int_util.hpp:90-138), at sizes the oracle finishes in seconds, plus size-independent
+properties at BASELINE sizes (round trips, agreement with oracle on sampled polys).
+Every test here needs a CUDA device; the engine has no CPU path.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import CYCLIC, HARVEY, IMPROVED, NEGA, NTL, SCOTT, SMONT
+
+import paper_2402_00675_b200.nttk as nttk
+from paper_2402_00675_b200.nttk import ButterflyKind as K
+
+pytestmark = pytest.mark.gpu
+
+DT = {2: np.uint16, 4: np.uint32, 8: np.uint64}
+SDT = {2: np.int16, 4: np.int32, 8: np.int64}
+TDT = {2: torch.int16, 4: torch.int32, 8: torch.int64}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    assert torch.cuda.is_available(), "GPU parity tests need a CUDA device"
+    assert nttk.device_available()
+    torch.cuda.init()
+
+
+def fnv(oracle, a):
+    return "%016x" % oracle.fnv(np.asarray(a).astype(np.int64).astype(np.uint64).ravel())
+
+
+def to_dev(a, elem, signed=False):
+    arr = np.ascontiguousarray(np.asarray(a).astype(SDT[elem] if signed else DT[elem]))
+    return torch.from_numpy(arr.view(SDT[elem])).cuda()
+
+
+def from_dev(t, signed=False):
+    a = t.cpu().numpy()
+    return a.astype(np.int64) if signed else a.view({2: np.uint16, 4: np.uint32, 8: np.uint64}[a.itemsize]).astype(np.uint64)
+
+
+def engine_params(p, N, n, kinds, tree=CYCLIC, layers=0, exact=False):
+    return nttk.build_params(p, N, n, kinds, tree=tree, layers=layers, exact_bound=exact)
+
+
+# ---------------------------------------------------------------------------
+# golden vectors of the reference (tests/golden/golden.json)
+
+def test_golden_forward_inverse_all_cases(oracle, golden):
+    for c in golden["cases"]:
+        p, N, n, kind = c["p"], c["N"], c["n_bits"], c["kind"]
+        f = oracle.rng(c["seed"], p, c["polys"] * N).reshape(c["polys"], N)
+        P = engine_params(p, N, n, [kind], exact=c["exact_bound"])
+        assert P.omega == c["omega"]
+        for elem in (8, 4, 2):
+            try:
+                x = to_dev(f, elem)
+                y = nttk.forward(P, kind, x)
+            except nttk.ContractViolation as e:
+                assert "cannot hold" in str(e) and elem < 8
+                continue
+            fwd = from_dev(y)
+            assert fnv(oracle, fwd) == c["fwd_fnv"], (c["label"], elem)
+            inv = from_dev(nttk.inverse(P, kind, y))
+            assert fnv(oracle, inv) == c["inv_fnv"], (c["label"], elem)
+            assert (inv == f).all()
+        # inverse of arbitrary in-range words (canonicalisation path, transform.hpp:243)
+        g = oracle.rng(c["seed"] + 1, 1 << 15, c["polys"] * N).reshape(c["polys"], N)
+        for elem in (8, 4, 2):
+            got = from_dev(nttk.inverse(P, kind, to_dev(g, elem)))
+            assert fnv(oracle, got) == c["inv_g_fnv"], (c["label"], elem)
+
+
+def test_golden_products(oracle, golden):
+    for c in golden["products"]:
+        p, N, n, kind = c["p"], c["N"], c["n_bits"], c["kind"]
+        a = oracle.rng(c["seed"], p, 4 * N).reshape(4, N)
+        b = oracle.rng(c["seed"] + 1, p, 4 * N).reshape(4, N)
+        P = engine_params(p, N, n, [kind])
+        fa = nttk.forward(P, kind, to_dev(a, 8))
+        fb = nttk.forward(P, kind, to_dev(b, 8))
+        assert fnv(oracle, from_dev(nttk.pointwise(P, kind, fa, fb))) == c["pointwise_fnv"]
+        conv = from_dev(nttk.polymul(P, kind, to_dev(a, 8), to_dev(b, 8)))
+        assert fnv(oracle, conv) == c["conv_fnv"]
+        host = nttk.polymul_batch(a, b, P, kind)
+        assert fnv(oracle, host) == c["conv_fnv"]
+
+
+def test_golden_reductions(golden):
+    for c in golden["reductions"]:
+        A = torch.tensor(c["A"], dtype=torch.int64, device="cuda")
+        B = torch.tensor(c["B"], dtype=torch.int64, device="cuda")
+        r = torch.empty(A.numel() * B.numel(), dtype=torch.int64, device="cuda")
+        s = nttk.modmul_sweep(c["variant"], c["p"], c["n_bits"], c["ell"], A, B, r)
+        assert "%016x" % s == c["checksum"], c
+        assert r[:64].cpu().tolist() == c["r_first"], c
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs vs the oracle, bit-exact
+
+KYBER, DILITHIUM = 3329, 8380417
+
+
+@pytest.mark.parametrize("kind,n", [(IMPROVED, 16), (HARVEY, 16), (SMONT, 16), (IMPROVED, 32),
+                                    (HARVEY, 32), (SMONT, 32)])
+@pytest.mark.parametrize("tree,layers", [(CYCLIC, 8), (NEGA, 7)])
+def test_kyber_transforms_vs_oracle(oracle, kind, n, tree, layers):
+    P = engine_params(KYBER, 256, n, [kind], tree=tree, layers=layers, exact=True)
+    Q = oracle.params(KYBER, 256, n, (kind,), tree=tree, layers=layers, exact=True)
+    assert kind in P.fast_path
+    B = 1027  # odd: exercises the half-warp tail
+    f = oracle.rng(12345 + kind, KYBER, B * 256).reshape(B, 256)
+    want = Q.forward(kind, f)
+    sgn = kind == SMONT
+    for elem in (2, 4, 8):
+        y = nttk.forward(P, kind, to_dev(f, elem))
+        got = from_dev(y, sgn)
+        assert (got.astype(np.int64) == want.astype(np.int64)).all(), elem
+        back = from_dev(nttk.inverse(P, kind, y))
+        assert (back == f).all(), elem
+
+
+@pytest.mark.parametrize("kind", [IMPROVED, HARVEY, SMONT])
+@pytest.mark.parametrize("tree,layers", [(CYCLIC, 8), (NEGA, 8)])
+def test_dilithium_transforms_vs_oracle(oracle, kind, tree, layers):
+    P = engine_params(DILITHIUM, 256, 32, [kind], tree=tree, layers=layers, exact=True)
+    Q = oracle.params(DILITHIUM, 256, 32, (kind,), tree=tree, layers=layers, exact=True)
+    assert kind in P.fast_path
+    B = 515
+    f = oracle.rng(777 + kind, DILITHIUM, B * 256).reshape(B, 256)
+    want = Q.forward(kind, f)
+    sgn = kind == SMONT
+    for elem in (4, 8):
+        y = nttk.forward(P, kind, to_dev(f, elem))
+        assert (from_dev(y, sgn).astype(np.int64) == want.astype(np.int64)).all(), elem
+        assert (from_dev(nttk.inverse(P, kind, y)) == f).all(), elem
+
+
+def test_dilithium_improved_matches_reference_exact_bound(oracle, golden):
+    """config 3: modified Plantard (64-bit constant) vs 32-bit Montgomery round trip."""
+    B = 4096
+    f = oracle.rng(3, DILITHIUM, B * 256).reshape(B, 256)
+    x = to_dev(f, 4)
+    for kind in (IMPROVED, HARVEY):
+        P = engine_params(DILITHIUM, 256, 32, [kind], exact=True)
+        Q = oracle.params(DILITHIUM, 256, 32, (kind,), exact=True)
+        y = nttk.forward(P, kind, x)
+        sample = [0, 1, 2047, 4095]
+        assert (from_dev(y)[sample] == Q.forward(kind, f[sample])).all()
+        assert torch.equal(nttk.inverse(P, kind, y), x)
+
+
+@pytest.mark.parametrize("kind,n,tree,layers", [(IMPROVED, 16, NEGA, 7), (HARVEY, 16, NEGA, 7),
+                                                (SMONT, 16, NEGA, 7), (IMPROVED, 16, CYCLIC, 8),
+                                                (IMPROVED, 32, NEGA, 8), (SMONT, 32, NEGA, 8)])
+def test_polymul_vs_schoolbook(oracle, kind, n, tree, layers):
+    p = KYBER if n == 16 else DILITHIUM
+    P = engine_params(p, 256, n, [kind], tree=tree, layers=layers, exact=True)
+    Q = oracle.params(p, 256, n, (kind,), tree=tree, layers=layers, exact=True)
+    B = 33
+    a = oracle.rng(10 + kind, p, B * 256).reshape(B, 256)
+    b = oracle.rng(20 + kind, p, B * 256).reshape(B, 256)
+    want = Q.polymul(kind, a, b)
+    elem = 2 if p == KYBER else 4
+    got = from_dev(nttk.polymul(P, kind, to_dev(a, elem), to_dev(b, elem)))
+    assert (got == want).all()
+    school = oracle.schoolbook_negacyclic if tree == NEGA else oracle.schoolbook_cyclic
+    for i in (0, B - 1):
+        assert (got[i] == school(a[i], b[i], p)).all()
+    if tree == NEGA and layers == 7:
+        fa = nttk.forward(P, kind, to_dev(a, elem))
+        fb = nttk.forward(P, kind, to_dev(b, elem))
+        bm = from_dev(nttk.basemul(P, kind, fa, fb))
+        assert (bm == Q.basemul(kind, Q.forward(kind, a), Q.forward(kind, b))).all()
+
+
+def test_all_reference_kinds_at_presets_via_host_api(oracle):
+    """Every ButterflyKind at the reference presets (generic kernel for N != 256 and n=32)."""
+    for name, p, N, n in (("kyber256", 7681, 256, 32), ("falcon512", 12289, 512, 32),
+                          ("falcon1024", 12289, 1024, 32), ("toy13", 13, 4, 8)):
+        P = nttk.preset(name)
+        kinds = (NTL, HARVEY, SCOTT, IMPROVED)
+        Q = oracle.params(p, N, n, kinds)
+        f = oracle.rng(99, p, 5 * N).reshape(5, N)
+        for k in kinds:
+            got = nttk.ntt_forward_batch(f, P, k)
+            assert (got == Q.forward(k, f)).all(), (name, k)
+            for k2 in kinds:  # every kind pair inverts every other (transform_test.cpp:61-93)
+                assert (nttk.intt_inverse_batch(got, P, k2) == f).all(), (name, k, k2)
+
+
+def test_reference_shaped_single_poly_calls():
+    """transform_test.cpp hand cases through the Python mirror of the reference API."""
+    P = nttk.build_params(17, 4, 16)
+    for k in nttk.all_butterfly_kinds():
+        s = nttk.ntt_forward([1, 2, 3, 4], P, k)
+        nat = [s.values[i] % 17 for i in (0, 2, 1, 3)]
+        assert nat == [10, 7, 15, 6]
+        assert nttk.intt_inverse(s, P, k) == [1, 2, 3, 4]
+        assert nttk.cyclic_convolution_via_ntt([1, 2, 3, 4], [1, 0, 0, 1], P, k) == [3, 5, 7, 5]
+    T = nttk.preset("toy13")
+    for k in nttk.all_butterfly_kinds():
+        s = nttk.ntt_forward([0, 1, 0, 0], T, k)
+        assert [s.values[i] % 13 for i in (0, 2, 1, 3)] == [1, 5, 12, 8]
+    lhs = nttk.Spectrum([1, 2, 3, 4])
+    rhs = nttk.Spectrum([51, 40, 27, 14])
+    out = nttk.pointwise_multiply(lhs, rhs, T, K.improved)
+    assert out.values == [l * (r % 13) % 13 for l, r in zip(lhs.values, rhs.values)]
+    assert nttk.pointwise_multiply(lhs, rhs, T, K.harvey).values == out.values
+
+
+def test_contracts_match_reference_messages():
+    T = nttk.preset("toy13")
+    with pytest.raises(nttk.ContractViolation, match="wrong input length"):
+        nttk.ntt_forward([1, 2], T, K.ntl)
+    with pytest.raises(nttk.ContractViolation, match="coefficients must be canonical"):
+        nttk.ntt_forward([13, 0, 0, 0], T, K.ntl)
+    with pytest.raises(nttk.ContractViolation, match="butterfly order"):
+        nttk.intt_inverse(nttk.Spectrum([1, 2, 3, 4], nttk.Ordering.natural), T, K.ntl)
+    only = nttk.build_params(13, 4, 8, [K.ntl])
+    with pytest.raises(nttk.ContractViolation, match="kind not built"):
+        nttk.ntt_forward([1, 2, 3, 4], only, K.harvey)
+    with pytest.raises(nttk.ContractViolation, match="mixed orderings"):
+        nttk.pointwise_multiply(nttk.Spectrum([1, 2, 3, 4]),
+                                nttk.Spectrum([1, 2, 3, 4], nttk.Ordering.natural), T, K.ntl)
+    with pytest.raises(nttk.ContractViolation, match=r"T must be < 2\^ell \* p"):
+        nttk.pointwise_multiply(nttk.Spectrum([1, 2, 3, 4]), nttk.Spectrum([52, 0, 0, 0]), T,
+                                K.improved)
+
+
+def test_edge_batches_and_extreme_values(oracle):
+    P = engine_params(KYBER, 256, 16, [IMPROVED], exact=True)
+    Q = oracle.params(KYBER, 256, 16, (IMPROVED,), exact=True)
+    # empty batch is a no-op
+    e = torch.empty(0, dtype=torch.int16, device="cuda")
+    assert nttk.forward(P, IMPROVED, e).numel() == 0
+    for B in (1, 2, 3, 31, 33):
+        f = np.full((B, 256), KYBER - 1, dtype=np.uint64)
+        f[0] = 0
+        got = from_dev(nttk.forward(P, IMPROVED, to_dev(f, 2)))
+        assert (got == Q.forward(IMPROVED, f)).all()
+    # every u16 word through the inverse's canonicalisation
+    w = np.arange(1 << 16, dtype=np.uint64).reshape(256, 256)
+    got = from_dev(nttk.inverse(P, IMPROVED, to_dev(w, 2)))
+    assert (got == Q.inverse(IMPROVED, w)).all()
+
+
+@pytest.mark.slow
+def test_large_batch_properties():
+    """BASELINE config 4 sizes: round trip identity over 2^22 Kyber + 2^21 Dilithium."""
+    g = torch.Generator(device="cuda").manual_seed(4)
+    for p, n, elem, B in ((KYBER, 16, 2, 1 << 22), (DILITHIUM, 32, 4, 1 << 21)):
+        P = engine_params(p, 256, n, [IMPROVED], exact=True)
+        x = torch.randint(0, p, (B, 256), generator=g, device="cuda", dtype=torch.int64).to(TDT[elem])
+        y = nttk.forward(P, IMPROVED, x)
+        assert int(y.to(torch.int64).min()) >= 0 and int(y.to(torch.int64).max()) < 9 * p
+        assert torch.equal(nttk.inverse(P, IMPROVED, y), x)
+        del x, y
+        torch.cuda.empty_cache()
+
+
+def test_sweep_vs_oracle_grid(oracle):
+    for p, n, ell in ((KYBER, 16, 2), (DILITHIUM, 32, 7)):
+        ctx = oracle.ctx(p, n, 0, ell)
+        rng = np.random.default_rng(5)
+        for variant in range(4):
+            na, nb = 96, 2100  # ragged: not a multiple of the 2048-column tile
+            if variant == 1:
+                A = rng.integers(0, p, na)
+                B = rng.integers(-(1 << (n - 1)), 1 << (n - 1), nb)
+            elif variant == 2:
+                A = rng.integers(0, p + 1, na)
+                B = rng.integers(0, p + 1, nb)
+            elif variant == 3:
+                A = rng.integers(0, p, na)
+                B = rng.integers(0, p << ell, nb)
+            else:
+                A = rng.integers(0, p, na)
+                B = rng.integers(0, p, nb)
+            want, s = oracle.sweep(variant, ctx, A, B)
+            dA = torch.tensor(A, dtype=torch.int64, device="cuda")
+            dB = torch.tensor(B, dtype=torch.int64, device="cuda")
+            r = torch.empty(na * nb, dtype=torch.int64, device="cuda")
+            got = nttk.modmul_sweep(variant, p, n, ell, dA, dB, r)
+            assert got == s and (r.cpu().numpy() == want).all(), (p, variant)
+            assert nttk.modmul_sweep(variant, p, n, ell, dA, dB) == s
+
+
+def test_launch_counter_moves():
+    before = nttk.launch_count()
+    P = engine_params(KYBER, 256, 16, [IMPROVED], exact=True)
+    x = torch.zeros(64, 256, dtype=torch.int16, device="cuda")
+    nttk.forward(P, IMPROVED, x)
+    assert nttk.launch_count() == before + 1

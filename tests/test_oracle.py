@@ -1,0 +1,257 @@
+"""Pins the CPU oracle (oracle/nttk_oracle.c) before it is trusted as the checker.
+
+(a) known-answer values from the reference's own GoogleTest suites
+    (proj/tests/reduction_test.cpp, butterfly_test.cpp, params_test.cpp,
+    transform_test.cpp, oracle_test.cpp);
+(b) golden vectors produced by the unmodified reference (tests/golden/golden.json,
+    tests/golden/make_golden.py via oracle/_ref);
+(c) when oracle/_ref is present, live cross-checks against the reference itself.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import (CYCLIC, HARVEY, IMPROVED, NEGA, NTL, SCOTT, SMONT, OracleError,
+                           Reference, reference_available)
+
+
+# ---- (a) reference known answers ------------------------------------------------
+
+def test_ctx_frozen_toy_constants(oracle):  # reduction_test.cpp:11-25
+    c = oracle.ctx(13, 8, 0, 2)
+    assert (c.beta, c.beta_mask, c.r2n_mask, c.mu, c.mu_centered) == (256, 255, 65535, 20165, 20165)
+    assert (c.p_inv_beta * 13) & 255 == 1 and (c.neg_p_inv_beta * 13 + 1) & 255 == 0
+    assert oracle.ctx(17, 5).p_inv_beta == 17
+
+
+def test_ctx_rejects_bad_parameters(oracle):  # reduction_test.cpp:27-35
+    for args in ((12, 8), (1, 8), (13, 1), (13, 33), (17, 4), (13, 8, 8), (13, 8, 0, 8)):
+        with pytest.raises(OracleError):
+            oracle.ctx(*args)
+
+
+def test_bound_predicates(oracle):  # reduction_test.cpp:37-46
+    L = oracle.lib
+    from ctypes import byref
+    assert L.or_ctx_fits_plantard(byref(oracle.ctx(13, 8)))
+    assert not L.or_ctx_fits_plantard(byref(oracle.ctx(13, 4)))
+    assert L.or_ctx_fits_lazy_plantard(byref(oracle.ctx(13, 8, 0, 2)))
+    assert not L.or_ctx_fits_lazy_plantard(byref(oracle.ctx(17, 8, 0, 2)))
+    assert L.or_ctx_fits_signed_montgomery(byref(oracle.ctx(13, 5)))
+    assert not L.or_ctx_fits_signed_montgomery(byref(oracle.ctx(31, 5)))
+
+
+def test_mont_redc_kat_and_exhaustive(oracle):  # reduction_test.cpp:48-68
+    c = oracle.ctx(17, 5)
+    assert oracle.mont_redc(100, c) == 1
+    inv32 = pow(32, -1, 17)
+    for T in range(17 * 17):
+        assert oracle.mont_redc(T, c) == T * inv32 % 17
+    for k in range(17):
+        assert oracle.mont_redc(17 * k, c) == 0
+    with pytest.raises(OracleError):
+        oracle.mont_redc(17 * 17, c)
+
+
+def test_signed_mont_redc_kat_and_range(oracle):  # reduction_test.cpp:70-86
+    c = oracle.ctx(17, 6)
+    assert oracle.signed_mont_redc(100, c) == 9
+    assert oracle.signed_mont_redc(-100, c) == -9
+    limit = 17 << 5
+    inv64 = pow(64, -1, 17)
+    for A in range(-limit + 1, limit):
+        r = oracle.signed_mont_redc(A, c)
+        assert -17 < r < 17 and (r - A * inv64) % 17 == 0
+    for A in (limit, -limit):
+        with pytest.raises(OracleError):
+            oracle.signed_mont_redc(A, c)
+
+
+def test_plantard_redc_kat_and_exhaustive(oracle):  # reduction_test.cpp:88-106
+    c = oracle.ctx(13, 8)
+    assert oracle.plantard_redc(5, 12, c) == 6
+    before = oracle.lib.or_plantard_fires()
+    neg = (-pow(65536, -1, 13)) % 13
+    for W in range(14):
+        for T in range(14):
+            assert oracle.plantard_redc(W, T, c) == W * T * neg % 13
+    assert oracle.lib.or_plantard_fires() == before
+    with pytest.raises(OracleError):
+        oracle.plantard_redc(14, 0, c)
+
+
+def test_modified_plantard_kat_exhaustive_and_exact_quotient(oracle):  # reduction_test.cpp:153-175
+    c = oracle.ctx(13, 8, 0, 2)
+    assert oracle.modified_plantard_mul(5, 20, c) == 10
+    assert oracle.modified_plantard_mul(1, 1, c) == 4
+    neg = (-pow(65536, -1, 13)) % 13
+    for W in range(13):
+        for T in range(13 * 4):
+            r = oracle.modified_plantard_mul(W, T, c)
+            assert r == W * T * neg % 13
+            h = (W * T * c.mu) & c.r2n_mask
+            num = h * 13 - W * T
+            assert num % 65536 == 0 and num // 65536 == r
+    with pytest.raises(OracleError):
+        oracle.modified_plantard_mul(13, 0, c)
+    with pytest.raises(OracleError):
+        oracle.modified_plantard_mul(0, 52, c)
+
+
+def test_domain_conversions(oracle):  # reduction_test.cpp:177-190
+    c = oracle.ctx(13, 8, 0, 2)
+    assert oracle.to_plantard_domain(7, c) == 5
+    for w in range(13):
+        assert oracle.to_montgomery_domain(w, c) == w * 256 % 13
+        assert oracle.to_plantard_domain(w, c) == (13 - w * (65536 % 13) % 13) % 13
+        assert oracle.modified_plantard_mul(oracle.to_plantard_domain(w, c), 1, c) == w
+
+
+def test_butterfly_hand_examples(oracle):  # butterfly_test.cpp:31-197
+    assert oracle.butterfly("ntl", 5, 9, 3, 59, c=oracle.ctx(13, 8)) == (1, 1)
+    assert oracle.butterfly("harvey", 100, 4000, 4583, c=oracle.ctx(7681, 16)) == (4100, 3662)
+    assert oracle.butterfly("scott", 5, 9, 3, 52, c=oracle.ctx(13, 8)) == (14, 3)
+    assert oracle.butterfly("improved_ct", 3, 20, 5, c=oracle.ctx(13, 8, 0, 2)) == (13, 6)
+    assert oracle.butterfly("improved_gs", 5, 9, 13, 5, c=oracle.ctx(13, 8, 0, 2)) == (14, 11)
+
+
+def test_scott_lazy_level(oracle):  # butterfly_test.cpp:96-109
+    from ctypes import byref
+    c = oracle.ctx(13, 8)
+    assert oracle.lib.or_scott_lazy_level(4, byref(c)) == 1
+    assert oracle.lib.or_scott_lazy_level(256, byref(c)) == 64
+
+
+def test_primitive_roots(oracle):  # params_test.cpp:10-28
+    for (p, N), w in {(17, 4): 4, (13, 4): 5, (7681, 256): 198, (12289, 512): 3,
+                      (12289, 1024): 49, (13, 1): 1}.items():
+        assert oracle.lib.or_find_primitive_root(p, N) == w
+
+
+def test_toy13_bundle_and_tables(oracle):  # params_test.cpp:56-69,112-149
+    P = oracle.params(13, 4, 8, (NTL, HARVEY, SCOTT, IMPROVED))
+    assert (P.omega, P.omega_inv, P.n_inv, P.scott_L) == (5, 8, 10, 1)
+    c = oracle.ctx(13, 8, 0, 2)
+    assert P.n_inv_hat == oracle.to_plantard_domain(10, c)
+    assert list(P.table("dif_w")) == [1, 5, 1]
+    assert list(P.table("gs_plain")) == [1, 8, 1]
+    P2 = oracle.params(7681, 256, 32, (NTL, HARVEY, SCOTT, IMPROVED))
+    assert P2.omega == 198 and len(P2.table("ct_plantard")) == 255 and P2.scott_L == 1
+
+
+def test_build_params_fault_messages(oracle):  # params_test.cpp:71-110
+    with pytest.raises(OracleError, match="p must be prime"):
+        oracle.params(15, 4, 8)
+    with pytest.raises(OracleError, match="N must divide p - 1"):
+        oracle.params(13, 8, 8)
+    with pytest.raises(OracleError) as e:
+        oracle.params(15, 6, 40)
+    assert "p must be prime" in str(e.value) and "power of two" in str(e.value) and "[2, 32]" in str(e.value)
+    with pytest.raises(OracleError, match=r"p < 2\^\{n-ell-2\}") as e:
+        oracle.params(7681, 256, 16, (IMPROVED,))
+    assert "7681" in str(e.value)
+
+
+def test_dft_hand_case_all_kinds(oracle):  # transform_test.cpp:39-48, oracle_test.cpp:47-52
+    kinds = (NTL, HARVEY, SCOTT, IMPROVED)
+    P = oracle.params(17, 4, 16, kinds)
+    f = np.array([1, 2, 3, 4], dtype=np.uint64)
+    assert list(oracle.naive_dft(f, 4, 17)) == [10, 7, 15, 6]
+    for k in kinds:
+        s = P.forward(k, f)[0]
+        nat = [int(s[int(oracle.lib.or_bit_reverse(i, 2))]) % 17 for i in range(4)]
+        assert nat == [10, 7, 15, 6]
+        assert list(P.inverse(k, s)[0]) == [1, 2, 3, 4]
+
+
+def test_convolution_hand_case(oracle):  # transform_test.cpp:373-383
+    assert list(oracle.schoolbook_cyclic([1, 2, 3, 4], [1, 0, 0, 1], 17)) == [3, 5, 7, 5]
+    P = oracle.params(17, 4, 16, (NTL, HARVEY, SCOTT, IMPROVED))
+    for k in (NTL, HARVEY, SCOTT, IMPROVED):
+        assert list(P.polymul(k, [1, 2, 3, 4], [1, 0, 0, 1])[0]) == [3, 5, 7, 5]
+
+
+def test_rng_stream(oracle):
+    # xoshiro256** values are what make the golden inputs reproducible
+    a = oracle.rng(12345, 3329, 8)
+    assert all(int(x) < 3329 for x in a)
+    if reference_available():
+        assert (Reference().rng(12345, 3329, 4096) == oracle.rng(12345, 3329, 4096)).all()
+
+
+# ---- (b) golden vectors from the reference ------------------------------------------
+
+def test_golden_transforms(oracle, golden):
+    for c in golden["cases"]:
+        p, N, n, kind = c["p"], c["N"], c["n_bits"], c["kind"]
+        f = oracle.rng(c["seed"], p, c["polys"] * N)
+        P = oracle.params(p, N, n, (kind,), exact=c["exact_bound"])
+        assert P.omega == c["omega"], c["label"]
+        fwd = P.forward(kind, f)
+        assert "%016x" % oracle.fnv(fwd) == c["fwd_fnv"], c["label"]
+        assert [int(v) for v in fwd[0][:16]] == c["fwd_first"], c["label"]
+        inv = P.inverse(kind, fwd)
+        assert "%016x" % oracle.fnv(inv) == c["inv_fnv"], c["label"]
+        g = oracle.rng(c["seed"] + 1, 1 << 15, c["polys"] * N)
+        assert "%016x" % oracle.fnv(P.inverse(kind, g)) == c["inv_g_fnv"], c["label"]
+
+
+def test_golden_products(oracle, golden):
+    for c in golden["products"]:
+        p, N, n, kind = c["p"], c["N"], c["n_bits"], c["kind"]
+        a = oracle.rng(c["seed"], p, 4 * N)
+        b = oracle.rng(c["seed"] + 1, p, 4 * N)
+        P = oracle.params(p, N, n, (kind,))
+        pw = P.pointwise(kind, P.forward(kind, a), P.forward(kind, b))
+        assert "%016x" % oracle.fnv(pw) == c["pointwise_fnv"]
+        assert "%016x" % oracle.fnv(P.polymul(kind, a, b)) == c["conv_fnv"]
+
+
+def test_golden_reductions(oracle, golden):
+    for c in golden["reductions"]:
+        ctx = oracle.ctx(c["p"], c["n_bits"], 0, c["ell"])
+        r, s = oracle.sweep(c["variant"], ctx, np.array(c["A"]), np.array(c["B"]))
+        assert "%016x" % s == c["checksum"]
+        assert [int(x) for x in r[:64]] == c["r_first"]
+    assert golden["plantard_fires"] == 0
+
+
+# ---- extension rows (parity unpinned by any reference test): naive evaluation ------
+
+@pytest.mark.parametrize("p,N,n,L,root", [(3329, 256, 16, 7, 0), (8380417, 256, 32, 8, 0),
+                                          (3329, 256, 32, 7, 0), (17, 8, 16, 2, 0)])
+def test_negacyclic_trees_against_naive(oracle, p, N, n, L, root):
+    kinds = (IMPROVED, HARVEY, SMONT)
+    P = oracle.params(p, N, n, kinds, tree=NEGA, layers=L, root=root, exact=True)
+    for seed in range(3):
+        a = oracle.rng(100 + seed, p, N)
+        b = oracle.rng(200 + seed, p, N)
+        ev = P.naive_eval(a)
+        want = oracle.schoolbook_negacyclic(a, b, p)
+        for k in kinds:
+            fa = P.forward(k, a)
+            assert ((fa.astype(np.int64) % p).astype(np.uint64).ravel() == ev).all()
+            assert (P.inverse(k, fa).ravel() == a).all()
+            assert (P.polymul(k, a, b).ravel() == want).all()
+
+
+def test_dilithium_root_is_the_standard_one(oracle):
+    assert oracle.lib.or_find_primitive_root(8380417, 512) == 1753
+    assert oracle.lib.or_find_primitive_root(3329, 256) == 17
+
+
+# ---- (c) live cross-check with the reference when oracle/_ref is built -------------
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+def test_live_against_reference(oracle):
+    ref = Reference()
+    for p, N, n, kinds in ((7681, 256, 32, (NTL, HARVEY, SCOTT, IMPROVED)),
+                           (12289, 1024, 32, (NTL, HARVEY, SCOTT, IMPROVED)),
+                           (8380417, 256, 32, (NTL, HARVEY, SCOTT)),
+                           (3329, 256, 16, (NTL, HARVEY))):
+        f = oracle.rng(4242, p, 3 * N)
+        P = oracle.params(p, N, n, kinds)
+        R = ref.params(p, N, n, kinds)
+        for k in kinds:
+            a, b = P.forward(k, f), R.forward(k, f)
+            assert (a == b).all()
+            assert (P.inverse(k, a) == R.inverse(k, b)).all()
