@@ -67,30 +67,49 @@ def workload_config(a, world):
 # clocks sampled DURING the timed region (B200_PROFILING.md clocks line)
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons via NVML every 10 ms (nvidia-smi as a fallback)."""
+
+    REASONS = {  # nvmlClocksEventReason* bits
+        "hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+        "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80,
+    }
 
     def __init__(self, device_index: int):
         self.dev = device_index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx), int(rs)))
+                self._stop.wait(0.01)
+            return
+        except Exception:
+            pass
+        fields = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
+                    ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={fields}",
                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+                s = [x.strip() for x in out.stdout.strip().split(",")]
+                self.samples.append((float(s[0]), float(s[1]), int(s[2], 16)))
             except Exception:
                 pass
             self._stop.wait(0.2)
 
     def __enter__(self):
         self._t.start()
+        time.sleep(0.05)
         return self
 
     def __exit__(self, *exc):
@@ -100,17 +119,11 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            for name, v in zip(names, s[3:7]):
-                if v.strip().lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for s in self.samples for name, bit in self.REASONS.items()
+                          if s[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples)}
 
 
 def measured_peaks():
@@ -319,9 +332,15 @@ def run_engine_arm(a, rank, world, local_rank):
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         threads = host_threads()
         smp_k, smp_d = threads * 4096, threads * 2048
-        rate, kind, t = cpu_reference_rate(smp_k, smp_d, threads)
+        tot_t, reps, kind = 0.0, 0, "reference"
+        while tot_t < 2.0 and reps < 50:  # ~2 s wall x all host threads of CPU work
+            _, kind, t = cpu_reference_rate(smp_k, smp_d, threads)
+            tot_t += t
+            reps += 1
+        rate = reps * (smp_k + smp_d) / tot_t
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"{smp_k} Kyber + {smp_d} Dilithium polys fwd+inv ({t:.1f} s wall)"}
+               "sample": (f"{reps} x ({smp_k} Kyber + {smp_d} Dilithium) polys fwd+inv, "
+                          f"{tot_t:.1f} s wall on {threads} threads")}
 
     if rank == 0:
         line = {

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -100,6 +101,16 @@ int check_storage(const HostParams& P, int kind, int elem, const char* who) {
   return NTTK_OK;
 }
 
+// canonical outputs (inverse, products) must fit the storage width
+int check_canonical_storage(const HostParams& P, int elem, const char* who) {
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, std::string(who) + ": elem_bytes must be 2, 4 or 8");
+  if (elem < 8 && uint64_t(P.p) > (uint64_t(1) << (8 * elem)))
+    return fail(NTTK_CONTRACT, std::string(who) + ": elem_bytes=" + std::to_string(elem) +
+                                   " cannot hold canonical coefficients of p=" + std::to_string(P.p));
+  return NTTK_OK;
+}
+
 bool use_fast(const HostParams& P, int kind) {
   return ((P.fast_mask >> kind) & 1u) && nttk_b200::fast256_supports(kind, P.layers, P.n_bits);
 }
@@ -115,7 +126,15 @@ int run_transform(const HostParams& P, int kind, int dir, const void* in, void* 
                   int elem, cudaStream_t st) {
   cudaError_t e;
   if (use_fast(P, kind)) {
-    e = nttk_b200::fast256_launch(P, kind, dir, in, out, batch, elem, st);
+    // NTTK_KERNEL=v1 selects the register-prefetch kernels (A/B comparisons)
+    static const bool v1 = [] {
+      const char* k = std::getenv("NTTK_KERNEL");
+      return k && std::string(k) == "v1";
+    }();
+    if (!v1 && nttk_b200::fast256_tma_supports(elem, in, out))
+      e = nttk_b200::fast256_tma_launch(P, kind, dir, in, out, batch, elem, st);
+    else
+      e = nttk_b200::fast256_launch(P, kind, dir, in, out, batch, elem, st);
     g_launches += batch ? 1 : 0;
   } else {
     std::string err;
@@ -341,8 +360,7 @@ int nttk_intt_inverse(nttk_params_t h, int kind, const void* d_in, void* d_out, 
                       int elem, void* stream) {
   if (!h) return fail(NTTK_CONTRACT, "intt_inverse: null params");
   if (int s = check_kind(h->P, kind, "intt_inverse")) return s;
-  if (elem != 2 && elem != 4 && elem != 8)
-    return fail(NTTK_CONTRACT, "intt_inverse: elem_bytes must be 2, 4 or 8");
+  if (int s = check_canonical_storage(h->P, elem, "intt_inverse")) return s;
   if (int s = need_device("intt_inverse")) return s;
   return run_transform(h->P, kind, 1, d_in, d_out, batch, elem, static_cast<cudaStream_t>(stream));
 }
@@ -351,8 +369,7 @@ int nttk_pointwise_multiply(nttk_params_t h, int kind, const void* d_l, const vo
                             void* d_out, size_t batch, int elem, void* stream) {
   if (!h) return fail(NTTK_CONTRACT, "pointwise_multiply: null params");
   if (int s = check_kind(h->P, kind, "pointwise_multiply")) return s;
-  if (elem != 2 && elem != 4 && elem != 8)
-    return fail(NTTK_CONTRACT, "pointwise_multiply: elem_bytes must be 2, 4 or 8");
+  if (int s = check_canonical_storage(h->P, elem, "pointwise_multiply")) return s;
   if (int s = need_device("pointwise_multiply")) return s;
   cudaError_t e = nttk_b200::generic_pointwise(h->P, kind, d_l, d_r, d_out, batch, elem,
                                                static_cast<cudaStream_t>(stream));
@@ -367,8 +384,7 @@ int nttk_basemul(nttk_params_t h, int kind, const void* d_l, const void* d_r, vo
   if (int s = check_kind(h->P, kind, "basemul")) return s;
   if ((h->P.N >> h->P.layers) != 2)
     return fail(NTTK_CONTRACT, "basemul: tree must end in degree-2 factors");
-  if (elem != 2 && elem != 4 && elem != 8)
-    return fail(NTTK_CONTRACT, "basemul: elem_bytes must be 2, 4 or 8");
+  if (int s = check_canonical_storage(h->P, elem, "basemul")) return s;
   if (int s = need_device("basemul")) return s;
   return run_product(h->P, kind, d_l, d_r, d_out, batch, elem, static_cast<cudaStream_t>(stream));
 }
@@ -415,8 +431,7 @@ int nttk_intt_inverse_host(nttk_params_t h, int kind, const void* h_in, void* h_
   if (!h) return fail(NTTK_CONTRACT, "intt_inverse: null params");
   const HostParams& P = h->P;
   if (int s = check_kind(P, kind, "intt_inverse")) return s;
-  if (elem != 2 && elem != 4 && elem != 8)
-    return fail(NTTK_CONTRACT, "intt_inverse: elem_bytes must be 2, 4 or 8");
+  if (int s = check_canonical_storage(P, elem, "intt_inverse")) return s;
   return host_pipeline(
       P, elem, batch, {h_in}, {{h_out, 1}},
       [&](cudaStream_t st, void** b, size_t n) { return run_transform(P, kind, 1, b[0], b[1], n, elem, st); },
@@ -446,8 +461,7 @@ int nttk_pointwise_multiply_host(nttk_params_t h, int kind, const void* h_l, con
   if (!h) return fail(NTTK_CONTRACT, "pointwise_multiply: null params");
   const HostParams& P = h->P;
   if (int s = check_kind(P, kind, "pointwise_multiply")) return s;
-  if (elem != 2 && elem != 4 && elem != 8)
-    return fail(NTTK_CONTRACT, "pointwise_multiply: elem_bytes must be 2, 4 or 8");
+  if (int s = check_canonical_storage(P, elem, "pointwise_multiply")) return s;
   // the improved product consumes a lazy right operand below 2^ell p
   // (modified_plantard_mul's contract, reduction.hpp:264-273)
   const bool chk = kind == NTTK_IMPROVED;

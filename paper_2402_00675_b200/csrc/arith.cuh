@@ -7,12 +7,22 @@
 //
 //   ImprovedN16 / ImprovedN32   Alg. 10-12 modified Plantard (reduction.hpp:252-258,
 //                               butterfly.hpp:224-243) with n = 16 / n = 32
-//   HarveyN16  / HarveyN32      Alg. 8 Montgomery lazy [0, 2p) (butterfly.hpp:92-106)
-//   SmontN16   / SmontN32       signed Montgomery (reduction.hpp:141-165) in CT/GS form
+//   Harvey<16|32, CT>           Alg. 8 Montgomery lazy [0, 2p) (butterfly.hpp:92-106);
+//                               CT = the CT-form twin used on the negacyclic tree
+//   Smont<16|32>                signed Montgomery (reduction.hpp:141-165) in CT/GS form
 //                               (extension)
 //
-// SASS per Plantard multiply (committed census: profiles/sass_census.txt):
-//   n=16: IMAD (h = t * w_hat mu) + IMAD.HI (r = hi32(h p))
+// Issue-slot economy (measured on B200, profiles/r01_imad_microbench.txt): IMAD runs at
+// 64 lanes/clk/SM on the fmaheavy pipe, IMAD.HI and IMAD.WIDE at half that, the ALU
+// pipe (IADD3, LOP3, SHF) at 64.  A butterfly is therefore fmaheavy-bound, so:
+//   * plain additions are written x + y + A.zero (A.zero == 0 at run time, opaque to
+//     ptxas): a three-input add only exists as IADD3 on the ALU pipe, which stops
+//     ptxas from moving the adds onto the saturated fmaheavy pipe as IMAD.IADD;
+//   * the n = 16 Plantard tail has two exact forms (below) with different pipe mixes.
+//
+// SASS per Plantard multiply (committed census: profiles/r01_sass_census.txt):
+//   n=16: IMAD (h = t * w_hat mu) + IMAD.HI (r = hi32(h p))        [umulhi form]
+//         IMAD + SHF + IMAD + SHF (r = (((h >> 16) + 1) p) >> 16)  [paper form]
 //   n=32: IMAD + IMAD.HI (h_hi + 1) + IMAD.HI (r = hi32((h_hi + 1) p))
 #pragma once
 
@@ -40,6 +50,16 @@ __device__ __forceinline__ uint32_t mod_u32(uint32_t x, const FastArgs& A) {
 __device__ __forceinline__ uint32_t mod_u16(uint32_t x, const FastArgs& A) {
   return x - __umulhi(x, A.canon_m16) * A.p;
 }
+// x mod p for x < 2^17 with the host-validated Barrett pair (A.flags bit 0):
+// IMAD + SHF + IMAD, no IMAD.HI
+__device__ __forceinline__ uint32_t mod_cb(uint32_t x, const FastArgs& A) {
+  return x - ((x * A.cb_m) >> A.cb_s) * A.p;
+}
+// x mod p for any 32-bit x via the host-validated shift reduction (A.flags bit 1)
+__device__ __forceinline__ uint32_t mod_cs(uint32_t x, const FastArgs& A) {
+  const uint32_t r = x - (x >> A.cs_s) * A.p;
+  return umin32(r, r - A.p);
+}
 // canonical residue of a two's complement 32-bit value
 __device__ __forceinline__ uint32_t mod_s32(uint32_t x, const FastArgs& A) {
   // x + 2^31 is non-negative; subtract 2^31 mod p afterwards
@@ -52,10 +72,10 @@ __device__ __forceinline__ uint32_t mod_s32(uint32_t x, const FastArgs& A) {
 // ---------------------------------------------------------------------------
 // Modified Plantard multiply (Alg. 10), twiddle premultiplied by mu.
 //   reference:  h = ((w t) mu) mod 2^{2n};  r = (((h >> n) + 1) p) >> n
-// n = 16: the paper form costs IMAD, SHF, IMAD, SHF.  On a 32-bit datapath the full
-// 2n-bit product h p is one IMAD.HI away, and Prop. 4's exact-quotient identity
-// r = (h p - w t) / 2^{2n} (asserted by reduction_test.cpp:166-170)
-// with 0 <= w t < 2^{2n} gives r = floor(h p / 2^{2n}) = hi32(h p) exactly.
+// n = 16, umulhi form: on a 32-bit datapath the full 2n-bit product h p is one
+// IMAD.HI away, and Prop. 4's exact-quotient identity r = (h p - w t) / 2^{2n}
+// (asserted by reduction_test.cpp:166-170) with 0 <= w t < 2^{2n}
+// gives r = floor(h p / 2^{2n}) = hi32(h p) exactly.
 template <bool PAPER_FORM>
 __device__ __forceinline__ uint32_t mp_n16(uint32_t t, uint32_t wm, uint32_t p) {
   const uint32_t h = t * wm;
@@ -72,47 +92,72 @@ __device__ __forceinline__ uint32_t mp_n32(uint32_t t, uint32_t lo, uint32_t hi,
 
 // ---------------------------------------------------------------------------
 // Policies.  Values live in 32-bit registers (signed kinds: two's complement).
-// fwd(x, y, w): forward butterfly (CT form unless noted); inv(x, y, w, off): GS form.
+//   fwd(x, y, w)        forward butterfly (CT form unless noted)
+//   fwd_alt(x, y, w)    same result, alternative pipe mix (n = 16 Plantard only)
+//   inv(x, y, w, off)   GS form, off = 2^{layer-1} p
+//   scale(v)            final N^{-1} pass (transform.hpp:323-335), canonical
+//   inv_last(x, y, off) last merge layer with the N^{-1} pass folded in (kFold)
 
 template <bool PAPER_FORM = false>
 struct ImprovedN16 {
   using Tw = uint32_t;
   static constexpr bool kSigned = false;
+  static constexpr bool kFold = true;
   __device__ static Tw tw(const FastArgs& A, int k) { return A.lo[k]; }
   // Alg. 11 (butterfly.hpp:224-230)
   __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
     const uint32_t r = mp_n16<PAPER_FORM>(y, w, A.p);
     y = x + A.p - r;
-    x = x + r;
+    x = x + r + A.zero;
   }
-  // Alg. 12 (butterfly.hpp:235-243), off = 2^{layer-1} p
+  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    const uint32_t r = mp_n16<!PAPER_FORM>(y, w, A.p);
+    y = x + A.p - r;
+    x = x + r + A.zero;
+  }
+  // Alg. 12 (butterfly.hpp:235-243)
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
-    x = x + y;
+    x = x + y + A.zero;
     y = mp_n16<PAPER_FORM>(t, w, A.p);
   }
-  // final N^{-1} pass (transform.hpp:323-330)
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return mp_n16<PAPER_FORM>(v, A.scale_lo, A.p);
+  }
+  // (X, Y) -> (MP(n^, X + Y), MP((w n^{-1})^, X + off - Y)): both canonical, so the
+  // result equals scale() applied after the last merge (canonical outputs are unique)
+  __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    x = mp_n16<true>(x + y + A.zero, A.scale_lo, A.p);
+    y = mp_n16<PAPER_FORM>(t, A.fold_lo, A.p);
   }
 };
 
 struct ImprovedN32 {
   using Tw = uint2;
   static constexpr bool kSigned = false;
+  static constexpr bool kFold = true;
   __device__ static Tw tw(const FastArgs& A, int k) { return make_uint2(A.lo[k], A.hi[k]); }
   __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
     const uint32_t r = mp_n32(y, w.x, w.y, A.p);
     y = x + A.p - r;
-    x = x + r;
+    x = x + r + A.zero;
+  }
+  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    fwd(x, y, w, A);
   }
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
-    x = x + y;
+    x = x + y + A.zero;
     y = mp_n32(t, w.x, w.y, A.p);
   }
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return mp_n32(v, A.scale_lo, A.scale_hi, A.p);
+  }
+  __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    x = mp_n32(x + y + A.zero, A.scale_lo, A.scale_hi, A.p);
+    y = mp_n32(t, A.fold_lo, A.fold_hi, A.p);
   }
 };
 
@@ -135,21 +180,25 @@ template <int N_BITS, bool CT_FORWARD>
 struct Harvey {
   using Tw = uint32_t;
   static constexpr bool kSigned = false;
+  static constexpr bool kFold = true;
   __device__ static Tw tw(const FastArgs& A, int k) { return A.lo[k]; }
   __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
     if (CT_FORWARD) {
       // CT-form harvey (extension for the negacyclic tree): all values in [0, 2p)
       const uint32_t r = harvey_mul<N_BITS>(y, w, A);
-      const uint32_t a = x + r, b = x + A.two_p - r;
+      const uint32_t a = x + r + A.zero, b = x + A.two_p - r;
       x = umin32(a, a - A.two_p);
       y = umin32(b, b - A.two_p);
     } else {
       dif(x, y, w, A);
     }
   }
+  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    fwd(x, y, w, A);
+  }
   // harvey_core (butterfly.hpp:92-106): X' = X + Y mod 2p (branchless), Y' lazy
   __device__ static void dif(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
-    const uint32_t s = x + y;
+    const uint32_t s = x + y + A.zero;
     const uint32_t t = x + A.two_p - y;
     x = umin32(s, s - A.two_p);
     y = harvey_mul<N_BITS>(t, w, A);
@@ -162,6 +211,13 @@ struct Harvey {
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     const uint32_t r = harvey_mul<N_BITS>(v, A.scale_lo, A);  // (0, 2p)
     return umin32(r, r - A.p);
+  }
+  __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t, const FastArgs& A) {
+    const uint32_t t = x + A.two_p - y;
+    const uint32_t a = harvey_mul<N_BITS>(x + y + A.zero, A.scale_lo, A);  // X + Y < 4p
+    const uint32_t b = harvey_mul<N_BITS>(t, A.fold_lo, A);
+    x = umin32(a, a - A.p);
+    y = umin32(b, b - A.p);
   }
 };
 
@@ -198,11 +254,15 @@ template <int N_BITS>
 struct Smont {
   using Tw = uint2;  // (w, w p^{-1} mod 2^n [n=16: << 16])
   static constexpr bool kSigned = true;
+  static constexpr bool kFold = false;
   __device__ static Tw tw(const FastArgs& A, int k) { return make_uint2(A.lo[k], A.hi[k]); }
   __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
     const int32_t t = smont_mul<N_BITS>(static_cast<int32_t>(y), static_cast<int32_t>(w.x), w.y, A);
     y = static_cast<uint32_t>(static_cast<int32_t>(x) - t);
-    x = static_cast<uint32_t>(static_cast<int32_t>(x) + t);
+    x = static_cast<uint32_t>(static_cast<int32_t>(x) + t) + A.zero;
+  }
+  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    fwd(x, y, w, A);
   }
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
     const int32_t xs = static_cast<int32_t>(x), ys = static_cast<int32_t>(y);
@@ -213,6 +273,11 @@ struct Smont {
     const int32_t r = smont_mul<N_BITS>(static_cast<int32_t>(v), static_cast<int32_t>(A.scale_lo),
                                         A.scale_hi, A);
     return static_cast<uint32_t>(r + (r < 0 ? static_cast<int32_t>(A.p) : 0));
+  }
+  __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
+    (void)off;
+    (void)x;
+    (void)y;
   }
 };
 

@@ -14,3 +14,12 @@ cudaError_t fast256_launch(const HostParams& P, int kind, int dir, const void* i
                            size_t batch, int elem_bytes, cudaStream_t st, int variant = 0);
 
 }  // namespace nttk_b200
+
+namespace nttk_b200 {
+
+// v2: TMA bulk-copy fed kernels (fast256_tma.cu), u16/u32 storage, 16-byte aligned buffers
+bool fast256_tma_supports(int elem_bytes, const void* in, const void* out);
+cudaError_t fast256_tma_launch(const HostParams& P, int kind, int dir, const void* in, void* out,
+                               size_t batch, int elem_bytes, cudaStream_t st);
+
+}  // namespace nttk_b200

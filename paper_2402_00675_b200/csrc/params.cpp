@@ -135,6 +135,49 @@ void fill_fast(HostParams& P, int kind) {
       A.sgn_off = static_cast<uint32_t>((half + P.p - 1) / P.p * P.p);
     }
     A.barrett_v = static_cast<uint32_t>(((u128(1) << (P.n_bits + 10)) + (P.p >> 1)) / P.p);
+    const uint64_t p = P.p;
+    // exact Barrett floor(x M / 2^S) = floor(x / p) for every x < 2^17:
+    // (2^17 - 1)(M p - 2^S) < 2^S, with the 32-bit product x M not wrapping
+    for (uint32_t S = 16; S < 32; ++S) {
+      const uint64_t M = ((uint64_t(1) << S) + p - 1) / p, xmax = (uint64_t(1) << 17) - 1;
+      if (xmax * M < (uint64_t(1) << 32) && xmax * (M * p - (uint64_t(1) << S)) < (uint64_t(1) << S)) {
+        A.cb_m = static_cast<uint32_t>(M);
+        A.cb_s = S;
+        A.flags |= 1;
+        break;
+      }
+    }
+    // shift reduction of a 32-bit x: r = x - (x >> s) p < 2^{32-s} (2^s - p) + 2^s, one
+    // conditional subtraction is enough when that bound is <= 2p
+    {
+      uint32_t s = 0;
+      while ((uint64_t(1) << s) < p) ++s;
+      if ((uint64_t(1) << (32 - s)) * ((uint64_t(1) << s) - p) + (uint64_t(1) << s) <= 2 * p) {
+        A.cs_s = s;
+        A.flags |= 2;
+      }
+    }
+    // fused first merge layer for u16 input (improved, n = 16): Y' = MP(w, X + K p - Y)
+    // with every T = X + K p - Y inside Prop. 4's exact range, X' = (X + Y) mod p
+    if (kind == NTTK_IMPROVED && n16 && (A.flags & 1)) {
+      const uint64_t K = ((uint64_t(1) << 16) - 1 + p - 1) / p, kp = K * p;
+      const uint64_t tmax = (uint64_t(1) << 16) - 1 + kp;
+      if (u128(p - 1) * tmax < u128(c.beta) * (c.beta - p)) {
+        A.kp = static_cast<uint32_t>(kp);
+        A.flags |= 4;
+      }
+    }
+    // last merge twiddle times N^{-1} (the final scaling folded into the last layer)
+    {
+      const uint64_t wl = static_cast<uint64_t>(u128(P.gs_plain.back()) * P.n_inv % p);
+      if (kind == NTTK_IMPROVED) {
+        const uint64_t fm = to_plantard(wl, c) * c.mu & c.r2n_mask;
+        A.fold_lo = static_cast<uint32_t>(fm);
+        A.fold_hi = static_cast<uint32_t>(fm >> 32);
+      } else if (kind == NTTK_HARVEY) {
+        A.fold_lo = static_cast<uint32_t>(to_mont(wl, c));
+      }
+    }
     const std::vector<uint64_t>* tab = nullptr;
     switch (kind) {
       case NTTK_IMPROVED: {

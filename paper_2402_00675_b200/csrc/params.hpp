@@ -54,6 +54,13 @@ struct FastArgs {
   uint32_t scale_lo = 0, scale_hi = 0;  // inverse final multiplier (per kind encoding)
   uint32_t barrett_v = 0;  // smont signed Barrett constant V (S = n + 10)
   uint32_t layers = 0;
+  // --- issue-slot economy (all host-validated, see params.cpp fill_fast) ---
+  uint32_t zero = 0;       // always 0: x + y + zero forces a 3-input IADD3 (ALU pipe)
+  uint32_t cb_m = 0, cb_s = 0;  // x mod p = x - ((x cb_m) >> cb_s) p, exact for x < 2^17
+  uint32_t cs_s = 0;       // x mod p = min(r, r - p), r = x - (x >> cs_s) p, exact for x < 2^32
+  uint32_t kp = 0;         // K p >= 2^16 - 1: fused first inverse layer offset (u16 input)
+  uint32_t flags = 0;      // bit0: cb valid; bit1: cs valid; bit2: fused first layer valid
+  uint32_t fold_lo = 0, fold_hi = 0;  // last merge twiddle times N^{-1}, kind encoding
   uint32_t lo[256] = {};   // twiddle words in reference table order
   uint32_t hi[256] = {};   // high words of 64-bit premultiplied Plantard twiddles
 };
