@@ -51,15 +51,19 @@ __device__ __forceinline__ uint32_t mod_u16(uint32_t x, const FastArgs& A) {
   return x - __umulhi(x, A.canon_m16) * A.p;
 }
 // x mod p for x < 2^17 with the host-validated Barrett pair (A.flags bit 0):
-// IMAD + SHF + IMAD, no IMAD.HI
+// IMAD + SHF + IMAD (x + q (-p): no negation op), no IMAD.HI
 __device__ __forceinline__ uint32_t mod_cb(uint32_t x, const FastArgs& A) {
-  return x - ((x * A.cb_m) >> A.cb_s) * A.p;
+  return x + ((x * A.cb_m) >> A.cb_s) * A.negp;
 }
 // x mod p for any 32-bit x via the host-validated shift reduction (A.flags bit 1)
 __device__ __forceinline__ uint32_t mod_cs(uint32_t x, const FastArgs& A) {
-  const uint32_t r = x - (x >> A.cs_s) * A.p;
+  const uint32_t r = x + (x >> A.cs_s) * A.negp;
   return umin32(r, r - A.p);
 }
+// Opaque identity (A.zero == 0): keeps ptxas from folding the following additions into
+// the preceding IMAD.HI as an addend -- it then re-issues a second IMAD.HI for the other
+// use of the same product, doubling the most expensive instruction.  One ALU op instead.
+__device__ __forceinline__ uint32_t fence_val(uint32_t r, const FastArgs& A) { return r ^ A.zero; }
 // canonical residue of a two's complement 32-bit value
 __device__ __forceinline__ uint32_t mod_s32(uint32_t x, const FastArgs& A) {
   // x + 2^31 is non-negative; subtract 2^31 mod p afterwards
@@ -82,12 +86,13 @@ __device__ __forceinline__ uint32_t mp_n16(uint32_t t, uint32_t wm, uint32_t p) 
   if (PAPER_FORM) return (((h >> 16) + 1u) * p) >> 16;
   return __umulhi(h, p);
 }
-// n = 32: only h_hi = hi32(h) is needed: h_hi + 1 = hi32(lo t) + hi t + 1 (mod 2^32)
-// and r = hi32((h_hi + 1) p) -- three IMADs, no shifts.
+// n = 32: only h_hi = hi32(h) is needed: h_hi = hi32(lo t) + hi t (mod 2^32), and
+// r = hi32((h_hi + 1) p) = hi32(h_hi p + p): IMAD.HI + IMAD + IMAD.WIDE whose 64-bit
+// addend {p, 0} is loop-invariant (a mad.hi with a register addend would need a zeroed
+// register pair rebuilt with IMAD.MOV per butterfly).
 __device__ __forceinline__ uint32_t mp_n32(uint32_t t, uint32_t lo, uint32_t hi, uint32_t p) {
-  const uint32_t a = hi * t + 1u;
-  const uint32_t h1 = mad_hi(lo, t, a);
-  return __umulhi(h1, p);
+  const uint32_t hh = hi * t + __umulhi(lo, t);
+  return static_cast<uint32_t>((static_cast<uint64_t>(hh) * p + p) >> 32);
 }
 
 // ---------------------------------------------------------------------------
@@ -119,7 +124,12 @@ struct ImprovedN16 {
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
     x = x + y + A.zero;
-    y = mp_n16<PAPER_FORM>(t, w, A.p);
+    y = fence_val(mp_n16<PAPER_FORM>(t, w, A.p), A);
+  }
+  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    x = x + y + A.zero;
+    y = mp_n16<!PAPER_FORM>(t, w, A.p);
   }
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return mp_n16<PAPER_FORM>(v, A.scale_lo, A.p);
@@ -149,7 +159,10 @@ struct ImprovedN32 {
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
     x = x + y + A.zero;
-    y = mp_n32(t, w.x, w.y, A.p);
+    y = fence_val(mp_n32(t, w.x, w.y, A.p), A);
+  }
+  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    inv(x, y, w, off, A);
   }
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return mp_n32(v, A.scale_lo, A.scale_hi, A.p);
@@ -205,6 +218,9 @@ struct Harvey {
   }
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
     dif(x, y, w, A);
+  }
+  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    inv(x, y, w, off, A);
   }
   // v in [0, 2p) -> v n^{-1} mod p, canonical (the reference's mul_mod,
   // transform.hpp:331-335; any exact method is bit-identical)
@@ -268,6 +284,9 @@ struct Smont {
     const int32_t xs = static_cast<int32_t>(x), ys = static_cast<int32_t>(y);
     x = static_cast<uint32_t>(sbarrett<N_BITS>(xs + ys, A));
     y = static_cast<uint32_t>(smont_mul<N_BITS>(xs - ys, static_cast<int32_t>(w.x), w.y, A));
+  }
+  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    inv(x, y, w, off, A);
   }
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     const int32_t r = smont_mul<N_BITS>(static_cast<int32_t>(v), static_cast<int32_t>(A.scale_lo),

@@ -99,6 +99,42 @@ __device__ __forceinline__ int swz(int i) {
   return (i & ~15) | ((((i >> 2) & 3) ^ ((i >> 5) & 3)) << 2) | (i & 3);
 }
 
+// Per-lane shared-window addresses into a half-warp's 272-word transpose tile, hoisted
+// out of the loop (32-bit registers + immediate offsets: no address IMADs per access).
+// Element i = j + 16 r (strided ownership, lane j) lives at word swz(i) = 16 r + (j ^ 4m),
+// m = (r >> 1) & 3; chunk c of row j (contiguous ownership) at 16 j + 4 (c ^ ((j>>1)&3)).
+struct Xpose {
+  uint32_t sp[4], cp[4];
+  __device__ __forceinline__ void init(const uint32_t* tile, int j) {
+    const uint32_t b = smem_addr(tile);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) sp[m] = b + 4u * uint32_t(j ^ (4 * m));
+    const int g = (j >> 1) & 3;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cp[c] = b + 64u * j + 16u * uint32_t(c ^ g);
+  }
+  __device__ __forceinline__ void put(int r, uint32_t v) const {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(sp[(r >> 1) & 3] + 64u * r), "r"(v) : "memory");
+  }
+  __device__ __forceinline__ uint32_t get(int r) const {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sp[(r >> 1) & 3] + 64u * r) : "memory");
+    return v;
+  }
+  __device__ __forceinline__ void put4(int c, uint32_t a, uint32_t b, uint32_t d, uint32_t e) const {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(cp[c]), "r"(a), "r"(b), "r"(d),
+                 "r"(e)
+                 : "memory");
+  }
+  __device__ __forceinline__ void get4(int c, uint32_t& a, uint32_t& b, uint32_t& d,
+                                       uint32_t& e) const {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(d), "=r"(e)
+                 : "r"(cp[c])
+                 : "memory");
+  }
+};
+
 template <class T>
 __device__ __forceinline__ T pin(T x) {  // opaque copy: value lives in registers
   if constexpr (sizeof(T) == 4) {
@@ -130,6 +166,16 @@ __device__ __forceinline__ uint32_t canon(uint32_t x, const FastArgs& A) {
 #ifndef NTTK_ALT_MASK
 #define NTTK_ALT_MASK 0x22  // forward layers (bit s) using the alternative Plantard form
 #endif
+#ifndef NTTK_INV_ALT_MASK
+#define NTTK_INV_ALT_MASK 0x0  // inverse merge layers (bit s) using the alternative form
+#endif
+
+template <class K, class Tw>
+__device__ __forceinline__ void inv_bf(int sl, uint32_t& x, uint32_t& y, Tw w, uint32_t off,
+                                       const FastArgs& A) {
+  if ((NTTK_INV_ALT_MASK >> sl) & 1) K::inv_alt(x, y, w, off, A);
+  else K::inv(x, y, w, off, A);
+}
 
 // producer: stream tiles of kTile polynomials into the stage ring
 template <class IO>
@@ -179,7 +225,8 @@ __global__ void __launch_bounds__(kThreads)
     return;
   }
   const int j = lane & 15, half = lane >> 4;
-  uint32_t* S = scratch + warp * kScratchWords + half * 272;
+  Xpose X;
+  X.init(scratch + warp * kScratchWords + half * 272, j);
 
   Tw twl[15];
   if (PER_INDEX) {
@@ -235,16 +282,10 @@ __global__ void __launch_bounds__(kThreads)
     }
     // transpose: strided -> contiguous ownership
 #pragma unroll
-    for (int r = 0; r < 16; ++r) S[swz(j + 16 * r)] = v[r];
+    for (int r = 0; r < 16; ++r) X.put(r, v[r]);
     __syncwarp();
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint4 w = *reinterpret_cast<const uint4*>(S + swz(16 * j + 4 * c));
-      v[4 * c + 0] = w.x;
-      v[4 * c + 1] = w.y;
-      v[4 * c + 2] = w.z;
-      v[4 * c + 3] = w.w;
-    }
+    for (int c = 0; c < 4; ++c) X.get4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     // phase 2: layers 5..L (index bits 3..0 in registers)
 #pragma unroll
     for (int sl = 5; sl <= 8; ++sl) {
@@ -320,6 +361,8 @@ __global__ void __launch_bounds__(kThreads)
   }
   const int j = lane & 15, half = lane >> 4;
   uint32_t* S = scratch + warp * kScratchWords + half * 272;
+  Xpose X;
+  X.init(S, j);
 
   Tw twl[15];
   twl[0] = pin(K::tw(A, TL - 32 + j));
@@ -372,7 +415,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int sl = 8; sl >= 5; --sl) {
       if (sl > L) continue;
       const int h = 1 << (8 - sl);
-      const uint32_t off = A.p << (L - sl);
+      const uint32_t off = A.off[L - sl + 1];
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         if (r & h) continue;
@@ -382,35 +425,33 @@ __global__ void __launch_bounds__(kThreads)
           if (sl == L) {
             const uint32_t x = v[r], y = v[r + h];
             v[r] = mod_cb(x + y + A.zero, A);
-            v[r + h] = mp_n16<false>(x + A.kp - y, w, A.p);
+            v[r + h] = fence_val(mp_n16<false>(x + A.kp - y, w, A.p), A);
           } else {
-            K::inv(v[r], v[r + h], w, off, A);
+            inv_bf<K>(sl, v[r], v[r + h], w, off, A);
           }
         } else {
-          K::inv(v[r], v[r + h], w, off, A);
+          inv_bf<K>(sl, v[r], v[r + h], w, off, A);
         }
       }
     }
     // transpose: contiguous -> strided ownership
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      *reinterpret_cast<uint4*>(S + swz(16 * j + 4 * c)) =
-          make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    for (int c = 0; c < 4; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     __syncwarp();
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = S[swz(j + 16 * r)];
+    for (int r = 0; r < 16; ++r) v[r] = X.get(r);
     // phase 2: merge layers s = 4..1, uniform twiddles
 #pragma unroll
     for (int sl = 4; sl >= 1; --sl) {
       const int h = 1 << (4 - sl);
-      const uint32_t off = A.p << (L - sl);
+      const uint32_t off = A.off[L - sl + 1];
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         if (r & h) continue;
         if (K::kFold && sl == 1)  // N^{-1} folded into the last merge layer
           K::inv_last(v[r], v[r + h], off, A);
         else
-          K::inv(v[r], v[r + h], K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl))), off, A);
+          inv_bf<K>(sl, v[r], v[r + h], K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl))), off, A);
       }
     }
     if (!K::kFold) {
@@ -420,7 +461,7 @@ __global__ void __launch_bounds__(kThreads)
     // strided -> contiguous through the scratch for coalesced 128-bit stores
     __syncwarp();
 #pragma unroll
-    for (int r = 0; r < 16; ++r) S[swz(j + 16 * r)] = v[r];
+    for (int r = 0; r < 16; ++r) X.put(r, v[r]);
     __syncwarp();
     if (poly < batch) {
       constexpr int PV = 16 / int(sizeof(IO));  // coefficients per 16-byte vector

@@ -126,6 +126,8 @@ void fill_fast(HostParams& P, int kind) {
     FastArgs& A = P.fast[kind][dir];
     A.p = P.p;
     A.two_p = 2 * P.p;
+    A.negp = static_cast<uint32_t>(0u - P.p);
+    for (unsigned m = 1; m < 10; ++m) A.off[m] = static_cast<uint32_t>(uint64_t(P.p) << (m - 1));
     A.layers = P.layers;
     A.canon_m = static_cast<uint32_t>(0xffffffffull / P.p);
     A.canon_m16 = static_cast<uint32_t>(((uint64_t(1) << 32) + P.p - 1) / P.p);

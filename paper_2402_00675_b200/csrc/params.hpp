@@ -56,6 +56,8 @@ struct FastArgs {
   uint32_t layers = 0;
   // --- issue-slot economy (all host-validated, see params.cpp fill_fast) ---
   uint32_t zero = 0;       // always 0: x + y + zero forces a 3-input IADD3 (ALU pipe)
+  uint32_t negp = 0;       // -p mod 2^32 (x - q p as one IMAD)
+  uint32_t off[10] = {};   // off[m] = 2^{m-1} p: GS offset of merge depth m (constant operand)
   uint32_t cb_m = 0, cb_s = 0;  // x mod p = x - ((x cb_m) >> cb_s) p, exact for x < 2^17
   uint32_t cs_s = 0;       // x mod p = min(r, r - p), r = x - (x >> cs_s) p, exact for x < 2^32
   uint32_t kp = 0;         // K p >= 2^16 - 1: fused first inverse layer offset (u16 input)

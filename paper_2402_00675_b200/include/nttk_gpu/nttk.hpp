@@ -1,0 +1,236 @@
+// nttk_gpu/nttk.hpp -- header-only C++ drop-in for the reference's nttk hot path.
+//
+// Same namespace, names, signatures and error behaviour as the reference library
+// (/root/reference/proj/include/nttk): swap
+//     #include "nttk/transform.hpp"      ->   #include "nttk_gpu/nttk.hpp"
+// and link libnttk_gpu.so.  Every call runs on the B200 through the C ABI
+// (include/nttk_gpu.h); contract violations throw nttk::contract_violation with the
+// reference's messages.  Batched overloads take many polynomials per call, which is
+// how the engine should be driven.
+//
+//   reference                                   here
+//   params.hpp:137  build_params(p,N,n,kinds)   build_params(p,N,n,kinds [, opts])
+//   params.hpp:303  preset(name)                preset(name)
+//   transform.hpp:220  ntt_forward              ntt_forward (+ batch overload)
+//   transform.hpp:228  ntt_forward_inplace      ntt_forward_inplace
+//   transform.hpp:339  intt_inverse             intt_inverse (+ batch overload)
+//   transform.hpp:349  pointwise_multiply       pointwise_multiply
+//   transform.hpp:372  cyclic_convolution_via_ntt  cyclic_convolution_via_ntt
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "nttk_gpu.h"
+
+namespace nttk {
+
+class contract_violation : public std::invalid_argument {  // int_util.hpp:17-21
+ public:
+  explicit contract_violation(const std::string& what) : std::invalid_argument(what) {}
+};
+
+class device_error : public std::runtime_error {
+ public:
+  explicit device_error(const std::string& what) : std::runtime_error(what) {}
+};
+
+enum class ButterflyKind { ntl, harvey, scott, improved, smont };  // butterfly.hpp:30 (+smont)
+enum class Ordering { natural, bit_reversed };                   // transform.hpp:26
+enum class Tree { cyclic = NTTK_CYCLIC, negacyclic = NTTK_NEGACYCLIC };
+
+using Polynomial = std::vector<uint64_t>;  // transform.hpp:28
+
+struct Spectrum {  // transform.hpp:30-33
+  std::vector<uint64_t> values;
+  Ordering ordering = Ordering::bit_reversed;
+};
+
+[[nodiscard]] constexpr const char* to_string(ButterflyKind k) {  // butterfly.hpp:32-40
+  switch (k) {
+    case ButterflyKind::ntl: return "ntl";
+    case ButterflyKind::harvey: return "harvey";
+    case ButterflyKind::scott: return "scott";
+    case ButterflyKind::improved: return "improved";
+    case ButterflyKind::smont: return "smont";
+  }
+  return "?";
+}
+
+[[nodiscard]] inline ButterflyKind butterfly_kind_from_string(std::string_view name) {
+  if (name == "ntl") return ButterflyKind::ntl;
+  if (name == "harvey") return ButterflyKind::harvey;
+  if (name == "scott") return ButterflyKind::scott;
+  if (name == "improved") return ButterflyKind::improved;
+  if (name == "smont") return ButterflyKind::smont;
+  throw contract_violation("unknown butterfly kind \"" + std::string(name) +
+                           "\" (ntl, harvey, scott, improved)");
+}
+
+[[nodiscard]] inline std::vector<ButterflyKind> all_butterfly_kinds() {
+  return {ButterflyKind::ntl, ButterflyKind::harvey, ButterflyKind::scott,
+          ButterflyKind::improved};
+}
+
+namespace detail {
+inline void check(int status) {
+  if (status == NTTK_OK) return;
+  const std::string msg = nttk_last_error();
+  if (status == NTTK_CONTRACT) throw contract_violation(msg);
+  throw device_error(msg);
+}
+struct HandleDeleter {
+  void operator()(nttk_params_s* h) const { nttk_params_destroy(h); }
+};
+}  // namespace detail
+
+struct BuildOptions {
+  Tree tree = Tree::cyclic;
+  uint32_t layers = 0;     // 0 = log2 N
+  uint64_t root = 0;       // 0 = smallest root of the required order
+  bool exact_bound = false;  // admit `improved` under Prop. 4's exact bound
+};
+
+// params.hpp:107-128: the scalar fields of the reference bundle plus the engine handle
+struct NttParams {
+  uint32_t p = 0, size = 0;
+  unsigned log2_size = 0, n_bits = 0, layers = 0;
+  uint64_t omega = 0, omega_inv = 0, n_inv = 0, n_inv_hat = 0;
+  std::vector<ButterflyKind> kinds;
+  std::shared_ptr<nttk_params_s> handle;
+
+  [[nodiscard]] bool has(ButterflyKind k) const {
+    for (auto x : kinds)
+      if (x == k) return true;
+    return false;
+  }
+  [[nodiscard]] std::vector<uint64_t> table(const char* name) const {
+    std::vector<uint64_t> v(nttk_params_table(handle.get(), name, nullptr, 0));
+    nttk_params_table(handle.get(), name, v.data(), v.size());
+    return v;
+  }
+};
+
+namespace detail {
+inline NttParams wrap(nttk_params_t h) {
+  NttParams P;
+  P.handle.reset(h, HandleDeleter{});
+  nttk_params_info info{};
+  check(nttk_params_get_info(h, &info));
+  P.p = static_cast<uint32_t>(info.p);
+  P.size = info.N;
+  P.log2_size = info.log2N;
+  P.n_bits = info.n_bits;
+  P.layers = info.layers;
+  P.omega = info.omega;
+  P.omega_inv = info.omega_inv;
+  P.n_inv = info.n_inv;
+  P.n_inv_hat = info.n_inv_hat;
+  for (int k = 0; k < 5; ++k)
+    if ((info.kinds_mask >> k) & 1u) P.kinds.push_back(static_cast<ButterflyKind>(k));
+  return P;
+}
+}  // namespace detail
+
+[[nodiscard]] inline NttParams build_params(uint64_t p, uint32_t N, unsigned n_bits,
+                                            std::vector<ButterflyKind> kinds = all_butterfly_kinds(),
+                                            const BuildOptions& opt = {}) {
+  nttk_params_desc d{};
+  d.p = p;
+  d.N = N;
+  d.n_bits = n_bits;
+  for (auto k : kinds) d.kinds_mask |= 1u << static_cast<int>(k);
+  d.tree = static_cast<uint32_t>(opt.tree);
+  d.layers = opt.layers;
+  d.root = opt.root;
+  d.flags = opt.exact_bound ? NTTK_EXACT_BOUND : 0;
+  nttk_params_t h = nullptr;
+  detail::check(nttk_build_params(&d, &h));
+  return detail::wrap(h);
+}
+
+[[nodiscard]] inline NttParams preset(const std::string& name) {
+  nttk_params_t h = nullptr;
+  detail::check(nttk_preset(name.c_str(), &h));
+  return detail::wrap(h);
+}
+
+// ---- batched host-memory calls (polys contiguous, P.size words each) ----------
+
+inline void ntt_forward_batch(const uint64_t* in, uint64_t* out, size_t batch, const NttParams& P,
+                              ButterflyKind kind) {
+  detail::check(nttk_ntt_forward_host(P.handle.get(), static_cast<int>(kind), in, out, batch, 8));
+}
+inline void intt_inverse_batch(const uint64_t* in, uint64_t* out, size_t batch, const NttParams& P,
+                               ButterflyKind kind) {
+  detail::check(nttk_intt_inverse_host(P.handle.get(), static_cast<int>(kind), in, out, batch, 8));
+}
+
+// ---- reference-shaped single-polynomial calls ------------------------------------
+
+[[nodiscard]] inline Spectrum ntt_forward(const Polynomial& f, const NttParams& P,
+                                          ButterflyKind kind) {
+  if (!P.has(kind)) throw contract_violation("ntt_forward: kind not built into these params");
+  if (f.size() != P.size) throw contract_violation("ntt_forward: wrong input length");
+  Spectrum s{std::vector<uint64_t>(P.size), Ordering::bit_reversed};
+  ntt_forward_batch(f.data(), s.values.data(), 1, P, kind);
+  return s;
+}
+
+inline void ntt_forward_inplace(std::vector<uint64_t>& a, const NttParams& P, ButterflyKind kind) {
+  ntt_forward_batch(a.data(), a.data(), a.size() / P.size, P, kind);
+}
+
+[[nodiscard]] inline Polynomial intt_inverse(const Spectrum& s, const NttParams& P,
+                                             ButterflyKind kind) {
+  if (!P.has(kind)) throw contract_violation("intt_inverse: kind not built into these params");
+  if (s.values.size() != P.size) throw contract_violation("intt_inverse: wrong input length");
+  if (s.ordering != Ordering::bit_reversed)
+    throw contract_violation("intt_inverse: spectrum must be in butterfly order");
+  Polynomial f(P.size);
+  intt_inverse_batch(s.values.data(), f.data(), 1, P, kind);
+  return f;
+}
+
+[[nodiscard]] inline Spectrum pointwise_multiply(const Spectrum& lhs, const Spectrum& rhs,
+                                                 const NttParams& P, ButterflyKind kind) {
+  if (lhs.values.size() != P.size || rhs.values.size() != P.size)
+    throw contract_violation("pointwise_multiply: wrong spectrum length");
+  if (lhs.ordering != rhs.ordering)
+    throw contract_violation("pointwise_multiply: mixed orderings");
+  Spectrum out{std::vector<uint64_t>(P.size), lhs.ordering};
+  detail::check(nttk_pointwise_multiply_host(P.handle.get(), static_cast<int>(kind),
+                                             lhs.values.data(), rhs.values.data(),
+                                             out.values.data(), 1, 8));
+  return out;
+}
+
+[[nodiscard]] inline Polynomial cyclic_convolution_via_ntt(
+    const Polynomial& x, const Polynomial& y, const NttParams& P,
+    ButterflyKind kind = ButterflyKind::improved) {
+  if (x.size() != P.size || y.size() != P.size)
+    throw contract_violation("ntt_forward: wrong input length");
+  Polynomial out(P.size);
+  detail::check(nttk_polymul_host(P.handle.get(), static_cast<int>(kind), x.data(), y.data(),
+                                  out.data(), 1, 8));
+  return out;
+}
+
+// ---- device-pointer batched calls (asynchronous on `stream`) ----------------------
+
+inline void ntt_forward_device(const NttParams& P, ButterflyKind kind, const void* d_in, void* d_out,
+                               size_t batch, int elem_bytes, void* stream = nullptr) {
+  detail::check(nttk_ntt_forward(P.handle.get(), static_cast<int>(kind), d_in, d_out, batch,
+                                 elem_bytes, stream));
+}
+inline void intt_inverse_device(const NttParams& P, ButterflyKind kind, const void* d_in,
+                                void* d_out, size_t batch, int elem_bytes, void* stream = nullptr) {
+  detail::check(nttk_intt_inverse(P.handle.get(), static_cast<int>(kind), d_in, d_out, batch,
+                                  elem_bytes, stream));
+}
+
+}  // namespace nttk

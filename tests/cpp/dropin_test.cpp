@@ -1,0 +1,185 @@
+// dropin_test.cpp -- the reference's transform/params test cases, run against the B200
+// engine through the C++ drop-in header (paper_2402_00675_b200/include/nttk_gpu/nttk.hpp).
+//
+// Mirrors proj/tests/transform_test.cpp and params_test.cpp case by case (hand-evaluated
+// spectra, every-kind round trips, convolution vs schoolbook, contract messages) with
+// plain checks instead of GoogleTest (absent in this image).  Exit code 0 = all passed.
+// Built and run by tests/test_cpp_dropin.py (-m gpu).
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <string>
+
+#include "nttk_gpu/nttk.hpp"
+
+using namespace nttk;
+
+static int g_fail = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    if (!(cond)) {                                                         \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);          \
+      ++g_fail;                                                            \
+    }                                                                      \
+  } while (0)
+
+template <class F>
+static bool throws_with(F&& f, const char* needle) {
+  try {
+    f();
+  } catch (const contract_violation& e) {
+    return std::string(e.what()).find(needle) != std::string::npos;
+  }
+  return false;
+}
+
+static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t p) {
+  return static_cast<uint64_t>((unsigned __int128)a * b % p);
+}
+
+static std::vector<uint64_t> natural(const Spectrum& s, uint64_t p) {  // bit-reversal + canon
+  const size_t N = s.values.size();
+  unsigned bits = 0;
+  while ((size_t(1) << bits) < N) ++bits;
+  std::vector<uint64_t> v(N);
+  for (size_t i = 0; i < N; ++i) {
+    size_t r = 0;
+    for (unsigned b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+    v[r] = s.values[i] % p;
+  }
+  return v;
+}
+
+static std::vector<uint64_t> naive_dft(const Polynomial& f, uint64_t w, uint64_t p) {
+  std::vector<uint64_t> out(f.size());
+  uint64_t x = 1;
+  for (size_t i = 0; i < f.size(); ++i, x = mulmod(x, w, p)) {
+    uint64_t acc = 0;
+    for (size_t j = f.size(); j-- > 0;) acc = (mulmod(acc, x, p) + f[j]) % p;
+    out[i] = acc;
+  }
+  return out;
+}
+
+static Polynomial schoolbook(const Polynomial& a, const Polynomial& b, uint64_t p) {
+  Polynomial c(a.size(), 0);
+  for (size_t i = 0; i < a.size(); ++i)
+    for (size_t j = 0; j < a.size(); ++j) {
+      const size_t k = (i + j) % a.size();
+      c[k] = (c[k] + mulmod(a[i], b[j], p)) % p;
+    }
+  return c;
+}
+
+static Polynomial random_poly(uint32_t N, uint64_t p, std::mt19937_64& rng) {
+  std::uniform_int_distribution<uint64_t> d(0, p - 1);
+  Polynomial f(N);
+  for (auto& c : f) c = d(rng);
+  return f;
+}
+
+int main() {
+  // params_test.cpp:56-69 -- toy13 bundle scalars
+  {
+    const auto P = preset("toy13");
+    CHECK(P.p == 13 && P.size == 4 && P.log2_size == 2);
+    CHECK(P.omega == 5 && P.omega_inv == 8 && P.n_inv == 10);
+    for (auto k : all_butterfly_kinds()) CHECK(P.has(k));
+  }
+  // params_test.cpp:71-110 -- fault collection and messages
+  CHECK(throws_with([] { (void)build_params(15, 4, 8); }, "p must be prime"));
+  CHECK(throws_with([] { (void)build_params(13, 8, 8); }, "N must divide p - 1"));
+  CHECK(throws_with([] { (void)build_params(15, 6, 40); }, "[2, 32]"));
+  CHECK(throws_with([] { (void)build_params(7681, 256, 16); }, "p < 2^{n-ell-2}"));
+  CHECK(throws_with([] { (void)preset("nope"); }, "unknown preset"));
+  CHECK(throws_with([] { (void)butterfly_kind_from_string("fancy"); }, "unknown butterfly kind"));
+  // transform_test.cpp:39-48 -- hand-evaluated DFT, every kind
+  {
+    const auto P = build_params(17, 4, 16);
+    const Polynomial f{1, 2, 3, 4};
+    const std::vector<uint64_t> want{10, 7, 15, 6};
+    CHECK(naive_dft(f, P.omega, P.p) == want);
+    for (auto k : all_butterfly_kinds()) CHECK(natural(ntt_forward(f, P, k), P.p) == want);
+  }
+  // transform_test.cpp:50-59 -- delta in slot one lists the root powers
+  {
+    const auto P = preset("toy13");
+    const std::vector<uint64_t> want{1, 5, 12, 8};
+    for (auto k : all_butterfly_kinds())
+      CHECK(natural(ntt_forward({0, 1, 0, 0}, P, k), P.p) == want);
+  }
+  // transform_test.cpp:61-93 -- kinds agree; every kind pair inverts every other
+  for (const char* name : {"toy13", "kyber256", "falcon512"}) {
+    const auto P = preset(name);
+    std::mt19937_64 rng(7);
+    const auto f = random_poly(P.size, P.p, rng);
+    const auto base = natural(ntt_forward(f, P, ButterflyKind::ntl), P.p);
+    CHECK(base == naive_dft(f, P.omega, P.p));
+    for (auto fk : all_butterfly_kinds()) {
+      const auto spec = ntt_forward(f, P, fk);
+      CHECK(natural(spec, P.p) == base);
+      for (auto ik : all_butterfly_kinds()) CHECK(intt_inverse(spec, P, ik) == f);
+    }
+  }
+  // transform_test.cpp:373-400 -- convolution vs schoolbook
+  {
+    const auto P = build_params(17, 4, 16);
+    for (auto k : all_butterfly_kinds())
+      CHECK(cyclic_convolution_via_ntt({1, 2, 3, 4}, {1, 0, 0, 1}, P, k) ==
+            (Polynomial{3, 5, 7, 5}));
+    const auto K = preset("kyber256");
+    std::mt19937_64 rng(31337);
+    for (int t = 0; t < 3; ++t) {
+      const auto a = random_poly(K.size, K.p, rng), b = random_poly(K.size, K.p, rng);
+      const auto want = schoolbook(a, b, K.p);
+      for (auto k : all_butterfly_kinds()) CHECK(cyclic_convolution_via_ntt(a, b, K, k) == want);
+    }
+  }
+  // transform_test.cpp:402-420 -- improved pointwise takes a lazy right operand
+  {
+    const auto P = preset("toy13");
+    const Spectrum lhs{{1, 2, 3, 4}}, rhs{{51, 40, 27, 14}};
+    const auto out = pointwise_multiply(lhs, rhs, P, ButterflyKind::improved);
+    for (int i = 0; i < 4; ++i) CHECK(out.values[i] == lhs.values[i] * (rhs.values[i] % 13) % 13);
+    CHECK(pointwise_multiply(lhs, rhs, P, ButterflyKind::harvey).values == out.values);
+    CHECK(throws_with(
+        [&] { (void)pointwise_multiply(lhs, Spectrum{{1, 2, 3, 4}, Ordering::natural}, P,
+                                       ButterflyKind::ntl); },
+        "mixed orderings"));
+  }
+  // transform_test.cpp:440-463 -- entry points validate their inputs
+  {
+    const auto P = preset("toy13");
+    CHECK(throws_with([&] { (void)ntt_forward({1, 2}, P, ButterflyKind::ntl); }, "wrong input length"));
+    CHECK(throws_with([&] { (void)ntt_forward({13, 0, 0, 0}, P, ButterflyKind::ntl); },
+                      "coefficients must be canonical"));
+    CHECK(throws_with(
+        [&] { (void)intt_inverse(Spectrum{{1, 2, 3, 4}, Ordering::natural}, P, ButterflyKind::ntl); },
+        "butterfly order"));
+    const auto only = build_params(13, 4, 8, {ButterflyKind::ntl});
+    CHECK(throws_with([&] { (void)ntt_forward({1, 2, 3, 4}, only, ButterflyKind::harvey); },
+                      "kind not built"));
+  }
+  // BASELINE moduli through the fast path: Kyber (n=16) and Dilithium (n=32) round trips
+  {
+    BuildOptions o;
+    o.exact_bound = true;
+    for (auto [p, n] : {std::pair<uint64_t, unsigned>{3329, 16}, {8380417, 32}}) {
+      const auto P = build_params(p, 256, n, {ButterflyKind::improved, ButterflyKind::harvey}, o);
+      std::mt19937_64 rng(p);
+      std::vector<uint64_t> batch(64 * 256);
+      for (auto& c : batch) c = rng() % p;
+      std::vector<uint64_t> spec(batch.size()), back(batch.size());
+      for (auto k : {ButterflyKind::improved, ButterflyKind::harvey}) {
+        ntt_forward_batch(batch.data(), spec.data(), 64, P, k);
+        intt_inverse_batch(spec.data(), back.data(), 64, P, k);
+        CHECK(back == batch);
+        const Polynomial f0(batch.begin(), batch.begin() + 256);
+        CHECK(natural(Spectrum{std::vector<uint64_t>(spec.begin(), spec.begin() + 256)}, p) ==
+              naive_dft(f0, P.omega, p));
+      }
+    }
+  }
+  std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
+  return g_fail ? 1 : 0;
+}

@@ -1,0 +1,110 @@
+"""CPU checks of the C-ABI boundary and the host-side logic (no GPU needed).
+
+* libnttk_gpu.so loads and exports every entry point include/nttk_gpu.h declares;
+* the host parameter builder (B200 counterpart of build_params, params.hpp:137-268)
+  produces the reference's tables bit for bit (checked against the pinned oracle) and
+  the reference's fault messages;
+* without a device every compute entry point fails loudly (no CPU fallback).
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle.oracle import CYCLIC, HARVEY, IMPROVED, NEGA, NTL, SCOTT, SMONT
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "nttk_gpu.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(nttk_\w+)\s*\(", txt, re.M)))
+
+
+def test_library_exports_every_declared_symbol(engine):
+    syms = header_symbols()
+    assert len(syms) >= 19, syms
+    lib = engine.lib()
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(syms) == set(engine.EXPORTS)
+
+
+def test_no_gpu_fails_loudly(engine):
+    if engine.device_available():
+        pytest.skip("a device is present")
+    P = engine.build_params(3329, 256, 16, [engine.ButterflyKind.improved], exact_bound=True)
+    with pytest.raises(engine.CudaError, match="no CUDA device"):
+        engine.ntt_forward_batch(np.zeros((2, 256), dtype=np.uint16), P, 3)
+
+
+CONFIGS = [
+    # (p, N, n, kinds, tree, layers, exact)
+    (3329, 256, 16, (IMPROVED, HARVEY, SMONT), CYCLIC, 0, True),
+    (3329, 256, 16, (IMPROVED, HARVEY, SMONT), NEGA, 7, True),
+    (3329, 256, 32, (NTL, HARVEY, SCOTT, IMPROVED), CYCLIC, 0, False),
+    (8380417, 256, 32, (NTL, HARVEY, SCOTT, IMPROVED, SMONT), CYCLIC, 0, True),
+    (8380417, 256, 32, (IMPROVED, HARVEY, SMONT), NEGA, 8, True),
+    (7681, 256, 32, (NTL, HARVEY, SCOTT, IMPROVED), CYCLIC, 0, False),
+    (12289, 1024, 32, (NTL, HARVEY, SCOTT, IMPROVED), CYCLIC, 0, False),
+    (13, 4, 8, (NTL, HARVEY, SCOTT, IMPROVED), CYCLIC, 0, False),
+    (17, 8, 16, (IMPROVED, HARVEY, SMONT), NEGA, 2, True),
+]
+TABLES = ("dif_w", "dif_wq", "dif_mont", "ct_plain", "ct_plantard", "ct_mont", "ct_smont",
+          "gs_plain", "gs_wq", "gs_mont", "gs_plantard", "gs_smont")
+
+
+@pytest.mark.parametrize("cfg", CONFIGS)
+def test_host_tables_match_oracle(engine, oracle, cfg):
+    p, N, n, kinds, tree, layers, exact = cfg
+    P = engine.build_params(p, N, n, kinds, tree=tree, layers=layers, exact_bound=exact)
+    Q = oracle.params(p, N, n, kinds, tree=tree, layers=layers, exact=exact)
+    assert (P.omega, P.omega_inv, P.n_inv) == (Q.omega, Q.omega_inv, Q.n_inv)
+    if IMPROVED in kinds:
+        assert P.n_inv_hat == Q.n_inv_hat
+    for t in TABLES:
+        a, b = P.table(t), Q.table(t)
+        if len(a) == 0 and t.startswith("dif"):
+            continue
+        assert len(a) == len(b) and (a == b).all(), t
+
+
+def test_fault_messages_match_reference(engine):
+    C = engine.ContractViolation
+    with pytest.raises(C, match="p must be prime"):
+        engine.build_params(15, 4, 8)
+    with pytest.raises(C, match="N must divide p - 1"):
+        engine.build_params(13, 8, 8)
+    with pytest.raises(C) as e:
+        engine.build_params(15, 6, 40)
+    assert all(s in str(e.value) for s in ("p must be prime", "power of two", "[2, 32]"))
+    with pytest.raises(C, match=r"p < 2\^\{n-ell-2\}"):
+        engine.build_params(7681, 256, 16)
+    with pytest.raises(C, match="unknown preset"):
+        engine.preset("nope")
+    with pytest.raises(C, match="at least one butterfly kind"):
+        engine.build_params(13, 4, 8, [])
+    with pytest.raises(C, match="unknown butterfly kind"):
+        engine.butterfly_kind_from_string("fancy")
+
+
+def test_presets_and_fast_path_selection(engine):
+    P = engine.preset("kyber256")
+    assert (P.p, P.size, P.n_bits, P.omega) == (7681, 256, 32, 198)
+    T = engine.preset("toy13")
+    assert (T.omega, T.omega_inv, T.n_inv) == (5, 8, 10)
+    K = engine.build_params(3329, 256, 16, [engine.ButterflyKind.improved], exact_bound=True)
+    assert engine.ButterflyKind.improved in K.fast_path
+    F = engine.preset("falcon512")
+    assert F.fast_path == []  # N = 512 runs on the generic kernel
+
+
+def test_exact_bound_admits_kyber_n16_and_dilithium_n32(engine):
+    with pytest.raises(engine.ContractViolation):
+        engine.build_params(3329, 256, 16, [engine.ButterflyKind.improved])
+    with pytest.raises(engine.ContractViolation):
+        engine.build_params(8380417, 256, 32, [engine.ButterflyKind.improved])
+    engine.build_params(3329, 256, 16, [engine.ButterflyKind.improved], exact_bound=True)
+    engine.build_params(8380417, 256, 32, [engine.ButterflyKind.improved], exact_bound=True)
