@@ -126,6 +126,28 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+NCU_KERNELS = {"kyber_fwd": "fwd256_tma_kernel<ImprovedN16", "kyber_inv": "inv256_tma_kernel<ImprovedN16",
+               "dil_fwd": "fwd256_tma_kernel<ImprovedN32", "dil_inv": "inv256_tma_kernel<ImprovedN32"}
+
+
+def ncu_traffic(kernel: str, nk: int, nd: int):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full
+    capture of this same bench configuration (profiles/rNN_ncu_full.json), else None."""
+    import glob
+
+    if (nk, nd) != (1 << 22, 1 << 21):
+        return None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full.json")))
+    if not files:
+        return None
+    with open(files[-1]) as fh:
+        caps = json.load(fh)["kernels"]
+    for k in caps:
+        if NCU_KERNELS[kernel] in k["kernel"].replace("nttk_b200::", "").replace("unnamed>::", ""):
+            return k["dram_bytes"]
+    return None
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -283,14 +305,35 @@ def run_engine_arm(a, rank, world, local_rank):
     polys_per_step = (nk + nd) * world
     value = polys_per_step * a.steps / (max_ms / 1e3)
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel: HBM (bytes in + out) and the IMAD issue roof
+    # (modmuls per poly x measured fmaheavy cost)
     dom = int(np.argmax(per_kernel))
     peak, peak_src = measured_peaks()
     achieved = alg_bytes[dom] / (per_kernel[dom] / 1e3) / 1e9
+    sm_hz = 1965e6 if not clk.samples else 1e6 * float(np.median([s[0] for s in clk.samples]))
+    n_sm = torch.cuda.get_device_properties(local_rank).multi_processor_count
+    # SM-cycles per modmul (fmaheavy: IMAD 1/64, IMAD.HI 1/32 per lane, measured):
+    # n=16 Plantard IMAD + IMAD.HI; n=32 IMAD + 2 IMAD.HI
+    cyc = [3 / 64, 3 / 64, 5 / 64, 5 / 64]
+    modmuls = [1024, 1024 + 256, 1024, 1024 + 256]  # fwd N/2 log N; inv + N scaling
+    polys = [nk, nk, nd, nd]
+    imad_roof_ms = [p_ * m * c / (n_sm * sm_hz) * 1e3 for p_, m, c in zip(polys, modmuls, cyc)]
+    hbm_roof_ms = [b / (peak * 1e9) * 1e3 for b in alg_bytes]
+    roof_ms = [max(a, b) for a, b in zip(imad_roof_ms, hbm_roof_ms)]
+    traffic = ncu_traffic(names[dom], nk, nd)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": names[dom],
+                "frac": achieved / peak, "traffic": traffic, "kernel": names[dom],
                 "peak_source": peak_src,
+                "binding_roof": "imad" if imad_roof_ms[dom] > hbm_roof_ms[dom] else "hbm",
+                "frac_of_binding_roof": roof_ms[dom] / per_kernel[dom],
+                "imad": {"achieved_modmul_per_s": polys[dom] * modmuls[dom] / (per_kernel[dom] / 1e3),
+                         "peak_modmul_per_s": n_sm * sm_hz / cyc[dom],
+                         "frac": imad_roof_ms[dom] / per_kernel[dom],
+                         "definition": "fmaheavy cycles of the modmul's IMAD/IMAD.HI (measured "
+                                       "rates, profiles/r01_imad_microbench.txt) x modmuls/poly"},
+                "step_frac_of_roofline": sum(roof_ms) / sum(per_kernel),
                 "per_kernel_ms": dict(zip(names, [round(x, 4) for x in per_kernel])),
+                "per_kernel_roof_ms": dict(zip(names, [round(x, 4) for x in roof_ms])),
                 "per_kernel_GBps": dict(zip(names, [round(b / (t / 1e3) / 1e9, 1)
                                                     for b, t in zip(alg_bytes, per_kernel)]))}
     fwd_rate = (nk + nd) * world / (max(per_kernel[0] + per_kernel[2], 1e-9) / 1e3)
