@@ -170,6 +170,12 @@ __device__ __forceinline__ uint32_t canon(uint32_t x, const FastArgs& A) {
 #define NTTK_INV_ALT_MASK 0x0  // inverse merge layers (bit s) using the alternative form
 #endif
 
+// Minimum CTAs per SM for the register allocator (shared memory admits 4 for u16 and 3
+// for u32 stages).  Measured: capping the n=32 kernels to 3 CTAs (72 regs) is ~2% slower.
+#ifndef NTTK_MINB
+#define NTTK_MINB(IO) 1
+#endif
+
 template <class K, class Tw>
 __device__ __forceinline__ void inv_bf(int sl, uint32_t& x, uint32_t& y, Tw w, uint32_t off,
                                        const FastArgs& A) {
@@ -201,7 +207,7 @@ __device__ __forceinline__ void produce(const IO* in, size_t batch, uint8_t* sta
 
 // ---------------------------------------------------------------------------
 template <class K, class IO, int L, bool PER_INDEX>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
   using G = Geo<IO>;
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(kThreads)
 // bits 0/1); 2: u16 input with the fused first merge layer (A.flags bit 2, improved n=16):
 // X' = (X + Y) mod p, Y' = MP(w, X + K p - Y) replaces canonicalise-then-merge
 template <class K, class IO, int L, int MODE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     inv256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
   using G = Geo<IO>;
