@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", action="store_true", help="NCCL-gather per-rank digests")
+    ap.add_argument("--no-extras", action="store_true", help="skip BASELINE configs 1/2/3/5")
     return ap.parse_args()
 
 
@@ -238,6 +239,100 @@ def run_reference_arm(a, rank, world):
 # ---------------------------------------------------------------------------
 # engine arm
 
+def _time_ms(torch, fn, iters, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def run_extras(dev):
+    """The other BASELINE.json configs, device-resident, CUDA events (secondary fields)."""
+    import torch
+
+    import paper_2402_00675_b200.nttk as nttk
+
+    K = nttk.ButterflyKind
+    NEG = nttk.Tree.negacyclic
+    g = torch.Generator(device=dev).manual_seed(99)
+    ex = {}
+    # config 1: Kyber-style forward, 4096 polys, 7 layers (degree-2 leaves), improved n=16
+    P1 = nttk.build_params(KYBER_Q, 256, 16, [K.improved], tree=NEG, layers=7, exact_bound=True)
+    x = torch.randint(0, KYBER_Q, (4096, 256), generator=g, device=dev, dtype=torch.int32).to(torch.int16)
+    y = torch.empty_like(x)
+    ms = _time_ms(torch, lambda: nttk.forward(P1, K.improved, x, y), 200, 10)
+    ex["config1_kyber7_fwd_4096"] = {"us_per_call": ms * 1e3, "polys_per_s": 4096 / (ms / 1e3)}
+    # config 2: Kyber-style polymul (7-layer fwd x2, basemul, inverse), 65536 pairs, per variant
+    B = 65536
+    xa = torch.randint(0, KYBER_Q, (B, 256), generator=g, device=dev, dtype=torch.int32).to(torch.int16)
+    xb = torch.randint(0, KYBER_Q, (B, 256), generator=g, device=dev, dtype=torch.int32).to(torch.int16)
+    xc = torch.empty_like(xa)
+    c2 = {}
+    for name, kind in (("modified_plantard", K.improved), ("montgomery_R2^16", K.harvey),
+                       ("signed_montgomery", K.smont)):
+        P2 = nttk.build_params(KYBER_Q, 256, 16, [kind], tree=NEG, layers=7, exact_bound=True)
+        ms = _time_ms(torch, lambda: nttk.polymul(P2, kind, xa, xb, xc), 20)
+        c2[name] = {"ms": ms, "products_per_s": B / (ms / 1e3)}
+    ex["config2_kyber_polymul_65536_fused"] = c2
+    # config 3: Dilithium round trip, 65536 polys, modified Plantard n=32 vs 32-bit Montgomery
+    xd = torch.randint(0, DIL_Q, (B, 256), generator=g, device=dev, dtype=torch.int32)
+    sd, od = torch.empty_like(xd), torch.empty_like(xd)
+    c3 = {}
+    for name, kind in (("modified_plantard_n32", K.improved), ("montgomery_n32", K.harvey)):
+        P3 = nttk.build_params(DIL_Q, 256, 32, [kind], exact_bound=True)
+
+        def rt():
+            nttk.forward(P3, kind, xd, sd)
+            nttk.inverse(P3, kind, sd, od)
+
+        ms = _time_ms(torch, rt, 20)
+        assert torch.equal(od, xd)
+        c3[name] = {"ms": ms, "polys_per_s": B / (ms / 1e3)}
+    ex["config3_dilithium_roundtrip_65536"] = c3
+    # config 5: reduction sweep, 2^30 operand pairs (2^15 x 2^15 grid) per (q, variant);
+    # IMAD roof = SM-cycles per mult of the variant's multiplies (IMAD 1/64, IMAD.HI and
+    # IMAD.WIDE 1/32 per lane-op, measured)
+    cost = {(16, 0): 3 / 64, (16, 1): 3 / 64, (16, 2): 2 / 64, (16, 3): 3 / 64,
+            (32, 0): 5 / 64, (32, 1): 5 / 64, (32, 2): 5 / 64, (32, 3): 5 / 64}
+    names = ["mont_redc", "signed_mont_redc", "plantard_redc", "modified_plantard_mul"]
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    c5 = {}
+    for q, n, ell in ((KYBER_Q, 16, 2), (DIL_Q, 32, 7)):
+        for v in range(4):
+            if v == 1:
+                A = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
+                Bv = torch.randint(-(1 << (n - 1)), 1 << (n - 1), (1 << 15,), generator=g, device=dev,
+                                   dtype=torch.int64)
+            elif v == 2:
+                A = torch.randint(0, q + 1, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
+                Bv = torch.randint(0, q + 1, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
+            elif v == 3:
+                A = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
+                Bv = torch.randint(0, q << ell, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
+            else:
+                A = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
+                Bv = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
+            nttk.modmul_sweep(v, q, n, ell, A, Bv)  # warm-up (module load, occupancy query)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            reps = 5
+            for _ in range(reps):
+                nttk.modmul_sweep(v, q, n, ell, A, Bv)  # synchronises (returns the checksum)
+            sec = (time.perf_counter() - t0) / reps
+            rate = (1 << 30) / sec
+            roof = n_sm * 1965e6 / cost[(n, v)]
+            c5[f"q{q}_{names[v]}"] = {"mults_per_s": rate, "imad_roof_mults_per_s": roof,
+                                      "frac": rate / roof}
+    ex["config5_sweep_2^30"] = c5
+    return ex
+
+
 def run_engine_arm(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -385,6 +480,10 @@ def run_engine_arm(a, rank, world, local_rank):
                "sample": (f"{reps} x ({smp_k} Kyber + {smp_d} Dilithium) polys fwd+inv, "
                           f"{tot_t:.1f} s wall on {threads} threads")}
 
+    extras = None
+    if rank == 0 and not a.no_extras:
+        extras = run_extras(dev)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
@@ -396,6 +495,8 @@ def run_engine_arm(a, rank, world, local_rank):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }
+        if extras is not None:
+            line["extras"] = extras
         if digest is not None:
             line["gathered_digests"] = digest
         print(json.dumps(line), flush=True)

@@ -115,6 +115,18 @@ bool use_fast(const HostParams& P, int kind) {
   return ((P.fast_mask >> kind) & 1u) && nttk_b200::fast256_supports(kind, P.layers, P.n_bits);
 }
 
+// one fused kernel for fwd(a), fwd(b), product, inverse (polymul_tma.cu); NTTK_KERNEL=v1
+// keeps the four-kernel composition for A/B runs
+bool use_fused_polymul(const HostParams& P, int kind, int elem, const void* a, const void* b,
+                       const void* out) {
+  static const bool v1 = [] {
+    const char* k = std::getenv("NTTK_KERNEL");
+    return k && std::string(k) == "v1";
+  }();
+  if (v1 || !use_fast(P, kind)) return false;
+  return nttk_b200::fast256_tma_supports(elem, a, out) && !(reinterpret_cast<uintptr_t>(b) & 15);
+}
+
 int current_device() {
   int d = 0;
   cudaGetDevice(&d);
@@ -398,6 +410,11 @@ int nttk_polymul(nttk_params_t h, int kind, const void* d_a, const void* d_b, vo
   if (int s = need_device("polymul")) return s;
   if (!batch) return NTTK_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_fused_polymul(P, kind, elem, d_a, d_b, d_out)) {
+    cudaError_t e = nttk_b200::polymul256_launch(P, kind, d_a, d_b, d_out, batch, elem, st);
+    ++g_launches;
+    return e == cudaSuccess ? NTTK_OK : cuda_fail(e, "polymul");
+  }
   void* tmp = nullptr;
   const size_t bytes = batch * P.N * size_t(elem);
   cudaError_t e = cudaMallocAsync(&tmp, bytes, st);
@@ -484,6 +501,11 @@ int nttk_polymul_host(nttk_params_t h, int kind, const void* h_a, const void* h_
   const int rc = host_pipeline(
       P, elem, batch, {h_a, h_b}, {{h_out, 2}},
       [&](cudaStream_t st, void** b, size_t n) {
+        if (use_fused_polymul(P, kind, elem, b[0], b[1], b[2])) {
+          cudaError_t e = nttk_b200::polymul256_launch(P, kind, b[0], b[1], b[2], n, elem, st);
+          ++g_launches;
+          return e == cudaSuccess ? int(NTTK_OK) : cuda_fail(e, "polymul");
+        }
         int r = run_transform(P, kind, 0, b[0], b[0], n, elem, st);
         if (!r) r = run_transform(P, kind, 0, b[1], b[1], n, elem, st);
         if (!r) r = run_product(P, kind, b[0], b[1], b[2], n, elem, st);

@@ -141,6 +141,15 @@ struct ImprovedN16 {
     x = mp_n16<true>(x + y + A.zero, A.scale_lo, A.p);
     y = mp_n16<PAPER_FORM>(t, A.fold_lo, A.p);
   }
+  // product stage (fused polymul): x -> (x (-2^{2n}) mod p) mu, then MP(.., y) = x y mod p
+  using Enc = uint32_t;
+  __device__ static Enc enc(uint32_t x, const ProdArgs& Q, const FastArgs& A) {
+    return mp_n16<false>(x, Q.enc_lo, A.p) * Q.mu_lo;
+  }
+  __device__ static Enc genc(int k, const ProdArgs& Q) { return Q.g_lo[k]; }
+  __device__ static uint32_t mulc(uint32_t y, Enc e, const FastArgs& A) {
+    return mp_n16<false>(y, e, A.p);
+  }
 };
 
 struct ImprovedN32 {
@@ -171,6 +180,15 @@ struct ImprovedN32 {
     const uint32_t t = x + off - y;
     x = mp_n32(x + y + A.zero, A.scale_lo, A.scale_hi, A.p);
     y = mp_n32(t, A.fold_lo, A.fold_hi, A.p);
+  }
+  using Enc = uint2;
+  __device__ static Enc enc(uint32_t x, const ProdArgs& Q, const FastArgs& A) {
+    const uint32_t xp = mp_n32(x, Q.enc_lo, Q.enc_hi, A.p);  // x (-2^{2n}) mod p
+    return make_uint2(xp * Q.mu_lo, __umulhi(xp, Q.mu_lo) + xp * Q.mu_hi);  // xp mu mod 2^64
+  }
+  __device__ static Enc genc(int k, const ProdArgs& Q) { return make_uint2(Q.g_lo[k], Q.g_hi[k]); }
+  __device__ static uint32_t mulc(uint32_t y, Enc e, const FastArgs& A) {
+    return mp_n32(y, e.x, e.y, A.p);
   }
 };
 
@@ -235,6 +253,16 @@ struct Harvey {
     x = umin32(a, a - A.p);
     y = umin32(b, b - A.p);
   }
+  // product stage: x -> x 2^n mod p (lazy, via R^2), then Montgomery product, canonical
+  using Enc = uint32_t;
+  __device__ static Enc enc(uint32_t x, const ProdArgs& Q, const FastArgs& A) {
+    return harvey_mul<N_BITS>(x, Q.enc_lo, A);
+  }
+  __device__ static Enc genc(int k, const ProdArgs& Q) { return Q.g_lo[k]; }
+  __device__ static uint32_t mulc(uint32_t y, Enc e, const FastArgs& A) {
+    const uint32_t r = harvey_mul<N_BITS>(y, e, A);
+    return umin32(r, r - A.p);
+  }
 };
 
 // Signed Montgomery (reduction.hpp:141-165): r = (A - m p) / 2^n, m = centered
@@ -297,6 +325,20 @@ struct Smont {
     (void)off;
     (void)x;
     (void)y;
+  }
+  // product stage: x -> x 2^n (signed Montgomery via R^2), then signed product
+  using Enc = uint2;
+  __device__ static Enc enc(uint32_t x, const ProdArgs& Q, const FastArgs& A) {
+    const int32_t xs = smont_mul<N_BITS>(static_cast<int32_t>(x), static_cast<int32_t>(Q.enc_lo),
+                                         Q.enc_hi, A);
+    const uint32_t q = N_BITS == 16 ? static_cast<uint32_t>(xs) * (A.pinv << 16)
+                                    : static_cast<uint32_t>(xs) * A.pinv;
+    return make_uint2(static_cast<uint32_t>(xs), q);
+  }
+  __device__ static Enc genc(int k, const ProdArgs& Q) { return make_uint2(Q.g_lo[k], Q.g_hi[k]); }
+  __device__ static uint32_t mulc(uint32_t y, Enc e, const FastArgs& A) {
+    const int32_t r = smont_mul<N_BITS>(static_cast<int32_t>(y), static_cast<int32_t>(e.x), e.y, A);
+    return static_cast<uint32_t>(r + (r < 0 ? static_cast<int32_t>(A.p) : 0));
   }
 };
 

@@ -23,3 +23,11 @@ cudaError_t fast256_tma_launch(const HostParams& P, int kind, int dir, const voi
                                size_t batch, int elem_bytes, cudaStream_t st);
 
 }  // namespace nttk_b200
+
+namespace nttk_b200 {
+
+// fused polymul (polymul_tma.cu): c = inverse(product(forward(a), forward(b)))
+cudaError_t polymul256_launch(const HostParams& P, int kind, const void* a, const void* b,
+                              void* out, size_t batch, int elem_bytes, cudaStream_t st);
+
+}  // namespace nttk_b200

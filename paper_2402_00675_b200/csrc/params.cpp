@@ -223,6 +223,45 @@ void fill_fast(HostParams& P, int kind) {
       }
     }
   }
+  // product stage of the fused polymul (ProdArgs): per-kind multiplier encodings
+  ProdArgs& Q = P.prod[kind];
+  const uint64_t p = P.p;
+  Q.basemul = (P.N >> P.layers) == 2 ? 1u : 0u;
+  const uint64_t r2 = static_cast<uint64_t>(u128(c.beta % p) * (c.beta % p) % p);  // 2^{2n} mod p
+  auto smont_pair = [&](uint64_t w, uint32_t& lo, uint32_t& hi) {
+    const int64_t ws = to_smont(w, c);  // centered w 2^n mod p
+    const uint64_t q = static_cast<uint64_t>(ws) * c.p_inv_beta & c.beta_mask;
+    lo = static_cast<uint32_t>(ws);
+    hi = n16 ? static_cast<uint32_t>(q << 16) : static_cast<uint32_t>(q);
+  };
+  switch (kind) {
+    case NTTK_IMPROVED: {
+      const uint64_t c4 = static_cast<uint64_t>(u128(r2) * r2 % p);  // 2^{4n} mod p
+      const uint64_t em = c4 * c.mu & c.r2n_mask;
+      Q.enc_lo = static_cast<uint32_t>(em);
+      Q.enc_hi = static_cast<uint32_t>(em >> 32);
+      Q.mu_lo = static_cast<uint32_t>(c.mu);
+      Q.mu_hi = static_cast<uint32_t>(c.mu >> 32);
+      for (size_t k = 0; k < P.gamma.size() && k < 128; ++k) {
+        const uint64_t gm = to_plantard(P.gamma[k], c) * c.mu & c.r2n_mask;
+        Q.g_lo[k] = static_cast<uint32_t>(gm);
+        Q.g_hi[k] = static_cast<uint32_t>(gm >> 32);
+      }
+      break;
+    }
+    case NTTK_HARVEY:
+      Q.enc_lo = static_cast<uint32_t>(r2);  // harvey_mul(x, R^2) = x R mod p, lazy
+      for (size_t k = 0; k < P.gamma.size() && k < 128; ++k)
+        Q.g_lo[k] = static_cast<uint32_t>(to_mont(P.gamma[k], c));
+      break;
+    case NTTK_SMONT: {
+      // multiplier R^2 in signed-Montgomery form: smont(x * R^2-encoding) = x R mod p
+      smont_pair(static_cast<uint64_t>(u128(r2) * inverse(c.beta % p, p) % p), Q.enc_lo, Q.enc_hi);
+      for (size_t k = 0; k < P.gamma.size() && k < 128; ++k)
+        smont_pair(P.gamma[k], Q.g_lo[k], Q.g_hi[k]);
+      break;
+    }
+  }
   P.fast_mask |= 1u << kind;
 }
 

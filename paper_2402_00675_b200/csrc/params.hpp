@@ -67,6 +67,22 @@ struct FastArgs {
   uint32_t hi[256] = {};   // high words of 64-bit premultiplied Plantard twiddles
 };
 
+// Product stage of the fused polymul kernel (slotwise product or degree-2 basemul of two
+// forward spectra).  The product is canonical, so any exact method is bit-identical with
+// the reference's pointwise_multiply (transform.hpp:349-370); each kind uses its own
+// reduction: `enc` turns a runtime operand into that kind's multiplier encoding.
+struct ProdArgs {
+  uint32_t enc_lo = 0, enc_hi = 0;  // improved: (2^{4n} mod p) mu; harvey: 2^{2n} mod p; smont: centered R^2 + quotient factor
+  uint32_t mu_lo = 0, mu_hi = 0;    // improved: p^{-1} mod 2^{2n}
+  uint32_t basemul = 0;             // 1: degree-2 leaves (x^2 - gamma), 0: slotwise
+  uint32_t g_lo[128] = {}, g_hi[128] = {};  // gamma per pair, kind encoding (basemul)
+};
+
+struct PolymulArgs {
+  FastArgs fwd, inv;
+  ProdArgs prod;
+};
+
 struct HostParams {
   nttk_params_desc desc{};
   uint32_t p = 0, N = 0, log2N = 0, n_bits = 0, tree = 0, layers = 0, kinds = 0;
@@ -85,6 +101,7 @@ struct HostParams {
   // fast-path images, indexed [kind][dir] (dir 0 forward, 1 inverse)
   uint32_t fast_mask = 0;
   FastArgs fast[5][2];
+  ProdArgs prod[5];
 
   mutable std::mutex mu_dev;
   mutable DeviceTables dev[64];

@@ -160,7 +160,9 @@ def test_dilithium_improved_matches_reference_exact_bound(oracle, golden):
 
 @pytest.mark.parametrize("kind,n,tree,layers", [(IMPROVED, 16, NEGA, 7), (HARVEY, 16, NEGA, 7),
                                                 (SMONT, 16, NEGA, 7), (IMPROVED, 16, CYCLIC, 8),
-                                                (IMPROVED, 32, NEGA, 8), (SMONT, 32, NEGA, 8)])
+                                                (HARVEY, 16, CYCLIC, 8), (SMONT, 16, CYCLIC, 8),
+                                                (IMPROVED, 32, NEGA, 8), (SMONT, 32, NEGA, 8),
+                                                (HARVEY, 32, CYCLIC, 8), (IMPROVED, 32, CYCLIC, 8)])
 def test_polymul_vs_schoolbook(oracle, kind, n, tree, layers):
     p = KYBER if n == 16 else DILITHIUM
     P = engine_params(p, 256, n, [kind], tree=tree, layers=layers, exact=True)
@@ -170,8 +172,14 @@ def test_polymul_vs_schoolbook(oracle, kind, n, tree, layers):
     b = oracle.rng(20 + kind, p, B * 256).reshape(B, 256)
     want = Q.polymul(kind, a, b)
     elem = 2 if p == KYBER else 4
-    got = from_dev(nttk.polymul(P, kind, to_dev(a, elem), to_dev(b, elem)))
+    got = from_dev(nttk.polymul(P, kind, to_dev(a, elem), to_dev(b, elem)))  # fused kernel
     assert (got == want).all()
+    got64 = from_dev(nttk.polymul(P, kind, to_dev(a, 8), to_dev(b, 8)))  # 4-kernel pipeline
+    assert (got64 == want).all()
+    # in-place (out aliases a)
+    xa = to_dev(a, elem)
+    nttk.polymul(P, kind, xa, to_dev(b, elem), out=xa)
+    assert (from_dev(xa) == want).all()
     school = oracle.schoolbook_negacyclic if tree == NEGA else oracle.schoolbook_cyclic
     for i in (0, B - 1):
         assert (got[i] == school(a[i], b[i], p)).all()
