@@ -345,15 +345,15 @@ template <class IO>
 __device__ __forceinline__ void store_contiguous(IO* out_poly, int j, const uint32_t (&v)[16]) {
   if constexpr (sizeof(IO) == 2) {
     uint4* dst = reinterpret_cast<uint4*>(out_poly) + 2 * j;
-    uint4 a, b;
-    a.x = (v[0] & 0xffffu) | (v[1] << 16);
-    a.y = (v[2] & 0xffffu) | (v[3] << 16);
-    a.z = (v[4] & 0xffffu) | (v[5] << 16);
-    a.w = (v[6] & 0xffffu) | (v[7] << 16);
-    b.x = (v[8] & 0xffffu) | (v[9] << 16);
-    b.y = (v[10] & 0xffffu) | (v[11] << 16);
-    b.z = (v[12] & 0xffffu) | (v[13] << 16);
-    b.w = (v[14] & 0xffffu) | (v[15] << 16);
+    uint4 a, b;  // PRMT packs two low halves in one ALU op
+    a.x = __byte_perm(v[0], v[1], 0x5410);
+    a.y = __byte_perm(v[2], v[3], 0x5410);
+    a.z = __byte_perm(v[4], v[5], 0x5410);
+    a.w = __byte_perm(v[6], v[7], 0x5410);
+    b.x = __byte_perm(v[8], v[9], 0x5410);
+    b.y = __byte_perm(v[10], v[11], 0x5410);
+    b.z = __byte_perm(v[12], v[13], 0x5410);
+    b.w = __byte_perm(v[14], v[15], 0x5410);
     __stcs(dst, a);
     __stcs(dst + 1, b);
   } else {
@@ -368,6 +368,30 @@ __device__ __forceinline__ void store_contiguous(IO* out_poly, int j, const uint
 template <class IO>
 __device__ __forceinline__ void store_strided(IO* out_poly, int j, const uint32_t (&v)[16],
                                               const uint32_t* S, const Xpose& X, bool valid) {
+  if constexpr (sizeof(IO) == 2) {
+    // u16 tile in natural order: 16 scalar 16-bit stores (two lanes share a word, one
+    // wavefront), then each lane reads two packed 16-byte vectors -- no pack ops, and
+    // consecutive lanes read consecutive chunks (conflict-free without a swizzle)
+    const uint32_t b = smem_addr(S);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(b + 2u * j + 32u * r), "h"(static_cast<unsigned short>(v[r]))
+                   : "memory");
+    __syncwarp();
+    if (!valid) return;
+    uint4* dst = reinterpret_cast<uint4*>(out_poly);
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      uint4 w;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                   : "r"(b + 16u * (j + 16 * kk))
+                   : "memory");
+      __stcs(dst + j + 16 * kk, w);
+    }
+    return;
+  }
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < 16; ++r) X.put(r, v[r]);
@@ -419,6 +443,21 @@ template <class IO, bool SGN>
 __device__ __forceinline__ void load_contiguous(uint32_t (&v)[16], const IO* poly, int j) {
   const uint4* src = reinterpret_cast<const uint4*>(poly) + j * (16 * int(sizeof(IO)) / 16);
   if constexpr (sizeof(IO) == 2) {
+#ifdef NTTK_U16_SCALAR_LOAD
+    // 16 scalar 16-bit loads instead of 2 vector loads + 16 unpack ops: measured slower
+    // (4-way bank conflicts on the MIO pipe outweigh the ALU saving), kept as an option
+
+    const uint32_t base = smem_addr(poly) + 32u * j;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      uint32_t x;
+      if (SGN)
+        asm volatile("ld.shared.s16 %0, [%1];" : "=r"(x) : "r"(base + 2u * r) : "memory");
+      else
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(base + 2u * r) : "memory");
+      v[r] = x;
+    }
+#else
     const uint4 a = src[0], b = src[1];
     const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
@@ -426,6 +465,7 @@ __device__ __forceinline__ void load_contiguous(uint32_t (&v)[16], const IO* pol
       v[2 * e] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] & 0xffffu));
       v[2 * e + 1] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] >> 16));
     }
+#endif
   } else {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
