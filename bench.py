@@ -284,8 +284,13 @@ def run_extras(dev):
     xd = torch.randint(0, DIL_Q, (B, 256), generator=g, device=dev, dtype=torch.int32)
     sd, od = torch.empty_like(xd), torch.empty_like(xd)
     c3 = {}
-    for name, kind in (("modified_plantard_n32", K.improved), ("montgomery_n32", K.harvey)):
+    # the paper's comparison set (Alg. 7-12): every butterfly kind at n = 32, each on its
+    # own fast kernel
+    for name, kind in (("modified_plantard_n32", K.improved), ("montgomery_n32", K.harvey),
+                       ("scott_montgomery_n32", K.scott), ("ntl_shoup_n32", K.ntl),
+                       ("signed_montgomery_n32", K.smont)):
         P3 = nttk.build_params(DIL_Q, 256, 32, [kind], exact_bound=True)
+        assert kind in P3.fast_path, name
 
         def rt():
             nttk.forward(P3, kind, xd, sd)
@@ -295,6 +300,28 @@ def run_extras(dev):
         assert torch.equal(od, xd)
         c3[name] = {"ms": ms, "polys_per_s": B / (ms / 1e3)}
     ex["config3_dilithium_roundtrip_65536"] = c3
+    # every butterfly kind at an HBM-resident batch (2^20 polys, 512 MiB / 1 GiB in + out):
+    # forward and inverse per kind, the GPU analogue of the paper's Table 2 comparison
+    kt = {}
+    for label, q, n, dt, kinds in (
+            ("kyber_u16_n16", KYBER_Q, 16, torch.int16, (K.improved, K.harvey, K.ntl, K.smont)),
+            ("dilithium_u32_n32", DIL_Q, 32, torch.int32,
+             (K.improved, K.harvey, K.scott, K.ntl, K.smont))):
+        Bk = 1 << 20
+        xk = torch.randint(0, q, (Bk, 256), generator=g, device=dev, dtype=torch.int32).to(dt)
+        sk, ok = torch.empty_like(xk), torch.empty_like(xk)
+        row = {}
+        for kind in kinds:
+            Pk = nttk.build_params(q, 256, n, [kind], exact_bound=True)
+            assert kind in Pk.fast_path, (label, kind)
+            fms = _time_ms(torch, lambda: nttk.forward(Pk, kind, xk, sk), 10)
+            ims = _time_ms(torch, lambda: nttk.inverse(Pk, kind, sk, ok), 10)
+            assert torch.equal(ok, xk), (label, kind)
+            row[kind.name] = {"fwd_ms": fms, "inv_ms": ims,
+                              "fwd_polys_per_s": Bk / (fms / 1e3), "inv_polys_per_s": Bk / (ims / 1e3)}
+        kt[label] = row
+        del xk, sk, ok
+    ex["kinds_2^20"] = kt
     # config 5: reduction sweep, 2^30 operand pairs (2^15 x 2^15 grid) per (q, variant);
     # IMAD roof = SM-cycles per mult of the variant's multiplies (IMAD 1/64, IMAD.HI and
     # IMAD.WIDE 1/32 per lane-op, measured)

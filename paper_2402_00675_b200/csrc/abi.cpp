@@ -123,7 +123,9 @@ bool use_fused_polymul(const HostParams& P, int kind, int elem, const void* a, c
     const char* k = std::getenv("NTTK_KERNEL");
     return k && std::string(k) == "v1";
   }();
-  if (v1 || !use_fast(P, kind)) return false;
+  // ntl / scott: no fused product stage (config 2 compares improved, harvey, smont); their
+  // polymul runs fwd, fwd, pointwise, inv as four kernels
+  if (v1 || !use_fast(P, kind) || kind == NTTK_NTL || kind == NTTK_SCOTT) return false;
   return nttk_b200::fast256_tma_supports(elem, a, out) && !(reinterpret_cast<uintptr_t>(b) & 15);
 }
 

@@ -265,6 +265,96 @@ struct Harvey {
   }
 };
 
+// scott_core's product at n = 32 (butterfly.hpp:172-184): (w t + q p) >> 32 with
+// q = -p^{-1} lo(w t) mod 2^32 (A.pinv); w < p, t < 2^32 keep w t + q p < 2^64 and the
+// result < 2p.  IMAD.WIDE + IMAD + IMAD.WIDE (64-bit accumulate), 10 fmaheavy cycles.
+__device__ __forceinline__ uint32_t scott_mul(uint32_t t, uint32_t w, const FastArgs& A) {
+  const uint64_t wt = static_cast<uint64_t>(w) * t;
+  const uint32_t q = static_cast<uint32_t>(wt) * A.pinv;
+  return static_cast<uint32_t>((wt + static_cast<uint64_t>(q) * A.p) >> 32);
+}
+
+// Alg. 9 (butterfly.hpp:172-184), n = 32: X' = X + Y unreduced, Y' = scott_mul(X + (N/L)p
+// - Y) in [0, 2p).  The same core runs the DIF forward (per-index twiddles) and the GS
+// merge layers (per-block), as in the reference.  Host-validated (fast_eligible): no T
+// underflows or overflows 32 bits, so every word equals the reference's uint64 word.
+struct Scott32 {
+  using Tw = uint32_t;
+  static constexpr bool kSigned = false;
+  static constexpr bool kFold = true;
+  __device__ static Tw tw(const FastArgs& A, int k) { return A.lo[k]; }
+  __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    const uint32_t t = x + A.soff - y;
+    x = x + y + A.zero;
+    y = scott_mul(t, w, A);
+  }
+  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    fwd(x, y, w, A);
+  }
+  __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
+    fwd(x, y, w, A);
+  }
+  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    inv(x, y, w, off, A);
+  }
+  // canonical v n^{-1} mod p (transform.hpp:331-335; any exact method is bit-identical)
+  __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
+    const uint32_t r = scott_mul(v, A.scale_lo, A);
+    return umin32(r, r - A.p);
+  }
+  __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t, const FastArgs& A) {
+    const uint32_t t = x + A.soff - y;
+    const uint32_t a = scott_mul(x + y + A.zero, A.scale_lo, A);
+    const uint32_t b = scott_mul(t, A.fold_lo, A);
+    x = umin32(a, a - A.p);
+    y = umin32(b, b - A.p);
+  }
+};
+
+// ntl_core's Shoup product (butterfly.hpp:60-71): q = (w' t) >> n, w' = floor(w 2^n / p);
+// w t - q p lies in [0, 2p) for every t < 2^n, then one conditional subtraction.  The
+// result is the canonical residue, so feeding t + p for X - Y mod p changes nothing.
+template <int N_BITS>
+__device__ __forceinline__ uint32_t shoup_mul(uint32_t t, uint32_t w, uint32_t wq,
+                                              const FastArgs& A) {
+  const uint32_t q = N_BITS == 16 ? (wq * t) >> 16 : __umulhi(wq, t);
+  const uint32_t r = w * t + q * A.negp;
+  return umin32(r, r - A.p);
+}
+
+// Alg. 7 (butterfly.hpp:60-71): canonical in, canonical out; DIF forward per-index,
+// GS merge per-block.  Outputs are unique residues, so these exact forms are bit-identical.
+template <int N_BITS>
+struct Ntl {
+  using Tw = uint2;  // (w, floor(w 2^n / p))
+  static constexpr bool kSigned = false;
+  static constexpr bool kFold = true;
+  __device__ static Tw tw(const FastArgs& A, int k) { return make_uint2(A.lo[k], A.hi[k]); }
+  __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    const uint32_t t = x + A.p - y;  // (0, 2p)
+    const uint32_t s = x + y + A.zero;
+    x = umin32(s, s - A.p);
+    y = shoup_mul<N_BITS>(t, w.x, w.y, A);
+  }
+  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    fwd(x, y, w, A);
+  }
+  __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
+    fwd(x, y, w, A);
+  }
+  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    inv(x, y, w, off, A);
+  }
+  __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
+    return shoup_mul<N_BITS>(v, A.scale_lo, A.scale_hi, A);
+  }
+  __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t, const FastArgs& A) {
+    const uint32_t t = x + A.p - y;
+    x = shoup_mul<N_BITS>(x + y + A.zero, A.scale_lo, A.scale_hi, A);
+    y = shoup_mul<N_BITS>(t, A.fold_lo, A.fold_hi, A);
+  }
+};
+
 // Signed Montgomery (reduction.hpp:141-165): r = (A - m p) / 2^n, m = centered
 // lo_n(A p^{-1}); A = w y with the premultiplied quotient factor (w p^{-1} mod 2^n).
 template <int N_BITS>

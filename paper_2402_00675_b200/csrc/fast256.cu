@@ -453,7 +453,8 @@ cudaError_t dispatch_io(int dir, int L, int elem, const void* in, void* out, siz
 bool fast256_supports(int kind, int layers, int n_bits) {
   if (layers != 7 && layers != 8) return false;
   if (n_bits != 16 && n_bits != 32) return false;
-  return kind == NTTK_IMPROVED || kind == NTTK_HARVEY || kind == NTTK_SMONT;
+  if (kind == NTTK_SCOTT) return n_bits == 32;
+  return kind == NTTK_IMPROVED || kind == NTTK_HARVEY || kind == NTTK_SMONT || kind == NTTK_NTL;
 }
 
 cudaError_t fast256_launch(const HostParams& P, int kind, int dir, const void* in, void* out,
@@ -481,6 +482,12 @@ cudaError_t fast256_launch(const HostParams& P, int kind, int dir, const void* i
     case NTTK_SMONT:
       return n16 ? dispatch_io<Smont<16>, false>(dir, L, elem_bytes, in, out, batch, A, st)
                  : dispatch_io<Smont<32>, false>(dir, L, elem_bytes, in, out, batch, A, st);
+    case NTTK_NTL:
+      return n16 ? dispatch_io<Ntl<16>, true>(dir, L, elem_bytes, in, out, batch, A, st)
+                 : dispatch_io<Ntl<32>, true>(dir, L, elem_bytes, in, out, batch, A, st);
+    case NTTK_SCOTT:
+      if (n16 || !cyclic) return cudaErrorInvalidValue;
+      return dispatch_io<Scott32, true>(dir, L, elem_bytes, in, out, batch, A, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -218,6 +218,12 @@ cudaError_t fast256_tma_launch(const HostParams& P, int kind, int dir, const voi
     case NTTK_SMONT:
       return n16 ? by_io<Smont<16>, false>(dir, L, elem_bytes, in, out, batch, A, st)
                  : by_io<Smont<32>, false>(dir, L, elem_bytes, in, out, batch, A, st);
+    case NTTK_NTL:
+      return n16 ? by_io<Ntl<16>, true>(dir, L, elem_bytes, in, out, batch, A, st)
+                 : by_io<Ntl<32>, true>(dir, L, elem_bytes, in, out, batch, A, st);
+    case NTTK_SCOTT:
+      if (n16 || !cyclic) return cudaErrorInvalidValue;
+      return by_io<Scott32, true>(dir, L, elem_bytes, in, out, batch, A, st);
     default: return cudaErrorInvalidValue;
   }
 }

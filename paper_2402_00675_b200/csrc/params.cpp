@@ -115,7 +115,17 @@ bool fast_eligible(const HostParams& P, int kind) {
     case NTTK_SMONT:  // signed values fit int32; Barrett constant fits 32 bits
       return (uint64_t(P.layers) + 2) * p < (uint64_t(1) << 31) &&
              (u128(1) << (P.n_bits + 10)) / p < (u128(1) << 32);
-    default: return false;  // ntl, scott: generic kernel
+    case NTTK_NTL: return 2 * p < P.ctx.beta;  // Shoup products are exact for t < 2^n
+    case NTTK_SCOTT: {
+      // n = 32 only (n = 16 is the reference's underflowing configuration, SURVEY §0 item
+      // 6; it stays on the 64-bit generic kernel).  Bit-exact on 32-bit registers when
+      // no T = X + off - Y underflows (off >= 2^{L-1} p, the largest Y) and none
+      // overflows (2^L p + off < 2^32); then w T + q p < 2^64 and Y' < 2p.
+      if (P.n_bits != 32 || !P.scott_L) return false;
+      const uint64_t off = uint64_t(P.N / P.scott_L) * p;
+      return off >= (p << (P.layers - 1)) && (p << P.layers) + off < (uint64_t(1) << 32);
+    }
+    default: return false;
   }
 }
 
@@ -176,8 +186,11 @@ void fill_fast(HostParams& P, int kind) {
         const uint64_t fm = to_plantard(wl, c) * c.mu & c.r2n_mask;
         A.fold_lo = static_cast<uint32_t>(fm);
         A.fold_hi = static_cast<uint32_t>(fm >> 32);
-      } else if (kind == NTTK_HARVEY) {
+      } else if (kind == NTTK_HARVEY || kind == NTTK_SCOTT) {
         A.fold_lo = static_cast<uint32_t>(to_mont(wl, c));
+      } else if (kind == NTTK_NTL) {
+        A.fold_lo = static_cast<uint32_t>(wl);
+        A.fold_hi = static_cast<uint32_t>((u128(wl) << P.n_bits) / p);
       }
     }
     const std::vector<uint64_t>* tab = nullptr;
@@ -202,6 +215,25 @@ void fill_fast(HostParams& P, int kind) {
         A.pinv = n16 ? static_cast<uint32_t>(c.p_inv_beta << 16)
                      : static_cast<uint32_t>(c.p_inv_beta);
         A.scale_lo = static_cast<uint32_t>(P.n_inv_mont);
+        break;
+      }
+      case NTTK_SCOTT: {  // forward: DIF per-index Montgomery twiddles; inverse: GS per-block
+        tab = dir == 0 ? &P.dif_mont : &P.gs_mont;
+        for (size_t k = 0; k < tab->size(); ++k) A.lo[k] = static_cast<uint32_t>((*tab)[k]);
+        A.pinv = static_cast<uint32_t>(c.neg_p_inv_beta);
+        A.scale_lo = static_cast<uint32_t>(P.n_inv_mont);
+        A.soff = static_cast<uint32_t>(uint64_t(P.N / P.scott_L) * P.p);
+        break;
+      }
+      case NTTK_NTL: {  // (w, floor(w 2^n / p)) pairs: dif_w/dif_wq forward, gs_w/gs_wq inverse
+        const std::vector<uint64_t>& w = dir == 0 ? P.dif_w : P.gs_plain;
+        const std::vector<uint64_t>& wq = dir == 0 ? P.dif_wq : P.gs_wq;
+        for (size_t k = 0; k < w.size(); ++k) {
+          A.lo[k] = static_cast<uint32_t>(w[k]);
+          A.hi[k] = static_cast<uint32_t>(wq[k]);
+        }
+        A.scale_lo = static_cast<uint32_t>(P.n_inv);
+        A.scale_hi = static_cast<uint32_t>((u128(P.n_inv) << P.n_bits) / p);
         break;
       }
       case NTTK_SMONT: {
@@ -476,7 +508,7 @@ int build_params(const nttk_params_desc& d, HostParams& P, std::string& err) {
   P.n_inv_mont = to_mont(P.n_inv, c);
   P.n_inv_smont = to_smont(P.n_inv, c);
 
-  for (int k : {NTTK_IMPROVED, NTTK_HARVEY, NTTK_SMONT})
+  for (int k : {NTTK_NTL, NTTK_HARVEY, NTTK_SCOTT, NTTK_IMPROVED, NTTK_SMONT})
     if (has(k) && fast_eligible(P, k)) fill_fast(P, k);
   return NTTK_OK;
 }

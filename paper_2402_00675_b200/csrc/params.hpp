@@ -47,7 +47,7 @@ struct DeviceTables {
 // operands of IMAD; lane-dependent ones are loaded once per thread at kernel start.
 struct FastArgs {
   uint32_t p = 0, two_p = 0;
-  uint32_t pinv = 0;       // harvey/smont: p^{-1} mod 2^n   (n=16: shifted left by 16)
+  uint32_t pinv = 0;       // harvey/smont: p^{-1} mod 2^n (n=16: shifted left by 16); scott: -p^{-1}
   uint32_t canon_m = 0;    // floor((2^32 - 1) / p): inverse-input canonicalisation
   uint32_t canon_m16 = 0;  // ceil(2^32 / p): exact floor(x / p) for x < 2^16
   uint32_t sgn_off = 0;    // K p >= 2^{bits-1}: lifts signed inputs to unsigned
@@ -63,6 +63,7 @@ struct FastArgs {
   uint32_t kp = 0;         // K p >= 2^16 - 1: fused first inverse layer offset (u16 input)
   uint32_t flags = 0;      // bit0: cb valid; bit1: cs valid; bit2: fused first layer valid
   uint32_t fold_lo = 0, fold_hi = 0;  // last merge twiddle times N^{-1}, kind encoding
+  uint32_t soff = 0;       // scott: butterfly offset (N/L) p (butterfly.hpp:172-184)
   uint32_t lo[256] = {};   // twiddle words in reference table order
   uint32_t hi[256] = {};   // high words of 64-bit premultiplied Plantard twiddles
 };

@@ -144,6 +144,42 @@ def test_dilithium_transforms_vs_oracle(oracle, kind, tree, layers):
         assert (from_dev(nttk.inverse(P, kind, y)) == f).all(), elem
 
 
+@pytest.mark.parametrize("p,n,kind", [(KYBER, 16, NTL), (KYBER, 32, NTL), (KYBER, 32, SCOTT),
+                                      (DILITHIUM, 32, NTL), (DILITHIUM, 32, SCOTT),
+                                      (7681, 32, SCOTT), (7681, 32, NTL)])
+def test_dif_kinds_fast_path_vs_oracle(oracle, p, n, kind):
+    """ntl (Alg. 7) and scott (Alg. 9) on the fast N=256 kernels (TMA for u16/u32, the
+    register-prefetch kernel for u64): forward words, inverse of arbitrary in-bound
+    spectra, round trips -- bit-exact with the oracle."""
+    P = engine_params(p, 256, n, [kind])
+    Q = oracle.params(p, 256, n, (kind,))
+    assert kind in P.fast_path
+    B = 291
+    f = oracle.rng(4242 + kind + n, p, B * 256).reshape(B, 256)
+    want = Q.forward(kind, f)
+    bound = p if kind == NTL else 256 * p  # spectrum_value_bound (transform.hpp:61-70)
+    elems = [e for e in (2, 4, 8) if bound <= (1 << (8 * e))]
+    for elem in elems:
+        y = nttk.forward(P, kind, to_dev(f, elem))
+        assert (from_dev(y) == want).all(), elem
+        assert (from_dev(nttk.inverse(P, kind, y)) == f).all(), elem
+    rng = np.random.default_rng(kind * 100 + n)
+    spec = rng.integers(0, bound, size=(B, 256), dtype=np.uint64)
+    want_inv = Q.inverse(kind, spec)
+    for elem in elems:
+        assert (from_dev(nttk.inverse(P, kind, to_dev(spec, elem))) == want_inv).all(), elem
+
+
+def test_scott_n16_stays_on_generic_kernel(oracle):
+    """scott at Kyber n=16 underflows uint64 in the reference; the engine
+    keeps that configuration on the 64-bit generic kernel, which replicates it word for word."""
+    P = engine_params(KYBER, 256, 16, [SCOTT])
+    assert SCOTT not in P.fast_path
+    Q = oracle.params(KYBER, 256, 16, (SCOTT,))
+    f = oracle.rng(5, KYBER, 7 * 256).reshape(7, 256)
+    assert (from_dev(nttk.forward(P, SCOTT, to_dev(f, 8))) == Q.forward(SCOTT, f)).all()
+
+
 def test_dilithium_improved_matches_reference_exact_bound(oracle, golden):
     """config 3: modified Plantard (64-bit constant) vs 32-bit Montgomery round trip."""
     B = 4096
