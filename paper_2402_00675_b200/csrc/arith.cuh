@@ -63,7 +63,14 @@ __device__ __forceinline__ uint32_t mod_cs(uint32_t x, const FastArgs& A) {
 // Opaque identity (A.zero == 0): keeps ptxas from folding the following additions into
 // the preceding IMAD.HI as an addend -- it then re-issues a second IMAD.HI for the other
 // use of the same product, doubling the most expensive instruction.  One ALU op instead.
-__device__ __forceinline__ uint32_t fence_val(uint32_t r, const FastArgs& A) { return r ^ A.zero; }
+__device__ __forceinline__ uint32_t fence_val(uint32_t r, const FastArgs& A) {
+#ifdef NTTK_NO_FENCE
+  (void)A;
+  return r;
+#else
+  return r ^ A.zero;
+#endif
+}
 // canonical residue of a two's complement 32-bit value
 __device__ __forceinline__ uint32_t mod_s32(uint32_t x, const FastArgs& A) {
   // x + 2^31 is non-negative; subtract 2^31 mod p afterwards
@@ -139,6 +146,46 @@ struct ImprovedN16 {
   __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
     x = mp_n16<true>(x + y + A.zero, A.scale_lo, A.p);
+    y = mp_n16<PAPER_FORM>(t, A.fold_lo, A.p);
+  }
+  // ---- lazy merge (inv_body_lazy, umulhi form only) ----
+  // A merge output Y' = MP(w, T) = hi32(h p) is carried as h = T w_hat mu; the consumer
+  // issues the IMAD.HI.  Lazy words only ever pair with lazy words (GS outputs at j + len
+  // meet at the next layer), so the consumer computes X = hi(h_X p) and takes the sum
+  // with Y's IMAD.HI as its addend: S = hi(h_Y p) + X, T = 2X + off - S.  Same words as
+  // inv(); per butterfly IMAD + IMAD.HI + 2 ALU ops, no fence op, no re-issued IMAD.HI.
+  static constexpr bool kLazy = !PAPER_FORM;
+  __device__ static uint32_t materialize(uint32_t h, const FastArgs& A) { return __umulhi(h, A.p); }
+  // materialised inputs -> (X + Y, lazy MP(w, X + off - Y))
+  __device__ static void inv_h(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    x = x + y + A.zero;
+    y = t * w;
+  }
+  // lazy inputs -> (X + Y, lazy MP(w, X + off - Y)).  The IMAD.HI addend is a 64-bit
+  // register pair, so a 32-bit addend costs a zeroing move; instead X comes out of a
+  // 64-bit product whose low word is w_X T_X (Prop. 4: h p = r 2^32 + w T exactly), and
+  // that pair is the addend of Y's product: hi(h_Y p + {w_X T_X, X}) = X + Y whenever
+  // w_X T_X + w_Y T_Y < 2^32 (host-validated, FastArgs flags bit 3).
+  __device__ static uint32_t sum_hh(uint32_t hx, uint32_t hy, uint32_t& X, const FastArgs& A) {
+    const uint64_t px = static_cast<uint64_t>(hx) * A.p;  // {w_X T_X, X}
+    uint32_t xh = static_cast<uint32_t>(px >> 32);
+    asm("mov.b32 %0, %0;" : "+r"(xh));  // opaque: keeps 2X from becoming a funnel shift
+    X = xh;
+    return static_cast<uint32_t>((static_cast<uint64_t>(hy) * A.p + px) >> 32);
+  }
+  __device__ static void inv_hh(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    uint32_t X;
+    const uint32_t S = sum_hh(x, y, X, A);
+    const uint32_t t = X + X + off - S + A.zero;
+    x = S;
+    y = t * w;
+  }
+  __device__ static void inv_last_hh(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
+    uint32_t X;
+    const uint32_t S = sum_hh(x, y, X, A);
+    const uint32_t t = X + X + off - S + A.zero;
+    x = mp_n16<true>(S, A.scale_lo, A.p);
     y = mp_n16<PAPER_FORM>(t, A.fold_lo, A.p);
   }
   // product stage (fused polymul): x -> (x (-2^{2n}) mod p) mu, then MP(.., y) = x y mod p

@@ -68,8 +68,9 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
 }
 
 // ---------------------------------------------------------------------------
-// MODE 0: generic canonicalisation; 1: host-validated fast canonicalisation (A.flags
-// bits 0/1); 2: u16 input with the fused first merge layer (A.flags bit 2, improved n=16).
+// MODE bits 0-1 -- 0: generic canonicalisation; 1: host-validated fast canonicalisation
+// (A.flags bits 0/1); 2: u16 input with the fused first merge layer (A.flags bit 2,
+// improved n=16).  MODE bit 2: lazy merge outputs (A.flags bit 3, improved n=16).
 template <class K, class IO, int L, int MODE>
 __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     inv256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
@@ -103,11 +104,12 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     load_contiguous<IO, K::kSigned>(
         v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
     release_stage(&empty[s], lane);
-    if (MODE != 2) {
+    constexpr int CM = MODE & 3;
+    if (CM != 2) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, MODE == 1>(v[r], A);
+      for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
     }
-    inv_body<K, L, MODE == 2>(v, twl, A, X);
+    inv_body<K, L, CM == 2, (MODE & 4) != 0>(v, twl, A, X);
     store_strided<IO>(out + poly * 256, j, v, S, X, poly < batch);
   }
 }
@@ -144,30 +146,33 @@ cudaError_t fwd_launch(const void* in, void* out, size_t batch, const FastArgs& 
   return cudaGetLastError();
 }
 
-template <class K, class IO, int L>
-cudaError_t inv_launch(const void* in, void* out, size_t batch, const FastArgs& A, cudaStream_t st) {
+template <class K, class IO, int L, int MODE>
+cudaError_t inv_launch_mode(const void* in, void* out, size_t batch, const FastArgs& A,
+                            cudaStream_t st) {
+  static int occ = 0;
+  auto kern = inv256_tma_kernel<K, IO, L, MODE>;
+  const int blocks = grid_for(kern, Geo<IO>::kSmem, occ, batch);
+  kern<<<blocks, kThreads, Geo<IO>::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out),
+                                                 batch, A);
+  return cudaGetLastError();
+}
+
+template <class K, class IO, int L, int LZ>
+cudaError_t inv_launch_canon(const void* in, void* out, size_t batch, const FastArgs& A,
+                             cudaStream_t st) {
   constexpr bool kCanFuse = sizeof(IO) == 2 && std::is_same<K, ImprovedN16<false>>::value;
   const unsigned fast_bit = sizeof(IO) == 2 ? 1u : 2u;
-  if (kCanFuse && (A.flags & 4)) {
-    static int occ = 0;
-    auto kern = inv256_tma_kernel<K, IO, L, kCanFuse ? 2 : 1>;
-    const int blocks = grid_for(kern, Geo<IO>::kSmem, occ, batch);
-    kern<<<blocks, kThreads, Geo<IO>::kSmem, st>>>(static_cast<const IO*>(in),
-                                                   static_cast<IO*>(out), batch, A);
-  } else if (!K::kSigned && (A.flags & fast_bit)) {
-    static int occ = 0;
-    auto kern = inv256_tma_kernel<K, IO, L, 1>;
-    const int blocks = grid_for(kern, Geo<IO>::kSmem, occ, batch);
-    kern<<<blocks, kThreads, Geo<IO>::kSmem, st>>>(static_cast<const IO*>(in),
-                                                   static_cast<IO*>(out), batch, A);
-  } else {
-    static int occ = 0;
-    auto kern = inv256_tma_kernel<K, IO, L, 0>;
-    const int blocks = grid_for(kern, Geo<IO>::kSmem, occ, batch);
-    kern<<<blocks, kThreads, Geo<IO>::kSmem, st>>>(static_cast<const IO*>(in),
-                                                   static_cast<IO*>(out), batch, A);
+  if (kCanFuse && (A.flags & 4)) return inv_launch_mode<K, IO, L, (kCanFuse ? 2 : 1) | LZ>(in, out, batch, A, st);
+  if (!K::kSigned && (A.flags & fast_bit)) return inv_launch_mode<K, IO, L, 1 | LZ>(in, out, batch, A, st);
+  return inv_launch_mode<K, IO, L, 0 | LZ>(in, out, batch, A, st);
+}
+
+template <class K, class IO, int L>
+cudaError_t inv_launch(const void* in, void* out, size_t batch, const FastArgs& A, cudaStream_t st) {
+  if constexpr (lazy_of<K>::value) {
+    if (A.flags & 8) return inv_launch_canon<K, IO, L, 4>(in, out, batch, A, st);
   }
-  return cudaGetLastError();
+  return inv_launch_canon<K, IO, L, 0>(in, out, batch, A, st);
 }
 
 template <class K, class IO, bool PER_INDEX>

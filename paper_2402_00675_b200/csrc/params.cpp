@@ -179,6 +179,14 @@ void fill_fast(HostParams& P, int kind) {
         A.flags |= 4;
       }
     }
+    // lazy merge outputs (ImprovedN16::sum_hh): the two Plantard products w T of a lazy
+    // pair must sum below 2^32.  Merge depth m has T < 2^m p (T < 2^16 + kp at depth 1
+    // when fused); lazily consumed products come from depths 1..L-1.
+    if (kind == NTTK_IMPROVED && n16) {
+      u128 tmax = u128(p) << (P.layers - 1);
+      if (A.flags & 4) tmax = std::max<u128>(tmax, (uint64_t(1) << 16) - 1 + A.kp);
+      if (2 * u128(p - 1) * tmax < (u128(1) << 32)) A.flags |= 8;
+    }
     // last merge twiddle times N^{-1} (the final scaling folded into the last layer)
     {
       const uint64_t wl = static_cast<uint64_t>(u128(P.gs_plain.back()) * P.n_inv % p);

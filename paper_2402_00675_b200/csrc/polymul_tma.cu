@@ -66,7 +66,7 @@ __device__ __forceinline__ void produce2(const IO* a, const IO* b, size_t batch,
   }
 }
 
-template <class K, class IO, int L, bool PER_INDEX>
+template <class K, class IO, int L, bool PER_INDEX, bool LAZY>
 __global__ void __launch_bounds__(kThreads)
     polymul256_tma_kernel(const IO* __restrict__ a, const IO* __restrict__ b, IO* __restrict__ out,
                           size_t batch, const __grid_constant__ PolymulArgs PA) {
@@ -128,18 +128,18 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int r = 0; r < 16; ++r) va[r] = K::mulc(vb[r], K::enc(va[r], PA.prod, AF), AF);
     }
-    inv_body<K, L, false>(va, twi, AI, X);
+    inv_body<K, L, false, LAZY>(va, twi, AI, X);
     store_strided<IO>(out + poly * 256, j, va, S, X, poly < batch);
   }
 }
 
 int g_sms2 = 0;
 
-template <class K, class IO, int L, bool PER_INDEX>
-cudaError_t launch(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
-                   cudaStream_t st) {
+template <class K, class IO, int L, bool PER_INDEX, bool LAZY>
+cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
+                      cudaStream_t st) {
   static int occ = 0;
-  auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX>;
+  auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY>;
   constexpr int smem = Geo2<IO>::kSmem;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -159,6 +159,15 @@ cudaError_t launch(const void* a, const void* b, void* out, size_t batch, const 
   kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(a), static_cast<const IO*>(b),
                                       static_cast<IO*>(out), batch, PA);
   return cudaGetLastError();
+}
+
+template <class K, class IO, int L, bool PER_INDEX>
+cudaError_t launch(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
+                   cudaStream_t st) {
+  if constexpr (lazy_of<K>::value) {
+    if (PA.inv.flags & 8) return launch_lz<K, IO, L, PER_INDEX, true>(a, b, out, batch, PA, st);
+  }
+  return launch_lz<K, IO, L, PER_INDEX, false>(a, b, out, batch, PA, st);
 }
 
 template <class K, bool PER_INDEX>

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "arith.cuh"
 
@@ -286,14 +287,92 @@ __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const typename K::Tw
   }
 }
 
+template <class K, class = void>
+struct lazy_of {
+  static constexpr bool value = false;
+};
+template <class K>
+struct lazy_of<K, std::void_t<decltype(K::kLazy)>> {
+  static constexpr bool value = K::kLazy;
+};
+
+// inv_body with lazy merge outputs (policy kLazy, see ImprovedN16::inv_hh): after a merge
+// layer of half-span h the words at (r & h) hold pre-quotient h-values; the next layer
+// (span 2h) pairs them with each other, so "both inputs lazy" is the compile-time test
+// r & (h_prev).  Lazy words are materialised before the transpose.
+template <class K, int L, bool FUSE>
+__device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
+                                              const FastArgs& A, const Xpose& X) {
+  using Tw = typename K::Tw;
+  constexpr int TL = 1 << L;
+#pragma unroll
+  for (int sl = 8; sl >= 5; --sl) {  // phase 1: merge layers s = L..5
+    if (sl > L) continue;
+    const int h = 1 << (8 - sl);
+    const uint32_t off = A.off[L - sl + 1];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      const int base = sl == 5 ? 0 : sl == 6 ? 1 : sl == 7 ? 3 : 7;
+      const Tw w = twl[base + (r >> (9 - sl))];
+      if (sl == L) {  // first merge layer: materialised (raw u16 if FUSE) inputs
+        const uint32_t x = v[r], y = v[r + h];
+        if constexpr (FUSE) {
+          v[r] = mod_cb(x + y + A.zero, A);
+          v[r + h] = (x + A.kp - y) * w;
+        } else {
+          K::inv_h(v[r], v[r + h], w, off, A);
+        }
+      } else if (r & (h >> 1)) {
+        K::inv_hh(v[r], v[r + h], w, off, A);
+      } else {
+        K::inv_h(v[r], v[r + h], w, off, A);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    if (r & 8) v[r] = K::materialize(v[r], A);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = X.get(r);
+#pragma unroll
+  for (int sl = 4; sl >= 1; --sl) {  // phase 2: merge layers s = 4..1, materialised start
+    const int h = 1 << (4 - sl);
+    const uint32_t off = A.off[L - sl + 1];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      const bool lazy = sl < 4 && (r & (h >> 1));
+      if (sl == 1) {  // N^{-1} folded into the last merge layer
+        if (lazy) K::inv_last_hh(v[r], v[r + h], off, A);
+        else K::inv_last(v[r], v[r + h], off, A);
+      } else {
+        const Tw w = K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl)));
+        if (lazy) K::inv_hh(v[r], v[r + h], w, off, A);
+        else K::inv_h(v[r], v[r + h], w, off, A);
+      }
+    }
+  }
+}
+
 // run_merge_layers + final N^{-1} (transform.hpp:99-116, 323-335): contiguous in
 // (canonical unless FUSE) -> strided out (canonical).  FUSE: u16 raw input, fused first
 // merge layer (A.flags bit 2, improved n = 16 only).
-template <class K, int L, bool FUSE>
+// LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3).
+template <class K, int L, bool FUSE, bool LAZY = false>
 __device__ __forceinline__ void inv_body(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
                                          const FastArgs& A, const Xpose& X) {
   using Tw = typename K::Tw;
   constexpr int TL = 1 << L;
+  if constexpr (LAZY) {
+    static_assert(lazy_of<K>::value, "policy has no lazy merge");
+    inv_body_lazy<K, L, FUSE>(v, twl, A, X);
+    return;
+  }
 #pragma unroll
   for (int sl = 8; sl >= 5; --sl) {  // phase 1: merge layers s = L..5
     if (sl > L) continue;

@@ -7,12 +7,15 @@ one loop iteration of a fast256 consumer warp transforms 2 polynomials, i.e. 64
 butterflies per thread (8 layers x 8) or 56 (7 layers).  The fmaheavy estimate uses the
 measured issue costs (profiles/r01_imad_microbench.txt): IMAD 2 cycles, IMAD.HI /
 IMAD.WIDE 4 cycles per warp instruction on one SM sub-partition.
-Usage: python tools/sass_census.py [lib.so] [name-regex]
+Usage: python tools/sass_census.py [lib.so] [name-regex] [--ops]   (--ops: opcode breakdown)
 """
 import re
 import subprocess
 import sys
 from collections import Counter
+
+OPS = "--ops" in sys.argv
+sys.argv = [a for a in sys.argv if a != "--ops"]
 
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2402_00675_b200/libnttk_gpu.so"
 pat = re.compile(sys.argv[2] if len(sys.argv) > 2 else r"tma_kernel.*(ImprovedN16ILb0EEEtLi8|ImprovedN32EjLi8|HarveyILi16ELb0EEEtLi8|HarveyILi32ELb0EEEjLi8|SmontILi16EEtLi8|SmontILi32EEjLi8)")
@@ -53,3 +56,5 @@ for part in re.split(r"\n\s+Function : ", txt)[1:]:
     short = re.sub(r"_ZN9nttk_b200\w*?_GLOBAL__N__\w+?\d+(fwd|inv)", r"\1", name)[:70]
     print(f"{short:70s} {n:5d} {imad:5d} {hi:4d} {wide:5d} {iadd:5d} {alu:4d} {lsu:4d} "
           f"{fcyc:12d} {fcyc / bfly:8.2f}")
+    if OPS:
+        print("    " + "  ".join(f"{k}:{v}" for k, v in c.most_common()))
