@@ -127,6 +127,13 @@ struct ImprovedN16 {
     y = x + A.p - r;
     x = x + r + A.zero;
   }
+  // twiddle w = omega^0 = 1: MP(w_hat, Y) is the canonical residue of Y, so r = Y for a
+  // canonical Y (layer 1) and r = min(Y, Y - p) for Y < 2p (layer 2) -- no multiply
+  __device__ static void fwd_w1(uint32_t& x, uint32_t& y, bool reduce, const FastArgs& A) {
+    const uint32_t r = reduce ? umin32(y, y - A.p) : y;
+    y = x + A.p - r;
+    x = x + r + A.zero;
+  }
   // Alg. 12 (butterfly.hpp:235-243)
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
@@ -211,6 +218,11 @@ struct ImprovedN32 {
   }
   __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
     fwd(x, y, w, A);
+  }
+  __device__ static void fwd_w1(uint32_t& x, uint32_t& y, bool reduce, const FastArgs& A) {
+    const uint32_t r = reduce ? umin32(y, y - A.p) : y;  // see ImprovedN16::fwd_w1
+    y = x + A.p - r;
+    x = x + r + A.zero;
   }
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;

@@ -30,7 +30,7 @@ namespace {
 using namespace tma;
 
 // ---------------------------------------------------------------------------
-template <class K, class IO, int L, bool PER_INDEX>
+template <class K, class IO, int L, bool PER_INDEX, bool W1>
 __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     load_strided<IO, K::kSigned>(
         v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
     release_stage(&empty[s], lane);
-    fwd_body<K, L, PER_INDEX>(v, twl, A, X);
+    fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
     if (poly < batch) store_contiguous<IO>(out + poly * 256, j, v);
   }
 }
@@ -136,14 +136,23 @@ int grid_for(Kern kern, int smem, int& occ, size_t batch) {
   return static_cast<int>(tiles < full ? tiles : full);
 }
 
-template <class K, class IO, int L, bool PER_INDEX>
-cudaError_t fwd_launch(const void* in, void* out, size_t batch, const FastArgs& A, cudaStream_t st) {
+template <class K, class IO, int L, bool PER_INDEX, bool W1>
+cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs& A,
+                         cudaStream_t st) {
   static int occ = 0;
-  auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX>;
+  auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1>;
   const int blocks = grid_for(kern, Geo<IO>::kSmem, occ, batch);
   kern<<<blocks, kThreads, Geo<IO>::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out),
                                                  batch, A);
   return cudaGetLastError();
+}
+
+template <class K, class IO, int L, bool PER_INDEX>
+cudaError_t fwd_launch(const void* in, void* out, size_t batch, const FastArgs& A, cudaStream_t st) {
+  if constexpr (w1_of<K>::value && !PER_INDEX) {
+    if (A.flags & 16) return fwd_launch_w<K, IO, L, PER_INDEX, true>(in, out, batch, A, st);
+  }
+  return fwd_launch_w<K, IO, L, PER_INDEX, false>(in, out, batch, A, st);
 }
 
 template <class K, class IO, int L, int MODE>

@@ -187,6 +187,11 @@ void fill_fast(HostParams& P, int kind) {
       if (A.flags & 4) tmax = std::max<u128>(tmax, (uint64_t(1) << 16) - 1 + A.kp);
       if (2 * u128(p - 1) * tmax < (u128(1) << 32)) A.flags |= 8;
     }
+    // forward block 0 of layers 1 and 2 has twiddle 1 (cyclic tree): multiply-free
+    // Plantard products (fwd_body W1)
+    if (kind == NTTK_IMPROVED && dir == 0 && P.ct_plain.size() >= 3 && P.ct_plain[0] == 1 &&
+        P.ct_plain[1] == 1)
+      A.flags |= 16;
     // last merge twiddle times N^{-1} (the final scaling folded into the last layer)
     {
       const uint64_t wl = static_cast<uint64_t>(u128(P.gs_plain.back()) * P.n_inv % p);

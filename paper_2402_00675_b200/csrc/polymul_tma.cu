@@ -66,7 +66,7 @@ __device__ __forceinline__ void produce2(const IO* a, const IO* b, size_t batch,
   }
 }
 
-template <class K, class IO, int L, bool PER_INDEX, bool LAZY>
+template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
 __global__ void __launch_bounds__(kThreads)
     polymul256_tma_kernel(const IO* __restrict__ a, const IO* __restrict__ b, IO* __restrict__ out,
                           size_t batch, const __grid_constant__ PolymulArgs PA) {
@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(kThreads)
     load_strided<IO, K::kSigned>(va, reinterpret_cast<const IO*>(base + G::poly_offset(warp, half, 0)), j);
     load_strided<IO, K::kSigned>(vb, reinterpret_cast<const IO*>(base + G::poly_offset(warp, half, 1)), j);
     release_stage(&empty[s], lane);
-    fwd_body<K, L, PER_INDEX>(va, twf, AF, X);
-    fwd_body<K, L, PER_INDEX>(vb, twf, AF, X);
+    fwd_body<K, L, PER_INDEX, W1>(va, twf, AF, X);
+    fwd_body<K, L, PER_INDEX, W1>(vb, twf, AF, X);
     // product stage (contiguous ownership, canonical results in va)
     if (PA.prod.basemul) {
 #pragma unroll
@@ -135,11 +135,11 @@ __global__ void __launch_bounds__(kThreads)
 
 int g_sms2 = 0;
 
-template <class K, class IO, int L, bool PER_INDEX, bool LAZY>
+template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
 cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
                       cudaStream_t st) {
   static int occ = 0;
-  auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY>;
+  auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY, W1>;
   constexpr int smem = Geo2<IO>::kSmem;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -164,10 +164,18 @@ cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, con
 template <class K, class IO, int L, bool PER_INDEX>
 cudaError_t launch(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
                    cudaStream_t st) {
-  if constexpr (lazy_of<K>::value) {
-    if (PA.inv.flags & 8) return launch_lz<K, IO, L, PER_INDEX, true>(a, b, out, batch, PA, st);
+  if constexpr (w1_of<K>::value && !PER_INDEX) {
+    if (PA.fwd.flags & 16) {
+      if constexpr (lazy_of<K>::value) {
+        if (PA.inv.flags & 8) return launch_lz<K, IO, L, PER_INDEX, true, true>(a, b, out, batch, PA, st);
+      }
+      return launch_lz<K, IO, L, PER_INDEX, false, true>(a, b, out, batch, PA, st);
+    }
   }
-  return launch_lz<K, IO, L, PER_INDEX, false>(a, b, out, batch, PA, st);
+  if constexpr (lazy_of<K>::value) {
+    if (PA.inv.flags & 8) return launch_lz<K, IO, L, PER_INDEX, true, false>(a, b, out, batch, PA, st);
+  }
+  return launch_lz<K, IO, L, PER_INDEX, false, false>(a, b, out, batch, PA, st);
 }
 
 template <class K, bool PER_INDEX>

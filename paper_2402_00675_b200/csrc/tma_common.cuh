@@ -151,7 +151,8 @@ __device__ __forceinline__ uint32_t canon(uint32_t x, const FastArgs& A) {
 }
 
 #ifndef NTTK_ALT_MASK
-#define NTTK_ALT_MASK 0x22  // forward layers (bit s) using the alternative Plantard form
+#define NTTK_ALT_MASK 0x0  // forward layers (bit s) using the alternative Plantard form
+// (measured: 0x22 balanced FMA/ALU at 378/358 cycles and ran 6% slower than 0x0 at 410/294)
 #endif
 #ifndef NTTK_INV_ALT_MASK
 #define NTTK_INV_ALT_MASK 0x0  // inverse merge layers (bit s) using the alternative form
@@ -239,8 +240,11 @@ __device__ __forceinline__ void inv_twiddles(typename K::Tw (&twl)[15], const Fa
   }
 }
 
-// run_split_layers (transform.hpp:77-96): strided in -> contiguous out
-template <class K, int L, bool PER_INDEX>
+// run_split_layers (transform.hpp:77-96): strided in -> contiguous out.
+// W1 (A.flags bit 4, improved kinds on the cyclic tree): block 0 of layers 1 and 2 has
+// twiddle omega^0 = 1 and canonical-or-< 2p inputs, so its Plantard product needs no
+// multiply (fwd_w1); input coefficients must be canonical (the ntt_forward contract).
+template <class K, int L, bool PER_INDEX, bool W1 = false>
 __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
                                          const FastArgs& A, const Xpose& X) {
   using Tw = typename K::Tw;
@@ -250,6 +254,12 @@ __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const typename K::Tw
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
+      if constexpr (W1 && !PER_INDEX) {
+        if (sl <= 2 && (r >> (5 - sl)) == 0) {
+          K::fwd_w1(v[r], v[r + h], sl == 2, A);
+          continue;
+        }
+      }
       Tw w;
       if (PER_INDEX) {
         const int base = sl == 1 ? 0 : sl == 2 ? 8 : sl == 3 ? 12 : 14;
@@ -294,6 +304,15 @@ struct lazy_of {
 template <class K>
 struct lazy_of<K, std::void_t<decltype(K::kLazy)>> {
   static constexpr bool value = K::kLazy;
+};
+
+template <class K, class = void>
+struct w1_of {
+  static constexpr bool value = false;
+};
+template <class K>
+struct w1_of<K, std::void_t<decltype(&K::fwd_w1)>> {
+  static constexpr bool value = true;
 };
 
 // inv_body with lazy merge outputs (policy kLazy, see ImprovedN16::inv_hh): after a merge
