@@ -31,7 +31,7 @@ using namespace tma;
 
 // ---------------------------------------------------------------------------
 template <class K, class IO, int L, bool PER_INDEX, bool W1>
-__global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
+__global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
   using G = Geo<IO>;

@@ -159,9 +159,14 @@ __device__ __forceinline__ uint32_t canon(uint32_t x, const FastArgs& A) {
 #endif
 
 // Minimum CTAs per SM for the register allocator (shared memory admits 4 for u16 and 3
-// for u32 stages).  Measured: capping the n=32 kernels to 3 CTAs (72 regs) is ~2% slower.
+// for u32 stages).  Measured on B200 (round 2): capping the u32 forward to 3 CTAs (72
+// regs, was 2 CTAs at 92) is 3.5% faster; the same cap on the u32 inverse is 1.7% slower
+// and capping the u16 kernels to 4 CTAs (56 regs) is 2-6% slower.
 #ifndef NTTK_MINB
 #define NTTK_MINB(IO) 1
+#endif
+#ifndef NTTK_FWD_MINB
+#define NTTK_FWD_MINB(IO) (sizeof(IO) == 4 ? 3 : 1)
 #endif
 
 template <class K, class Tw>
@@ -381,17 +386,11 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const typename 
 // run_merge_layers + final N^{-1} (transform.hpp:99-116, 323-335): contiguous in
 // (canonical unless FUSE) -> strided out (canonical).  FUSE: u16 raw input, fused first
 // merge layer (A.flags bit 2, improved n = 16 only).
-// LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3).
-template <class K, int L, bool FUSE, bool LAZY = false>
-__device__ __forceinline__ void inv_body(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
-                                         const FastArgs& A, const Xpose& X) {
+template <class K, int L, bool FUSE>
+__device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
+                                               const FastArgs& A, const Xpose& X) {
   using Tw = typename K::Tw;
   constexpr int TL = 1 << L;
-  if constexpr (LAZY) {
-    static_assert(lazy_of<K>::value, "policy has no lazy merge");
-    inv_body_lazy<K, L, FUSE>(v, twl, A, X);
-    return;
-  }
 #pragma unroll
   for (int sl = 8; sl >= 5; --sl) {  // phase 1: merge layers s = L..5
     if (sl > L) continue;
@@ -435,6 +434,18 @@ __device__ __forceinline__ void inv_body(uint32_t (&v)[16], const typename K::Tw
   if (!K::kFold) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = K::scale(v[r], A);
+  }
+}
+
+// LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3).
+template <class K, int L, bool FUSE, bool LAZY = false>
+__device__ __forceinline__ void inv_body(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
+                                         const FastArgs& A, const Xpose& X) {
+  if constexpr (LAZY) {
+    static_assert(lazy_of<K>::value, "policy has no lazy merge");
+    inv_body_lazy<K, L, FUSE>(v, twl, A, X);
+  } else {
+    inv_body_eager<K, L, FUSE>(v, twl, A, X);
   }
 }
 
