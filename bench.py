@@ -322,6 +322,25 @@ def run_extras(dev):
         kt[label] = row
         del xk, sk, ok
     ex["kinds_2^20"] = kt
+    # the paper's Table 2 parameter sets (params.hpp:273-306 presets, n = 32, u32 storage):
+    # every kind, forward and inverse, 2^16 polys
+    t2 = {}
+    for name in ("kyber256", "newhope512", "newhope1024"):
+        Pp = nttk.preset(name)
+        Np, qp = Pp.size, Pp.p
+        Bp = 1 << 16
+        xp = torch.randint(0, qp, (Bp, Np), generator=g, device=dev, dtype=torch.int32)
+        sp, op = torch.empty_like(xp), torch.empty_like(xp)
+        row = {}
+        for kind in (K.ntl, K.harvey, K.scott, K.improved):
+            fms = _time_ms(torch, lambda: nttk.forward(Pp, kind, xp, sp), 10)
+            ims = _time_ms(torch, lambda: nttk.inverse(Pp, kind, sp, op), 10)
+            assert torch.equal(op, xp), (name, kind)
+            row[kind.name] = {"fwd_ns_per_poly": fms * 1e6 / Bp, "inv_ns_per_poly": ims * 1e6 / Bp,
+                              "fast_path": kind in Pp.fast_path}
+        t2[name] = row
+        del xp, sp, op
+    ex["table2_presets_2^16"] = t2
     # config 5: reduction sweep, 2^30 operand pairs (2^15 x 2^15 grid) per (q, variant);
     # IMAD roof = SM-cycles per mult of the variant's multiplies (IMAD 1/64, IMAD.HI and
     # IMAD.WIDE 1/32 per lane-op, measured)

@@ -19,6 +19,7 @@
 
 #include "../../include/nttk_gpu.h"
 #include "fast256.hpp"
+#include "fastn.hpp"
 #include "generic.hpp"
 #include "params.hpp"
 #include "sweep.hpp"
@@ -112,7 +113,9 @@ int check_canonical_storage(const HostParams& P, int elem, const char* who) {
 }
 
 bool use_fast(const HostParams& P, int kind) {
-  return ((P.fast_mask >> kind) & 1u) && nttk_b200::fast256_supports(kind, P.layers, P.n_bits);
+  if (!((P.fast_mask >> kind) & 1u)) return false;
+  if (P.N != 256) return true;  // fastn_tma.cu (N = 512 / 1024, full trees; fast_eligible)
+  return nttk_b200::fast256_supports(kind, P.layers, P.n_bits);
 }
 
 // one fused kernel for fwd(a), fwd(b), product, inverse (polymul_tma.cu); NTTK_KERNEL=v1
@@ -125,7 +128,7 @@ bool use_fused_polymul(const HostParams& P, int kind, int elem, const void* a, c
   }();
   // ntl / scott: no fused product stage (config 2 compares improved, harvey, smont); their
   // polymul runs fwd, fwd, pointwise, inv as four kernels
-  if (v1 || !use_fast(P, kind) || kind == NTTK_NTL || kind == NTTK_SCOTT) return false;
+  if (v1 || P.N != 256 || !use_fast(P, kind) || kind == NTTK_NTL || kind == NTTK_SCOTT) return false;
   return nttk_b200::fast256_tma_supports(elem, a, out) && !(reinterpret_cast<uintptr_t>(b) & 15);
 }
 
@@ -139,7 +142,13 @@ int current_device() {
 int run_transform(const HostParams& P, int kind, int dir, const void* in, void* out, size_t batch,
                   int elem, cudaStream_t st) {
   cudaError_t e;
-  if (use_fast(P, kind)) {
+  if (P.N != 256 && use_fast(P, kind) && nttk_b200::fastn_supports(P, elem, in, out)) {
+    std::string err;
+    const uint32_t* tab = P.fastn_table(current_device(), kind, dir, err);
+    if (!tab) return fail(NTTK_CUDA, err);
+    e = nttk_b200::fastn_launch(P, kind, dir, in, out, batch, elem, tab, st);
+    g_launches += batch ? 1 : 0;
+  } else if (P.N == 256 && use_fast(P, kind)) {
     // NTTK_KERNEL=v1 selects the register-prefetch kernels (A/B comparisons)
     static const bool v1 = [] {
       const char* k = std::getenv("NTTK_KERNEL");

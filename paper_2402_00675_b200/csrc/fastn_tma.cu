@@ -1,0 +1,506 @@
+// fastn_tma.cu -- TMA-fed batched NTT for N = 512 and N = 1024 (the paper's Table 2
+// parameter sets: newhope/falcon/remblem 512, newhope/falcon/hila5 1024, params.hpp:273-306).
+//
+// Same pipeline as fast256_tma.cu (one producer warp streaming tiles with cp.async.bulk on
+// an mbarrier ring, 8 consumer warps) and the same butterfly policies (arith.cuh), scaled
+// to 32 coefficients per lane: G = N / 32 lanes own a polynomial (a half-warp at N = 512,
+// a warp at N = 1024), so 5 layers are register-local per phase:
+//   strided ownership     v[k] = a[j + G k]    (index bits LOGN-1..LOGN-5 in k)
+//   contiguous ownership  v[k] = a[32 j + k]   (index bits 4..0 in k)
+// Forward: layers 1..5 strided, one XOR-swizzled transpose, layers 6..LOGN contiguous.
+// Inverse: merge layers LOGN..6 contiguous, transpose, 5..1 strided (N^{-1} folded into
+// the last layer), natural-order coalesced stores through the same tile.
+// Twiddles: the warp-uniform ones are constant-bank operands (FastArgs, compact order
+// written by params.cpp fill_fast); the lane-dependent ones come from a shared-memory copy
+// of the whole direction table (HostParams::fastn_table).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "arith.cuh"
+#include "fastn.hpp"
+#include "tma_common.cuh"
+
+namespace nttk_b200 {
+namespace {
+
+using namespace tma;
+
+template <int LOGN, class IO>
+struct GeoN {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int G = N / 32;                  // lanes per polynomial
+  static constexpr int PPW = 32 / G;                // polynomials per warp (2 or 1)
+  static constexpr int kTileN = kConsumers * PPW;   // polynomials per stage
+  static constexpr int kPolyBytes = N * int(sizeof(IO));
+  static constexpr int kHalfBytes = kConsumers * kPolyBytes;
+  static constexpr int kPad = PPW == 2 ? 64 : 0;    // second half-warp: disjoint bank half
+  static constexpr int kStages = sizeof(IO) == 2 ? 3 : 2;
+  static constexpr int kStageBytes = (PPW * kHalfBytes + kPad + 127) / 128 * 128;
+  static constexpr int kRegionWords = N + (PPW == 2 ? 16 : 0);  // transpose tile per poly
+  static constexpr int kScratchWords = PPW * kRegionWords;       // per warp
+  static constexpr int kSmem = kStages * kStageBytes + kConsumers * kScratchWords * 4 +
+                               N * 8 /* twiddle table */ + 2 * kStages * 8;
+  __device__ static constexpr int poly_offset(int w, int h) {
+    return h * (kHalfBytes + kPad) + w * kPolyBytes;
+  }
+};
+
+// Transpose tile of one polynomial: 32-word rows, 16-byte chunk c of row r stored at chunk
+// c ^ (r & 7).  Strided puts/gets (lane j, register k, element j + G k) and contiguous
+// 128-bit gets/puts (lane j, row j) are both bank-conflict-free; the two polynomials of
+// a half-warp pair sit 16 words apart.  Addresses are hoisted 32-bit shared-window words.
+template <int G>
+struct XposeN {
+  uint32_t sp[8], cp[8], base;
+  __device__ __forceinline__ void init(const uint32_t* tile, int j) {
+    base = smem_addr(tile);
+    // strided element i = j + G k: row = (G k + j) >> 5, column = (G k + j) & 31
+    // G = 32: row k, col j -> chunk (j >> 2) ^ (k & 7)
+    // G = 16: row k >> 1, col j + 16 (k & 1) -> chunk (j >> 2) ^ ((k >> 1) & 7) ^ 4 (k & 1)
+#pragma unroll
+    for (int m = 0; m < 8; ++m) sp[m] = base + 4u * ((uint32_t((j >> 2) ^ m) << 2) | uint32_t(j & 3));
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cp[c] = base + 4u * (32u * j + (uint32_t(c ^ (j & 7)) << 2));
+  }
+  __device__ __forceinline__ uint32_t saddr(int k) const {
+    if constexpr (G == 32) return sp[k & 7] + 128u * k;
+    else return sp[((k >> 1) & 7) ^ (4 * (k & 1))] + 128u * (k >> 1);
+  }
+  __device__ __forceinline__ void put(int k, uint32_t v) const {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(saddr(k)), "r"(v) : "memory");
+  }
+  __device__ __forceinline__ uint32_t get(int k) const {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr(k)) : "memory");
+    return v;
+  }
+  __device__ __forceinline__ void put4(int c, uint32_t a, uint32_t b, uint32_t d, uint32_t e) const {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(cp[c]), "r"(a), "r"(b), "r"(d),
+                 "r"(e)
+                 : "memory");
+  }
+  __device__ __forceinline__ void get4(int c, uint32_t& a, uint32_t& b, uint32_t& d, uint32_t& e) const {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(d), "=r"(e)
+                 : "r"(cp[c])
+                 : "memory");
+  }
+  // chunk q (natural order: elements 4q..4q+3) of the tile
+  __device__ __forceinline__ uint4 chunk(int q) const {
+    const int row = q >> 3, c = q & 7;
+    uint4 w;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                 : "r"(base + 128u * row + 16u * uint32_t(c ^ (row & 7)))
+                 : "memory");
+    return w;
+  }
+};
+
+template <class Tw>
+__device__ __forceinline__ Tw mk_tw(uint2 e) {
+  if constexpr (std::is_same<Tw, uint32_t>::value) return e.x;
+  else return e;
+}
+
+template <class Tw>
+__device__ __forceinline__ Tw tw_smem(const uint2* tws, int idx) {
+  return mk_tw<Tw>(tws[idx]);
+}
+
+template <int LOGN, class IO>
+__device__ __forceinline__ void produce_n(const IO* in, size_t batch, uint8_t* stages, uint64_t* full,
+                                          uint64_t* empty) {
+  using GN = GeoN<LOGN, IO>;
+  const size_t ntiles = (batch + GN::kTileN - 1) / GN::kTileN;
+  int k = 0;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % GN::kStages;
+    if (k >= GN::kStages) mbar_wait(&empty[s], ((k / GN::kStages) & 1) ^ 1);
+    const size_t first = t * GN::kTileN;
+    const int n = batch - first < size_t(GN::kTileN) ? int(batch - first) : GN::kTileN;
+    const int n0 = n < kConsumers ? n : kConsumers, n1 = n - n0;
+    mbar_expect_tx(&full[s], uint32_t(n) * GN::kPolyBytes);
+    uint8_t* base = stages + s * GN::kStageBytes;
+    bulk_g2s(base, in + first * GN::N, uint32_t(n0) * GN::kPolyBytes, &full[s]);
+    if (n1 > 0)
+      bulk_g2s(base + GN::poly_offset(0, 1), in + (first + kConsumers) * GN::N,
+               uint32_t(n1) * GN::kPolyBytes, &full[s]);
+  }
+}
+
+// strided read v[k] = a[j + G k] from a landed stage slot (consecutive lanes, consecutive
+// words: conflict-free)
+template <class IO, int G, bool SGN>
+__device__ __forceinline__ void load_strided_n(uint32_t (&v)[32], const IO* src, int j) {
+  const uint32_t b = smem_addr(src) + uint32_t(sizeof(IO)) * j;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    uint32_t x;
+    if constexpr (sizeof(IO) == 2) {
+      if (SGN)
+        asm volatile("ld.shared.s16 %0, [%1];" : "=r"(x) : "r"(b + 2u * G * k) : "memory");
+      else
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(b + 2u * G * k) : "memory");
+    } else {
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(b + 4u * G * k) : "memory");
+    }
+    v[k] = x;
+  }
+}
+
+// contiguous read v[k] = a[32 j + k]
+template <class IO, bool SGN>
+__device__ __forceinline__ void load_contiguous_n(uint32_t (&v)[32], const IO* poly, int j) {
+  const uint4* src = reinterpret_cast<const uint4*>(poly + 32 * j);
+  if constexpr (sizeof(IO) == 2) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 a = src[c];
+      const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[8 * c + 2 * e] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] & 0xffffu));
+        v[8 * c + 2 * e + 1] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] >> 16));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 a = src[c];
+      v[4 * c] = a.x;
+      v[4 * c + 1] = a.y;
+      v[4 * c + 2] = a.z;
+      v[4 * c + 3] = a.w;
+    }
+  }
+}
+
+// contiguous ownership -> global (lane j writes its 32 consecutive coefficients)
+template <class IO>
+__device__ __forceinline__ void store_contiguous_n(IO* out_poly, int j, const uint32_t (&v)[32]) {
+  uint4* dst = reinterpret_cast<uint4*>(out_poly + 32 * j);
+  if constexpr (sizeof(IO) == 2) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      __stcs(dst + c, make_uint4(__byte_perm(v[8 * c], v[8 * c + 1], 0x5410),
+                                 __byte_perm(v[8 * c + 2], v[8 * c + 3], 0x5410),
+                                 __byte_perm(v[8 * c + 4], v[8 * c + 5], 0x5410),
+                                 __byte_perm(v[8 * c + 6], v[8 * c + 7], 0x5410)));
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      __stcs(dst + c, make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
+  }
+}
+
+// strided ownership -> natural-order coalesced 128-bit stores through the transpose tile
+template <class IO, int G>
+__device__ __forceinline__ void store_strided_n(IO* out_poly, int j, const uint32_t (&v)[32],
+                                                const XposeN<G>& X, bool valid) {
+  constexpr int N = 32 * G;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) X.put(k, v[k]);
+  __syncwarp();
+  if (!valid) return;
+  uint4* dst = reinterpret_cast<uint4*>(out_poly);
+  if constexpr (sizeof(IO) == 2) {  // 8 coefficients per 16-byte vector
+#pragma unroll
+    for (int t = 0; t < N / 8 / G; ++t) {
+      const int q = j + G * t;
+      const uint4 a = X.chunk(2 * q), b = X.chunk(2 * q + 1);
+      __stcs(dst + q, make_uint4(__byte_perm(a.x, a.y, 0x5410), __byte_perm(a.z, a.w, 0x5410),
+                                 __byte_perm(b.x, b.y, 0x5410), __byte_perm(b.z, b.w, 0x5410)));
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < N / 4 / G; ++t) {
+      const int q = j + G * t;
+      __stcs(dst + q, X.chunk(q));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward: run_split_layers (transform.hpp:77-96) for N = 2^LOGN, strided in ->
+// contiguous out.  PER_INDEX: DIF per-index schedule (ntl / harvey / scott, cyclic).
+template <class K, int LOGN, bool PER_INDEX>
+__device__ __forceinline__ void fwd_body_n(uint32_t (&v)[32], const uint2* tws, const FastArgs& A,
+                                           const XposeN<(1 << LOGN) / 32>& X, int j) {
+  using Tw = typename K::Tw;
+  constexpr int N = 1 << LOGN, G = N / 32;
+#pragma unroll
+  for (int s = 1; s <= 5; ++s) {  // phase 1: register distance h = 2^{5-s}
+    const int h = 16 >> (s - 1);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      Tw w;
+      if (PER_INDEX)  // index within the half block: j + G (k mod h); cursor N - 2^{LOGN-s+1}
+        w = tw_smem<Tw>(tws, N - (N >> (s - 1)) + j + G * (k & (h - 1)));
+      else  // block k >> (6 - s), CT per-block cursor 2^{s-1} - 1 (constant bank)
+        w = K::tw(A, (1 << (s - 1)) - 1 + (k >> (6 - s)));
+      K::fwd(v[k], v[k + h], w, A);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) X.put(k, v[k]);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X.get4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+#pragma unroll
+  for (int s = 6; s <= LOGN; ++s) {  // phase 2: register distance h = 2^{LOGN-s}
+    const int h = 1 << (LOGN - s);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      Tw w;
+      if (PER_INDEX)  // uniform index k mod h, compact constant-bank order
+        w = K::tw(A, 32 - 2 * h + (k & (h - 1)));
+      else  // block (32 j + k) >> (LOGN - s + 1)
+        w = tw_smem<Tw>(tws, (1 << (s - 1)) - 1 + ((32 * j + k) >> (LOGN - s + 1)));
+      K::fwd(v[k], v[k + h], w, A);
+    }
+  }
+}
+
+// inverse: run_merge_layers + N^{-1} (transform.hpp:99-116, 323-335), contiguous
+// canonical in -> strided canonical out
+template <class K, int LOGN>
+__device__ __forceinline__ void inv_body_n(uint32_t (&v)[32], const uint2* tws, const FastArgs& A,
+                                           const XposeN<(1 << LOGN) / 32>& X, int j) {
+  using Tw = typename K::Tw;
+  constexpr int N = 1 << LOGN;
+#pragma unroll
+  for (int s = LOGN; s >= 6; --s) {  // phase 1: merge depth m = LOGN - s + 1
+    const int h = 1 << (LOGN - s);
+    const uint32_t off = A.off[LOGN - s + 1];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      const Tw w = tw_smem<Tw>(tws, N - (2 << (s - 1)) + ((32 * j + k) >> (LOGN - s + 1)));
+      inv_bf<K>(s, v[k], v[k + h], w, off, A);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = X.get(k);
+#pragma unroll
+  for (int s = 5; s >= 1; --s) {  // phase 2: register distance h = 2^{5-s}
+    const int h = 1 << (5 - s);
+    const uint32_t off = A.off[LOGN - s + 1];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      if (K::kFold && s == 1)
+        K::inv_last(v[k], v[k + h], off, A);
+      else  // block k >> (6 - s), compact merge order 32 - 2^s + b (constant bank)
+        inv_bf<K>(s, v[k], v[k + h], K::tw(A, 32 - (2 << (s - 1)) + (k >> (6 - s))), off, A);
+    }
+  }
+  if (!K::kFold) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = K::scale(v[k], A);
+  }
+}
+
+template <int LOGN, class IO>
+__device__ __forceinline__ void stage_table(uint2* tws, const uint32_t* tab) {
+  constexpr int N = 1 << LOGN;
+  const uint2* src = reinterpret_cast<const uint2*>(tab);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tws[i] = src[i];
+}
+
+template <class K, class IO, int LOGN, bool PER_INDEX>
+__global__ void __launch_bounds__(kThreads)
+    fwdn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
+                    const uint32_t* __restrict__ tab, const __grid_constant__ FastArgs A) {
+  using GN = GeoN<LOGN, IO>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* stages = smem;
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + GN::kStages * GN::kStageBytes);
+  uint2* tws = reinterpret_cast<uint2*>(scratch + kConsumers * GN::kScratchWords);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tws + GN::N);
+  uint64_t* empty = full + GN::kStages;
+  stage_table<LOGN, IO>(tws, tab);
+  init_barriers(full, empty, GN::kStages);  // __syncthreads: table visible
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == kConsumers) {
+    if (lane == 0) produce_n<LOGN, IO>(in, batch, stages, full, empty);
+    return;
+  }
+  constexpr int G = GN::G;
+  const int j = lane & (G - 1), half = GN::PPW == 2 ? lane >> 4 : 0;
+  XposeN<G> X;
+  X.init(scratch + warp * GN::kScratchWords + half * GN::kRegionWords, j);
+  const size_t ntiles = (batch + GN::kTileN - 1) / GN::kTileN;
+  int it = 0;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % GN::kStages;
+    const size_t poly = t * GN::kTileN + half * kConsumers + warp;
+    mbar_wait(&full[s], (it / GN::kStages) & 1);
+    uint32_t v[32];
+    load_strided_n<IO, G, K::kSigned>(
+        v, reinterpret_cast<const IO*>(stages + s * GN::kStageBytes + GN::poly_offset(warp, half)), j);
+    release_stage(&empty[s], lane);
+    fwd_body_n<K, LOGN, PER_INDEX>(v, tws, A, X, j);
+    if (poly < batch) store_contiguous_n<IO>(out + poly * GN::N, j, v);
+  }
+}
+
+// MODE 0: generic canonicalisation of the input words; 1: host-validated fast form
+template <class K, class IO, int LOGN, int MODE>
+__global__ void __launch_bounds__(kThreads)
+    invn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
+                    const uint32_t* __restrict__ tab, const __grid_constant__ FastArgs A) {
+  using GN = GeoN<LOGN, IO>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* stages = smem;
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + GN::kStages * GN::kStageBytes);
+  uint2* tws = reinterpret_cast<uint2*>(scratch + kConsumers * GN::kScratchWords);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tws + GN::N);
+  uint64_t* empty = full + GN::kStages;
+  stage_table<LOGN, IO>(tws, tab);
+  init_barriers(full, empty, GN::kStages);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == kConsumers) {
+    if (lane == 0) produce_n<LOGN, IO>(in, batch, stages, full, empty);
+    return;
+  }
+  constexpr int G = GN::G;
+  const int j = lane & (G - 1), half = GN::PPW == 2 ? lane >> 4 : 0;
+  XposeN<G> X;
+  X.init(scratch + warp * GN::kScratchWords + half * GN::kRegionWords, j);
+  const size_t ntiles = (batch + GN::kTileN - 1) / GN::kTileN;
+  int it = 0;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % GN::kStages;
+    const size_t poly = t * GN::kTileN + half * kConsumers + warp;
+    mbar_wait(&full[s], (it / GN::kStages) & 1);
+    uint32_t v[32];
+    load_contiguous_n<IO, K::kSigned>(
+        v, reinterpret_cast<const IO*>(stages + s * GN::kStageBytes + GN::poly_offset(warp, half)), j);
+    release_stage(&empty[s], lane);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = canon<IO, K::kSigned, MODE == 1>(v[k], A);
+    inv_body_n<K, LOGN>(v, tws, A, X, j);
+    store_strided_n<IO, G>(out + poly * GN::N, j, v, X, poly < batch);
+  }
+}
+
+int g_sms_n = 0;
+
+template <class Kern>
+int grid_n(Kern kern, int smem, int& occ, size_t tiles) {
+  if (!occ) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem);
+    occ = o > 0 ? o : 1;
+    if (!g_sms_n) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&g_sms_n, cudaDevAttrMultiProcessorCount, dev);
+      if (g_sms_n <= 0) g_sms_n = 148;
+    }
+  }
+  const size_t full = size_t(g_sms_n) * occ;
+  return static_cast<int>(tiles < full ? tiles : full);
+}
+
+template <class K, class IO, int LOGN, bool PER_INDEX>
+cudaError_t fwd_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
+                  cudaStream_t st) {
+  using GN = GeoN<LOGN, IO>;
+  static int occ = 0;
+  auto kern = fwdn_tma_kernel<K, IO, LOGN, PER_INDEX>;
+  const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN);
+  kern<<<blocks, kThreads, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,
+                                            tab, A);
+  return cudaGetLastError();
+}
+
+template <class K, class IO, int LOGN, int MODE>
+cudaError_t inv_n_mode(const void* in, void* out, size_t batch, const uint32_t* tab,
+                       const FastArgs& A, cudaStream_t st) {
+  using GN = GeoN<LOGN, IO>;
+  static int occ = 0;
+  auto kern = invn_tma_kernel<K, IO, LOGN, MODE>;
+  const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN);
+  kern<<<blocks, kThreads, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,
+                                            tab, A);
+  return cudaGetLastError();
+}
+
+template <class K, class IO, int LOGN>
+cudaError_t inv_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
+                  cudaStream_t st) {
+  const unsigned fast_bit = sizeof(IO) == 2 ? 1u : 2u;
+  if (!K::kSigned && (A.flags & fast_bit)) return inv_n_mode<K, IO, LOGN, 1>(in, out, batch, tab, A, st);
+  return inv_n_mode<K, IO, LOGN, 0>(in, out, batch, tab, A, st);
+}
+
+template <class K, bool PER_INDEX, class IO>
+cudaError_t by_logn(int dir, int logn, const void* in, void* out, size_t batch, const uint32_t* tab,
+                    const FastArgs& A, cudaStream_t st) {
+  if (logn == 9)
+    return dir == 0 ? fwd_n<K, IO, 9, PER_INDEX>(in, out, batch, tab, A, st)
+                    : inv_n<K, IO, 9>(in, out, batch, tab, A, st);
+  if (logn == 10)
+    return dir == 0 ? fwd_n<K, IO, 10, PER_INDEX>(in, out, batch, tab, A, st)
+                    : inv_n<K, IO, 10>(in, out, batch, tab, A, st);
+  return cudaErrorInvalidValue;
+}
+
+template <class K, bool PER_INDEX>
+cudaError_t by_elem(int dir, int logn, int elem, const void* in, void* out, size_t batch,
+                    const uint32_t* tab, const FastArgs& A, cudaStream_t st) {
+  if (elem == 2) return by_logn<K, PER_INDEX, uint16_t>(dir, logn, in, out, batch, tab, A, st);
+  if (elem == 4) return by_logn<K, PER_INDEX, uint32_t>(dir, logn, in, out, batch, tab, A, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+bool fastn_supports(const HostParams& P, int elem_bytes, const void* in, const void* out) {
+  return (P.N == 512 || P.N == 1024) && P.layers == P.log2N && (elem_bytes == 2 || elem_bytes == 4) &&
+         !(reinterpret_cast<uintptr_t>(in) & 15) && !(reinterpret_cast<uintptr_t>(out) & 15);
+}
+
+cudaError_t fastn_launch(const HostParams& P, int kind, int dir, const void* in, void* out,
+                         size_t batch, int elem_bytes, const uint32_t* tab, cudaStream_t st) {
+  const FastArgs& A = P.fast[kind][dir];
+  const int logn = static_cast<int>(P.log2N);
+  const bool n16 = P.n_bits == 16, cyclic = P.tree == NTTK_CYCLIC;
+  if (batch == 0) return cudaSuccess;
+  switch (kind) {
+    case NTTK_IMPROVED:
+      return n16 ? by_elem<ImprovedN16<false>, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st)
+                 : by_elem<ImprovedN32, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st);
+    case NTTK_HARVEY:
+      if (cyclic)
+        return n16 ? by_elem<Harvey<16, false>, true>(dir, logn, elem_bytes, in, out, batch, tab, A, st)
+                   : by_elem<Harvey<32, false>, true>(dir, logn, elem_bytes, in, out, batch, tab, A, st);
+      return n16 ? by_elem<Harvey<16, true>, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st)
+                 : by_elem<Harvey<32, true>, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st);
+    case NTTK_SMONT:
+      return n16 ? by_elem<Smont<16>, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st)
+                 : by_elem<Smont<32>, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st);
+    case NTTK_NTL:
+      return n16 ? by_elem<Ntl<16>, true>(dir, logn, elem_bytes, in, out, batch, tab, A, st)
+                 : by_elem<Ntl<32>, true>(dir, logn, elem_bytes, in, out, batch, tab, A, st);
+    case NTTK_SCOTT:
+      if (n16 || !cyclic) return cudaErrorInvalidValue;
+      return by_elem<Scott32, true>(dir, logn, elem_bytes, in, out, batch, tab, A, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace nttk_b200

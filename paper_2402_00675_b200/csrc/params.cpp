@@ -9,6 +9,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 
 namespace nttk_b200 {
@@ -105,7 +106,12 @@ void add_fault(std::string& s, const std::string& f) { s += "\n  - " + f; }
 // ---- device images for the N=256 fast kernels (fast256.cu) ----
 
 bool fast_eligible(const HostParams& P, int kind) {
-  if (P.N != 256 || P.layers < 5 || !(P.n_bits == 16 || P.n_bits == 32)) return false;
+  if (!(P.n_bits == 16 || P.n_bits == 32)) return false;
+  if (P.N == 256) {
+    if (P.layers < 5) return false;
+  } else if (!((P.N == 512 || P.N == 1024) && P.layers == P.log2N)) {
+    return false;  // fastn_tma.cu: full trees only
+  }
   const uint64_t p = P.p;
   switch (kind) {
     case NTTK_IMPROVED:  // every intermediate < 2^layers p must fit a 32-bit register
@@ -137,7 +143,7 @@ void fill_fast(HostParams& P, int kind) {
     A.p = P.p;
     A.two_p = 2 * P.p;
     A.negp = static_cast<uint32_t>(0u - P.p);
-    for (unsigned m = 1; m < 10; ++m) A.off[m] = static_cast<uint32_t>(uint64_t(P.p) << (m - 1));
+    for (unsigned m = 1; m < 12; ++m) A.off[m] = static_cast<uint32_t>(uint64_t(P.p) << (m - 1));
     A.layers = P.layers;
     A.canon_m = static_cast<uint32_t>(0xffffffffull / P.p);
     A.canon_m16 = static_cast<uint32_t>(((uint64_t(1) << 32) + P.p - 1) / P.p);
@@ -206,6 +212,8 @@ void fill_fast(HostParams& P, int kind) {
         A.fold_hi = static_cast<uint32_t>((u128(wl) << P.n_bits) / p);
       }
     }
+    // full per-direction twiddle words (reference table order) in the kind's encoding
+    std::vector<uint32_t> tl(P.N, 0), th(P.N, 0);
     const std::vector<uint64_t>* tab = nullptr;
     switch (kind) {
       case NTTK_IMPROVED: {
@@ -213,8 +221,8 @@ void fill_fast(HostParams& P, int kind) {
         const uint64_t mu = c.mu;  // p^{-1} mod 2^{2n}
         for (size_t k = 0; k < tab->size(); ++k) {
           const uint64_t wm = (*tab)[k] * mu & c.r2n_mask;  // w_hat mu mod 2^{2n}
-          A.lo[k] = static_cast<uint32_t>(wm);
-          A.hi[k] = static_cast<uint32_t>(wm >> 32);
+          tl[k] = static_cast<uint32_t>(wm);
+          th[k] = static_cast<uint32_t>(wm >> 32);
         }
         const uint64_t sm = P.n_inv_hat * mu & c.r2n_mask;
         A.scale_lo = static_cast<uint32_t>(sm);
@@ -224,7 +232,7 @@ void fill_fast(HostParams& P, int kind) {
       case NTTK_HARVEY: {
         if (dir == 0) tab = P.tree == NTTK_CYCLIC ? &P.dif_mont : &P.ct_mont;
         else tab = &P.gs_mont;
-        for (size_t k = 0; k < tab->size(); ++k) A.lo[k] = static_cast<uint32_t>((*tab)[k]);
+        for (size_t k = 0; k < tab->size(); ++k) tl[k] = static_cast<uint32_t>((*tab)[k]);
         A.pinv = n16 ? static_cast<uint32_t>(c.p_inv_beta << 16)
                      : static_cast<uint32_t>(c.p_inv_beta);
         A.scale_lo = static_cast<uint32_t>(P.n_inv_mont);
@@ -232,7 +240,7 @@ void fill_fast(HostParams& P, int kind) {
       }
       case NTTK_SCOTT: {  // forward: DIF per-index Montgomery twiddles; inverse: GS per-block
         tab = dir == 0 ? &P.dif_mont : &P.gs_mont;
-        for (size_t k = 0; k < tab->size(); ++k) A.lo[k] = static_cast<uint32_t>((*tab)[k]);
+        for (size_t k = 0; k < tab->size(); ++k) tl[k] = static_cast<uint32_t>((*tab)[k]);
         A.pinv = static_cast<uint32_t>(c.neg_p_inv_beta);
         A.scale_lo = static_cast<uint32_t>(P.n_inv_mont);
         A.soff = static_cast<uint32_t>(uint64_t(P.N / P.scott_L) * P.p);
@@ -242,8 +250,8 @@ void fill_fast(HostParams& P, int kind) {
         const std::vector<uint64_t>& w = dir == 0 ? P.dif_w : P.gs_plain;
         const std::vector<uint64_t>& wq = dir == 0 ? P.dif_wq : P.gs_wq;
         for (size_t k = 0; k < w.size(); ++k) {
-          A.lo[k] = static_cast<uint32_t>(w[k]);
-          A.hi[k] = static_cast<uint32_t>(wq[k]);
+          tl[k] = static_cast<uint32_t>(w[k]);
+          th[k] = static_cast<uint32_t>(wq[k]);
         }
         A.scale_lo = static_cast<uint32_t>(P.n_inv);
         A.scale_hi = static_cast<uint32_t>((u128(P.n_inv) << P.n_bits) / p);
@@ -253,11 +261,11 @@ void fill_fast(HostParams& P, int kind) {
         const std::vector<int64_t>& st = dir == 0 ? P.ct_smont : P.gs_smont;
         for (size_t k = 0; k < st.size(); ++k) {
           const int64_t w = st[k];
-          A.lo[k] = static_cast<uint32_t>(w);
+          tl[k] = static_cast<uint32_t>(w);
           // premultiplied Montgomery quotient factor w p^{-1} mod 2^n (n=16: in the
           // high half so a 32-bit multiply leaves the n-bit product there)
           const uint64_t wp = static_cast<uint64_t>(w) * c.p_inv_beta & c.beta_mask;
-          A.hi[k] = n16 ? static_cast<uint32_t>(wp << 16) : static_cast<uint32_t>(wp);
+          th[k] = n16 ? static_cast<uint32_t>(wp << 16) : static_cast<uint32_t>(wp);
         }
         const int64_t f = P.n_inv_smont;
         A.scale_lo = static_cast<uint32_t>(f);
@@ -265,6 +273,44 @@ void fill_fast(HostParams& P, int kind) {
         A.scale_hi = n16 ? static_cast<uint32_t>(fp << 16) : static_cast<uint32_t>(fp);
         A.pinv = static_cast<uint32_t>(c.p_inv_beta);
         break;
+      }
+    }
+    const size_t tsize = kind == NTTK_SMONT ? (dir == 0 ? P.ct_smont.size() : P.gs_smont.size())
+                         : kind == NTTK_NTL  ? (dir == 0 ? P.dif_w.size() : P.gs_plain.size())
+                                             : tab->size();
+    if (P.N == 256) {
+      for (size_t k = 0; k < tsize && k < 256; ++k) {
+        A.lo[k] = tl[k];
+        A.hi[k] = th[k];
+      }
+    } else {
+      // N = 512 / 1024 (fastn_tma.cu): the uniform twiddles become constant-bank words
+      // in a compact order, the lane-dependent ones are read from a device copy of the
+      // whole table (fastn_tab, staged into shared memory)
+      const unsigned L = P.layers;
+      const bool per_index = dir == 0 && P.tree == NTTK_CYCLIC &&
+                             (kind == NTTK_NTL || kind == NTTK_HARVEY || kind == NTTK_SCOTT);
+      auto put = [&](size_t dst, size_t src) {
+        A.lo[dst] = tl[src];
+        A.hi[dst] = th[src];
+      };
+      if (dir == 0 && !per_index) {  // CT per-block, layers 1..5 (strided phase)
+        for (size_t k = 0; k < 31; ++k) put(k, k);
+      } else if (dir == 0) {  // DIF per-index, layers 6..L (contiguous phase)
+        for (unsigned st = 6; st <= L; ++st) {
+          const size_t cur = P.N - (P.N >> (st - 1)), cnt = P.N >> st;
+          for (size_t e = 0; e < cnt; ++e) put(32 - 2 * cnt + e, cur + e);
+        }
+      } else {  // GS merge order, layers 5..1 (strided phase)
+        for (unsigned st = 1; st <= 5; ++st)
+          for (size_t b = 0; b < (size_t(1) << (st - 1)); ++b)
+            put(32 - (size_t(1) << st) + b, (size_t(1) << L) - (size_t(1) << st) + b);
+      }
+      std::vector<uint32_t>& F = P.fastn_tab[kind][dir];
+      F.assign(2 * tsize, 0);
+      for (size_t k = 0; k < tsize; ++k) {
+        F[2 * k] = tl[k];
+        F[2 * k + 1] = th[k];
       }
     }
   }
@@ -315,6 +361,35 @@ void fill_fast(HostParams& P, int kind) {
 HostParams::~HostParams() {
   for (auto& d : dev)
     if (d.base) cudaFree(d.base);
+  for (auto* d : fastn_dev)
+    if (d) cudaFree(d);
+}
+
+// one allocation per device holding every (kind, dir) table, [kind][dir] at a fixed
+// stride of 2N words
+const uint32_t* HostParams::fastn_table(int device, int kind, int dir, std::string& err) const {
+  if (device < 0 || device >= 64) {
+    err = "device ordinal out of range";
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu_dev);
+  if (!fastn_dev[device]) {
+    const size_t stride = 2 * size_t(N);
+    std::vector<uint32_t> host(10 * stride, 0);
+    for (int k = 0; k < 5; ++k)
+      for (int d = 0; d < 2; ++d)
+        std::copy(fastn_tab[k][d].begin(), fastn_tab[k][d].end(), host.begin() + (2 * k + d) * stride);
+    uint32_t* buf = nullptr;
+    cudaError_t e = cudaMalloc(&buf, host.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(buf, host.data(), host.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      if (buf) cudaFree(buf);
+      err = std::string("fastn table upload: ") + cudaGetErrorString(e);
+      return nullptr;
+    }
+    fastn_dev[device] = buf;
+  }
+  return fastn_dev[device] + (2 * kind + dir) * 2 * size_t(N);
 }
 
 const DeviceTables* HostParams::device_tables(int device, std::string& err) const {

@@ -57,7 +57,7 @@ struct FastArgs {
   // --- issue-slot economy (all host-validated, see params.cpp fill_fast) ---
   uint32_t zero = 0;       // always 0: x + y + zero forces a 3-input IADD3 (ALU pipe)
   uint32_t negp = 0;       // -p mod 2^32 (x - q p as one IMAD)
-  uint32_t off[10] = {};   // off[m] = 2^{m-1} p: GS offset of merge depth m (constant operand)
+  uint32_t off[12] = {};   // off[m] = 2^{m-1} p: GS offset of merge depth m (constant operand)
   uint32_t cb_m = 0, cb_s = 0;  // x mod p = x - ((x cb_m) >> cb_s) p, exact for x < 2^17
   uint32_t cs_s = 0;       // x mod p = min(r, r - p), r = x - (x >> cs_s) p, exact for x < 2^32
   uint32_t kp = 0;         // K p >= 2^16 - 1: fused first inverse layer offset (u16 input)
@@ -105,6 +105,11 @@ struct HostParams {
   uint32_t fast_mask = 0;
   FastArgs fast[5][2];
   ProdArgs prod[5];
+  // N = 512 / 1024 fast kernels: whole per-direction tables, interleaved (lo, hi) words,
+  // uploaded once per device on first use
+  std::vector<uint32_t> fastn_tab[5][2];
+  mutable uint32_t* fastn_dev[64] = {};
+  const uint32_t* fastn_table(int device, int kind, int dir, std::string& err) const;
 
   mutable std::mutex mu_dev;
   mutable DeviceTables dev[64];

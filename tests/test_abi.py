@@ -97,8 +97,11 @@ def test_presets_and_fast_path_selection(engine):
     assert (T.omega, T.omega_inv, T.n_inv) == (5, 8, 10)
     K = engine.build_params(3329, 256, 16, [engine.ButterflyKind.improved], exact_bound=True)
     assert engine.ButterflyKind.improved in K.fast_path
-    F = engine.preset("falcon512")
-    assert F.fast_path == []  # N = 512 runs on the generic kernel
+    F = engine.preset("falcon512")  # N = 512: fastn_tma.cu for every kind
+    assert sorted(F.fast_path) == sorted(engine.ButterflyKind)[:4]
+    # partial trees at N = 512 and N = 2048 stay on the generic kernel
+    G = engine.build_params(12289, 2048, 32, [engine.ButterflyKind.harvey])
+    assert G.fast_path == []
 
 
 def test_exact_bound_admits_kyber_n16_and_dilithium_n32(engine):

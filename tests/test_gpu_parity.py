@@ -170,6 +170,53 @@ def test_dif_kinds_fast_path_vs_oracle(oracle, p, n, kind):
         assert (from_dev(nttk.inverse(P, kind, to_dev(spec, elem))) == want_inv).all(), elem
 
 
+FASTN_CASES = [(32, NTL, CYCLIC), (32, HARVEY, CYCLIC), (32, SCOTT, CYCLIC), (32, IMPROVED, CYCLIC),
+               (32, SMONT, CYCLIC), (16, NTL, CYCLIC), (16, HARVEY, CYCLIC),
+               (32, IMPROVED, NEGA), (32, HARVEY, NEGA), (32, SMONT, NEGA), (16, HARVEY, NEGA)]
+
+
+@pytest.mark.parametrize("N", [512, 1024])
+@pytest.mark.parametrize("n,kind,tree", FASTN_CASES)
+def test_fastn_transforms_vs_oracle(oracle, N, n, kind, tree):
+    """N = 512 / 1024 fast kernels (fastn_tma.cu; the paper's Table 2 sizes, q = 12289):
+    forward words, round trips and the inverse of arbitrary in-bound spectra, bit-exact."""
+    p = 12289
+    P = engine_params(p, N, n, [kind], tree=tree)
+    Q = oracle.params(p, N, n, (kind,), tree=tree)
+    assert kind in P.fast_path
+    B = 37  # ragged: partial tiles, odd half-warp split at N = 512
+    f = oracle.rng(900 + N + 10 * kind + n, p, B * N).reshape(B, N)
+    want = Q.forward(kind, f)
+    sgn = kind == SMONT
+    L = N.bit_length() - 1
+    bound = {NTL: p, HARVEY: 2 * p, SCOTT: N * p, IMPROVED: (L + 1) * p, SMONT: (L + 2) * p}[kind]
+    lim = {2: 1 << 15, 4: 1 << 31, 8: 1 << 63} if sgn else {2: 1 << 16, 4: 1 << 32, 8: 1 << 64}
+    elems = [e for e in (2, 4, 8) if bound <= lim[e]]
+    for elem in elems:
+        y = nttk.forward(P, kind, to_dev(f, elem, sgn))
+        assert (from_dev(y, sgn).astype(np.int64) == want.astype(np.int64)).all(), elem
+        assert (from_dev(nttk.inverse(P, kind, y)) == f).all(), elem
+    if not sgn:
+        rng = np.random.default_rng(N + kind + n)
+        spec = rng.integers(0, bound, size=(B, N), dtype=np.uint64)
+        want_inv = Q.inverse(kind, spec)
+        for elem in elems:
+            assert (from_dev(nttk.inverse(P, kind, to_dev(spec, elem))) == want_inv).all(), elem
+
+
+def test_fastn_presets_all_kinds(oracle):
+    """The reference presets at N = 512 / 1024 (params.hpp:280-289) on the fast kernels."""
+    for name, p, N in (("newhope512", 12289, 512), ("falcon1024", 12289, 1024)):
+        P = nttk.preset(name)
+        kinds = (NTL, HARVEY, SCOTT, IMPROVED)
+        Q = oracle.params(p, N, 32, kinds)
+        f = oracle.rng(4, p, 19 * N).reshape(19, N)
+        for k in kinds:
+            assert k in P.fast_path, (name, k)
+            got = from_dev(nttk.forward(P, k, to_dev(f, 4)))
+            assert (got == Q.forward(k, f)).all(), (name, k)
+
+
 def test_scott_n16_stays_on_generic_kernel(oracle):
     """scott at Kyber n=16 underflows uint64 in the reference; the engine
     keeps that configuration on the 64-bit generic kernel, which replicates it word for word."""
