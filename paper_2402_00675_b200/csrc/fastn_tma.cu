@@ -224,6 +224,15 @@ __device__ __forceinline__ void store_strided_n(IO* out_poly, int j, const uint3
   }
 }
 
+// Stage the direction table into shared memory.  The lane-dependent segments (per-block
+// layers s >= 6: lane j reads blocks j c + q, q < c = 2^{s-1} / G) are stored transposed,
+// entry j c + q at q G + j, so a warp's reads hit consecutive words; without this layer
+// LOGN has lanes 128 B apart (a 32-way bank conflict).  SEG(s) = first entry of layer s.
+template <int LOGN, bool MERGE>
+__device__ __forceinline__ constexpr int seg_base(int s) {
+  return MERGE ? (1 << LOGN) - (2 << (s - 1)) : (1 << (s - 1)) - 1;
+}
+
 // ---------------------------------------------------------------------------
 // forward: run_split_layers (transform.hpp:77-96) for N = 2^LOGN, strided in ->
 // contiguous out.  PER_INDEX: DIF per-index schedule (ntl / harvey / scott, cyclic).
@@ -261,8 +270,8 @@ __device__ __forceinline__ void fwd_body_n(uint32_t (&v)[32], const uint2* tws, 
       Tw w;
       if (PER_INDEX)  // uniform index k mod h, compact constant-bank order
         w = K::tw(A, 32 - 2 * h + (k & (h - 1)));
-      else  // block (32 j + k) >> (LOGN - s + 1)
-        w = tw_smem<Tw>(tws, (1 << (s - 1)) - 1 + ((32 * j + k) >> (LOGN - s + 1)));
+      else  // block (32 j + k) >> (LOGN - s + 1) = j c + (k >> (LOGN - s + 1)), transposed
+        w = tw_smem<Tw>(tws, seg_base<LOGN, false>(s) + (k >> (LOGN - s + 1)) * G + j);
       K::fwd(v[k], v[k + h], w, A);
     }
   }
@@ -274,7 +283,7 @@ template <class K, int LOGN>
 __device__ __forceinline__ void inv_body_n(uint32_t (&v)[32], const uint2* tws, const FastArgs& A,
                                            const XposeN<(1 << LOGN) / 32>& X, int j) {
   using Tw = typename K::Tw;
-  constexpr int N = 1 << LOGN;
+  constexpr int G = (1 << LOGN) / 32;
 #pragma unroll
   for (int s = LOGN; s >= 6; --s) {  // phase 1: merge depth m = LOGN - s + 1
     const int h = 1 << (LOGN - s);
@@ -282,7 +291,7 @@ __device__ __forceinline__ void inv_body_n(uint32_t (&v)[32], const uint2* tws, 
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       if (k & h) continue;
-      const Tw w = tw_smem<Tw>(tws, N - (2 << (s - 1)) + ((32 * j + k) >> (LOGN - s + 1)));
+      const Tw w = tw_smem<Tw>(tws, seg_base<LOGN, true>(s) + (k >> (LOGN - s + 1)) * G + j);
       inv_bf<K>(s, v[k], v[k + h], w, off, A);
     }
   }
@@ -311,11 +320,24 @@ __device__ __forceinline__ void inv_body_n(uint32_t (&v)[32], const uint2* tws, 
   }
 }
 
-template <int LOGN, class IO>
+template <int LOGN, bool TRANSPOSE, bool MERGE>
 __device__ __forceinline__ void stage_table(uint2* tws, const uint32_t* tab) {
-  constexpr int N = 1 << LOGN;
+  constexpr int N = 1 << LOGN, G = N / 32;
   const uint2* src = reinterpret_cast<const uint2*>(tab);
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tws[i] = src[i];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    int dst = i;
+    if (TRANSPOSE) {
+#pragma unroll
+      for (int s = 6; s <= LOGN; ++s) {
+        const int b0 = seg_base<LOGN, MERGE>(s), size = 1 << (s - 1), c = size / G;
+        if (i >= b0 && i < b0 + size) {
+          const int b = i - b0;
+          dst = b0 + (b % c) * G + b / c;
+        }
+      }
+    }
+    tws[dst] = src[i];
+  }
 }
 
 template <class K, class IO, int LOGN, bool PER_INDEX>
@@ -329,7 +351,7 @@ __global__ void __launch_bounds__(kThreads)
   uint2* tws = reinterpret_cast<uint2*>(scratch + kConsumers * GN::kScratchWords);
   uint64_t* full = reinterpret_cast<uint64_t*>(tws + GN::N);
   uint64_t* empty = full + GN::kStages;
-  stage_table<LOGN, IO>(tws, tab);
+  stage_table<LOGN, !PER_INDEX, false>(tws, tab);
   init_barriers(full, empty, GN::kStages);  // __syncthreads: table visible
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kConsumers) {
@@ -367,7 +389,7 @@ __global__ void __launch_bounds__(kThreads)
   uint2* tws = reinterpret_cast<uint2*>(scratch + kConsumers * GN::kScratchWords);
   uint64_t* full = reinterpret_cast<uint64_t*>(tws + GN::N);
   uint64_t* empty = full + GN::kStages;
-  stage_table<LOGN, IO>(tws, tab);
+  stage_table<LOGN, true, true>(tws, tab);
   init_barriers(full, empty, GN::kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kConsumers) {
