@@ -252,6 +252,29 @@ def _time_ms(torch, fn, iters, warm=3):
     return e0.elapsed_time(e1) / iters
 
 
+def table2_cpu_reference(name, q, N):
+    """The reference's own path at a Table 2 preset on ONE host thread (the reference is
+    single-threaded), per kind: ntt_forward_inplace, and forward + intt_inverse, over a
+    bounded sample (oracle/_ref, the unmodified reference headers); None if not built."""
+    from oracle.oracle import HARVEY, IMPROVED, NTL, SCOTT, Oracle, Reference, reference_available
+
+    if not reference_available():
+        return None
+    ref = Reference()
+    kinds = {"ntl": NTL, "harvey": HARVEY, "scott": SCOTT, "improved": IMPROVED}
+    rp = ref.params(q, N, 32, tuple(kinds.values()))
+    n = 256 if N <= 512 else 128
+    a = Oracle().rng(77, q, n * N)
+    out = {}
+    for kname, k in kinds.items():
+        tf = rp.time_batch(k, 0, a.copy(), 1)
+        tr = rp.time_batch(k, 1, a.copy(), 1)
+        out[kname] = {"cpu_ref_fwd_ns_per_poly": tf * 1e9 / n,
+                      "cpu_ref_inv_ns_per_poly": max(tr - tf, 0.0) * 1e9 / n,
+                      "cpu_ref_sample": f"{n} polys, 1 thread"}
+    return out
+
+
 def run_extras(dev):
     """The other BASELINE.json configs, device-resident, CUDA events (secondary fields)."""
     import torch
@@ -338,6 +361,10 @@ def run_extras(dev):
             assert torch.equal(op, xp), (name, kind)
             row[kind.name] = {"fwd_ns_per_poly": fms * 1e6 / Bp, "inv_ns_per_poly": ims * 1e6 / Bp,
                               "fast_path": kind in Pp.fast_path}
+        cpu = table2_cpu_reference(name, qp, Np)
+        if cpu:
+            for kname, v in cpu.items():
+                row[kname].update(v)
         t2[name] = row
         del xp, sp, op
     ex["table2_presets_2^16"] = t2
