@@ -1,0 +1,133 @@
+"""Device-side property suites: the reference's verify.hpp patterns
+run on the B200 engine, with the pinned oracle as the checker.
+
+* reductions (verify_montgomery / _signed_montgomery / _plantard / _modified_plantard,
+  verify.hpp:65-213): exhaustive operand grids on the toy radices and 10^6 seeded random
+  pairs on each production context (verify.hpp:114-122, 201-211), bit-exact;
+* transforms (verify_transform, verify.hpp:375-483): every butterfly kind's forward
+  spectrum equals the naive DFT (cyclic) or the naive evaluation at the tree's roots
+  (negacyclic) modulo p, in butterfly order, and every kind's inverse inverts every
+  other kind's forward -- on toy sizes (generic kernel) and on the production sizes
+  N = 256 / 512 / 1024 (fast kernels).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import CYCLIC, HARVEY, IMPROVED, NEGA, NTL, SCOTT, SMONT, OracleError
+
+import paper_2402_00675_b200.nttk as nttk
+
+pytestmark = pytest.mark.gpu
+
+MONT, SMONT_R, PLANTARD, MPLANTARD = 0, 1, 2, 3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    assert torch.cuda.is_available() and nttk.device_available()
+
+
+def operand_ranges(variant, p, n, ell):
+    """Valid operand domains per reduction (reduction.hpp)."""
+    if variant == MONT:
+        return (0, p), (0, p)
+    if variant == SMONT_R:
+        return (0, p), (-(1 << (n - 1)), 1 << (n - 1))
+    if variant == PLANTARD:
+        return (0, p + 1), (0, p + 1)
+    return (0, p), (0, p << ell)
+
+
+def run_sweep(oracle, variant, p, n, ell, A, B):
+    ctx = oracle.ctx(p, n, 0, ell)
+    want, s = oracle.sweep(variant, ctx, A, B)
+    dA = torch.tensor(A, dtype=torch.int64, device="cuda")
+    dB = torch.tensor(B, dtype=torch.int64, device="cuda")
+    r = torch.empty(A.size * B.size, dtype=torch.int64, device="cuda")
+    got = nttk.modmul_sweep(variant, p, n, ell, dA, dB, r)
+    return want, s, r.cpu().numpy(), got
+
+
+TOY = [(13, 8, 2), (17, 6, 1), (17, 8, 2), (31, 8, 1), (97, 12, 2)]
+
+
+@pytest.mark.parametrize("p,n,ell", TOY)
+@pytest.mark.parametrize("variant", [MONT, SMONT_R, PLANTARD, MPLANTARD])
+def test_reductions_exhaustive_toy(oracle, p, n, ell, variant):
+    """Every operand pair of the variant's domain on a toy radix."""
+    (a0, a1), (b0, b1) = operand_ranges(variant, p, n, ell)
+    A = np.arange(a0, a1, dtype=np.int64)
+    B = np.arange(b0, b1, dtype=np.int64)
+    try:
+        want, s, got, gs = run_sweep(oracle, variant, p, n, ell, A, B)
+    except (OracleError, nttk.ContractViolation) as e:
+        pytest.skip(f"context not admitted: {e}")
+    assert gs == s and (got == want).all()
+
+
+@pytest.mark.parametrize("p,n,ell", [(3329, 16, 2), (8380417, 32, 7)])
+@pytest.mark.parametrize("variant", [MONT, SMONT_R, PLANTARD, MPLANTARD])
+def test_reductions_random_production(oracle, p, n, ell, variant):
+    """10^6 seeded random pairs (1000 x 1000 grid) plus the domain boundaries."""
+    rng = np.random.default_rng(12345 + 31 * variant + n)
+    (a0, a1), (b0, b1) = operand_ranges(variant, p, n, ell)
+    A = rng.integers(a0, a1, 1000, dtype=np.int64)
+    B = rng.integers(b0, b1, 1000, dtype=np.int64)
+    A[:3] = [a0, a0 + 1, a1 - 1]
+    B[:3] = [b0, b0 + 1, b1 - 1]
+    want, s, got, gs = run_sweep(oracle, variant, p, n, ell, A, B)
+    assert gs == s and (got == want).all()
+
+
+def bitrev(i, bits):
+    return int(format(i, f"0{bits}b")[::-1], 2) if bits else 0
+
+
+TRANSFORMS = [  # (p, N, n, tree, exact)
+    (17, 8, 16, CYCLIC, False), (97, 16, 16, CYCLIC, False), (7681, 64, 32, CYCLIC, False),
+    (3329, 256, 16, CYCLIC, True), (8380417, 256, 32, CYCLIC, True), (12289, 512, 32, CYCLIC, False),
+    (12289, 1024, 32, CYCLIC, False), (97, 16, 16, NEGA, False), (7681, 256, 32, NEGA, False),
+    (12289, 1024, 32, NEGA, False),
+]
+
+
+def kinds_for(tree, p, N, n):
+    ks = [HARVEY, IMPROVED, SMONT] if tree == NEGA else [NTL, HARVEY, SCOTT, IMPROVED, SMONT]
+    out = []
+    for k in ks:
+        try:
+            nttk.build_params(p, N, n, [k], tree=tree, exact_bound=True)
+            out.append(k)
+        except nttk.ContractViolation:
+            pass
+    return out
+
+
+@pytest.mark.parametrize("p,N,n,tree,exact", TRANSFORMS)
+def test_transform_properties(oracle, p, N, n, tree, exact):
+    kinds = kinds_for(tree, p, N, n)
+    assert kinds, "no kind admitted"
+    B = 9
+    f = oracle.rng(4000 + N + n, p, B * N).reshape(B, N)
+    bits = N.bit_length() - 1
+    spectra = {}
+    for k in kinds:
+        P = nttk.build_params(p, N, n, [k], tree=tree, exact_bound=True)
+        x = torch.from_numpy(f.astype(np.int64)).cuda()
+        y = nttk.forward(P, k, x).cpu().numpy().astype(np.int64) % p
+        if tree == CYCLIC:
+            for b in range(B):
+                dft = oracle.naive_dft(f[b], P.omega, p).astype(np.int64)
+                assert (y[b] == dft[[bitrev(i, bits) for i in range(N)]]).all(), (k, b)
+        else:
+            Q = oracle.params(p, N, n, (k,), tree=tree, exact=True)
+            for b in range(B):  # naive_eval takes one polynomial
+                assert (y[b] == Q.naive_eval(f[b]).astype(np.int64)).all(), (k, b)
+        spectra[k] = (P, nttk.forward(P, k, x))
+    for k, (P, y) in spectra.items():  # every inverse undoes every forward (same residues)
+        for k2, (P2, _) in spectra.items():
+            if (k == SMONT) != (k2 == SMONT):
+                continue  # signed spectra are two's complement words: only smont reads them
+            back = nttk.inverse(P2, k2, y)
+            assert (back.cpu().numpy() == f).all(), (k, k2)
