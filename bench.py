@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", action="store_true", help="NCCL-gather per-rank digests")
     ap.add_argument("--no-extras", action="store_true", help="skip BASELINE configs 1/2/3/5")
+    ap.add_argument("--bench-report", metavar="DIR",
+                    help="write the reference BenchReport schema (bench.hpp:365-424) for the GPU "
+                         "and for the reference's own run_bench, then exit")
     return ap.parse_args()
 
 
@@ -577,8 +580,93 @@ def run_engine_arm(a, rank, world, local_rank):
     return 0
 
 
+KIND_ORDER = ("ntl", "harvey", "scott", "improved")  # all_butterfly_kinds()
+
+
+def pairwise_gains(results):
+    """bench.hpp:146-175: later-over-earlier kind pairs per preset, (base - kind)/base %."""
+    out = []
+    for preset in dict.fromkeys(r["preset"] for r in results):
+        mean = {r["kind"]: r["mean_us"] for r in results if r["preset"] == preset}
+        for b in range(len(KIND_ORDER)):
+            for k in range(b + 1, len(KIND_ORDER)):
+                kb, kk = KIND_ORDER[b], KIND_ORDER[k]
+                if kb in mean and kk in mean:
+                    out.append({"preset": preset, "kind": kk, "baseline": kb,
+                                "gain_percent": (mean[kb] - mean[kk]) / mean[kb] * 100.0})
+    return out
+
+
+def bench_report(outdir, presets=("kyber256", "falcon512", "falcon1024"), seed=12345):
+    """GPU rows in the reference's BenchReport schema 1 (transform mode: per-polynomial
+    forward time), next to the reference's own run_bench on one host thread."""
+    import platform
+
+    import torch
+
+    import paper_2402_00675_b200.nttk as nttk
+
+    K = nttk.ButterflyKind
+    B, R = 1 << 16, 10
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    results = []
+    for name in presets:
+        P = nttk.preset(name)
+        x = torch.randint(0, P.p, (B, P.size), generator=g, device="cuda", dtype=torch.int32)
+        y = torch.empty_like(x)
+        for kname in KIND_ORDER:
+            kind = K[kname]
+            for _ in range(3):
+                nttk.forward(P, kind, x, y)
+            samples = []
+            for _ in range(R):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                nttk.forward(P, kind, x, y)
+                e1.record()
+                torch.cuda.synchronize()
+                samples.append(e0.elapsed_time(e1) * 1e3 / B)  # us per polynomial
+            m = float(np.mean(samples))
+            results.append({"preset": name, "kind": kname, "iters": B * R, "mean_us": m,
+                            "std_us": float(np.std(samples, ddof=1))})
+    try:
+        nv = subprocess.run(["nvcc", "--version"], capture_output=True, text=True).stdout.strip()
+        nv = nv.splitlines()[-1]
+    except Exception:
+        nv = "nvcc"
+    gpu = {"schema": 1, "mode": "transform", "iters": B * R, "seed": seed,
+           "machine": {"os": f"{platform.system()} {platform.release()} {platform.machine()}",
+                       "cpu": f"{torch.cuda.get_device_name(0)} (sm_100a), batched 2^16 polys/launch",
+                       "compiler": nv,
+                       "flags": "-O3 -gencode arch=compute_100a,code=sm_100a"},
+           "results": results, "gains": pairwise_gains(results)}
+    os.makedirs(outdir, exist_ok=True)
+    with open(os.path.join(outdir, "gpu_bench_report.json"), "w") as fh:
+        json.dump(gpu, fh, indent=1)
+    cpu = None
+    from oracle.oracle import Reference, reference_available
+
+    if reference_available():
+        cpu = Reference().run_bench(presets, iters=2000, seed=seed)
+        with open(os.path.join(outdir, "cpu_reference_bench_report.json"), "w") as fh:
+            json.dump(cpu, fh, indent=1)
+    lines = ["| preset | kind | GPU us/poly | CPU reference us/poly (1 thread) | ratio |",
+             "|---|---|---|---|---|"]
+    cmap = {(r["preset"], r["kind"]): r["mean_us"] for r in (cpu or {}).get("results", [])}
+    for r in results:
+        c = cmap.get((r["preset"], r["kind"]))
+        lines.append(f"| {r['preset']} | {r['kind']} | {r['mean_us']:.5f} | "
+                     f"{'' if c is None else f'{c:.3f}'} | {'' if c is None else f'{c / r['mean_us']:.0f}x'} |")
+    with open(os.path.join(outdir, "bench_report.md"), "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    return 0
+
+
 def main():
     a = parse()
+    if a.bench_report:
+        return bench_report(a.bench_report)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

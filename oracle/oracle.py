@@ -318,12 +318,31 @@ class Reference:
             L.ref_naive_dft.argtypes = [u64p, C.c_size_t, C.c_uint64, C.c_uint64, u64p]
             L.ref_time_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, u64p, C.c_size_t, C.c_int,
                                          C.POINTER(C.c_uint64)]
+            if hasattr(L, "ref_run_bench"):
+                L.ref_run_bench.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int,
+                                            C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
             Reference._lib = L
         self.lib = Reference._lib
 
     def _check(self, st):
         if st != 0:
             raise OracleError(st, self.lib.ref_last_error().decode())
+
+    def run_bench(self, presets=("kyber256", "falcon512", "falcon1024"), iters=2000, seed=12345,
+                  micro=False) -> dict:
+        """The reference's own run_bench (bench.hpp:334-361) -> its BenchReport JSON
+        (schema 1, bench.hpp:365-424), single-threaded as the reference is."""
+        import json
+
+        need = C.c_size_t(0)
+        args = (",".join(presets).encode(), iters, seed, int(micro))
+        cap = 1 << 20
+        while True:  # each call re-runs the benchmark: size the buffer generously
+            buf = C.create_string_buffer(cap)
+            self._check(self.lib.ref_run_bench(*args, buf, cap, C.byref(need)))
+            if need.value < cap:
+                return json.loads(buf.value.decode())
+            cap = 2 * need.value
 
     def params(self, p, N, n_bits, kinds=(IMPROVED,), exact=False) -> "RefParams":
         mask = 0

@@ -17,6 +17,10 @@
 #include <thread>
 #include <vector>
 
+#if __has_include("json.hpp")
+#define NTTK_REF_HAS_BENCH 1
+#include "nttk/bench.hpp"  // the reference's own timing harness (needs nlohmann json.hpp)
+#endif
 #include "nttk/oracle.hpp"
 #include "nttk/params.hpp"
 #include "nttk/reduction.hpp"
@@ -280,6 +284,46 @@ int ref_time_batch(void* hv, int kind, int mode, uint64_t* a, size_t batch, int 
         std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
     if (failed) throw contract_violation("ref_time_batch: a worker failed");
   });
+}
+
+// The reference's own run_bench (bench.hpp:334-361) at the given presets, serialised by
+// its own to_json (schema 1, bench.hpp:365-424) -- the CPU rows of the paper's Table 2.
+// Writes at most cap bytes of JSON into out; *need = full length.  Status 3 when this
+// shim was built without json.hpp.
+int ref_run_bench(const char* presets_csv, uint64_t iters, uint64_t seed, int micro, char* out,
+                  size_t cap, size_t* need) {
+#ifdef NTTK_REF_HAS_BENCH
+  return guarded([&] {
+    BenchOptions opt;
+    opt.presets.clear();
+    std::string cur;
+    for (const char* c = presets_csv;; ++c) {
+      if (*c == ',' || *c == 0) {
+        if (!cur.empty()) opt.presets.push_back(cur);
+        cur.clear();
+        if (*c == 0) break;
+      } else {
+        cur += *c;
+      }
+    }
+    opt.iters = iters;
+    opt.seed = seed;
+    opt.micro = micro != 0;
+    const BenchReport rep = run_bench(opt);
+    nlohmann::json j = rep;
+    const std::string txt = j.dump();
+    *need = txt.size();
+    if (out && cap) {
+      const size_t n = txt.size() < cap - 1 ? txt.size() : cap - 1;
+      std::memcpy(out, txt.data(), n);
+      out[n] = 0;
+    }
+  });
+#else
+  (void)presets_csv, (void)iters, (void)seed, (void)micro, (void)out, (void)cap, (void)need;
+  g_err = "ref_run_bench: shim built without json.hpp";
+  return 3;
+#endif
 }
 
 }  // extern "C"
