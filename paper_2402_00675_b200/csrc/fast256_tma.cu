@@ -40,8 +40,18 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + G::kStages * G::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + kConsumers * kScratchWords);
   uint64_t* empty = full + G::kStages;
+  using Tw = typename K::Tw;
+  Tw* tws = reinterpret_cast<Tw*>(smem + G::kSmem);  // lane twiddles (tws_on)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  init_barriers(full, empty, G::kStages);
+  if constexpr (tws_on<IO, 0>()) {
+    if (threadIdx.x < 16) {
+      Tw t[15];
+      fwd_twiddles<K, L, PER_INDEX>(t, A, threadIdx.x);
+#pragma unroll
+      for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
+    }
+  }
+  init_barriers(full, empty, G::kStages);  // __syncthreads: table visible
   if (warp == kConsumers) {
     if (lane == 0) produce<IO>(in, batch, stages, full, empty);
     return;
@@ -49,21 +59,27 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
   const int j = lane & 15, half = lane >> 4;
   Xpose X;
   X.init(scratch + warp * kScratchWords + half * 272, j);
-  typename K::Tw twl[15];
-  fwd_twiddles<K, L, PER_INDEX>(twl, A, j);
-
-  const size_t ntiles = (batch + kTile - 1) / kTile;
-  int k = 0;
-  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k % G::kStages;
-    const size_t poly = t * kTile + half * kConsumers + warp;
-    mbar_wait(&full[s], (k / G::kStages) & 1);
-    uint32_t v[16];
-    load_strided<IO, K::kSigned>(
-        v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
-    release_stage(&empty[s], lane);
-    fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
-    if (poly < batch) store_contiguous<IO>(out + poly * 256, j, v);
+  auto run = [&](const auto& twl) {
+    const size_t ntiles = (batch + kTile - 1) / kTile;
+    int k = 0;
+    for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+      const int s = k % G::kStages;
+      const size_t poly = t * kTile + half * kConsumers + warp;
+      mbar_wait(&full[s], (k / G::kStages) & 1);
+      uint32_t v[16];
+      load_strided<IO, K::kSigned>(
+          v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
+      release_stage(&empty[s], lane);
+      fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
+      if (poly < batch) store_contiguous<IO>(out + poly * 256, j, v);
+    }
+  };
+  if constexpr (tws_on<IO, 0>()) {
+    run(TwSmem<Tw>{tws + j});
+  } else {
+    Tw twl[15];
+    fwd_twiddles<K, L, PER_INDEX>(twl, A, j);
+    run(twl);
   }
 }
 
@@ -81,8 +97,18 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + G::kStages * G::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + kConsumers * kScratchWords);
   uint64_t* empty = full + G::kStages;
+  using Tw = typename K::Tw;
+  Tw* tws = reinterpret_cast<Tw*>(smem + G::kSmem);  // lane twiddles (tws_on)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  init_barriers(full, empty, G::kStages);
+  if constexpr (tws_on<IO, 1>()) {
+    if (threadIdx.x < 16) {
+      Tw t[15];
+      inv_twiddles<K, L>(t, A, threadIdx.x);
+#pragma unroll
+      for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
+    }
+  }
+  init_barriers(full, empty, G::kStages);  // __syncthreads: table visible
   if (warp == kConsumers) {
     if (lane == 0) produce<IO>(in, batch, stages, full, empty);
     return;
@@ -91,26 +117,32 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
   uint32_t* S = scratch + warp * kScratchWords + half * 272;
   Xpose X;
   X.init(S, j);
-  typename K::Tw twl[15];
-  inv_twiddles<K, L>(twl, A, j);
-
-  const size_t ntiles = (batch + kTile - 1) / kTile;
-  int k = 0;
-  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k % G::kStages;
-    const size_t poly = t * kTile + half * kConsumers + warp;
-    mbar_wait(&full[s], (k / G::kStages) & 1);
-    uint32_t v[16];
-    load_contiguous<IO, K::kSigned>(
-        v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
-    release_stage(&empty[s], lane);
-    constexpr int CM = MODE & 3;
-    if (CM != 2) {
+  auto run = [&](const auto& twl) {
+    const size_t ntiles = (batch + kTile - 1) / kTile;
+    int k = 0;
+    for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+      const int s = k % G::kStages;
+      const size_t poly = t * kTile + half * kConsumers + warp;
+      mbar_wait(&full[s], (k / G::kStages) & 1);
+      uint32_t v[16];
+      load_contiguous<IO, K::kSigned>(
+          v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
+      release_stage(&empty[s], lane);
+      constexpr int CM = MODE & 3;
+      if (CM != 2) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
+        for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
+      }
+      inv_body<K, L, CM == 2, (MODE & 4) != 0>(v, twl, A, X);
+      store_strided<IO>(out + poly * 256, j, v, S, X, poly < batch);
     }
-    inv_body<K, L, CM == 2, (MODE & 4) != 0>(v, twl, A, X);
-    store_strided<IO>(out + poly * 256, j, v, S, X, poly < batch);
+  };
+  if constexpr (tws_on<IO, 1>()) {
+    run(TwSmem<Tw>{tws + j});
+  } else {
+    Tw twl[15];
+    inv_twiddles<K, L>(twl, A, j);
+    run(twl);
   }
 }
 
@@ -141,9 +173,9 @@ cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs
                          cudaStream_t st) {
   static int occ = 0;
   auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1>;
-  const int blocks = grid_for(kern, Geo<IO>::kSmem, occ, batch);
-  kern<<<blocks, kThreads, Geo<IO>::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out),
-                                                 batch, A);
+  constexpr int smem = Geo<IO>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  const int blocks = grid_for(kern, smem, occ, batch);
+  kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
   return cudaGetLastError();
 }
 
@@ -160,9 +192,9 @@ cudaError_t inv_launch_mode(const void* in, void* out, size_t batch, const FastA
                             cudaStream_t st) {
   static int occ = 0;
   auto kern = inv256_tma_kernel<K, IO, L, MODE>;
-  const int blocks = grid_for(kern, Geo<IO>::kSmem, occ, batch);
-  kern<<<blocks, kThreads, Geo<IO>::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out),
-                                                 batch, A);
+  constexpr int smem = Geo<IO>::kSmem + (tws_on<IO, 1>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  const int blocks = grid_for(kern, smem, occ, batch);
+  kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
   return cudaGetLastError();
 }
 

@@ -176,6 +176,26 @@ __device__ __forceinline__ void inv_bf(int sl, uint32_t& x, uint32_t& y, Tw w, u
   else K::inv(x, y, w, off, A);
 }
 
+// Lane-dependent twiddles read from shared memory instead of 15 registers per lane
+// (NTTK_TWS_MASK): entry i of lane j at S[16 i + j] -- consecutive lanes, consecutive
+// words, the two half-warps broadcast.  Frees 15 (n = 16) or 30 (n = 32) registers.
+template <class Tw>
+struct TwSmem {
+  const Tw* base;  // S + j
+  __device__ __forceinline__ Tw operator[](int i) const { return base[16 * i]; }
+};
+
+// Measured (B200, round 2): every combination is slower than registers -- e.g. the u32
+// inverse drops from 96 to 70 registers (2 -> 3 CTAs/SM) yet runs 1.7 % slower (1.032 ->
+// 1.050 ms): these kernels are bound by FMA/ALU pipe scheduling, not by occupancy.
+#ifndef NTTK_TWS_MASK
+#define NTTK_TWS_MASK 0x0  // bit0 fwd u16, bit1 fwd u32, bit2 inv u16, bit3 inv u32
+#endif
+template <class IO, int DIR>
+__host__ __device__ constexpr bool tws_on() {
+  return (NTTK_TWS_MASK >> (2 * DIR + (sizeof(IO) == 4 ? 1 : 0))) & 1;
+}
+
 // producer: stream tiles of kTile polynomials into the stage ring
 template <class IO>
 __device__ __forceinline__ void produce(const IO* in, size_t batch, uint8_t* stages, uint64_t* full,
@@ -249,9 +269,9 @@ __device__ __forceinline__ void inv_twiddles(typename K::Tw (&twl)[15], const Fa
 // W1 (A.flags bit 4, improved kinds on the cyclic tree): block 0 of layers 1 and 2 has
 // twiddle omega^0 = 1 and canonical-or-< 2p inputs, so its Plantard product needs no
 // multiply (fwd_w1); input coefficients must be canonical (the ntt_forward contract).
-template <class K, int L, bool PER_INDEX, bool W1 = false>
-__device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
-                                         const FastArgs& A, const Xpose& X) {
+template <class K, int L, bool PER_INDEX, bool W1 = false, class TWL>
+__device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                         const Xpose& X) {
   using Tw = typename K::Tw;
 #pragma unroll
   for (int sl = 1; sl <= 4; ++sl) {  // phase 1: layers 1..4
@@ -324,9 +344,9 @@ struct w1_of<K, std::void_t<decltype(&K::fwd_w1)>> {
 // layer of half-span h the words at (r & h) hold pre-quotient h-values; the next layer
 // (span 2h) pairs them with each other, so "both inputs lazy" is the compile-time test
 // r & (h_prev).  Lazy words are materialised before the transpose.
-template <class K, int L, bool FUSE>
-__device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
-                                              const FastArgs& A, const Xpose& X) {
+template <class K, int L, bool FUSE, class TWL>
+__device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                              const Xpose& X) {
   using Tw = typename K::Tw;
   constexpr int TL = 1 << L;
 #pragma unroll
@@ -386,9 +406,9 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const typename 
 // run_merge_layers + final N^{-1} (transform.hpp:99-116, 323-335): contiguous in
 // (canonical unless FUSE) -> strided out (canonical).  FUSE: u16 raw input, fused first
 // merge layer (A.flags bit 2, improved n = 16 only).
-template <class K, int L, bool FUSE>
-__device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
-                                               const FastArgs& A, const Xpose& X) {
+template <class K, int L, bool FUSE, class TWL>
+__device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                               const Xpose& X) {
   using Tw = typename K::Tw;
   constexpr int TL = 1 << L;
 #pragma unroll
@@ -438,9 +458,9 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const typename
 }
 
 // LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3).
-template <class K, int L, bool FUSE, bool LAZY = false>
-__device__ __forceinline__ void inv_body(uint32_t (&v)[16], const typename K::Tw (&twl)[15],
-                                         const FastArgs& A, const Xpose& X) {
+template <class K, int L, bool FUSE, bool LAZY = false, class TWL>
+__device__ __forceinline__ void inv_body(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                         const Xpose& X) {
   if constexpr (LAZY) {
     static_assert(lazy_of<K>::value, "policy has no lazy merge");
     inv_body_lazy<K, L, FUSE>(v, twl, A, X);
