@@ -204,6 +204,30 @@ def test_fastn_transforms_vs_oracle(oracle, N, n, kind, tree):
             assert (from_dev(nttk.inverse(P, kind, to_dev(spec, elem))) == want_inv).all(), elem
 
 
+@pytest.mark.parametrize("N", [512, 1024])
+def test_fastn_inplace_and_misaligned(oracle, N):
+    """In-place calls (d_in == d_out) on the fast N = 512/1024 kernels, and a buffer that
+    is not 16-byte aligned (falls back to the generic kernel) -- same words either way."""
+    p = 12289
+    P = engine_params(p, N, 32, [IMPROVED])
+    Q = oracle.params(p, N, 32, (IMPROVED,))
+    B = 21
+    f = oracle.rng(31 + N, p, B * N).reshape(B, N)
+    want = Q.forward(IMPROVED, f)
+    x = to_dev(f, 4)
+    nttk.forward(P, IMPROVED, x, x)  # in place
+    assert (from_dev(x) == want).all()
+    nttk.inverse(P, IMPROVED, x, x)
+    assert (from_dev(x) == f).all()
+    # offset by one coefficient: 4-byte aligned only
+    buf = torch.zeros(B * N + 1, dtype=torch.int32, device="cuda")
+    view = buf[1:].view(B, N)
+    view.copy_(to_dev(f, 4))
+    out = torch.zeros_like(buf)[1:].view(B, N)
+    nttk.forward(P, IMPROVED, view, out)
+    assert (from_dev(out) == want).all()
+
+
 def test_fastn_presets_all_kinds(oracle):
     """The reference presets at N = 512 / 1024 (params.hpp:280-289) on the fast kernels."""
     for name, p, N in (("newhope512", 12289, 512), ("falcon1024", 12289, 1024)):
