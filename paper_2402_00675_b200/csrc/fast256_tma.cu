@@ -70,7 +70,11 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
       load_strided<IO, K::kSigned>(
           v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
       release_stage(&empty[s], lane);
+#ifndef NTTK_COPY_ONLY  // A/B: the pipeline alone (loads, stores; no butterflies)
       fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
+#else
+      (void)twl;
+#endif
       if (poly < batch) store_contiguous<IO>(out + poly * 256, j, v);
     }
   };
