@@ -70,13 +70,45 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
       load_strided<IO, K::kSigned>(
           v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
       release_stage(&empty[s], lane);
+#ifdef NTTK_BULK_STORE
+      if (j == 0) bulk_wait_read();  // previous tile's bulk store has read the tile
+      __syncwarp();
+#endif
 #ifndef NTTK_COPY_ONLY  // A/B: the pipeline alone (loads, stores; no butterflies)
       fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
 #else
       (void)twl;
 #endif
+#ifdef NTTK_BULK_STORE
+      // A/B: natural-order poly into this half-warp's transpose tile, one 256-coefficient
+      // bulk store (async proxy) instead of per-lane 16-byte stores.  Measured (round 2):
+      // lifts the copy-only u32 pipeline 5.56 -> 5.72 TB/s, but with the butterflies the
+      // extra shared stores and waits make the forward 5-9 % slower -- off by default.
+      {
+        uint32_t* T = scratch + warp * kScratchWords + half * 272;
+        __syncwarp();
+        if constexpr (sizeof(IO) == 4) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            reinterpret_cast<uint4*>(T)[4 * j + c] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            reinterpret_cast<uint4*>(T)[2 * j + c] =
+                make_uint4(__byte_perm(v[8 * c], v[8 * c + 1], 0x5410), __byte_perm(v[8 * c + 2], v[8 * c + 3], 0x5410),
+                           __byte_perm(v[8 * c + 4], v[8 * c + 5], 0x5410), __byte_perm(v[8 * c + 6], v[8 * c + 7], 0x5410));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (j == 0 && poly < batch) bulk_s2g(out + poly * 256, T, 256 * sizeof(IO));
+      }
+#else
       if (poly < batch) store_contiguous<IO>(out + poly * 256, j, v);
+#endif
     }
+#ifdef NTTK_BULK_STORE
+    if (j == 0) bulk_wait_all();
+#endif
   };
   if constexpr (tws_on<IO, 0>()) {
     run(TwSmem<Tw>{tws + j});
