@@ -152,6 +152,41 @@ enum nttk_redc {
 int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, const int64_t* d_A,
                       size_t na, const int64_t* d_B, size_t nb, int64_t* d_r,
                       uint64_t* h_checksum, void* stream);
+/* ---- reduction.hpp on arrays (the drop-in behind nttk::mont_redc & co.) ---------- */
+
+/* ReductionContext (reduction.hpp:44-78): every precomputed constant of (p, n, alpha, ell) */
+typedef struct nttk_reduction_ctx {
+  uint64_t p;
+  uint32_t n_bits, alpha, ell, pad_;
+  uint64_t beta, beta_mask, r2n_mask;
+  uint64_t p_inv_beta, neg_p_inv_beta, mu;
+  int64_t mu_centered;
+  uint64_t beta_mod_p, r2n_mod_p;
+} nttk_reduction_ctx;
+
+/* make_reduction_context (reduction.hpp:80-117): same validation, same messages */
+int nttk_make_reduction_context(uint64_t p, uint32_t n_bits, uint32_t alpha, uint32_t ell,
+                                nttk_reduction_ctx* out);
+
+enum nttk_reduce_op {
+  NTTK_OP_MONT_REDC = 0,              /* x = T in [0, p^2)          reduction.hpp:125-135 */
+  NTTK_OP_SIGNED_MONT_REDC = 1,       /* x = A, |A| < p 2^{n-1}     reduction.hpp:141-165 */
+  NTTK_OP_PLANTARD_REDC = 2,          /* x = W, y = T in [0, p]     reduction.hpp:178-191 */
+  NTTK_OP_MODIFIED_PLANTARD_MUL = 3,  /* x = W < p, y = T < 2^ell p reduction.hpp:264-273 */
+  NTTK_OP_TO_PLANTARD_DOMAIN = 4,     /* x = w < p                  reduction.hpp:279-283 */
+  NTTK_OP_TO_MONTGOMERY_DOMAIN = 5    /* x = w < p                  reduction.hpp:287-291 */
+};
+
+/* out[i] = op(x[i] [, y[i]]) for i < n on device arrays of int64 words (the unsigned ops
+ * read them as uint64).  The context bound of the op and every operand are checked like the
+ * reference's NTTK_REQUIRE; a violation returns NTTK_CONTRACT with the reference's message
+ * (operands are checked on the device: the call synchronises `stream`). */
+int nttk_reduce(int op, const nttk_reduction_ctx* ctx, const int64_t* d_x, const int64_t* d_y,
+                int64_t* d_out, size_t n, void* stream);
+/* same on host arrays (staged through the device; synchronous) */
+int nttk_reduce_host(int op, const nttk_reduction_ctx* ctx, const int64_t* h_x, const int64_t* h_y,
+                     int64_t* h_out, size_t n);
+
 /* ---- diagnostics ------------------------------------------------------------ */
 
 /* message of the last failing call on this host thread ("" when none) */

@@ -22,6 +22,7 @@
 #include "fastn.hpp"
 #include "generic.hpp"
 #include "params.hpp"
+#include "reduce.hpp"
 #include "sweep.hpp"
 
 struct nttk_params_s {
@@ -565,6 +566,124 @@ int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, co
   if (d_sum) cudaFreeAsync(d_sum, st);
   if (e != cudaSuccess) return cuda_fail(e, "modmul_sweep");
   if (h_checksum) *h_checksum = sum;
+  return NTTK_OK;
+}
+
+// reduction.hpp:80-117
+int nttk_make_reduction_context(uint64_t p, uint32_t n_bits, uint32_t alpha, uint32_t ell,
+                                nttk_reduction_ctx* out) {
+  if (!out) return fail(NTTK_CONTRACT, "reduction context: null output");
+  if (n_bits < 2 || n_bits > 32)
+    return fail(NTTK_CONTRACT, "reduction context: word size n must be in [2, 32]");
+  if (p < 3 || !(p & 1)) return fail(NTTK_CONTRACT, "reduction context: p must be odd and >= 3");
+  if (p >= (uint64_t(1) << n_bits)) return fail(NTTK_CONTRACT, "reduction context: p must be < 2^n");
+  if (alpha >= n_bits) return fail(NTTK_CONTRACT, "reduction context: alpha must be < n");
+  if (ell >= n_bits) return fail(NTTK_CONTRACT, "reduction context: ell must be < n");
+  const nttk_b200::Ctx c = nttk_b200::make_ctx(p, n_bits, ell);
+  std::memset(out, 0, sizeof *out);
+  out->p = p;
+  out->n_bits = n_bits;
+  out->alpha = alpha;
+  out->ell = ell;
+  out->beta = c.beta;
+  out->beta_mask = c.beta_mask;
+  out->r2n_mask = c.r2n_mask;
+  out->p_inv_beta = c.p_inv_beta;
+  out->neg_p_inv_beta = c.neg_p_inv_beta;
+  out->mu = c.mu;
+  if (2 * n_bits == 64) {
+    out->mu_centered = static_cast<int64_t>(c.mu);
+  } else {
+    const uint64_t half = uint64_t(1) << (2 * n_bits - 1);
+    out->mu_centered = c.mu >= half ? static_cast<int64_t>(c.mu) -
+                                          static_cast<int64_t>(uint64_t(1) << (2 * n_bits))
+                                    : static_cast<int64_t>(c.mu);
+  }
+  out->beta_mod_p = c.beta_mod_p;
+  out->r2n_mod_p = c.r2n_mod_p;
+  return NTTK_OK;
+}
+
+namespace {
+// per-op context bound and the operand-range messages (reduction.hpp:64-77, 125-291)
+int reduce_precheck(int op, const nttk_reduction_ctx* c) {
+  using nttk_b200::u128;
+  if (!c) return fail(NTTK_CONTRACT, "reduce: null context");
+  if (op < NTTK_OP_MONT_REDC || op > NTTK_OP_TO_MONTGOMERY_DOMAIN)
+    return fail(NTTK_CONTRACT, "reduce: unknown operation");
+  const uint64_t p = c->p;
+  const unsigned n = c->n_bits;
+  if (op == NTTK_OP_SIGNED_MONT_REDC && !(u128(2) * p < (u128(1) << n)))
+    return fail(NTTK_CONTRACT, "signed_mont_redc: requires 2p < 2^n");
+  if (op == NTTK_OP_PLANTARD_REDC) {
+    const u128 d = (u128(1) << (n + 1)) - p;
+    if (!(u128(5) * p * p < d * d)) return fail(NTTK_CONTRACT, "plantard_redc: requires p*phi < 2^n");
+  }
+  if (op == NTTK_OP_MODIFIED_PLANTARD_MUL &&
+      !(c->ell + 2 < n && u128(p) < (u128(1) << (n - c->ell - 2))))
+    return fail(NTTK_CONTRACT, "modified_plantard_mul: requires p < 2^{n-ell-2}");
+  return NTTK_OK;
+}
+
+int reduce_flag_message(int op, unsigned flag) {
+  static const char* const first[] = {
+      "mont_redc: T must be < p^2", "signed_mont_redc: A out of (-p*2^{n-1}, p*2^{n-1})",
+      "plantard_redc: inputs exceed p", "modified_plantard_mul: W must be < p",
+      "to_plantard_domain: w must be < p", "to_montgomery_domain: w must be < p"};
+  if (flag & 1u) return fail(NTTK_CONTRACT, first[op]);
+  return fail(NTTK_CONTRACT, "modified_plantard_mul: T must be < 2^ell * p");
+}
+}  // namespace
+
+int nttk_reduce(int op, const nttk_reduction_ctx* ctx, const int64_t* d_x, const int64_t* d_y,
+                int64_t* d_out, size_t n, void* stream) {
+  if (int s = reduce_precheck(op, ctx)) return s;
+  const bool binary = op == NTTK_OP_PLANTARD_REDC || op == NTTK_OP_MODIFIED_PLANTARD_MUL;
+  if (n && (!d_x || !d_out || (binary && !d_y))) return fail(NTTK_CONTRACT, "reduce: null buffer");
+  if (int s = need_device("reduce")) return s;
+  if (!n) return NTTK_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned* d_flag = nullptr;
+  cudaError_t e = cudaMallocAsync(&d_flag, sizeof(unsigned), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_flag, 0, sizeof(unsigned), st);
+  if (e == cudaSuccess) e = nttk_b200::reduce_launch(op, *ctx, d_x, d_y, d_out, n, d_flag, st);
+  ++g_launches;
+  unsigned flag = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, d_flag, sizeof flag, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (d_flag) cudaFreeAsync(d_flag, st);
+  if (e != cudaSuccess) return cuda_fail(e, "reduce");
+  if (flag) return reduce_flag_message(op, flag);
+  return NTTK_OK;
+}
+
+int nttk_reduce_host(int op, const nttk_reduction_ctx* ctx, const int64_t* h_x, const int64_t* h_y,
+                     int64_t* h_out, size_t n) {
+  if (int s = reduce_precheck(op, ctx)) return s;
+  const bool binary = op == NTTK_OP_PLANTARD_REDC || op == NTTK_OP_MODIFIED_PLANTARD_MUL;
+  if (n && (!h_x || !h_out || (binary && !h_y))) return fail(NTTK_CONTRACT, "reduce: null buffer");
+  if (int s = need_device("reduce")) return s;
+  if (!n) return NTTK_OK;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  int64_t* d = nullptr;
+  const size_t bytes = n * sizeof(int64_t);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d, 3 * bytes, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, h_x, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && binary) e = cudaMemcpyAsync(d + n, h_y, bytes, cudaMemcpyHostToDevice, st);
+  int rc = NTTK_OK;
+  if (e == cudaSuccess) {
+    rc = nttk_reduce(op, ctx, d, d + n, d + 2 * n, n, st);
+    if (rc == NTTK_OK) e = cudaMemcpyAsync(h_out, d + 2 * n, bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  if (d) cudaFreeAsync(d, st);
+  if (st) {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
+  if (rc != NTTK_OK) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "reduce");
   return NTTK_OK;
 }
 

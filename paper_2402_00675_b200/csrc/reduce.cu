@@ -1,0 +1,118 @@
+// reduce.cu -- the reference's word-level reductions (reduction.hpp:125-291) applied
+// elementwise to device arrays: the drop-in behind nttk::mont_redc & co.
+//
+// Each op restates the published formula in exact 64/128-bit arithmetic (bit-identical with
+// the reference for every admitted input) and checks its operand range on the device like
+// the reference's NTTK_REQUIRE; a violation sets a bit in *flag (the host turns it into the
+// reference's message) and the element is left unwritten.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "reduce.hpp"
+
+namespace nttk_b200 {
+namespace {
+
+using u128 = unsigned __int128;
+
+struct RArgs {
+  uint64_t p, beta_mask, r2n_mask, p_inv_beta, neg_p_inv_beta, mu, beta, beta_mod_p, r2n_mod_p;
+  uint32_t n_bits, ell;
+};
+
+template <int OP>
+__global__ void reduce_kernel(const int64_t* __restrict__ x, const int64_t* __restrict__ y,
+                              int64_t* __restrict__ out, size_t n, RArgs R, unsigned* flag) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const uint64_t p = R.p;
+    if (OP == NTTK_OP_MONT_REDC) {  // reduction.hpp:125-135
+      const uint64_t T = static_cast<uint64_t>(x[i]);
+      if (!(T < p * p)) {
+        atomicOr(flag, 1u);
+        continue;
+      }
+      const uint64_t m = ((T & R.beta_mask) * R.neg_p_inv_beta) & R.beta_mask;
+      uint64_t t = static_cast<uint64_t>((u128(T) + u128(m) * p) >> R.n_bits);
+      if (t >= p) t -= p;
+      out[i] = static_cast<int64_t>(t);
+    } else if (OP == NTTK_OP_SIGNED_MONT_REDC) {  // reduction.hpp:141-165
+      const int64_t A = x[i];
+      const __int128 limit = (__int128(p) << R.n_bits) / 2;
+      if (!(-limit < A && A < limit)) {
+        atomicOr(flag, 1u);
+        continue;
+      }
+      const int64_t a1 = A >> R.n_bits;
+      const uint64_t a0 = static_cast<uint64_t>(A) & R.beta_mask;
+      const uint64_t mu = (a0 * R.p_inv_beta) & R.beta_mask;
+      const int64_t m = mu >= R.beta / 2 ? static_cast<int64_t>(mu) - static_cast<int64_t>(R.beta)
+                                         : static_cast<int64_t>(mu);
+      out[i] = a1 - ((m * static_cast<int64_t>(p)) >> R.n_bits);
+    } else if (OP == NTTK_OP_PLANTARD_REDC || OP == NTTK_OP_MODIFIED_PLANTARD_MUL) {
+      const uint64_t W = static_cast<uint64_t>(x[i]), T = static_cast<uint64_t>(y[i]);
+      if (OP == NTTK_OP_PLANTARD_REDC) {  // reduction.hpp:178-191
+        if (!(W <= p && T <= p)) {
+          atomicOr(flag, 1u);
+          continue;
+        }
+      } else {  // reduction.hpp:264-273: W checked first, then T
+        if (!(W < p)) {
+          atomicOr(flag, 1u);
+          continue;
+        }
+        if (!(T < (p << R.ell))) {
+          atomicOr(flag, 2u);
+          continue;
+        }
+      }
+      const uint64_t h = ((W * T) * R.mu) & R.r2n_mask;
+      const uint64_t r = (((h >> R.n_bits) + 1) * p) >> R.n_bits;
+      out[i] = static_cast<int64_t>(OP == NTTK_OP_PLANTARD_REDC && r == p ? 0 : r);
+    } else {  // domain encodings, reduction.hpp:279-291
+      const uint64_t w = static_cast<uint64_t>(x[i]);
+      if (!(w < p)) {
+        atomicOr(flag, 1u);
+        continue;
+      }
+      const uint64_t v = OP == NTTK_OP_TO_PLANTARD_DOMAIN
+                             ? (p - static_cast<uint64_t>(u128(w) * R.r2n_mod_p % p)) % p
+                             : static_cast<uint64_t>(u128(w) * R.beta_mod_p % p);
+      out[i] = static_cast<int64_t>(v);
+    }
+  }
+}
+
+template <int OP>
+cudaError_t launch(const int64_t* x, const int64_t* y, int64_t* out, size_t n, const RArgs& R,
+                   unsigned* flag, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t want = (n + 255) / 256, cap = size_t(sms) * 8;
+  reduce_kernel<OP><<<static_cast<unsigned>(want < cap ? (want ? want : 1) : cap), 256, 0, st>>>(
+      x, y, out, n, R, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t reduce_launch(int op, const nttk_reduction_ctx& c, const int64_t* x, const int64_t* y,
+                          int64_t* out, size_t n, unsigned* d_flag, cudaStream_t st) {
+  RArgs R{c.p,          c.beta_mask, c.r2n_mask,   c.p_inv_beta, c.neg_p_inv_beta, c.mu,
+          c.beta,       c.beta_mod_p, c.r2n_mod_p, c.n_bits,     c.ell};
+  switch (op) {
+    case NTTK_OP_MONT_REDC: return launch<NTTK_OP_MONT_REDC>(x, y, out, n, R, d_flag, st);
+    case NTTK_OP_SIGNED_MONT_REDC: return launch<NTTK_OP_SIGNED_MONT_REDC>(x, y, out, n, R, d_flag, st);
+    case NTTK_OP_PLANTARD_REDC: return launch<NTTK_OP_PLANTARD_REDC>(x, y, out, n, R, d_flag, st);
+    case NTTK_OP_MODIFIED_PLANTARD_MUL:
+      return launch<NTTK_OP_MODIFIED_PLANTARD_MUL>(x, y, out, n, R, d_flag, st);
+    case NTTK_OP_TO_PLANTARD_DOMAIN: return launch<NTTK_OP_TO_PLANTARD_DOMAIN>(x, y, out, n, R, d_flag, st);
+    case NTTK_OP_TO_MONTGOMERY_DOMAIN:
+      return launch<NTTK_OP_TO_MONTGOMERY_DOMAIN>(x, y, out, n, R, d_flag, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace nttk_b200

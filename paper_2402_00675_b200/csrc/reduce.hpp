@@ -1,0 +1,17 @@
+// reduce.hpp -- launcher of the elementwise reduction kernels (reduce.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/nttk_gpu.h"
+
+namespace nttk_b200 {
+
+// out[i] = op(x[i] [, y[i]]); operand-range violations OR bits into *d_flag
+cudaError_t reduce_launch(int op, const nttk_reduction_ctx& c, const int64_t* x, const int64_t* y,
+                          int64_t* out, size_t n, unsigned* d_flag, cudaStream_t st);
+
+}  // namespace nttk_b200

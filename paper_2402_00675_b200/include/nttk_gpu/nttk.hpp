@@ -233,4 +233,134 @@ inline void intt_inverse_device(const NttParams& P, ButterflyKind kind, const vo
                                   elem_bytes, stream));
 }
 
+// ---- reductions (reduction.hpp:44-291), executed on the GPU ------------------------
+// Same names, arguments, results and contract messages as the reference; every call runs
+// the device kernel (reduce.cu).  The scalar overloads are for drop-in compatibility; the
+// std::vector overloads amortise the launch over many operands.
+
+struct ReductionContext {  // reduction.hpp:44-78
+  uint32_t p = 0;
+  unsigned n_bits = 0, alpha = 0, ell = 0;
+  uint64_t beta = 0, beta_mask = 0, r2n_mask = 0;
+  uint64_t p_inv_beta = 0, neg_p_inv_beta = 0, mu = 0;
+  int64_t mu_centered = 0;
+  uint64_t beta_mod_p = 0, r2n_mod_p = 0;
+
+  [[nodiscard]] unsigned two_n() const { return 2 * n_bits; }
+  [[nodiscard]] bool fits_plantard_bound() const {
+    const unsigned __int128 lhs = (unsigned __int128)5 * p * p;
+    const unsigned __int128 d = ((unsigned __int128)1 << (n_bits + 1)) - p;
+    return lhs < d * d;
+  }
+  [[nodiscard]] bool fits_signed_plantard_bound() const {
+    return alpha + 1 < n_bits && (unsigned __int128)p < ((unsigned __int128)1 << (n_bits - alpha - 1));
+  }
+  [[nodiscard]] bool fits_lazy_plantard_bound() const {
+    return ell + 2 < n_bits && (unsigned __int128)p < ((unsigned __int128)1 << (n_bits - ell - 2));
+  }
+  [[nodiscard]] bool fits_signed_montgomery_bound() const {
+    return (unsigned __int128)2 * p < ((unsigned __int128)1 << n_bits);
+  }
+  [[nodiscard]] nttk_reduction_ctx raw() const {
+    nttk_reduction_ctx c{};
+    c.p = p;
+    c.n_bits = n_bits;
+    c.alpha = alpha;
+    c.ell = ell;
+    c.beta = beta;
+    c.beta_mask = beta_mask;
+    c.r2n_mask = r2n_mask;
+    c.p_inv_beta = p_inv_beta;
+    c.neg_p_inv_beta = neg_p_inv_beta;
+    c.mu = mu;
+    c.mu_centered = mu_centered;
+    c.beta_mod_p = beta_mod_p;
+    c.r2n_mod_p = r2n_mod_p;
+    return c;
+  }
+};
+
+[[nodiscard]] inline ReductionContext make_reduction_context(uint64_t p, unsigned n_bits,
+                                                             unsigned alpha = 0, unsigned ell = 0) {
+  nttk_reduction_ctx c{};
+  detail::check(nttk_make_reduction_context(p, n_bits, alpha, ell, &c));
+  ReductionContext r;
+  r.p = static_cast<uint32_t>(c.p);
+  r.n_bits = c.n_bits;
+  r.alpha = c.alpha;
+  r.ell = c.ell;
+  r.beta = c.beta;
+  r.beta_mask = c.beta_mask;
+  r.r2n_mask = c.r2n_mask;
+  r.p_inv_beta = c.p_inv_beta;
+  r.neg_p_inv_beta = c.neg_p_inv_beta;
+  r.mu = c.mu;
+  r.mu_centered = c.mu_centered;
+  r.beta_mod_p = c.beta_mod_p;
+  r.r2n_mod_p = c.r2n_mod_p;
+  return r;
+}
+
+namespace detail {
+template <class Out, class In>
+inline std::vector<Out> reduce(int op, const ReductionContext& ctx, const std::vector<In>& x,
+                               const std::vector<In>* y = nullptr) {
+  if (y && y->size() != x.size()) throw contract_violation("reduce: operand lengths differ");
+  const nttk_reduction_ctx c = ctx.raw();
+  std::vector<int64_t> out(x.size());
+  check(nttk_reduce_host(op, &c, reinterpret_cast<const int64_t*>(x.data()),
+                         y ? reinterpret_cast<const int64_t*>(y->data()) : nullptr, out.data(),
+                         x.size()));
+  return std::vector<Out>(out.begin(), out.end());
+}
+}  // namespace detail
+
+[[nodiscard]] inline std::vector<uint64_t> mont_redc(const std::vector<uint64_t>& T,
+                                                     const ReductionContext& ctx) {
+  return detail::reduce<uint64_t>(NTTK_OP_MONT_REDC, ctx, T);
+}
+[[nodiscard]] inline std::vector<int64_t> signed_mont_redc(const std::vector<int64_t>& A,
+                                                           const ReductionContext& ctx) {
+  return detail::reduce<int64_t>(NTTK_OP_SIGNED_MONT_REDC, ctx, A);
+}
+[[nodiscard]] inline std::vector<uint64_t> plantard_redc(const std::vector<uint64_t>& W,
+                                                         const std::vector<uint64_t>& T,
+                                                         const ReductionContext& ctx) {
+  return detail::reduce<uint64_t>(NTTK_OP_PLANTARD_REDC, ctx, W, &T);
+}
+[[nodiscard]] inline std::vector<uint64_t> modified_plantard_mul(const std::vector<uint64_t>& W,
+                                                                 const std::vector<uint64_t>& T,
+                                                                 const ReductionContext& ctx) {
+  return detail::reduce<uint64_t>(NTTK_OP_MODIFIED_PLANTARD_MUL, ctx, W, &T);
+}
+[[nodiscard]] inline std::vector<uint64_t> to_plantard_domain(const std::vector<uint64_t>& w,
+                                                              const ReductionContext& ctx) {
+  return detail::reduce<uint64_t>(NTTK_OP_TO_PLANTARD_DOMAIN, ctx, w);
+}
+[[nodiscard]] inline std::vector<uint64_t> to_montgomery_domain(const std::vector<uint64_t>& w,
+                                                                const ReductionContext& ctx) {
+  return detail::reduce<uint64_t>(NTTK_OP_TO_MONTGOMERY_DOMAIN, ctx, w);
+}
+
+// scalar signatures of reduction.hpp
+[[nodiscard]] inline uint64_t mont_redc(uint64_t T, const ReductionContext& ctx) {
+  return mont_redc(std::vector<uint64_t>{T}, ctx)[0];
+}
+[[nodiscard]] inline int64_t signed_mont_redc(int64_t A, const ReductionContext& ctx) {
+  return signed_mont_redc(std::vector<int64_t>{A}, ctx)[0];
+}
+[[nodiscard]] inline uint64_t plantard_redc(uint64_t W, uint64_t T, const ReductionContext& ctx) {
+  return plantard_redc(std::vector<uint64_t>{W}, std::vector<uint64_t>{T}, ctx)[0];
+}
+[[nodiscard]] inline uint64_t modified_plantard_mul(uint64_t W, uint64_t T,
+                                                    const ReductionContext& ctx) {
+  return modified_plantard_mul(std::vector<uint64_t>{W}, std::vector<uint64_t>{T}, ctx)[0];
+}
+[[nodiscard]] inline uint64_t to_plantard_domain(uint64_t w, const ReductionContext& ctx) {
+  return to_plantard_domain(std::vector<uint64_t>{w}, ctx)[0];
+}
+[[nodiscard]] inline uint64_t to_montgomery_domain(uint64_t w, const ReductionContext& ctx) {
+  return to_montgomery_domain(std::vector<uint64_t>{w}, ctx)[0];
+}
+
 }  // namespace nttk

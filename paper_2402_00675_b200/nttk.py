@@ -90,6 +90,30 @@ class _Desc(C.Structure):
                 ("root", C.c_uint64), ("flags", C.c_uint32)]
 
 
+class ReductionContext(C.Structure):
+    """reduction.hpp:44-78 (nttk_reduction_ctx); build with make_reduction_context()."""
+    _fields_ = [("p", C.c_uint64), ("n_bits", C.c_uint32), ("alpha", C.c_uint32),
+                ("ell", C.c_uint32), ("pad_", C.c_uint32), ("beta", C.c_uint64),
+                ("beta_mask", C.c_uint64), ("r2n_mask", C.c_uint64), ("p_inv_beta", C.c_uint64),
+                ("neg_p_inv_beta", C.c_uint64), ("mu", C.c_uint64), ("mu_centered", C.c_int64),
+                ("beta_mod_p", C.c_uint64), ("r2n_mod_p", C.c_uint64)]
+
+    def two_n(self) -> int:
+        return 2 * self.n_bits
+
+    def fits_plantard_bound(self) -> bool:
+        return 5 * self.p * self.p < ((1 << (self.n_bits + 1)) - self.p) ** 2
+
+    def fits_signed_plantard_bound(self) -> bool:
+        return self.alpha + 1 < self.n_bits and self.p < (1 << (self.n_bits - self.alpha - 1))
+
+    def fits_lazy_plantard_bound(self) -> bool:
+        return self.ell + 2 < self.n_bits and self.p < (1 << (self.n_bits - self.ell - 2))
+
+    def fits_signed_montgomery_bound(self) -> bool:
+        return 2 * self.p < (1 << self.n_bits)
+
+
 class _Info(C.Structure):
     _fields_ = [("p", C.c_uint64), ("omega", C.c_uint64), ("omega_inv", C.c_uint64),
                 ("n_inv", C.c_uint64), ("n_inv_hat", C.c_uint64), ("mu", C.c_uint64),
@@ -103,8 +127,8 @@ EXPORTS = (
     "nttk_params_table", "nttk_ntt_forward", "nttk_intt_inverse", "nttk_pointwise_multiply",
     "nttk_basemul", "nttk_polymul", "nttk_ntt_forward_host", "nttk_intt_inverse_host",
     "nttk_roundtrip_host", "nttk_pointwise_multiply_host", "nttk_polymul_host",
-    "nttk_modmul_sweep", "nttk_last_error", "nttk_launch_count", "nttk_device_available",
-    "nttk_version",
+    "nttk_modmul_sweep", "nttk_make_reduction_context", "nttk_reduce", "nttk_reduce_host",
+    "nttk_last_error", "nttk_launch_count", "nttk_device_available", "nttk_version",
 )
 
 _lib_handle = None
@@ -137,6 +161,10 @@ def lib() -> C.CDLL:
             getattr(L, f).argtypes = [vp, C.c_int, vp, vp, vp, sz, C.c_int]
         L.nttk_modmul_sweep.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, vp, sz, vp,
                                         sz, vp, C.POINTER(C.c_uint64), vp]
+        L.nttk_make_reduction_context.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                                  C.POINTER(ReductionContext)]
+        L.nttk_reduce.argtypes = [C.c_int, C.POINTER(ReductionContext), vp, vp, vp, sz, vp]
+        L.nttk_reduce_host.argtypes = [C.c_int, C.POINTER(ReductionContext), vp, vp, vp, sz]
         L.nttk_last_error.restype = C.c_char_p
         L.nttk_launch_count.restype = C.c_uint64
         L.nttk_version.restype = C.c_char_p
@@ -472,3 +500,78 @@ def modmul_sweep(variant, p: int, n_bits: int, ell: int, A, B, r=None, stream=No
                                    B.data_ptr(), B.numel(), r.data_ptr() if r is not None else None,
                                    C.byref(s), _stream_ptr(stream)))
     return int(s.value)
+
+
+# ---------------------------------------------------------------------------
+# reduction.hpp: make_reduction_context + the word-level reductions, run on the GPU
+# (reduce.cu).  Scalars in -> scalar out (reference signatures); numpy arrays in ->
+# arrays out (one launch); `reduce` is the device-tensor form.
+
+OP_MONT_REDC, OP_SIGNED_MONT_REDC, OP_PLANTARD_REDC, OP_MODIFIED_PLANTARD_MUL = 0, 1, 2, 3
+OP_TO_PLANTARD_DOMAIN, OP_TO_MONTGOMERY_DOMAIN = 4, 5
+
+
+def make_reduction_context(p: int, n_bits: int, alpha: int = 0, ell: int = 0) -> ReductionContext:
+    """reduction.hpp:80-117 (same validation and messages)."""
+    c = ReductionContext()
+    _check(lib().nttk_make_reduction_context(p, n_bits, alpha, ell, C.byref(c)))
+    return c
+
+
+def _reduce_host(op, ctx, x, y=None):
+    scalar = np.isscalar(x)
+    xs = np.ascontiguousarray(np.atleast_1d(np.asarray(x)).astype(np.int64 if op == 1 else np.uint64)
+                              .view(np.int64))
+    ys = None
+    if y is not None:
+        ys = np.ascontiguousarray(np.atleast_1d(np.asarray(y)).astype(np.uint64).view(np.int64))
+        if ys.size != xs.size:
+            raise ContractViolation("reduce: operand lengths differ")
+    out = np.empty_like(xs)
+    _check(lib().nttk_reduce_host(op, C.byref(ctx), xs.ctypes.data,
+                                  ys.ctypes.data if ys is not None else None, out.ctypes.data,
+                                  xs.size))
+    res = out if op == OP_SIGNED_MONT_REDC else out.view(np.uint64)
+    return int(res[0]) if scalar else res
+
+
+def mont_redc(T, ctx: ReductionContext):
+    """reduction.hpp:125-135: T in [0, p^2) -> T 2^{-n} mod p."""
+    return _reduce_host(OP_MONT_REDC, ctx, T)
+
+
+def signed_mont_redc(A, ctx: ReductionContext):
+    """reduction.hpp:141-165: A in (-p 2^{n-1}, p 2^{n-1}) -> A 2^{-n} mod p in (-p, p)."""
+    return _reduce_host(OP_SIGNED_MONT_REDC, ctx, A)
+
+
+def plantard_redc(W, T, ctx: ReductionContext):
+    """reduction.hpp:178-191: W, T in [0, p] -> W T (-2^{-2n}) mod p."""
+    return _reduce_host(OP_PLANTARD_REDC, ctx, W, T)
+
+
+def modified_plantard_mul(W, T, ctx: ReductionContext):
+    """reduction.hpp:264-273: W < p, T < 2^ell p -> W T (-2^{-2n}) mod p (Alg. 10)."""
+    return _reduce_host(OP_MODIFIED_PLANTARD_MUL, ctx, W, T)
+
+
+def to_plantard_domain(w, ctx: ReductionContext):
+    """reduction.hpp:279-283."""
+    return _reduce_host(OP_TO_PLANTARD_DOMAIN, ctx, w)
+
+
+def to_montgomery_domain(w, ctx: ReductionContext):
+    """reduction.hpp:287-291."""
+    return _reduce_host(OP_TO_MONTGOMERY_DOMAIN, ctx, w)
+
+
+def reduce(op: int, ctx: ReductionContext, x, y=None, out=None, stream=None):
+    """Elementwise reduction on int64 CUDA tensors (synchronises `stream`: operand ranges
+    are checked on the device like the reference's NTTK_REQUIRE)."""
+    import torch
+
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().nttk_reduce(int(op), C.byref(ctx), x.data_ptr(),
+                             y.data_ptr() if y is not None else None, out.data_ptr(), x.numel(),
+                             _stream_ptr(stream)))
+    return out

@@ -180,6 +180,41 @@ int main() {
       }
     }
   }
+  // reduction.hpp through the GPU: the reference's known answers (reduction_test.cpp:11-190)
+  {
+    const ReductionContext c = make_reduction_context(13, 8, 0, 2);
+    CHECK(c.mu == 20165 && c.fits_plantard_bound() && c.fits_lazy_plantard_bound());
+    CHECK(mont_redc(100, make_reduction_context(17, 5)) == 1);
+    const ReductionContext s = make_reduction_context(17, 6);
+    CHECK(signed_mont_redc(100, s) == 9 && signed_mont_redc(-100, s) == -9);
+    CHECK(plantard_redc(5, 12, make_reduction_context(13, 8)) == 6);
+    CHECK(modified_plantard_mul(5, 20, c) == 10 && modified_plantard_mul(1, 1, c) == 4);
+    CHECK(to_plantard_domain(7, c) == 5);
+    for (uint64_t w = 0; w < 13; ++w) {
+      CHECK(to_montgomery_domain(w, c) == w * 256 % 13);
+      CHECK(modified_plantard_mul(to_plantard_domain(w, c), 1, c) == w);
+    }
+    // batched: the exhaustive Montgomery range of (17, n=5) in one call
+    const ReductionContext m = make_reduction_context(17, 5);
+    std::vector<uint64_t> T(17 * 17);
+    for (uint64_t t = 0; t < T.size(); ++t) T[t] = t;
+    const auto r = mont_redc(T, m);
+    uint64_t inv32 = 0;  // 2^{-5} mod 17
+    for (uint64_t v = 1; v < 17; ++v)
+      if (v * 32 % 17 == 1) inv32 = v;
+    bool all = true;
+    for (uint64_t t = 0; t < T.size(); ++t) all = all && r[t] == t * inv32 % 17;
+    CHECK(all);
+    // contract messages of the reference
+    CHECK(throws_with([&] { (void)mont_redc(17 * 17, m); }, "mont_redc: T must be < p^2"));
+    CHECK(throws_with([&] { (void)modified_plantard_mul(13, 0, c); }, "W must be < p"));
+    CHECK(throws_with([&] { (void)modified_plantard_mul(0, 52, c); }, "T must be < 2^ell * p"));
+    CHECK(throws_with([&] { (void)plantard_redc(14, 0, make_reduction_context(13, 8)); },
+                      "inputs exceed p"));
+    CHECK(throws_with([] { (void)make_reduction_context(12, 8); }, "p must be odd"));
+    CHECK(throws_with([] { (void)modified_plantard_mul(1, 1, make_reduction_context(17, 8, 0, 2)); },
+                      "requires p < 2^{n-ell-2}"));
+  }
   std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }

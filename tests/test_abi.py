@@ -38,6 +38,27 @@ def test_no_gpu_fails_loudly(engine):
     P = engine.build_params(3329, 256, 16, [engine.ButterflyKind.improved], exact_bound=True)
     with pytest.raises(engine.CudaError, match="no CUDA device"):
         engine.ntt_forward_batch(np.zeros((2, 256), dtype=np.uint16), P, 3)
+    with pytest.raises(engine.CudaError, match="no CUDA device"):  # reductions too
+        engine.mont_redc(100, engine.make_reduction_context(17, 5))
+
+
+@pytest.mark.parametrize("p,n,alpha,ell", [(13, 8, 0, 2), (17, 5, 0, 0), (3329, 16, 1, 2),
+                                           (8380417, 32, 0, 7), (4294967291, 32, 3, 1)])
+def test_reduction_context_matches_oracle(engine, oracle, p, n, alpha, ell):
+    """make_reduction_context (reduction.hpp:80-117): host precompute == the oracle's."""
+    c = engine.make_reduction_context(p, n, alpha, ell)
+    o = oracle.ctx(p, n, alpha, ell)
+    for f in ("p", "n_bits", "alpha", "ell", "beta", "beta_mask", "r2n_mask", "p_inv_beta",
+              "neg_p_inv_beta", "mu", "mu_centered", "beta_mod_p", "r2n_mod_p"):
+        assert getattr(c, f) == getattr(o, f), f
+
+
+def test_reduction_context_messages(engine):
+    for args, msg in (((13, 1), "word size n must be in [2, 32]"), ((12, 8), "odd and >= 3"),
+                      ((301, 8), "p must be < 2^n"), ((13, 8, 8), "alpha must be < n"),
+                      ((13, 8, 0, 8), "ell must be < n")):
+        with pytest.raises(engine.ContractViolation, match=re.escape(msg)):
+            engine.make_reduction_context(*args)
 
 
 CONFIGS = [

@@ -131,3 +131,89 @@ def test_transform_properties(oracle, p, N, n, tree, exact):
                 continue  # signed spectra are two's complement words: only smont reads them
             back = nttk.inverse(P2, k2, y)
             assert (back.cpu().numpy() == f).all(), (k, k2)
+
+
+# ---------------------------------------------------------------------------
+# reduction.hpp signatures on the GPU (nttk_reduce): the reference's known answers,
+# exhaustive toy ranges and random production operands vs the oracle, contract messages
+
+def test_reductions_known_answers():
+    c = nttk.make_reduction_context(13, 8, 0, 2)
+    assert c.mu == 20165
+    assert nttk.mont_redc(100, nttk.make_reduction_context(17, 5)) == 1
+    s = nttk.make_reduction_context(17, 6)
+    assert nttk.signed_mont_redc(100, s) == 9 and nttk.signed_mont_redc(-100, s) == -9
+    assert nttk.plantard_redc(5, 12, nttk.make_reduction_context(13, 8)) == 6
+    assert nttk.modified_plantard_mul(5, 20, c) == 10 and nttk.modified_plantard_mul(1, 1, c) == 4
+    assert nttk.to_plantard_domain(7, c) == 5
+
+
+@pytest.mark.parametrize("p,n,alpha,ell", [(13, 8, 0, 2), (17, 6, 0, 1), (31, 8, 1, 1)])
+def test_elementwise_reductions_exhaustive_toy(oracle, p, n, alpha, ell):
+    c = nttk.make_reduction_context(p, n, alpha, ell)
+    o = oracle.ctx(p, n, alpha, ell)
+    T = np.arange(p * p, dtype=np.uint64)
+    assert (nttk.mont_redc(T, c) == [oracle.mont_redc(int(t), o) for t in T]).all()
+    if c.fits_signed_montgomery_bound():
+        lim = p << (n - 1)
+        A = np.arange(-lim + 1, lim, dtype=np.int64)
+        assert (nttk.signed_mont_redc(A, c) == [oracle.signed_mont_redc(int(a), o) for a in A]).all()
+    W, Tt = np.meshgrid(np.arange(p + 1, dtype=np.uint64), np.arange(p + 1, dtype=np.uint64))
+    W, Tt = W.ravel(), Tt.ravel()
+    if c.fits_plantard_bound():
+        assert (nttk.plantard_redc(W, Tt, c) ==
+                [oracle.plantard_redc(int(a), int(b), o) for a, b in zip(W, Tt)]).all()
+    if c.fits_lazy_plantard_bound():
+        W2, T2 = np.meshgrid(np.arange(p, dtype=np.uint64), np.arange(p << ell, dtype=np.uint64))
+        W2, T2 = W2.ravel(), T2.ravel()
+        assert (nttk.modified_plantard_mul(W2, T2, c) ==
+                [oracle.modified_plantard_mul(int(a), int(b), o) for a, b in zip(W2, T2)]).all()
+    w = np.arange(p, dtype=np.uint64)
+    assert (nttk.to_plantard_domain(w, c) == [oracle.to_plantard_domain(int(v), o) for v in w]).all()
+    assert (nttk.to_montgomery_domain(w, c) == [oracle.to_montgomery_domain(int(v), o) for v in w]).all()
+
+
+@pytest.mark.parametrize("p,n,ell", [(3329, 16, 2), (8380417, 32, 7)])
+def test_elementwise_reductions_random_production(oracle, p, n, ell):
+    """10^5 random operands per op through the device-tensor API vs the oracle."""
+    rng = np.random.default_rng(p + n)
+    c = nttk.make_reduction_context(p, n, 0, ell)
+    o = oracle.ctx(p, n, 0, ell)
+    m = 100000
+    cases = [(nttk.OP_MONT_REDC, rng.integers(0, p * p, m, dtype=np.uint64), None,
+              lambda a, b: oracle.mont_redc(a, o)),
+             (nttk.OP_SIGNED_MONT_REDC, rng.integers(-(p << (n - 1)) + 1, p << (n - 1), m,
+                                                     dtype=np.int64), None,
+              lambda a, b: oracle.signed_mont_redc(a, o)),
+             (nttk.OP_MODIFIED_PLANTARD_MUL, rng.integers(0, p, m, dtype=np.uint64),
+              rng.integers(0, p << ell, m, dtype=np.uint64),
+              lambda a, b: oracle.modified_plantard_mul(a, b, o))]
+    if c.fits_plantard_bound():
+        cases.append((nttk.OP_PLANTARD_REDC, rng.integers(0, p + 1, m, dtype=np.uint64),
+                      rng.integers(0, p + 1, m, dtype=np.uint64),
+                      lambda a, b: oracle.plantard_redc(a, b, o)))
+    for op, x, y, ref in cases:
+        dx = torch.from_numpy(x.view(np.int64)).cuda()
+        dy = torch.from_numpy(y.view(np.int64)).cuda() if y is not None else None
+        got = nttk.reduce(op, c, dx, dy).cpu().numpy()
+        idx = rng.integers(0, m, 2000)
+        want = [ref(int(x[i]), int(y[i]) if y is not None else 0) for i in idx]
+        got_i = got[idx] if op == nttk.OP_SIGNED_MONT_REDC else got[idx].view(np.uint64)
+        assert (got_i.astype(np.int64) == np.array(want, dtype=np.int64)).all(), op
+
+
+def test_reduction_contract_messages():
+    c = nttk.make_reduction_context(13, 8, 0, 2)
+    m = nttk.make_reduction_context(17, 5)
+    for call, msg in ((lambda: nttk.mont_redc(17 * 17, m), "mont_redc: T must be < p^2"),
+                      (lambda: nttk.modified_plantard_mul(13, 0, c), "W must be < p"),
+                      (lambda: nttk.modified_plantard_mul(0, 52, c), "T must be < 2^ell * p"),
+                      (lambda: nttk.plantard_redc(14, 0, nttk.make_reduction_context(13, 8)),
+                       "inputs exceed p"),
+                      (lambda: nttk.to_plantard_domain(13, c), "w must be < p"),
+                      (lambda: nttk.signed_mont_redc(1, nttk.make_reduction_context(31, 5)),
+                       "requires 2p < 2^n"),
+                      (lambda: nttk.modified_plantard_mul(1, 1, nttk.make_reduction_context(17, 8, 0, 2)),
+                       "requires p < 2^{n-ell-2}")):
+        with pytest.raises(nttk.ContractViolation, match=__import__("re").escape(msg)):
+            call()
