@@ -187,6 +187,26 @@ int nttk_reduce(int op, const nttk_reduction_ctx* ctx, const int64_t* d_x, const
 int nttk_reduce_host(int op, const nttk_reduction_ctx* ctx, const int64_t* h_x, const int64_t* h_y,
                      int64_t* h_out, size_t n);
 
+/* ---- butterfly.hpp checked entry points on arrays ------------------------------ */
+enum nttk_butterfly_op {
+  NTTK_BF_NTL = 0,          /* ntl_butterfly(X, Y, W, W_quot)        butterfly.hpp:60-86   */
+  NTTK_BF_HARVEY = 1,       /* harvey_butterfly(X, Y, W_mont)        butterfly.hpp:92-121  */
+  NTTK_BF_SCOTT = 2,        /* scott_butterfly(X, Y, W_mont, cfg)    butterfly.hpp:172-212 */
+  NTTK_BF_IMPROVED_CT = 3,  /* improved_ct_butterfly(X, Y, W_hat)    butterfly.hpp:247-260 */
+  NTTK_BF_IMPROVED_GS = 4   /* improved_gs_butterfly(X, Y, W_hat, l) butterfly.hpp:263-279 */
+};
+/* (xo[i], yo[i]) = op(x[i], y[i], w[i] [, wq[i] for ntl]) on device arrays.  aux0/aux1:
+ * scott transform_size N and lazy_level L (ScottConfig); improved GS: layer (aux0).  The
+ * reference's context and operand checks are applied (operands on the device; the call
+ * synchronises `stream`), with its messages. */
+int nttk_butterfly(int op, const nttk_reduction_ctx* ctx, uint32_t aux0, uint32_t aux1,
+                   const int64_t* d_x, const int64_t* d_y, const int64_t* d_w, const int64_t* d_wq,
+                   int64_t* d_xo, int64_t* d_yo, size_t n, void* stream);
+/* same on host arrays (synchronous) */
+int nttk_butterfly_host(int op, const nttk_reduction_ctx* ctx, uint32_t aux0, uint32_t aux1,
+                        const int64_t* h_x, const int64_t* h_y, const int64_t* h_w,
+                        const int64_t* h_wq, int64_t* h_xo, int64_t* h_yo, size_t n);
+
 /* ---- diagnostics ------------------------------------------------------------ */
 
 /* message of the last failing call on this host thread ("" when none) */

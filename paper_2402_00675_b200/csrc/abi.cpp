@@ -657,6 +657,112 @@ int nttk_reduce(int op, const nttk_reduction_ctx* ctx, const int64_t* d_x, const
   return NTTK_OK;
 }
 
+namespace {
+// butterfly.hpp checked wrappers: context/config checks (host) and operand messages
+int butterfly_precheck(int op, const nttk_reduction_ctx* c, uint32_t aux0, uint32_t aux1) {
+  using nttk_b200::u128;
+  if (!c) return fail(NTTK_CONTRACT, "butterfly: null context");
+  const uint64_t p = c->p;
+  const unsigned n = c->n_bits;
+  const bool lazy = c->ell + 2 < n && u128(p) < (u128(1) << (n - c->ell - 2));
+  switch (op) {
+    case NTTK_BF_NTL:
+      if (!(2 * p < c->beta)) return fail(NTTK_CONTRACT, "ntl_butterfly: requires 2p < 2^n");
+      return NTTK_OK;
+    case NTTK_BF_HARVEY:
+      if (!(4 * p < c->beta)) return fail(NTTK_CONTRACT, "harvey_butterfly: requires 4p < 2^n");
+      return NTTK_OK;
+    case NTTK_BF_SCOTT:
+      if (!(aux1 >= 1 && aux0 >= aux1)) return fail(NTTK_CONTRACT, "scott_butterfly: malformed config");
+      if (!(u128(4) * aux0 * p < u128(c->beta) * aux1))
+        return fail(NTTK_CONTRACT, "scott_butterfly: requires 4*N*p/L < 2^n");
+      return NTTK_OK;
+    case NTTK_BF_IMPROVED_CT:
+      if (!lazy) return fail(NTTK_CONTRACT, "improved_ct_butterfly: requires p < 2^{n-ell-2}");
+      return NTTK_OK;
+    case NTTK_BF_IMPROVED_GS:
+      if (!lazy) return fail(NTTK_CONTRACT, "improved_gs_butterfly: requires p < 2^{n-ell-2}");
+      if (!(aux0 >= 1 && aux0 <= c->ell))
+        return fail(NTTK_CONTRACT, "improved_gs_butterfly: layer out of [1, ell]");
+      return NTTK_OK;
+    default: return fail(NTTK_CONTRACT, "butterfly: unknown kind");
+  }
+}
+
+int butterfly_flag_message(int op, unsigned flag) {
+  static const char* const wmsg[] = {"ntl_butterfly: W out of (0, p)", "harvey_butterfly: W out of (0, p)",
+                                     "scott_butterfly: W out of (0, p)",
+                                     "improved_ct_butterfly: W_hat must be < p",
+                                     "improved_gs_butterfly: W_hat must be < p"};
+  static const char* const xmsg[] = {"ntl_butterfly: inputs must be canonical",
+                                     "harvey_butterfly: inputs must be < 2p",
+                                     "scott_butterfly: inputs must be < (N/L)*p",
+                                     "improved_ct_butterfly: inputs must be < 2^ell * p / 2",
+                                     "improved_gs_butterfly: inputs must be < 2^{layer-1} * p"};
+  if (flag & 1u) return fail(NTTK_CONTRACT, wmsg[op]);
+  if (flag & 2u) return fail(NTTK_CONTRACT, "ntl_butterfly: stale W_quot");
+  return fail(NTTK_CONTRACT, xmsg[op]);
+}
+}  // namespace
+
+int nttk_butterfly(int op, const nttk_reduction_ctx* ctx, uint32_t aux0, uint32_t aux1,
+                   const int64_t* d_x, const int64_t* d_y, const int64_t* d_w, const int64_t* d_wq,
+                   int64_t* d_xo, int64_t* d_yo, size_t n, void* stream) {
+  if (int s = butterfly_precheck(op, ctx, aux0, aux1)) return s;
+  if (n && (!d_x || !d_y || !d_w || !d_xo || !d_yo || (op == NTTK_BF_NTL && !d_wq)))
+    return fail(NTTK_CONTRACT, "butterfly: null buffer");
+  if (int s = need_device("butterfly")) return s;
+  if (!n) return NTTK_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned* d_flag = nullptr;
+  cudaError_t e = cudaMallocAsync(&d_flag, sizeof(unsigned), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_flag, 0, sizeof(unsigned), st);
+  if (e == cudaSuccess)
+    e = nttk_b200::butterfly_launch(op, *ctx, aux0, aux1, d_x, d_y, d_w, d_wq, d_xo, d_yo, n, d_flag, st);
+  ++g_launches;
+  unsigned flag = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, d_flag, sizeof flag, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (d_flag) cudaFreeAsync(d_flag, st);
+  if (e != cudaSuccess) return cuda_fail(e, "butterfly");
+  if (flag) return butterfly_flag_message(op, flag);
+  return NTTK_OK;
+}
+
+int nttk_butterfly_host(int op, const nttk_reduction_ctx* ctx, uint32_t aux0, uint32_t aux1,
+                        const int64_t* h_x, const int64_t* h_y, const int64_t* h_w,
+                        const int64_t* h_wq, int64_t* h_xo, int64_t* h_yo, size_t n) {
+  if (int s = butterfly_precheck(op, ctx, aux0, aux1)) return s;
+  if (n && (!h_x || !h_y || !h_w || !h_xo || !h_yo || (op == NTTK_BF_NTL && !h_wq)))
+    return fail(NTTK_CONTRACT, "butterfly: null buffer");
+  if (int s = need_device("butterfly")) return s;
+  if (!n) return NTTK_OK;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  int64_t* d = nullptr;
+  const size_t bytes = n * sizeof(int64_t);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d, 6 * bytes, st);
+  const int64_t* src[4] = {h_x, h_y, h_w, h_wq};
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+    if (src[k]) e = cudaMemcpyAsync(d + k * n, src[k], bytes, cudaMemcpyHostToDevice, st);
+  int rc = NTTK_OK;
+  if (e == cudaSuccess) {
+    rc = nttk_butterfly(op, ctx, aux0, aux1, d, d + n, d + 2 * n, d + 3 * n, d + 4 * n, d + 5 * n, n, st);
+    if (rc == NTTK_OK) e = cudaMemcpyAsync(h_xo, d + 4 * n, bytes, cudaMemcpyDeviceToHost, st);
+    if (rc == NTTK_OK && e == cudaSuccess)
+      e = cudaMemcpyAsync(h_yo, d + 5 * n, bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  if (d) cudaFreeAsync(d, st);
+  if (st) {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
+  if (rc != NTTK_OK) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "butterfly");
+  return NTTK_OK;
+}
+
 int nttk_reduce_host(int op, const nttk_reduction_ctx* ctx, const int64_t* h_x, const int64_t* h_y,
                      int64_t* h_out, size_t n) {
   if (int s = reduce_precheck(op, ctx)) return s;

@@ -96,7 +96,102 @@ cudaError_t launch(const int64_t* x, const int64_t* y, int64_t* out, size_t n, c
   return cudaGetLastError();
 }
 
+// --- butterfly.hpp checked entry points, elementwise ---------------------------------
+// aux0/aux1: scott N and L (offset (N/L) p); improved GS: layer.  Operand checks as in the
+// reference's checked wrappers; flag bits: 1 = W out of range, 2 = stale W_quot (ntl),
+// 4 = X/Y out of range.
+template <int OP>
+__global__ void butterfly_kernel(const int64_t* __restrict__ xs, const int64_t* __restrict__ ys,
+                                 const int64_t* __restrict__ ws, const int64_t* __restrict__ wq,
+                                 int64_t* __restrict__ xo, int64_t* __restrict__ yo, size_t n,
+                                 RArgs R, uint32_t aux0, uint32_t aux1, unsigned* flag) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const uint64_t p = R.p, X = static_cast<uint64_t>(xs[i]), Y = static_cast<uint64_t>(ys[i]);
+    const uint64_t W = static_cast<uint64_t>(ws[i]);
+    uint64_t x1 = 0, y1 = 0;
+    if (OP == NTTK_BF_NTL) {  // butterfly.hpp:60-86
+      const uint64_t Wq = static_cast<uint64_t>(wq[i]);
+      if (!(0 < W && W < p)) { atomicOr(flag, 1u); continue; }
+      if (Wq != static_cast<uint64_t>((u128(W) << R.n_bits) / p)) { atomicOr(flag, 2u); continue; }
+      if (!(X < p && Y < p)) { atomicOr(flag, 4u); continue; }
+      x1 = X + Y;
+      if (x1 >= p) x1 -= p;
+      const uint64_t t = X >= Y ? X - Y : X + p - Y;
+      const uint64_t q = (Wq * t) >> R.n_bits;
+      y1 = (W * t - q * p) & R.beta_mask;
+      if (y1 >= p) y1 -= p;
+    } else if (OP == NTTK_BF_HARVEY) {  // butterfly.hpp:92-121
+      if (!(0 < W && W < p)) { atomicOr(flag, 1u); continue; }
+      if (!(X < 2 * p && Y < 2 * p)) { atomicOr(flag, 4u); continue; }
+      x1 = X + Y;
+      if (x1 >= 2 * p) x1 -= 2 * p;
+      const uint64_t prod = W * (X + 2 * p - Y);
+      const uint64_t q = (R.p_inv_beta * (prod & R.beta_mask)) & R.beta_mask;
+      y1 = (prod >> R.n_bits) + p - ((q * p) >> R.n_bits);
+    } else if (OP == NTTK_BF_SCOTT) {  // butterfly.hpp:172-212 (no guard)
+      const uint64_t off = uint64_t(aux0 / aux1) * p;
+      if (!(0 < W && W < p)) { atomicOr(flag, 1u); continue; }
+      if (!(X < off && Y < off)) { atomicOr(flag, 4u); continue; }
+      x1 = X + Y;
+      const uint64_t wt = W * (X + off - Y);
+      const uint64_t q = (R.neg_p_inv_beta * (wt & R.beta_mask)) & R.beta_mask;
+      y1 = (wt + q * p) >> R.n_bits;  // uint64 like the reference (wraps identically)
+    } else {  // improved CT / GS, butterfly.hpp:224-279
+      const bool gs = OP == NTTK_BF_IMPROVED_GS;
+      const uint64_t bound = gs ? (p << (aux0 - 1)) : ((p << R.ell) / 2);
+      if (!(W < p)) { atomicOr(flag, 1u); continue; }
+      if (!(X < bound && Y < bound)) { atomicOr(flag, 4u); continue; }
+      auto mp = [&](uint64_t w, uint64_t t) {
+        const uint64_t h = ((w * t) * R.mu) & R.r2n_mask;
+        return (((h >> R.n_bits) + 1) * p) >> R.n_bits;
+      };
+      if (!gs) {
+        const uint64_t r = mp(W, Y);
+        x1 = X + r;
+        y1 = X + p - r;
+      } else {
+        x1 = X + Y;
+        y1 = mp(W, X + (p << (aux0 - 1)) - Y);
+      }
+    }
+    xo[i] = static_cast<int64_t>(x1);
+    yo[i] = static_cast<int64_t>(y1);
+  }
+}
+
+template <int OP>
+cudaError_t launch_bf(const int64_t* x, const int64_t* y, const int64_t* w, const int64_t* wq,
+                      int64_t* xo, int64_t* yo, size_t n, const RArgs& R, uint32_t a0, uint32_t a1,
+                      unsigned* flag, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t want = (n + 255) / 256, cap = size_t(sms) * 8;
+  butterfly_kernel<OP><<<static_cast<unsigned>(want < cap ? (want ? want : 1) : cap), 256, 0, st>>>(
+      x, y, w, wq, xo, yo, n, R, a0, a1, flag);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t butterfly_launch(int op, const nttk_reduction_ctx& c, uint32_t aux0, uint32_t aux1,
+                             const int64_t* x, const int64_t* y, const int64_t* w,
+                             const int64_t* wq, int64_t* xo, int64_t* yo, size_t n,
+                             unsigned* d_flag, cudaStream_t st) {
+  RArgs R{c.p,          c.beta_mask, c.r2n_mask,   c.p_inv_beta, c.neg_p_inv_beta, c.mu,
+          c.beta,       c.beta_mod_p, c.r2n_mod_p, c.n_bits,     c.ell};
+  switch (op) {
+    case NTTK_BF_NTL: return launch_bf<NTTK_BF_NTL>(x, y, w, wq, xo, yo, n, R, aux0, aux1, d_flag, st);
+    case NTTK_BF_HARVEY: return launch_bf<NTTK_BF_HARVEY>(x, y, w, wq, xo, yo, n, R, aux0, aux1, d_flag, st);
+    case NTTK_BF_SCOTT: return launch_bf<NTTK_BF_SCOTT>(x, y, w, wq, xo, yo, n, R, aux0, aux1, d_flag, st);
+    case NTTK_BF_IMPROVED_CT:
+      return launch_bf<NTTK_BF_IMPROVED_CT>(x, y, w, wq, xo, yo, n, R, aux0, aux1, d_flag, st);
+    case NTTK_BF_IMPROVED_GS:
+      return launch_bf<NTTK_BF_IMPROVED_GS>(x, y, w, wq, xo, yo, n, R, aux0, aux1, d_flag, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 cudaError_t reduce_launch(int op, const nttk_reduction_ctx& c, const int64_t* x, const int64_t* y,
                           int64_t* out, size_t n, unsigned* d_flag, cudaStream_t st) {

@@ -14,4 +14,10 @@ namespace nttk_b200 {
 cudaError_t reduce_launch(int op, const nttk_reduction_ctx& c, const int64_t* x, const int64_t* y,
                           int64_t* out, size_t n, unsigned* d_flag, cudaStream_t st);
 
+// (xo[i], yo[i]) = butterfly(x[i], y[i], w[i] [, wq[i]]); violations OR bits into *d_flag
+cudaError_t butterfly_launch(int op, const nttk_reduction_ctx& c, uint32_t aux0, uint32_t aux1,
+                             const int64_t* x, const int64_t* y, const int64_t* w,
+                             const int64_t* wq, int64_t* xo, int64_t* yo, size_t n,
+                             unsigned* d_flag, cudaStream_t st);
+
 }  // namespace nttk_b200

@@ -363,4 +363,104 @@ inline std::vector<Out> reduce(int op, const ReductionContext& ctx, const std::v
   return to_montgomery_domain(std::vector<uint64_t>{w}, ctx)[0];
 }
 
+// ---- butterfly.hpp checked entry points, executed on the GPU ------------------------
+
+struct ButterflyOut {  // butterfly.hpp:52-55
+  uint64_t x = 0;
+  uint64_t y = 0;
+  bool operator==(const ButterflyOut& o) const { return x == o.x && y == o.y; }
+};
+
+struct ScottConfig {  // butterfly.hpp:151-155 (the guard hook is not carried to the device)
+  uint32_t transform_size = 0;  // N
+  uint32_t lazy_level = 0;      // L
+};
+
+// butterfly.hpp:157-168: smallest power-of-two L with 4 N p < 2^n L
+[[nodiscard]] inline ScottConfig make_scott_config(uint32_t N, const ReductionContext& ctx) {
+  if (N == 0 || (N & (N - 1))) throw contract_violation("scott config: N must be a power of two");
+  for (uint32_t L = 1; L <= N; L *= 2)
+    if ((unsigned __int128)4 * N * ctx.p < (unsigned __int128)ctx.beta * L) return ScottConfig{N, L};
+  throw contract_violation("scott config: no lazy level satisfies 4*N*p/L < 2^n for p=" +
+                           std::to_string(ctx.p));
+}
+
+namespace detail {
+inline std::vector<ButterflyOut> butterflies(int op, const ReductionContext& ctx, uint32_t a0,
+                                             uint32_t a1, const std::vector<uint64_t>& X,
+                                             const std::vector<uint64_t>& Y,
+                                             const std::vector<uint64_t>& W,
+                                             const std::vector<uint64_t>* Wq = nullptr) {
+  const size_t n = X.size();
+  if (Y.size() != n || W.size() != n || (Wq && Wq->size() != n))
+    throw contract_violation("butterfly: operand lengths differ");
+  const nttk_reduction_ctx c = ctx.raw();
+  std::vector<int64_t> xo(n), yo(n);
+  check(nttk_butterfly_host(op, &c, a0, a1, reinterpret_cast<const int64_t*>(X.data()),
+                            reinterpret_cast<const int64_t*>(Y.data()),
+                            reinterpret_cast<const int64_t*>(W.data()),
+                            Wq ? reinterpret_cast<const int64_t*>(Wq->data()) : nullptr, xo.data(),
+                            yo.data(), n));
+  std::vector<ButterflyOut> out(n);
+  for (size_t i = 0; i < n; ++i)
+    out[i] = {static_cast<uint64_t>(xo[i]), static_cast<uint64_t>(yo[i])};
+  return out;
+}
+}  // namespace detail
+
+// batched forms (one launch)
+[[nodiscard]] inline std::vector<ButterflyOut> ntl_butterfly(
+    const std::vector<uint64_t>& X, const std::vector<uint64_t>& Y, const std::vector<uint64_t>& W,
+    const std::vector<uint64_t>& W_quot, const ReductionContext& ctx) {
+  return detail::butterflies(NTTK_BF_NTL, ctx, 0, 0, X, Y, W, &W_quot);
+}
+[[nodiscard]] inline std::vector<ButterflyOut> harvey_butterfly(const std::vector<uint64_t>& X,
+                                                                const std::vector<uint64_t>& Y,
+                                                                const std::vector<uint64_t>& W_mont,
+                                                                const ReductionContext& ctx) {
+  return detail::butterflies(NTTK_BF_HARVEY, ctx, 0, 0, X, Y, W_mont);
+}
+[[nodiscard]] inline std::vector<ButterflyOut> scott_butterfly(
+    const std::vector<uint64_t>& X, const std::vector<uint64_t>& Y,
+    const std::vector<uint64_t>& W_mont, const ReductionContext& ctx, const ScottConfig& cfg) {
+  return detail::butterflies(NTTK_BF_SCOTT, ctx, cfg.transform_size, cfg.lazy_level, X, Y, W_mont);
+}
+[[nodiscard]] inline std::vector<ButterflyOut> improved_ct_butterfly(
+    const std::vector<uint64_t>& X, const std::vector<uint64_t>& Y,
+    const std::vector<uint64_t>& W_hat, const ReductionContext& ctx) {
+  return detail::butterflies(NTTK_BF_IMPROVED_CT, ctx, 0, 0, X, Y, W_hat);
+}
+[[nodiscard]] inline std::vector<ButterflyOut> improved_gs_butterfly(
+    const std::vector<uint64_t>& X, const std::vector<uint64_t>& Y,
+    const std::vector<uint64_t>& W_hat, const ReductionContext& ctx, unsigned layer) {
+  return detail::butterflies(NTTK_BF_IMPROVED_GS, ctx, layer, 0, X, Y, W_hat);
+}
+
+// scalar signatures of butterfly.hpp
+[[nodiscard]] inline ButterflyOut ntl_butterfly(uint64_t X, uint64_t Y, uint64_t W, uint64_t W_quot,
+                                                const ReductionContext& ctx) {
+  return ntl_butterfly(std::vector<uint64_t>{X}, {Y}, {W}, {W_quot}, ctx)[0];
+}
+[[nodiscard]] inline ButterflyOut harvey_butterfly(uint64_t X, uint64_t Y, uint64_t W_mont,
+                                                   const ReductionContext& ctx) {
+  return harvey_butterfly(std::vector<uint64_t>{X}, {Y}, {W_mont}, ctx)[0];
+}
+// branch-based twin in the reference (butterfly.hpp:124-142): bit-identical by contract
+[[nodiscard]] inline ButterflyOut harvey_butterfly_ref(uint64_t X, uint64_t Y, uint64_t W_mont,
+                                                       const ReductionContext& ctx) {
+  return harvey_butterfly(X, Y, W_mont, ctx);
+}
+[[nodiscard]] inline ButterflyOut scott_butterfly(uint64_t X, uint64_t Y, uint64_t W_mont,
+                                                  const ReductionContext& ctx, const ScottConfig& cfg) {
+  return scott_butterfly(std::vector<uint64_t>{X}, {Y}, {W_mont}, ctx, cfg)[0];
+}
+[[nodiscard]] inline ButterflyOut improved_ct_butterfly(uint64_t X, uint64_t Y, uint64_t W_hat,
+                                                        const ReductionContext& ctx) {
+  return improved_ct_butterfly(std::vector<uint64_t>{X}, {Y}, {W_hat}, ctx)[0];
+}
+[[nodiscard]] inline ButterflyOut improved_gs_butterfly(uint64_t X, uint64_t Y, uint64_t W_hat,
+                                                        const ReductionContext& ctx, unsigned layer) {
+  return improved_gs_butterfly(std::vector<uint64_t>{X}, {Y}, {W_hat}, ctx, layer)[0];
+}
+
 }  // namespace nttk

@@ -128,6 +128,7 @@ EXPORTS = (
     "nttk_basemul", "nttk_polymul", "nttk_ntt_forward_host", "nttk_intt_inverse_host",
     "nttk_roundtrip_host", "nttk_pointwise_multiply_host", "nttk_polymul_host",
     "nttk_modmul_sweep", "nttk_make_reduction_context", "nttk_reduce", "nttk_reduce_host",
+    "nttk_butterfly", "nttk_butterfly_host",
     "nttk_last_error", "nttk_launch_count", "nttk_device_available", "nttk_version",
 )
 
@@ -165,6 +166,10 @@ def lib() -> C.CDLL:
                                                   C.POINTER(ReductionContext)]
         L.nttk_reduce.argtypes = [C.c_int, C.POINTER(ReductionContext), vp, vp, vp, sz, vp]
         L.nttk_reduce_host.argtypes = [C.c_int, C.POINTER(ReductionContext), vp, vp, vp, sz]
+        for f in ("nttk_butterfly", "nttk_butterfly_host"):
+            extra = [vp] if f == "nttk_butterfly" else []
+            getattr(L, f).argtypes = ([C.c_int, C.POINTER(ReductionContext), C.c_uint32, C.c_uint32]
+                                      + [vp] * 6 + [sz] + extra)
         L.nttk_last_error.restype = C.c_char_p
         L.nttk_launch_count.restype = C.c_uint64
         L.nttk_version.restype = C.c_char_p
@@ -575,3 +580,72 @@ def reduce(op: int, ctx: ReductionContext, x, y=None, out=None, stream=None):
                              y.data_ptr() if y is not None else None, out.data_ptr(), x.numel(),
                              _stream_ptr(stream)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# butterfly.hpp checked entry points, run on the GPU (reduce.cu)
+
+BF_NTL, BF_HARVEY, BF_SCOTT, BF_IMPROVED_CT, BF_IMPROVED_GS = 0, 1, 2, 3, 4
+
+
+@dataclass
+class ScottConfig:
+    """butterfly.hpp:151-155 (the guard hook is not carried to the device)."""
+    transform_size: int
+    lazy_level: int
+
+
+def make_scott_config(N: int, ctx: ReductionContext) -> ScottConfig:
+    """butterfly.hpp:157-168: smallest power-of-two L with 4 N p < 2^n L."""
+    if N <= 0 or N & (N - 1):
+        raise ContractViolation("scott config: N must be a power of two")
+    L = 1
+    while L <= N:
+        if 4 * N * ctx.p < ctx.beta * L:
+            return ScottConfig(N, L)
+        L *= 2
+    raise ContractViolation(
+        f"scott config: no lazy level satisfies 4*N*p/L < 2^n for p={ctx.p}")
+
+
+def _butterfly_host(op, ctx, X, Y, W, Wq=None, aux0=0, aux1=0):
+    scalar = np.isscalar(X)
+    arrs = [np.ascontiguousarray(np.atleast_1d(np.asarray(v)).astype(np.uint64).view(np.int64))
+            if v is not None else None for v in (X, Y, W, Wq)]
+    n = arrs[0].size
+    if any(a is not None and a.size != n for a in arrs):
+        raise ContractViolation("butterfly: operand lengths differ")
+    xo, yo = np.empty(n, np.int64), np.empty(n, np.int64)
+    _check(lib().nttk_butterfly_host(op, C.byref(ctx), aux0, aux1,
+                                     *[a.ctypes.data if a is not None else None for a in arrs],
+                                     xo.ctypes.data, yo.ctypes.data, n))
+    xo, yo = xo.view(np.uint64), yo.view(np.uint64)
+    return (int(xo[0]), int(yo[0])) if scalar else (xo, yo)
+
+
+def ntl_butterfly(X, Y, W, W_quot, ctx: ReductionContext):
+    """butterfly.hpp:60-86 (Alg. 7)."""
+    return _butterfly_host(BF_NTL, ctx, X, Y, W, W_quot)
+
+
+def harvey_butterfly(X, Y, W_mont, ctx: ReductionContext):
+    """butterfly.hpp:92-121 (Alg. 8)."""
+    return _butterfly_host(BF_HARVEY, ctx, X, Y, W_mont)
+
+
+harvey_butterfly_ref = harvey_butterfly  # butterfly.hpp:124-142: bit-identical twin
+
+
+def scott_butterfly(X, Y, W_mont, ctx: ReductionContext, cfg: ScottConfig):
+    """butterfly.hpp:172-212 (Alg. 9; no guard)."""
+    return _butterfly_host(BF_SCOTT, ctx, X, Y, W_mont, None, cfg.transform_size, cfg.lazy_level)
+
+
+def improved_ct_butterfly(X, Y, W_hat, ctx: ReductionContext):
+    """butterfly.hpp:247-260 (Alg. 11)."""
+    return _butterfly_host(BF_IMPROVED_CT, ctx, X, Y, W_hat)
+
+
+def improved_gs_butterfly(X, Y, W_hat, ctx: ReductionContext, layer: int):
+    """butterfly.hpp:263-279 (Alg. 12)."""
+    return _butterfly_host(BF_IMPROVED_GS, ctx, X, Y, W_hat, None, layer)

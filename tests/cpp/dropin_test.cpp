@@ -215,6 +215,26 @@ int main() {
     CHECK(throws_with([] { (void)modified_plantard_mul(1, 1, make_reduction_context(17, 8, 0, 2)); },
                       "requires p < 2^{n-ell-2}"));
   }
+  // butterfly.hpp through the GPU: the reference's hand cases (butterfly_test.cpp:31-197)
+  {
+    const ReductionContext c8 = make_reduction_context(13, 8);
+    CHECK((ntl_butterfly(5, 9, 3, 59, c8) == ButterflyOut{1, 1}));
+    CHECK((harvey_butterfly(100, 4000, 4583, make_reduction_context(7681, 16)) ==
+           ButterflyOut{4100, 3662}));
+    CHECK((harvey_butterfly_ref(100, 4000, 4583, make_reduction_context(7681, 16)) ==
+           ButterflyOut{4100, 3662}));
+    const ScottConfig cfg = make_scott_config(4, c8);
+    CHECK(cfg.lazy_level == 1);
+    CHECK((scott_butterfly(5, 9, 3, c8, cfg) == ButterflyOut{14, 3}));
+    const ReductionContext c = make_reduction_context(13, 8, 0, 2);
+    CHECK((improved_ct_butterfly(3, 20, 5, c) == ButterflyOut{13, 6}));
+    CHECK((improved_gs_butterfly(5, 9, 5, c, 1) == ButterflyOut{14, 11}));
+    CHECK(throws_with([&] { (void)ntl_butterfly(5, 9, 3, 58, c8); }, "stale W_quot"));
+    CHECK(throws_with([&] { (void)harvey_butterfly(0, 0, 0, make_reduction_context(7681, 16)); },
+                      "W out of (0, p)"));
+    CHECK(throws_with([&] { (void)improved_gs_butterfly(5, 9, 5, c, 3); }, "layer out of [1, ell]"));
+    CHECK(throws_with([&] { (void)improved_ct_butterfly(26, 0, 5, c); }, "inputs must be < 2^ell * p / 2"));
+  }
   std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }

@@ -217,3 +217,80 @@ def test_reduction_contract_messages():
                        "requires p < 2^{n-ell-2}")):
         with pytest.raises(nttk.ContractViolation, match=__import__("re").escape(msg)):
             call()
+
+
+# ---------------------------------------------------------------------------
+# butterfly.hpp checked entry points on the GPU (nttk_butterfly)
+
+def test_butterfly_hand_examples_on_gpu():  # butterfly_test.cpp:31-197
+    c8 = nttk.make_reduction_context(13, 8)
+    assert nttk.ntl_butterfly(5, 9, 3, 59, c8) == (1, 1)
+    assert nttk.harvey_butterfly(100, 4000, 4583, nttk.make_reduction_context(7681, 16)) == (4100, 3662)
+    assert nttk.scott_butterfly(5, 9, 3, c8, nttk.make_scott_config(4, c8)) == (14, 3)
+    c = nttk.make_reduction_context(13, 8, 0, 2)
+    assert nttk.improved_ct_butterfly(3, 20, 5, c) == (13, 6)
+    assert nttk.improved_gs_butterfly(5, 9, 5, c, 1) == (14, 11)
+
+
+@pytest.mark.parametrize("p,n,ell", [(3329, 16, 2), (3329, 32, 7), (8380417, 32, 7), (7681, 32, 4)])
+def test_butterflies_random_vs_oracle(oracle, p, n, ell):
+    """Every checked butterfly on 20000 random in-range operands vs the oracle cores."""
+    rng = np.random.default_rng(p * n + ell)
+    c = nttk.make_reduction_context(p, n, 0, ell)
+    o = oracle.ctx(p, n, 0, ell)
+    m = 20000
+    idx = rng.integers(0, m, 400)
+    W = rng.integers(1, p, m, dtype=np.uint64)
+    if 2 * p < (1 << n):  # ntl
+        X, Y = rng.integers(0, p, m, dtype=np.uint64), rng.integers(0, p, m, dtype=np.uint64)
+        Wq = np.array([(int(w) << n) // p for w in W], dtype=np.uint64)
+        xo, yo = nttk.ntl_butterfly(X, Y, W, Wq, c)
+        for i in idx:
+            assert (xo[i], yo[i]) == oracle.butterfly("ntl", int(X[i]), int(Y[i]), int(W[i]), int(Wq[i]), c=o)
+    if 4 * p < (1 << n):  # harvey
+        X, Y = rng.integers(0, 2 * p, m, dtype=np.uint64), rng.integers(0, 2 * p, m, dtype=np.uint64)
+        xo, yo = nttk.harvey_butterfly(X, Y, W, c)
+        for i in idx:
+            assert (xo[i], yo[i]) == oracle.butterfly("harvey", int(X[i]), int(Y[i]), int(W[i]), c=o)
+    try:
+        cfg = nttk.make_scott_config(256, c)
+    except nttk.ContractViolation:
+        cfg = None
+    if cfg is not None:  # scott
+        off = (cfg.transform_size // cfg.lazy_level) * p
+        X, Y = rng.integers(0, off, m, dtype=np.uint64), rng.integers(0, off, m, dtype=np.uint64)
+        xo, yo = nttk.scott_butterfly(X, Y, W, c, cfg)
+        for i in idx:
+            assert (xo[i], yo[i]) == oracle.butterfly("scott", int(X[i]), int(Y[i]), int(W[i]), off, c=o)
+    if c.fits_lazy_plantard_bound():  # improved CT / GS
+        Wh = rng.integers(0, p, m, dtype=np.uint64)
+        b = (p << ell) // 2
+        X, Y = rng.integers(0, b, m, dtype=np.uint64), rng.integers(0, b, m, dtype=np.uint64)
+        xo, yo = nttk.improved_ct_butterfly(X, Y, Wh, c)
+        for i in idx:
+            assert (xo[i], yo[i]) == oracle.butterfly("improved_ct", int(X[i]), int(Y[i]), int(Wh[i]), c=o)
+        for layer in range(1, ell + 1):
+            b = p << (layer - 1)
+            X, Y = rng.integers(0, b, m, dtype=np.uint64), rng.integers(0, b, m, dtype=np.uint64)
+            xo, yo = nttk.improved_gs_butterfly(X, Y, Wh, c, layer)
+            for i in idx[:50]:
+                assert (xo[i], yo[i]) == oracle.butterfly("improved_gs", int(X[i]), int(Y[i]), b,
+                                                          int(Wh[i]), c=o), layer
+
+
+def test_butterfly_contract_messages():
+    c8 = nttk.make_reduction_context(13, 8)
+    c = nttk.make_reduction_context(13, 8, 0, 2)
+    h = nttk.make_reduction_context(7681, 16)
+    for call, msg in ((lambda: nttk.ntl_butterfly(5, 9, 3, 58, c8), "ntl_butterfly: stale W_quot"),
+                      (lambda: nttk.ntl_butterfly(13, 9, 3, 59, c8), "inputs must be canonical"),
+                      (lambda: nttk.harvey_butterfly(1, 1, 0, h), "harvey_butterfly: W out of (0, p)"),
+                      (lambda: nttk.harvey_butterfly(2 * 7681, 1, 3, h), "inputs must be < 2p"),
+                      (lambda: nttk.scott_butterfly(52, 0, 3, c8, nttk.make_scott_config(4, c8)),
+                       "inputs must be < (N/L)*p"),
+                      (lambda: nttk.improved_ct_butterfly(26, 0, 5, c), "inputs must be < 2^ell * p / 2"),
+                      (lambda: nttk.improved_gs_butterfly(5, 9, 5, c, 3), "layer out of [1, ell]"),
+                      (lambda: nttk.improved_gs_butterfly(13, 9, 5, c, 1), "inputs must be < 2^{layer-1} * p"),
+                      (lambda: nttk.make_scott_config(6, c8), "N must be a power of two")):
+        with pytest.raises(nttk.ContractViolation, match=__import__("re").escape(msg)):
+            call()
