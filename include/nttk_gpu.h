@@ -174,7 +174,8 @@ enum nttk_reduce_op {
   NTTK_OP_PLANTARD_REDC = 2,          /* x = W, y = T in [0, p]     reduction.hpp:178-191 */
   NTTK_OP_MODIFIED_PLANTARD_MUL = 3,  /* x = W < p, y = T < 2^ell p reduction.hpp:264-273 */
   NTTK_OP_TO_PLANTARD_DOMAIN = 4,     /* x = w < p                  reduction.hpp:279-283 */
-  NTTK_OP_TO_MONTGOMERY_DOMAIN = 5    /* x = w < p                  reduction.hpp:287-291 */
+  NTTK_OP_TO_MONTGOMERY_DOMAIN = 5,   /* x = w < p                  reduction.hpp:287-291 */
+  NTTK_OP_MOD_P = 6                   /* x mod p, any 64-bit word   transform.hpp:38-40   */
 };
 
 /* out[i] = op(x[i] [, y[i]]) for i < n on device arrays of int64 words (the unsigned ops

@@ -609,7 +609,7 @@ namespace {
 int reduce_precheck(int op, const nttk_reduction_ctx* c) {
   using nttk_b200::u128;
   if (!c) return fail(NTTK_CONTRACT, "reduce: null context");
-  if (op < NTTK_OP_MONT_REDC || op > NTTK_OP_TO_MONTGOMERY_DOMAIN)
+  if (op < NTTK_OP_MONT_REDC || op > NTTK_OP_MOD_P)
     return fail(NTTK_CONTRACT, "reduce: unknown operation");
   const uint64_t p = c->p;
   const unsigned n = c->n_bits;

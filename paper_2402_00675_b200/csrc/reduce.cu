@@ -70,6 +70,8 @@ __global__ void reduce_kernel(const int64_t* __restrict__ x, const int64_t* __re
       const uint64_t h = ((W * T) * R.mu) & R.r2n_mask;
       const uint64_t r = (((h >> R.n_bits) + 1) * p) >> R.n_bits;
       out[i] = static_cast<int64_t>(OP == NTTK_OP_PLANTARD_REDC && r == p ? 0 : r);
+    } else if (OP == NTTK_OP_MOD_P) {  // canonicalize, transform.hpp:38-40
+      out[i] = static_cast<int64_t>(static_cast<uint64_t>(x[i]) % p);
     } else {  // domain encodings, reduction.hpp:279-291
       const uint64_t w = static_cast<uint64_t>(x[i]);
       if (!(w < p)) {
@@ -206,6 +208,7 @@ cudaError_t reduce_launch(int op, const nttk_reduction_ctx& c, const int64_t* x,
     case NTTK_OP_TO_PLANTARD_DOMAIN: return launch<NTTK_OP_TO_PLANTARD_DOMAIN>(x, y, out, n, R, d_flag, st);
     case NTTK_OP_TO_MONTGOMERY_DOMAIN:
       return launch<NTTK_OP_TO_MONTGOMERY_DOMAIN>(x, y, out, n, R, d_flag, st);
+    case NTTK_OP_MOD_P: return launch<NTTK_OP_MOD_P>(x, y, out, n, R, d_flag, st);
     default: return cudaErrorInvalidValue;
   }
 }

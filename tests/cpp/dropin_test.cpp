@@ -235,6 +235,33 @@ int main() {
     CHECK(throws_with([&] { (void)improved_gs_butterfly(5, 9, 5, c, 3); }, "layer out of [1, ell]"));
     CHECK(throws_with([&] { (void)improved_ct_butterfly(26, 0, 5, c); }, "inputs must be < 2^ell * p / 2"));
   }
+  // params.hpp / transform.hpp helpers and the NttParams tables (params_test.cpp patterns)
+  {
+    const auto P = preset("kyber256");
+    CHECK(find_primitive_root(7681, 256) == P.omega && P.omega == 198);
+    CHECK(ct_forward_plain_twiddles(256, P.omega, P.p) == P.table("ct_plain"));
+    CHECK(gs_inverse_plain_twiddles(256, P.omega, P.p) == P.table("gs_plain"));
+    const auto dif = dif_forward_plain_twiddles(256, P.omega, P.p);
+    CHECK(dif.size() == P.fwd.dif_ntl.size() && P.fwd.dif_ntl[5].w == dif[5]);
+    CHECK(P.fwd.ct_plantard.size() == 255 && P.inv.gs_plantard.size() == 255);
+    CHECK(P.ctx.p == 7681 && P.ctx.ell == 8 && P.scott.lazy_level >= 1);
+    // decode the encoded tables back against the plain schedules (on the device)
+    const auto ct = P.table("ct_plain");
+    bool ok = true;
+    for (size_t i = 0; i < ct.size(); ++i)
+      ok = ok && P.fwd.ct_plantard[i] == to_plantard_domain(ct[i], P.ctx) &&
+           P.fwd.dif_mont[i] == to_montgomery_domain(dif[i], P.ctx);
+    CHECK(ok);
+    CHECK(spectrum_value_bound(P, ButterflyKind::improved) == 9 * 7681ull);
+    CHECK(spectrum_value_bound(P, ButterflyKind::scott) == 256 * 7681ull);
+    std::vector<uint64_t> v{7681, 7682, 15363, ~0ull};
+    canonicalize(v, 7681);
+    CHECK((v == std::vector<uint64_t>{0, 1, 1, ~0ull % 7681}));
+    const Spectrum sp{{0, 1, 2, 3, 4, 5, 6, 7}};
+    CHECK((to_natural_order(sp) == std::vector<uint64_t>{0, 4, 2, 6, 1, 5, 3, 7}));
+    CHECK(preset_spec("falcon1024").size == 1024);
+    CHECK(throws_with([] { (void)preset_spec("nope"); }, "unknown preset"));
+  }
   std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }
