@@ -577,7 +577,7 @@ def run_engine_arm(a, rank, world, local_rank):
                           f"{tot_t:.1f} s wall on {threads} threads")}
 
     extras = None
-    if rank == 0 and not a.no_extras:
+    if rank == 0 and world == 1 and not a.no_extras:  # single-GPU configs: N = 1 runs only
         extras = run_extras(dev)
 
     if rank == 0:
