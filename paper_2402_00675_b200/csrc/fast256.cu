@@ -27,6 +27,7 @@
 
 #include "arith.cuh"
 #include "fast256.hpp"
+#include "launch_cache.hpp"
 
 namespace nttk_b200 {
 namespace {
@@ -376,35 +377,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 }
 
 // ---------------------------------------------------------------------------
-int g_sm_count = 0;
-
-int sm_count() {
-  if (!g_sm_count) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sm_count <= 0) g_sm_count = 148;
-  }
-  return g_sm_count;
-}
-
 template <class Kern>
-int blocks_for(Kern kern, int& occ, size_t batch) {
-  if (!occ) {  // cached per kernel instantiation by the caller
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kWarpsPerBlock * 32, 0);
-    occ = o > 0 ? o : 1;
-  }
+int blocks_for(Kern kern, OccCache& occ, size_t batch) {  // occ: per kernel instantiation
   const size_t pairs = (batch + 1) / 2;
   const size_t need = (pairs + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const size_t full = size_t(sm_count()) * occ;
+  const size_t full =
+      size_t(sm_count_current()) * occupancy_current(kern, kWarpsPerBlock * 32, 0, occ);
   return static_cast<int>(need < full ? need : full);
 }
 
 template <class K, class IO, int L, bool PER_INDEX>
 cudaError_t fwd_launch(const void* in, void* out, size_t batch, const FastArgs& A,
                        cudaStream_t st) {
-  static int occ = 0;
+  static OccCache occ;
   auto kern = fwd256_kernel<K, IO, L, PER_INDEX>;
   const int blocks = blocks_for(kern, occ, batch);
   kern<<<blocks, kWarpsPerBlock * 32, 0, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out),
@@ -415,7 +400,7 @@ cudaError_t fwd_launch(const void* in, void* out, size_t batch, const FastArgs& 
 template <class K, class IO, int L>
 cudaError_t inv_launch(const void* in, void* out, size_t batch, const FastArgs& A,
                        cudaStream_t st) {
-  static int occ = 0;
+  static OccCache occ;
   auto kern = inv256_kernel<K, IO, L>;
   const int blocks = blocks_for(kern, occ, batch);
   kern<<<blocks, kWarpsPerBlock * 32, 0, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out),

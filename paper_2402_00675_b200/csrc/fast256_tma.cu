@@ -22,6 +22,7 @@
 
 #include "arith.cuh"
 #include "fast256.hpp"
+#include "launch_cache.hpp"
 #include "tma_common.cuh"
 
 namespace nttk_b200 {
@@ -183,31 +184,19 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
 }
 
 // ---------------------------------------------------------------------------
-int g_sms = 0;
-
 template <class Kern>
-int grid_for(Kern kern, int smem, int& occ, size_t batch) {
-  if (!occ) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem);
-    occ = o > 0 ? o : 1;
-    if (!g_sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-      if (g_sms <= 0) g_sms = 148;
-    }
-  }
+int grid_for(Kern kern, int smem, OccCache& occ, size_t batch) {
+  const int o = occupancy_current(kern, kThreads, smem, occ);
+  const int g_sms = sm_count_current();
   const size_t tiles = (batch + kTile - 1) / kTile;
-  const size_t full = size_t(g_sms) * occ;
+  const size_t full = size_t(g_sms) * o;
   return static_cast<int>(tiles < full ? tiles : full);
 }
 
 template <class K, class IO, int L, bool PER_INDEX, bool W1>
 cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs& A,
                          cudaStream_t st) {
-  static int occ = 0;
+  static OccCache occ;
   auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1>;
   constexpr int smem = Geo<IO>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
   const int blocks = grid_for(kern, smem, occ, batch);
@@ -226,7 +215,7 @@ cudaError_t fwd_launch(const void* in, void* out, size_t batch, const FastArgs& 
 template <class K, class IO, int L, int MODE>
 cudaError_t inv_launch_mode(const void* in, void* out, size_t batch, const FastArgs& A,
                             cudaStream_t st) {
-  static int occ = 0;
+  static OccCache occ;
   auto kern = inv256_tma_kernel<K, IO, L, MODE>;
   constexpr int smem = Geo<IO>::kSmem + (tws_on<IO, 1>() ? 240 * int(sizeof(typename K::Tw)) : 0);
   const int blocks = grid_for(kern, smem, occ, batch);

@@ -20,6 +20,7 @@
 
 #include "arith.cuh"
 #include "fastn.hpp"
+#include "launch_cache.hpp"
 #include "tma_common.cuh"
 
 namespace nttk_b200 {
@@ -417,23 +418,9 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-int g_sms_n = 0;
-
 template <class Kern>
-int grid_n(Kern kern, int smem, int& occ, size_t tiles) {
-  if (!occ) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem);
-    occ = o > 0 ? o : 1;
-    if (!g_sms_n) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&g_sms_n, cudaDevAttrMultiProcessorCount, dev);
-      if (g_sms_n <= 0) g_sms_n = 148;
-    }
-  }
-  const size_t full = size_t(g_sms_n) * occ;
+int grid_n(Kern kern, int smem, OccCache& occ, size_t tiles) {
+  const size_t full = size_t(sm_count_current()) * occupancy_current(kern, kThreads, smem, occ);
   return static_cast<int>(tiles < full ? tiles : full);
 }
 
@@ -441,7 +428,7 @@ template <class K, class IO, int LOGN, bool PER_INDEX>
 cudaError_t fwd_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
                   cudaStream_t st) {
   using GN = GeoN<LOGN, IO>;
-  static int occ = 0;
+  static OccCache occ;
   auto kern = fwdn_tma_kernel<K, IO, LOGN, PER_INDEX>;
   const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN);
   kern<<<blocks, kThreads, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,
@@ -453,7 +440,7 @@ template <class K, class IO, int LOGN, int MODE>
 cudaError_t inv_n_mode(const void* in, void* out, size_t batch, const uint32_t* tab,
                        const FastArgs& A, cudaStream_t st) {
   using GN = GeoN<LOGN, IO>;
-  static int occ = 0;
+  static OccCache occ;
   auto kern = invn_tma_kernel<K, IO, LOGN, MODE>;
   const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN);
   kern<<<blocks, kThreads, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,

@@ -18,6 +18,7 @@
 
 #include "arith.cuh"
 #include "fast256.hpp"
+#include "launch_cache.hpp"
 #include "tma_common.cuh"
 
 namespace nttk_b200 {
@@ -133,28 +134,17 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-int g_sms2 = 0;
 
 template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
 cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
                       cudaStream_t st) {
-  static int occ = 0;
+  static OccCache occ;
   auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY, W1>;
   constexpr int smem = Geo2<IO>::kSmem;
-  if (!occ) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, smem);
-    occ = o > 0 ? o : 1;
-    if (!g_sms2) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&g_sms2, cudaDevAttrMultiProcessorCount, dev);
-      if (g_sms2 <= 0) g_sms2 = 148;
-    }
-  }
+  const int g_sms2 = sm_count_current();
+  const int o = occupancy_current(kern, kThreads, smem, occ);
   const size_t tiles = (batch + kTile - 1) / kTile;
-  const size_t full = size_t(g_sms2) * occ;
+  const size_t full = size_t(g_sms2) * o;
   const int blocks = static_cast<int>(tiles < full ? tiles : full);
   kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(a), static_cast<const IO*>(b),
                                       static_cast<IO*>(out), batch, PA);

@@ -1,0 +1,66 @@
+"""Concurrent host threads through the C ABI (ctypes drops the GIL): first-call launch
+caches, per-thread error state and per-stream launches must hold up.  Runs in a fresh
+process so the per-kernel caches are populated concurrently."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import sys, threading
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+import paper_2402_00675_b200.nttk as nttk
+K = nttk.ButterflyKind
+jobs = [(3329, 256, 16, K.improved, torch.int16, True), (8380417, 256, 32, K.improved, torch.int32, True),
+        (3329, 256, 16, K.harvey, torch.int16, True), (12289, 1024, 32, K.improved, torch.int32, False),
+        (12289, 512, 32, K.ntl, torch.int32, False), (8380417, 256, 32, K.scott, torch.int32, False),
+        (3329, 256, 16, K.smont, torch.int16, True), (7681, 256, 32, K.ntl, torch.int16, False)]
+inputs, want = [], []
+for j, (p, N, n, k, dt, ex) in enumerate(jobs):
+    g = torch.Generator(device="cuda").manual_seed(j)
+    inputs.append(torch.randint(0, p, (1031, N), generator=g, device="cuda", dtype=torch.int32).to(dt))
+errors, results = [], [None] * len(jobs)
+barrier = threading.Barrier(len(jobs))
+def work(j):
+    try:
+        p, N, n, k, dt, ex = jobs[j]
+        P = nttk.build_params(p, N, n, [k], exact_bound=ex)
+        s = torch.cuda.Stream()
+        barrier.wait()
+        with torch.cuda.stream(s):
+            for _ in range(20):
+                y = nttk.forward(P, k, inputs[j], stream=s)
+                z = nttk.inverse(P, k, y, stream=s)
+        s.synchronize()
+        results[j] = (y.cpu(), z.cpu())
+        try:  # per-thread error state: this thread's message, not another's
+            nttk.build_params(15, N, n, [k])
+        except nttk.ContractViolation as e:
+            assert "p must be prime" in str(e), str(e)
+    except Exception as e:
+        errors.append(repr(e))
+ts = [threading.Thread(target=work, args=(j,)) for j in range(len(jobs))]
+[t.start() for t in ts]; [t.join() for t in ts]
+assert not errors, errors
+for j, (p, N, n, k, dt, ex) in enumerate(jobs):  # single-threaded replay must agree
+    P = nttk.build_params(p, N, n, [k], exact_bound=ex)
+    y = nttk.forward(P, k, inputs[j])
+    assert torch.equal(y.cpu(), results[j][0]), j
+    assert torch.equal(results[j][1], inputs[j].cpu()), j
+print("threads ok")
+'''
+
+
+def test_concurrent_threads_fresh_process(tmp_path):
+    script = tmp_path / "threads.py"
+    script.write_text(SCRIPT)
+    r = subprocess.run([sys.executable, str(script), ROOT], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "threads ok" in r.stdout, r.stdout + r.stderr
