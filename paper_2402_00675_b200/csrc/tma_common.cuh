@@ -92,7 +92,9 @@ __device__ __forceinline__ void bulk_wait_all() {
 // proxy fence orders this warp's reads before the refill (WAR across proxies), the
 // warp barrier collects all lanes, one lane arrives.
 __device__ __forceinline__ void release_stage(uint64_t* empty, int lane) {
+#ifndef NTTK_NO_PROXY_FENCE  // A/B only: without it the refill races the reads (stress test)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
   __syncwarp();
   if (lane == 0) mbar_arrive(empty);
 }
