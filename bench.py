@@ -572,9 +572,13 @@ def run_engine_arm(a, rank, world, local_rank):
             tot_t += t
             reps += 1
         rate = reps * (smp_k + smp_d) / tot_t
+        # the reference is single-threaded: one core, same workload mix
+        _, _, t1 = cpu_reference_rate(16384, 8192, 1)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
                "sample": (f"{reps} x ({smp_k} Kyber + {smp_d} Dilithium) polys fwd+inv, "
-                          f"{tot_t:.1f} s wall on {threads} threads")}
+                          f"{tot_t:.1f} s wall on {threads} threads"),
+               "value_1_core": 24576 / t1,
+               "sample_1_core": f"16384 Kyber + 8192 Dilithium polys fwd+inv, 1 thread, {t1:.2f} s"}
 
     extras = None
     if rank == 0 and world == 1 and not a.no_extras:  # single-GPU configs: N = 1 runs only
