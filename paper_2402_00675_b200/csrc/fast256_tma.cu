@@ -61,12 +61,15 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
   Xpose X;
   X.init(scratch + warp * kScratchWords + half * 272, j);
   auto run = [&](const auto& twl) {
-    const size_t ntiles = (batch + kTile - 1) / kTile;
-    int k = 0;
-    for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-      const int s = k % G::kStages;
-      const size_t poly = t * kTile + half * kConsumers + warp;
-      mbar_wait(&full[s], (k / G::kStages) & 1);
+    // 32-bit tile/poly counters (the launcher splits batches >= 2^31), a stride pointer for
+    // the output and incremental stage/phase: loop bookkeeping off the 64-bit datapath
+    const uint32_t ntiles = static_cast<uint32_t>((batch + kTile - 1) / kTile);
+    const uint32_t nb = static_cast<uint32_t>(batch), pstep = gridDim.x * kTile;
+    uint32_t poly = blockIdx.x * kTile + half * kConsumers + warp, s = 0, phase = 0;
+    IO* optr = out + size_t(poly) * 256;
+    const size_t ostep = size_t(pstep) * 256;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&full[s], phase);
       uint32_t v[16];
       load_strided<IO, K::kSigned>(
           v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
@@ -101,11 +104,17 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (j == 0 && poly < batch) bulk_s2g(out + poly * 256, T, 256 * sizeof(IO));
+        if (j == 0 && poly < nb) bulk_s2g(optr, T, 256 * sizeof(IO));
       }
 #else
-      if (poly < batch) store_contiguous<IO>(out + poly * 256, j, v);
+      if (poly < nb) store_contiguous<IO>(optr, j, v);
 #endif
+      poly += pstep;
+      optr += ostep;
+      if (++s == G::kStages) {
+        s = 0;
+        phase ^= 1;
+      }
     }
 #ifdef NTTK_BULK_STORE
     if (j == 0) bulk_wait_all();
@@ -155,12 +164,13 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
   Xpose X;
   X.init(S, j);
   auto run = [&](const auto& twl) {
-    const size_t ntiles = (batch + kTile - 1) / kTile;
-    int k = 0;
-    for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-      const int s = k % G::kStages;
-      const size_t poly = t * kTile + half * kConsumers + warp;
-      mbar_wait(&full[s], (k / G::kStages) & 1);
+    const uint32_t ntiles = static_cast<uint32_t>((batch + kTile - 1) / kTile);
+    const uint32_t nb = static_cast<uint32_t>(batch), pstep = gridDim.x * kTile;
+    uint32_t poly = blockIdx.x * kTile + half * kConsumers + warp, s = 0, phase = 0;
+    IO* optr = out + size_t(poly) * 256;
+    const size_t ostep = size_t(pstep) * 256;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&full[s], phase);
       uint32_t v[16];
       load_contiguous<IO, K::kSigned>(
           v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
@@ -171,7 +181,13 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
         for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
       }
       inv_body<K, L, CM == 2, (MODE & 4) != 0>(v, twl, A, X);
-      store_strided<IO>(out + poly * 256, j, v, S, X, poly < batch);
+      store_strided<IO>(optr, j, v, S, X, poly < nb);
+      poly += pstep;
+      optr += ostep;
+      if (++s == G::kStages) {
+        s = 0;
+        phase ^= 1;
+      }
     }
   };
   if constexpr (tws_on<IO, 1>()) {
@@ -269,8 +285,27 @@ bool fast256_tma_supports(int elem_bytes, const void* in, const void* out) {
          !(reinterpret_cast<uintptr_t>(in) & 15) && !(reinterpret_cast<uintptr_t>(out) & 15);
 }
 
+cudaError_t fast256_tma_launch_one(const HostParams& P, int kind, int dir, const void* in,
+                                   void* out, size_t batch, int elem_bytes, cudaStream_t st);
+
+// the kernels count polynomials in 32 bits: split batches of 2^31 or more (more than any
+// B200 holds at N = 256, kept for safety)
 cudaError_t fast256_tma_launch(const HostParams& P, int kind, int dir, const void* in, void* out,
                                size_t batch, int elem_bytes, cudaStream_t st) {
+  constexpr size_t kMax = size_t(1) << 30;
+  const size_t bytes = size_t(256) * elem_bytes;
+  for (size_t done = 0; done < batch;) {
+    const size_t n = batch - done < kMax ? batch - done : kMax;
+    const cudaError_t e = fast256_tma_launch_one(P, kind, dir, static_cast<const char*>(in) + done * bytes,
+                                                 static_cast<char*>(out) + done * bytes, n, elem_bytes, st);
+    if (e != cudaSuccess) return e;
+    done += n;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t fast256_tma_launch_one(const HostParams& P, int kind, int dir, const void* in,
+                                   void* out, size_t batch, int elem_bytes, cudaStream_t st) {
   const FastArgs& A = P.fast[kind][dir];
   const int L = static_cast<int>(P.layers);
   const bool n16 = P.n_bits == 16;
