@@ -100,12 +100,14 @@ __global__ void __launch_bounds__(kThreads)
     for (int q = 0; q < 8; ++q) gam[q] = pin(K::genc(8 * j + q, PA.prod));
   }
 
-  const size_t ntiles = (batch + kTile - 1) / kTile;
-  int k = 0;
-  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k % G::kStages;
-    const size_t poly = t * kTile + half * kConsumers + warp;
-    mbar_wait(&full[s], (k / G::kStages) & 1);
+  // 32-bit counters, stride pointer, incremental stage/phase (launcher splits >= 2^30)
+  const uint32_t ntiles = static_cast<uint32_t>((batch + kTile - 1) / kTile);
+  const uint32_t nb = static_cast<uint32_t>(batch), pstep = gridDim.x * kTile;
+  uint32_t poly = blockIdx.x * kTile + half * kConsumers + warp, s = 0, phase = 0;
+  IO* optr = out + size_t(poly) * 256;
+  const size_t ostep = size_t(pstep) * 256;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&full[s], phase);
     const uint8_t* base = stages + s * G::kStageBytes;
     uint32_t va[16], vb[16];
     load_strided<IO, K::kSigned>(va, reinterpret_cast<const IO*>(base + G::poly_offset(warp, half, 0)), j);
@@ -130,7 +132,13 @@ __global__ void __launch_bounds__(kThreads)
       for (int r = 0; r < 16; ++r) va[r] = K::mulc(vb[r], K::enc(va[r], PA.prod, AF), AF);
     }
     inv_body<K, L, false, LAZY>(va, twi, AI, X);
-    store_strided<IO>(out + poly * 256, j, va, S, X, poly < batch);
+    store_strided<IO>(optr, j, va, S, X, poly < nb);
+    poly += pstep;
+    optr += ostep;
+    if (++s == G::kStages) {
+      s = 0;
+      phase ^= 1;
+    }
   }
 }
 
@@ -183,8 +191,26 @@ cudaError_t by_io(int L, int elem, const void* a, const void* b, void* out, size
 
 }  // namespace
 
+cudaError_t polymul256_launch_one(const HostParams& P, int kind, const void* a, const void* b,
+                                  void* out, size_t batch, int elem_bytes, cudaStream_t st);
+
 cudaError_t polymul256_launch(const HostParams& P, int kind, const void* a, const void* b,
                               void* out, size_t batch, int elem_bytes, cudaStream_t st) {
+  constexpr size_t kMax = size_t(1) << 30;  // the kernel counts polynomials in 32 bits
+  const size_t bytes = size_t(256) * elem_bytes;
+  for (size_t done = 0; done < batch;) {
+    const size_t n = batch - done < kMax ? batch - done : kMax;
+    const cudaError_t e = polymul256_launch_one(
+        P, kind, static_cast<const char*>(a) + done * bytes, static_cast<const char*>(b) + done * bytes,
+        static_cast<char*>(out) + done * bytes, n, elem_bytes, st);
+    if (e != cudaSuccess) return e;
+    done += n;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t polymul256_launch_one(const HostParams& P, int kind, const void* a, const void* b,
+                                  void* out, size_t batch, int elem_bytes, cudaStream_t st) {
   if (batch == 0) return cudaSuccess;
   PolymulArgs PA;
   PA.fwd = P.fast[kind][0];
