@@ -235,6 +235,43 @@ struct ImprovedN32 {
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return mp_n32(v, A.scale_lo, A.scale_hi, A.p);
   }
+  // ---- lazy merge (see ImprovedN16) at n = 32 ----
+  // The lazy word is h = h_hi (the first two multiplies of mp_n32); r = hi32(h p + p).
+  // lo32(h p + p) = p + (W T - h_lo p) / 2^32 lies in (0, 2p) (Prop. 4 with 2n = 64), so
+  // h_X p + 2p = {lo_X + p, X} (no carry) and hi(h_Y p + (h_X p + 2p)) = X + Y: both pair
+  // addends are loop-invariant {p, 0} / {2p, 0} register pairs (flag bit 3, always valid on
+  // the fast path).
+  static constexpr bool kLazy = true;
+  __device__ static uint32_t hprime(uint32_t t, Tw w) { return w.y * t + __umulhi(w.x, t); }
+  __device__ static uint32_t materialize(uint32_t h, const FastArgs& A) {
+    return static_cast<uint32_t>((static_cast<uint64_t>(h) * A.p + A.p) >> 32);
+  }
+  __device__ static uint32_t sum_hh(uint32_t hx, uint32_t hy, uint32_t& X, const FastArgs& A) {
+    const uint64_t px = static_cast<uint64_t>(hx) * A.p + A.two_p;  // {lo_X + p, X}
+    uint32_t xh = static_cast<uint32_t>(px >> 32);
+    asm("mov.b32 %0, %0;" : "+r"(xh));  // opaque: keeps 2X from becoming a funnel shift
+    X = xh;
+    return static_cast<uint32_t>((static_cast<uint64_t>(hy) * A.p + px) >> 32);
+  }
+  __device__ static void inv_h(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    x = x + y + A.zero;
+    y = hprime(t, w);
+  }
+  __device__ static void inv_hh(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    uint32_t X;
+    const uint32_t S = sum_hh(x, y, X, A);
+    const uint32_t t = X + X + off - S + A.zero;
+    x = S;
+    y = hprime(t, w);
+  }
+  __device__ static void inv_last_hh(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
+    uint32_t X;
+    const uint32_t S = sum_hh(x, y, X, A);
+    const uint32_t t = X + X + off - S + A.zero;
+    x = mp_n32(S, A.scale_lo, A.scale_hi, A.p);
+    y = mp_n32(t, A.fold_lo, A.fold_hi, A.p);
+  }
   __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
     x = mp_n32(x + y + A.zero, A.scale_lo, A.scale_hi, A.p);

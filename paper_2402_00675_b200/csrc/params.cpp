@@ -193,6 +193,8 @@ void fill_fast(HostParams& P, int kind) {
       if (A.flags & 4) tmax = std::max<u128>(tmax, (uint64_t(1) << 16) - 1 + A.kp);
       if (2 * u128(p - 1) * tmax < (u128(1) << 32)) A.flags |= 8;
     }
+    // n = 32: lo32(h' p) < 2p for every fast-path operand (ImprovedN32 lazy merge)
+    if (kind == NTTK_IMPROVED && !n16 && u128(4) * p < (u128(1) << 32)) A.flags |= 8;
     // forward block 0 of layers 1 and 2 has twiddle 1 (cyclic tree): multiply-free
     // Plantard products (fwd_body W1)
     if (kind == NTTK_IMPROVED && dir == 0 && P.ct_plain.size() >= 3 && P.ct_plain[0] == 1 &&
