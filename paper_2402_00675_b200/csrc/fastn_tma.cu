@@ -321,6 +321,58 @@ __device__ __forceinline__ void inv_body_n(uint32_t (&v)[32], const uint2* tws, 
   }
 }
 
+// inv_body_n with lazy merge outputs (policy kLazy, A.flags bit 3; see tma_common.cuh
+// inv_body_lazy): after a layer of register half-span h the words at (k & h) hold
+// pre-quotient values, paired with each other by the next layer; materialised before the
+// transpose, and phase 2 starts materialised.
+template <class K, int LOGN>
+__device__ __forceinline__ void inv_body_n_lazy(uint32_t (&v)[32], const uint2* tws,
+                                                const FastArgs& A,
+                                                const XposeN<(1 << LOGN) / 32>& X, int j) {
+  using Tw = typename K::Tw;
+  constexpr int G = (1 << LOGN) / 32;
+#pragma unroll
+  for (int s = LOGN; s >= 6; --s) {  // phase 1: contiguous, register half-span h = 2^{LOGN-s}
+    const int h = 1 << (LOGN - s);
+    const uint32_t off = A.off[LOGN - s + 1];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      const Tw w = tw_smem<Tw>(tws, seg_base<LOGN, true>(s) + (k >> (LOGN - s + 1)) * G + j);
+      if (s < LOGN && (k & (h >> 1))) K::inv_hh(v[k], v[k + h], w, off, A);
+      else K::inv_h(v[k], v[k + h], w, off, A);
+    }
+  }
+  constexpr int hl = 1 << (LOGN - 6);  // half-span of the last phase-1 layer: lazy words
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k & hl) v[k] = K::materialize(v[k], A);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = X.get(k);
+#pragma unroll
+  for (int s = 5; s >= 1; --s) {  // phase 2: strided, h = 2^{5-s}, materialised start
+    const int h = 1 << (5 - s);
+    const uint32_t off = A.off[LOGN - s + 1];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      const bool lazy = s < 5 && (k & (h >> 1));
+      if (s == 1) {
+        if (lazy) K::inv_last_hh(v[k], v[k + h], off, A);
+        else K::inv_last(v[k], v[k + h], off, A);
+      } else {
+        const Tw w = K::tw(A, 32 - (2 << (s - 1)) + (k >> (6 - s)));
+        if (lazy) K::inv_hh(v[k], v[k + h], w, off, A);
+        else K::inv_h(v[k], v[k + h], w, off, A);
+      }
+    }
+  }
+}
+
 template <int LOGN, bool TRANSPOSE, bool MERGE>
 __device__ __forceinline__ void stage_table(uint2* tws, const uint32_t* tab) {
   constexpr int N = 1 << LOGN, G = N / 32;
@@ -378,7 +430,8 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// MODE 0: generic canonicalisation of the input words; 1: host-validated fast form
+// MODE bits 0-1 -- 0: generic canonicalisation of the input words; 1: host-validated fast
+// form.  MODE bit 2: lazy merge (policy kLazy, A.flags bit 3).
 template <class K, class IO, int LOGN, int MODE>
 __global__ void __launch_bounds__(kThreads)
     invn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
@@ -412,8 +465,9 @@ __global__ void __launch_bounds__(kThreads)
         v, reinterpret_cast<const IO*>(stages + s * GN::kStageBytes + GN::poly_offset(warp, half)), j);
     release_stage(&empty[s], lane);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = canon<IO, K::kSigned, MODE == 1>(v[k], A);
-    inv_body_n<K, LOGN>(v, tws, A, X, j);
+    for (int k = 0; k < 32; ++k) v[k] = canon<IO, K::kSigned, (MODE & 3) == 1>(v[k], A);
+    if constexpr ((MODE & 4) != 0) inv_body_n_lazy<K, LOGN>(v, tws, A, X, j);
+    else inv_body_n<K, LOGN>(v, tws, A, X, j);
     store_strided_n<IO, G>(out + poly * GN::N, j, v, X, poly < batch);
   }
 }
@@ -448,12 +502,22 @@ cudaError_t inv_n_mode(const void* in, void* out, size_t batch, const uint32_t* 
   return cudaGetLastError();
 }
 
+template <class K, class IO, int LOGN, int LZ>
+cudaError_t inv_n_canon(const void* in, void* out, size_t batch, const uint32_t* tab,
+                        const FastArgs& A, cudaStream_t st) {
+  const unsigned fast_bit = sizeof(IO) == 2 ? 1u : 2u;
+  if (!K::kSigned && (A.flags & fast_bit))
+    return inv_n_mode<K, IO, LOGN, 1 | LZ>(in, out, batch, tab, A, st);
+  return inv_n_mode<K, IO, LOGN, 0 | LZ>(in, out, batch, tab, A, st);
+}
+
 template <class K, class IO, int LOGN>
 cudaError_t inv_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
                   cudaStream_t st) {
-  const unsigned fast_bit = sizeof(IO) == 2 ? 1u : 2u;
-  if (!K::kSigned && (A.flags & fast_bit)) return inv_n_mode<K, IO, LOGN, 1>(in, out, batch, tab, A, st);
-  return inv_n_mode<K, IO, LOGN, 0>(in, out, batch, tab, A, st);
+  if constexpr (lazy_of<K>::value) {
+    if (A.flags & 8) return inv_n_canon<K, IO, LOGN, 4>(in, out, batch, tab, A, st);
+  }
+  return inv_n_canon<K, IO, LOGN, 0>(in, out, batch, tab, A, st);
 }
 
 template <class K, bool PER_INDEX, class IO>
