@@ -45,12 +45,15 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(NTTK_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-int device_count() {
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
+int device_count() {  // probed once per process (the device set does not change)
+  static const int n = [] {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return c;
+  }();
   return n;
 }
 
@@ -193,9 +196,11 @@ struct Workspace {
   std::mutex mu;
   int device = -1;
   cudaStream_t st[3] = {};
+  cudaEvent_t ev[3] = {};  // stream joins (no timing)
   void* buf[3][3] = {};
   size_t cap = 0;  // bytes per buffer
   unsigned* d_flag = nullptr;
+  unsigned* h_flag = nullptr;  // pinned: the flag read stays asynchronous until the one sync
 };
 
 Workspace* workspace(int dev) {
@@ -208,7 +213,10 @@ Workspace* workspace(int dev) {
     w->device = dev;
     for (auto& s : w->st)
       if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    for (auto& e : w->ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
     if (cudaMalloc(&w->d_flag, sizeof(unsigned)) != cudaSuccess) return nullptr;
+    if (cudaMallocHost(&w->h_flag, sizeof(unsigned)) != cudaSuccess) return nullptr;
     ws[dev] = std::move(w);
   }
   return ws[dev].get();
@@ -249,12 +257,17 @@ int host_pipeline(const HostParams& P, int elem, size_t batch, const std::vector
   size_t chunk = std::max<size_t>(1, kChunkBytes / poly_bytes);
   if (chunk > batch) chunk = batch ? batch : 1;
   if (int s = ensure_cap(*W, chunk * poly_bytes)) return s;
-  cudaError_t e = cudaMemset(W->d_flag, 0, sizeof(unsigned));
+  // only as many streams as chunks; stream 0 clears the flag, the others wait for it
+  const size_t nchunks = (batch + chunk - 1) / chunk;
+  const int nst = nchunks < 3 ? static_cast<int>(nchunks ? nchunks : 1) : 3;
+  cudaError_t e = cudaMemsetAsync(W->d_flag, 0, sizeof(unsigned), W->st[0]);
+  if (e == cudaSuccess && nst > 1) e = cudaEventRecord(W->ev[0], W->st[0]);
+  for (int i = 1; i < nst && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(W->st[i], W->ev[0], 0);
   if (e != cudaSuccess) return cuda_fail(e, who);
   size_t k = 0;
   for (size_t done = 0; done < batch; done += chunk, ++k) {
     const size_t n = std::min(chunk, batch - done);
-    const int s = static_cast<int>(k % 3);
+    const int s = static_cast<int>(k % nst);
     cudaStream_t st = W->st[s];
     for (size_t i = 0; i < h_in.size(); ++i) {
       e = cudaMemcpyAsync(W->buf[s][i], static_cast<const char*>(h_in[i]) + done * poly_bytes,
@@ -274,14 +287,16 @@ int host_pipeline(const HostParams& P, int elem, size_t batch, const std::vector
       if (e != cudaSuccess) return cuda_fail(e, who);
     }
   }
-  for (auto& st : W->st) {
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, who);
+  // join the other streams into stream 0, read the flag there, one host sync
+  for (int i = 1; i < nst && e == cudaSuccess; ++i) {
+    e = cudaEventRecord(W->ev[i], W->st[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(W->st[0], W->ev[i], 0);
   }
-  unsigned flag = 0;
-  e = cudaMemcpy(&flag, W->d_flag, sizeof flag, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(W->h_flag, W->d_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, W->st[0]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(W->st[0]);
   if (e != cudaSuccess) return cuda_fail(e, who);
-  if (flag) return NTTK_PROPERTY;  // caller turns it into its contract message
+  if (*W->h_flag) return NTTK_PROPERTY;  // caller turns it into its contract message
   return NTTK_OK;
 }
 

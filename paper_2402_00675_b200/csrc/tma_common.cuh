@@ -27,7 +27,13 @@ struct Geo {
   static constexpr int kPolyBytes = 256 * int(sizeof(IO));
   static constexpr int kPad = sizeof(IO) == 2 ? 32 : 64;
   static constexpr int kHalfBytes = kConsumers * kPolyBytes;
-  static constexpr int kStages = sizeof(IO) == 2 ? 4 : 3;
+#ifndef NTTK_STAGES16
+#define NTTK_STAGES16 4
+#endif
+#ifndef NTTK_STAGES32
+#define NTTK_STAGES32 3
+#endif
+  static constexpr int kStages = sizeof(IO) == 2 ? NTTK_STAGES16 : NTTK_STAGES32;
   static constexpr int kStageBytes = 2 * kHalfBytes + kPad + 64;  // keep stages 128B-aligned
   static constexpr int kSmem = kStages * kStageBytes + kConsumers * kScratchWords * 4 +
                                2 * kStages * 8;
