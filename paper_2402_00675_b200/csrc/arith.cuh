@@ -127,10 +127,13 @@ struct ImprovedN16 {
     y = x + A.p - r;
     x = x + r + A.zero;
   }
-  // twiddle w = omega^0 = 1: MP(w_hat, Y) is the canonical residue of Y, so r = Y for a
-  // canonical Y (layer 1) and r = min(Y, Y - p) for Y < 2p (layer 2) -- no multiply
-  __device__ static void fwd_w1(uint32_t& x, uint32_t& y, bool reduce, const FastArgs& A) {
-    const uint32_t r = reduce ? umin32(y, y - A.p) : y;
+  // twiddle w = omega^0 = 1: MP(w_hat, Y) is the canonical residue of Y -- no multiply.
+  // Layer s inputs are < s p: r = Y (s = 1), min(Y, Y - p) (s = 2), and for s = 3, 4 first
+  // min(Y, Y - 2p) < 2p, then min(., . - p)
+  __device__ static void fwd_w1(uint32_t& x, uint32_t& y, int layer, const FastArgs& A) {
+    uint32_t r = y;
+    if (layer >= 3) r = umin32(r, r - A.two_p);
+    if (layer >= 2) r = umin32(r, r - A.p);
     y = x + A.p - r;
     x = x + r + A.zero;
   }
@@ -219,8 +222,10 @@ struct ImprovedN32 {
   __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
     fwd(x, y, w, A);
   }
-  __device__ static void fwd_w1(uint32_t& x, uint32_t& y, bool reduce, const FastArgs& A) {
-    const uint32_t r = reduce ? umin32(y, y - A.p) : y;  // see ImprovedN16::fwd_w1
+  __device__ static void fwd_w1(uint32_t& x, uint32_t& y, int layer, const FastArgs& A) {
+    uint32_t r = y;  // see ImprovedN16::fwd_w1
+    if (layer >= 3) r = umin32(r, r - A.two_p);
+    if (layer >= 2) r = umin32(r, r - A.p);
     y = x + A.p - r;
     x = x + r + A.zero;
   }

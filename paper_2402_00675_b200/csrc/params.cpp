@@ -195,10 +195,11 @@ void fill_fast(HostParams& P, int kind) {
     }
     // n = 32: lo32(h' p) < 2p for every fast-path operand (ImprovedN32 lazy merge)
     if (kind == NTTK_IMPROVED && !n16 && u128(4) * p < (u128(1) << 32)) A.flags |= 8;
-    // forward block 0 of layers 1 and 2 has twiddle 1 (cyclic tree): multiply-free
+    // forward block 0 of layers 1..4 has twiddle 1 (cyclic tree): multiply-free
     // Plantard products (fwd_body W1)
-    if (kind == NTTK_IMPROVED && dir == 0 && P.ct_plain.size() >= 3 && P.ct_plain[0] == 1 &&
-        P.ct_plain[1] == 1)
+    if (kind == NTTK_IMPROVED && dir == 0 && P.layers >= 4 && P.ct_plain.size() >= 8 &&
+        P.ct_plain[0] == 1 && P.ct_plain[1] == 1 && P.ct_plain[3] == 1 && P.ct_plain[7] == 1 &&
+        uint64_t(4) * P.p < (uint64_t(1) << 32))
       A.flags |= 16;
     // last merge twiddle times N^{-1} (the final scaling folded into the last layer)
     {

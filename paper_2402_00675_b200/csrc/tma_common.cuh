@@ -288,10 +288,18 @@ __device__ __forceinline__ void inv_twiddles(typename K::Tw (&twl)[15], const Fa
   }
 }
 
+// Forward layers whose block-0 product is multiply-free (1..4).  Measured (round 2): 2 is
+// best for Kyber (0.996 ms vs 1.014 at 3 or 4 -- the extra min ops and the changed
+// schedule cost more than the 3 saved multiplies); Dilithium is flat within noise.
+#ifndef NTTK_W1_LAYERS
+#define NTTK_W1_LAYERS 2
+#endif
+
 // run_split_layers (transform.hpp:77-96): strided in -> contiguous out.
-// W1 (A.flags bit 4, improved kinds on the cyclic tree): block 0 of layers 1 and 2 has
-// twiddle omega^0 = 1 and canonical-or-< 2p inputs, so its Plantard product needs no
-// multiply (fwd_w1); input coefficients must be canonical (the ntt_forward contract).
+// W1 (A.flags bit 4, improved kinds on the cyclic tree): block 0 of layers 1..4 has
+// twiddle omega^0 = 1 and inputs below s p, so its Plantard product is a canonical
+// reduction without a multiply (fwd_w1); input coefficients must be canonical (the
+// ntt_forward contract).
 template <class K, int L, bool PER_INDEX, bool W1 = false, class TWL>
 __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                          const Xpose& X) {
@@ -303,8 +311,8 @@ __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const TWL& twl, cons
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
       if constexpr (W1 && !PER_INDEX) {
-        if (sl <= 2 && (r >> (5 - sl)) == 0) {
-          K::fwd_w1(v[r], v[r + h], sl == 2, A);
+        if (sl <= NTTK_W1_LAYERS && (r >> (5 - sl)) == 0) {
+          K::fwd_w1(v[r], v[r + h], sl, A);
           continue;
         }
       }
