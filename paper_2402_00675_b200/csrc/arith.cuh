@@ -11,19 +11,23 @@
 //                               CT = the CT-form twin used on the negacyclic tree
 //   Smont<16|32>                signed Montgomery (reduction.hpp:141-165) in CT/GS form
 //                               (extension)
+//   Scott32, Ntl<16|32>         Alg. 9 / Alg. 7 (butterfly.hpp:172-184, 60-71)
 //
-// Issue-slot economy (measured on B200, profiles/r01_imad_microbench.txt): IMAD runs at
-// 64 lanes/clk/SM on the fmaheavy pipe, IMAD.HI and IMAD.WIDE at half that, the ALU
-// pipe (IADD3, LOP3, SHF) at 64.  A butterfly is therefore fmaheavy-bound, so:
+// Issue-slot economy (measured on B200, profiles/r01_imad_microbench.txt and
+// r02_bf_microbench*.txt): IMAD runs at 64 lanes/clk/SM on the fmaheavy pipe, IMAD.HI and
+// IMAD.WIDE at half that, the ALU pipe at 64; mixed into a butterfly stream every non-FMA
+// instruction costs about 0.8 cycles on top of the FMA cycles.  So:
 //   * plain additions are written x + y + A.zero (A.zero == 0 at run time, opaque to
 //     ptxas): a three-input add only exists as IADD3 on the ALU pipe, which stops
-//     ptxas from moving the adds onto the saturated fmaheavy pipe as IMAD.IADD;
-//   * the n = 16 Plantard tail has two exact forms (below) with different pipe mixes.
+//     ptxas from moving the adds onto the fmaheavy pipe as IMAD.IADD;
+//   * ALU work is removed where the algebra allows (lazy merge outputs instead of fence
+//     ops, multiply-free twiddle-1 blocks), and the umulhi form is used everywhere by
+//     default (the paper form trades 2 FMA cycles for 2 shifts, measured slower).
 //
-// SASS per Plantard multiply (committed census: profiles/r01_sass_census.txt):
+// SASS per Plantard multiply (census: profiles/r02_sass_census.txt):
 //   n=16: IMAD (h = t * w_hat mu) + IMAD.HI (r = hi32(h p))        [umulhi form]
 //         IMAD + SHF + IMAD + SHF (r = (((h >> 16) + 1) p) >> 16)  [paper form]
-//   n=32: IMAD + IMAD.HI (h_hi + 1) + IMAD.HI (r = hi32((h_hi + 1) p))
+//   n=32: IMAD + IMAD.HI (h_hi) + IMAD.HI/IMAD.WIDE (r = hi32(h_hi p + p))
 #pragma once
 
 #include <cstdint>
