@@ -649,3 +649,106 @@ def improved_ct_butterfly(X, Y, W_hat, ctx: ReductionContext):
 def improved_gs_butterfly(X, Y, W_hat, ctx: ReductionContext, layer: int):
     """butterfly.hpp:263-279 (Alg. 12)."""
     return _butterfly_host(BF_IMPROVED_GS, ctx, X, Y, W_hat, None, layer)
+
+
+# ---------------------------------------------------------------------------
+# transform.hpp / params.hpp helpers (same names as the reference)
+
+def spectrum_value_bound(P: NttParams, kind) -> int:
+    """transform.hpp:61-70 (smont: bound on |value|)."""
+    k = ButterflyKind(kind)
+    return {ButterflyKind.ntl: P.p, ButterflyKind.harvey: 2 * P.p,
+            ButterflyKind.scott: P.size * P.p, ButterflyKind.improved: (P.log2_size + 1) * P.p,
+            ButterflyKind.smont: (P.log2_size + 2) * P.p}[k]
+
+
+def canonicalize(v, p: int):
+    """transform.hpp:38-40: every word mod p, on the device (returns a new array)."""
+    a = np.ascontiguousarray(np.atleast_1d(np.asarray(v)).astype(np.uint64))
+    c = ReductionContext()
+    c.p, c.n_bits = p, 32  # the mod-p op reads only p
+    out = np.empty_like(a)
+    _check(lib().nttk_reduce_host(6, C.byref(c), a.ctypes.data, None, out.ctypes.data, a.size))
+    return out
+
+
+def bit_reverse_permutation(v) -> list:
+    """transform.hpp:42-52 (index permutation only)."""
+    n = len(v)
+    if n == 0 or n & (n - 1):
+        raise ContractViolation("bit_reverse_permutation: size must be a power of two")
+    bits = n.bit_length() - 1
+    out = [0] * n
+    for i, x in enumerate(v):
+        out[int(format(i, f"0{bits}b")[::-1], 2) if bits else 0] = x
+    return out
+
+
+def to_natural_order(s: Spectrum) -> list:
+    """transform.hpp:54-58."""
+    return list(s.values) if s.ordering == Ordering.natural else bit_reverse_permutation(s.values)
+
+
+PRESET_TABLE = (("kyber256", 7681, 256, 32), ("kcl256", 7681, 256, 32),
+                ("newhope512", 12289, 512, 32), ("falcon512", 12289, 512, 32),
+                ("remblem512", 12289, 512, 32), ("newhope1024", 12289, 1024, 32),
+                ("falcon1024", 12289, 1024, 32), ("hila5-1024", 12289, 1024, 32),
+                ("toy13", 13, 4, 8))  # params.hpp:280-289
+
+
+def preset_spec(name: str):
+    """params.hpp:291-301 -> (name, p, size, n_bits)."""
+    for spec in PRESET_TABLE:
+        if spec[0] == name:
+            return spec
+    preset(name)  # raises the engine's "unknown preset ... (known: ...)" message
+    raise ContractViolation(f"unknown preset '{name}'")
+
+
+def find_primitive_root(p: int, N: int) -> int:
+    """params.hpp:30-43: smallest w with w^N = 1 and w^{N/2} != 1 (host parameter search)."""
+    if N <= 0 or N & (N - 1):
+        raise ContractViolation("find_primitive_root: N must be a power of two")
+    if (p - 1) % N:
+        raise ContractViolation("find_primitive_root: N must divide p - 1")
+    if N == 1:
+        return 1
+    for w in range(2, p):
+        if pow(w, N, p) == 1 and pow(w, N // 2, p) != 1:
+            return w
+    raise ContractViolation("find_primitive_root: no root found")
+
+
+def dif_forward_plain_twiddles(N: int, omega: int, p: int) -> list:
+    """params.hpp:47-58."""
+    out, ln = [], N // 2
+    while ln >= 1:
+        step = N // (2 * ln)
+        out += [pow(omega, j * step, p) for j in range(ln)]
+        ln //= 2
+    return out
+
+
+def ct_forward_plain_twiddles(N: int, omega: int, p: int) -> list:
+    """params.hpp:60-72."""
+    out, ln = [], N // 2
+    while ln >= 1:
+        blocks = N // (2 * ln)
+        lvl = blocks.bit_length() - 1
+        out += [pow(omega, ln * (int(format(b, f"0{lvl}b")[::-1], 2) if lvl else 0), p)
+                for b in range(blocks)]
+        ln //= 2
+    return out
+
+
+def gs_inverse_plain_twiddles(N: int, omega: int, p: int) -> list:
+    """params.hpp:74-88."""
+    out, ln = [], 1
+    while ln < N:
+        blocks = N // (2 * ln)
+        lvl = blocks.bit_length() - 1
+        for b in range(blocks):
+            e = ln * (int(format(b, f"0{lvl}b")[::-1], 2) if lvl else 0) % N
+            out.append(pow(omega, N - e if e else 0, p))
+        ln *= 2
+    return out

@@ -132,3 +132,20 @@ def test_exact_bound_admits_kyber_n16_and_dilithium_n32(engine):
         engine.build_params(8380417, 256, 32, [engine.ButterflyKind.improved])
     engine.build_params(3329, 256, 16, [engine.ButterflyKind.improved], exact_bound=True)
     engine.build_params(8380417, 256, 32, [engine.ButterflyKind.improved], exact_bound=True)
+
+
+def test_params_helpers_match_engine_tables(engine):
+    """params.hpp / transform.hpp helpers of the Python mirror (host parameter logic) against
+    the engine's own tables and the reference's known values."""
+    for name in ("kyber256", "falcon512", "toy13"):
+        P = engine.preset(name)
+        assert engine.find_primitive_root(P.p, P.size) == P.omega
+        assert engine.ct_forward_plain_twiddles(P.size, P.omega, P.p) == list(P.table("ct_plain"))
+        assert engine.gs_inverse_plain_twiddles(P.size, P.omega, P.p) == list(P.table("gs_plain"))
+        assert engine.dif_forward_plain_twiddles(P.size, P.omega, P.p) == list(P.table("dif_w"))
+        assert engine.preset_spec(name)[1:3] == (P.p, P.size)
+    P = engine.preset("kyber256")
+    assert engine.spectrum_value_bound(P, engine.ButterflyKind.scott) == 256 * 7681
+    assert engine.to_natural_order(engine.Spectrum([0, 1, 2, 3])) == [0, 2, 1, 3]
+    with pytest.raises(engine.ContractViolation, match="unknown preset"):
+        engine.preset_spec("nope")

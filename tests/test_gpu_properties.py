@@ -294,3 +294,10 @@ def test_butterfly_contract_messages():
                       (lambda: nttk.make_scott_config(6, c8), "N must be a power of two")):
         with pytest.raises(nttk.ContractViolation, match=__import__("re").escape(msg)):
             call()
+
+
+def test_canonicalize_on_device():
+    """transform.hpp:38-40 through the device mod-p op."""
+    v = np.array([0, 7680, 7681, 7682, 2**63 + 5, 2**64 - 1], dtype=np.uint64)
+    got = nttk.canonicalize(v, 7681)
+    assert got.tolist() == [int(x) % 7681 for x in v.tolist()]
