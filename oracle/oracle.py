@@ -318,6 +318,8 @@ class Reference:
             L.ref_naive_dft.argtypes = [u64p, C.c_size_t, C.c_uint64, C.c_uint64, u64p]
             L.ref_time_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, u64p, C.c_size_t, C.c_int,
                                          C.POINTER(C.c_uint64)]
+            L.ref_run_all_suites.argtypes = [C.c_uint64, C.c_char_p, C.c_size_t,
+                                             C.POINTER(C.c_uint64)]
             if hasattr(L, "ref_run_bench"):
                 L.ref_run_bench.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int,
                                             C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
@@ -327,6 +329,15 @@ class Reference:
     def _check(self, st):
         if st != 0:
             raise OracleError(st, self.lib.ref_last_error().decode())
+
+    def run_all_suites(self, random_cases=100000):
+        """verify.hpp run_all_suites of the unmodified reference -> ([(name, cases, failures)],
+        total failures)."""
+        buf = C.create_string_buffer(1 << 14)
+        f = C.c_uint64()
+        self._check(self.lib.ref_run_all_suites(random_cases, buf, len(buf), C.byref(f)))
+        rows = [ln.rsplit(" ", 2) for ln in buf.value.decode().strip().splitlines()]
+        return [(n, int(c), int(k)) for n, c, k in rows], f.value
 
     def run_bench(self, presets=("kyber256", "falcon512", "falcon1024"), iters=2000, seed=12345,
                   micro=False) -> dict:

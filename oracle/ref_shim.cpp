@@ -22,6 +22,7 @@
 #include "nttk/bench.hpp"  // the reference's own timing harness (needs nlohmann json.hpp)
 #endif
 #include "nttk/oracle.hpp"
+#include "nttk/verify.hpp"  // the reference's own property suites
 #include "nttk/params.hpp"
 #include "nttk/reduction.hpp"
 #include "nttk/transform.hpp"
@@ -283,6 +284,27 @@ int ref_time_batch(void* hv, int kind, int mode, uint64_t* a, size_t batch, int 
     *ns = static_cast<uint64_t>(
         std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
     if (failed) throw contract_violation("ref_time_batch: a worker failed");
+  });
+}
+
+// The reference's own property suites (verify.hpp:576-584 run_all_suites): writes one line
+// "name cases failures" per suite into out; returns the total failure count in *failures.
+int ref_run_all_suites(uint64_t random_cases, char* out, size_t cap, uint64_t* failures) {
+  return guarded([&] {
+    VerifyOptions opt;
+    opt.random_cases = random_cases;
+    std::string txt;
+    uint64_t f = 0;
+    for (const auto& r : run_all_suites(opt)) {
+      txt += r.name + " " + std::to_string(r.cases) + " " + std::to_string(r.failures) + "\n";
+      f += r.failures;
+    }
+    *failures = f;
+    if (out && cap) {
+      const size_t n = txt.size() < cap - 1 ? txt.size() : cap - 1;
+      std::memcpy(out, txt.data(), n);
+      out[n] = 0;
+    }
   });
 }
 

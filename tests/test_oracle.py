@@ -255,3 +255,18 @@ def test_live_against_reference(oracle):
             a, b = P.forward(k, f), R.forward(k, f)
             assert (a == b).all()
             assert (P.inverse(k, a) == R.inverse(k, b)).all()
+
+
+def test_reference_self_verification_suites():
+    """The unmodified reference's own property suites (verify.hpp run_all_suites) pass
+    when built here: the checker behind the golden vectors verifies itself first."""
+    from oracle.oracle import Reference, reference_available
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not built (no /root/reference on this host)")
+    rows, failures = Reference().run_all_suites(100000)
+    names = {n for n, _, _ in rows}
+    assert {"montgomery", "signed-montgomery", "plantard", "modified-plantard", "butterflies",
+            "transform"} <= names
+    assert failures == 0, rows
+    assert all(c > 0 for _, c, _ in rows)
