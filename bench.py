@@ -64,6 +64,7 @@ def workload_config(a, world):
         "dilithium_polys_per_gpu": 1 << a.dil_log2,
         "parallelism": f"dp{world} (batch sharding, no collective on the compute path)",
         "l2": "working set 8 GiB/GPU >> 126 MB L2: no flush needed",
+        "storage": "int16 (Kyber) / int32 (Dilithium) words; arithmetic on 32-bit registers",
     }
 
 
@@ -588,7 +589,7 @@ def run_engine_arm(a, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": max_ms / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32 (int16/int32 storage)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic uniform [0,q) (torch.randint, seeded)",
             "config": workload_config(a, world),
             "fwd_only_polys_per_s": fwd_rate,
