@@ -152,6 +152,17 @@ enum nttk_redc {
 int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, const int64_t* d_A,
                       size_t na, const int64_t* d_B, size_t nb, int64_t* d_r,
                       uint64_t* h_checksum, void* stream);
+/* ---- observed transforms (transform.hpp:207-217, 233-337) ------------------------ */
+/* One polynomial (u64 words), run one layer per launch; after every layer the state is
+ * copied back and observer(layer, state, N, user) runs on the calling thread, with layers
+ * numbered as the reference's run_split_layers / run_merge_layers number them.  The
+ * forward checks its input is canonical ("ntt_forward: coefficients must be canonical"). */
+typedef void (*nttk_layer_observer)(unsigned layer, const uint64_t* state, size_t n, void* user);
+int nttk_ntt_forward_observed(nttk_params_t P, int kind, const uint64_t* h_in, uint64_t* h_out,
+                              nttk_layer_observer observer, void* user);
+int nttk_intt_inverse_observed(nttk_params_t P, int kind, const uint64_t* h_in, uint64_t* h_out,
+                               nttk_layer_observer observer, void* user);
+
 /* ---- reduction.hpp on arrays (the drop-in behind nttk::mont_redc & co.) ---------- */
 
 /* ReductionContext (reduction.hpp:44-78): every precomputed constant of (p, n, alpha, ell) */

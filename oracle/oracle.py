@@ -320,6 +320,7 @@ class Reference:
                                          C.POINTER(C.c_uint64)]
             L.ref_run_all_suites.argtypes = [C.c_uint64, C.c_char_p, C.c_size_t,
                                              C.POINTER(C.c_uint64)]
+            L.ref_observed.argtypes = [C.c_void_p, C.c_int, C.c_int, u64p, u64p, u64p]
             if hasattr(L, "ref_run_bench"):
                 L.ref_run_bench.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int,
                                             C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
@@ -423,6 +424,14 @@ class RefParams:
         out = np.empty_like(x)
         self.r._check(self.r.lib.ref_convolution(self.h, kind, x, y, out, x.shape[0]))
         return out
+
+    def observed(self, kind, dir, a, layers):
+        """The reference's *_observed on one polynomial -> (states[layers, N], output)."""
+        a = np.ascontiguousarray(np.array(a, dtype=np.uint64).reshape(self.N))
+        states = np.zeros((layers, self.N), dtype=np.uint64)
+        out = np.empty(self.N, dtype=np.uint64)
+        self.r._check(self.r.lib.ref_observed(self.h, kind, dir, a, states, out))
+        return states, out
 
     def time_batch(self, kind, mode, a, threads):
         a = np.ascontiguousarray(a, dtype=np.uint64)

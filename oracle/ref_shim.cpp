@@ -287,6 +287,26 @@ int ref_time_batch(void* hv, int kind, int mode, uint64_t* a, size_t batch, int 
   });
 }
 
+// ntt_forward_observed / intt_inverse_observed of the reference (transform.hpp:207-337):
+// one polynomial; states[(layer - 1) * N ...] receives the state after each layer
+int ref_observed(void* hv, int kind, int dir, const uint64_t* in, uint64_t* states, uint64_t* out) {
+  return guarded([&] {
+    const auto& P = static_cast<Handle*>(hv)->P;
+    const size_t N = P.size;
+    auto obs = [&](unsigned layer, const std::vector<uint64_t>& v) {
+      std::memcpy(states + size_t(layer - 1) * N, v.data(), N * 8);
+    };
+    if (dir == 0) {
+      const Spectrum s = ntt_forward_observed(Polynomial(in, in + N), P, to_kind(kind), obs);
+      std::memcpy(out, s.values.data(), N * 8);
+    } else {
+      const Polynomial f = intt_inverse_observed(
+          Spectrum{std::vector<uint64_t>(in, in + N), Ordering::bit_reversed}, P, to_kind(kind), obs);
+      std::memcpy(out, f.data(), N * 8);
+    }
+  });
+}
+
 // The reference's own property suites (verify.hpp:576-584 run_all_suites): writes one line
 // "name cases failures" per suite into out; returns the total failure count in *failures.
 int ref_run_all_suites(uint64_t random_cases, char* out, size_t cap, uint64_t* failures) {

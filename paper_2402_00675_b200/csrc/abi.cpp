@@ -584,6 +584,60 @@ int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, co
   return NTTK_OK;
 }
 
+// transform.hpp:207-217, 233-337 (observed transforms): one polynomial through the
+// generic per-layer kernel, observer called after every layer
+static int observed(nttk_params_t h, int kind, int dir, const uint64_t* h_in, uint64_t* h_out,
+                    nttk_layer_observer obs, void* user) {
+  const char* who = dir ? "intt_inverse" : "ntt_forward";
+  if (!h) return fail(NTTK_CONTRACT, std::string(who) + ": null params");
+  if (int s = check_kind(h->P, kind, who)) return s;
+  if (!h_in || !h_out) return fail(NTTK_CONTRACT, std::string(who) + ": null buffer");
+  const HostParams& P = h->P;
+  if (dir == 0)
+    for (uint32_t i = 0; i < P.N; ++i)  // contract check of the reference (input words)
+      if (h_in[i] >= P.p) return fail(NTTK_CONTRACT, "ntt_forward: coefficients must be canonical");
+  if (int s = need_device(who)) return s;
+  std::string err;
+  const nttk_b200::DeviceTables* T = P.device_tables(current_device(), err);
+  if (!T) return fail(NTTK_CUDA, err);
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  uint64_t* d = nullptr;
+  uint64_t* hs = nullptr;
+  const size_t bytes = size_t(P.N) * 8;
+  if (e == cudaSuccess) e = cudaMallocAsync(&d, bytes, st);
+  if (e == cudaSuccess) e = cudaMallocHost(&hs, bytes);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, h_in, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = nttk_b200::generic_transform_observed(
+        P, *T, kind, dir, d, hs,
+        [&](unsigned layer) {
+          if (obs) obs(layer, hs, P.N, user);
+        },
+        st);
+  g_launches += P.layers + 2;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_out, d, bytes, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (d) cudaFreeAsync(d, st);
+  if (st) {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
+  if (hs) cudaFreeHost(hs);
+  if (e != cudaSuccess) return cuda_fail(e, who);
+  return NTTK_OK;
+}
+
+int nttk_ntt_forward_observed(nttk_params_t h, int kind, const uint64_t* h_in, uint64_t* h_out,
+                              nttk_layer_observer obs, void* user) {
+  return observed(h, kind, 0, h_in, h_out, obs, user);
+}
+
+int nttk_intt_inverse_observed(nttk_params_t h, int kind, const uint64_t* h_in, uint64_t* h_out,
+                               nttk_layer_observer obs, void* user) {
+  return observed(h, kind, 1, h_in, h_out, obs, user);
+}
+
 // reduction.hpp:80-117
 int nttk_make_reduction_context(uint64_t p, uint32_t n_bits, uint32_t alpha, uint32_t ell,
                                 nttk_reduction_ctx* out) {

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 
 #include "generic.hpp"
 
@@ -416,6 +417,52 @@ cudaError_t generic_transform(const HostParams& P, const DeviceTables& T, int ki
     case 8: return transform_io<uint64_t>(P, T, kind, dir, in, out, batch, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// ntt_forward_observed / intt_inverse_observed (transform.hpp:77-116, 207-337): one
+// polynomial, one launch per layer; after each layer the u64 state is read back and
+// observe(layer, state) runs on the host (layers numbered as the reference's
+// run_split_layers / run_merge_layers do).  d_io holds N u64 words (input, then output).
+cudaError_t generic_transform_observed(const HostParams& P, const DeviceTables& T, int kind,
+                                       int dir, uint64_t* d_io, uint64_t* h_state,
+                                       const std::function<void(unsigned)>& observe,
+                                       cudaStream_t st) {
+  const GCtx c = make_gctx(P);
+  const size_t n = P.N;
+  uint64_t* w = nullptr;
+  cudaError_t e = cudaMallocAsync(&w, n * 8, st);
+  if (e != cudaSuccess) return e;
+  const bool sgn = kind == NTTK_SMONT;
+  load_u64_kernel<uint64_t><<<grid_for(n, 256), 256, 0, st>>>(d_io, w, n, sgn, dir == 1, P.p);
+  const bool per_index = P.tree == NTTK_CYCLIC && kind != NTTK_IMPROVED && kind != NTTK_SMONT;
+  auto after = [&](unsigned layer) -> cudaError_t {
+    cudaError_t x = cudaMemcpyAsync(h_state, w, n * 8, cudaMemcpyDeviceToHost, st);
+    if (x == cudaSuccess) x = cudaStreamSynchronize(st);
+    if (x == cudaSuccess) observe(layer);
+    return x;
+  };
+  size_t cursor = 0;
+  if (dir == 0) {
+    for (uint32_t s = 1; s <= P.layers && e == cudaSuccess; ++s) {
+      layer_kernel<<<grid_for(P.N / 2, 256), 256, 0, st>>>(kind, 0, w, 1, s, cursor, 0, c, T);
+      cursor += per_index ? (P.N >> s) : (size_t(1) << (s - 1));
+      e = after(s);
+    }
+  } else {
+    unsigned m = 0;
+    for (uint32_t s = P.layers; s >= 1 && e == cudaSuccess; --s) {
+      ++m;
+      layer_kernel<<<grid_for(P.N / 2, 256), 256, 0, st>>>(kind, 1, w, 1, s, cursor, m, c, T);
+      cursor += size_t(1) << (s - 1);
+      e = after(m);
+    }
+  }
+  if (e == cudaSuccess) {
+    store_u64_kernel<uint64_t><<<grid_for(n, 256), 256, 0, st>>>(w, d_io, n, kind, dir == 1, c);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(w, st);
+  return e;
 }
 
 cudaError_t generic_pointwise(const HostParams& P, int kind, const void* l, const void* r,

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
+
 #include "params.hpp"
 
 namespace nttk_b200 {
@@ -10,6 +12,11 @@ namespace nttk_b200 {
 cudaError_t generic_transform(const HostParams& P, const DeviceTables& T, int kind, int dir,
                               const void* in, void* out, size_t batch, int elem_bytes,
                               cudaStream_t st);
+// one polynomial, layer by layer, observe(layer) after each (state copied to h_state)
+cudaError_t generic_transform_observed(const HostParams& P, const DeviceTables& T, int kind,
+                                       int dir, uint64_t* d_io, uint64_t* h_state,
+                                       const std::function<void(unsigned)>& observe,
+                                       cudaStream_t st);
 cudaError_t generic_pointwise(const HostParams& P, int kind, const void* l, const void* r,
                               void* out, size_t batch, int elem_bytes, cudaStream_t st);
 // d_gamma: N/2 per-pair basemul moduli gamma_k (x^2 - gamma_k), device memory

@@ -26,6 +26,8 @@
 #pragma once
 
 #include <cstdint>
+#include <exception>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -485,6 +487,54 @@ inline void ntt_forward_inplace(std::vector<uint64_t>& a, const NttParams& P, Bu
   detail::check(nttk_polymul_host(P.handle.get(), static_cast<int>(kind), x.data(), y.data(),
                                   out.data(), 1, 8));
   return out;
+}
+
+// ---- observed transforms (transform.hpp:207-217, 233-337) -------------------------
+using LayerObserver = std::function<void(unsigned layer, const std::vector<uint64_t>& state)>;
+
+namespace detail {
+struct ObserverCtx {
+  const LayerObserver* fn;
+  std::exception_ptr error;
+};
+inline void observer_trampoline(unsigned layer, const uint64_t* state, size_t n, void* user) {
+  auto* c = static_cast<ObserverCtx*>(user);
+  if (c->error || !*c->fn) return;
+  try {
+    (*c->fn)(layer, std::vector<uint64_t>(state, state + n));
+  } catch (...) {  // never unwind through the C ABI: rethrown after the call returns
+    c->error = std::current_exception();
+  }
+}
+}  // namespace detail
+
+[[nodiscard]] inline Spectrum ntt_forward_observed(const Polynomial& f, const NttParams& P,
+                                                   ButterflyKind kind, const LayerObserver& observer) {
+  if (!P.has(kind)) throw contract_violation("ntt_forward: kind not built into these params");
+  if (f.size() != P.size) throw contract_violation("ntt_forward: wrong input length");
+  Spectrum s{std::vector<uint64_t>(P.size), Ordering::bit_reversed};
+  detail::ObserverCtx c{&observer, nullptr};
+  const int st = nttk_ntt_forward_observed(P.handle.get(), static_cast<int>(kind), f.data(),
+                                           s.values.data(), detail::observer_trampoline, &c);
+  if (c.error) std::rethrow_exception(c.error);
+  detail::check(st);
+  return s;
+}
+
+[[nodiscard]] inline Polynomial intt_inverse_observed(const Spectrum& s, const NttParams& P,
+                                                      ButterflyKind kind,
+                                                      const LayerObserver& observer) {
+  if (!P.has(kind)) throw contract_violation("intt_inverse: kind not built into these params");
+  if (s.values.size() != P.size) throw contract_violation("intt_inverse: wrong input length");
+  if (s.ordering != Ordering::bit_reversed)
+    throw contract_violation("intt_inverse: spectrum must be in butterfly order");
+  Polynomial f(P.size);
+  detail::ObserverCtx c{&observer, nullptr};
+  const int st = nttk_intt_inverse_observed(P.handle.get(), static_cast<int>(kind), s.values.data(),
+                                            f.data(), detail::observer_trampoline, &c);
+  if (c.error) std::rethrow_exception(c.error);
+  detail::check(st);
+  return f;
 }
 
 // ---- device-pointer batched calls (asynchronous on `stream`) ----------------------

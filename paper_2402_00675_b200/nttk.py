@@ -114,6 +114,9 @@ class ReductionContext(C.Structure):
         return 2 * self.p < (1 << self.n_bits)
 
 
+_OBSERVER = C.CFUNCTYPE(None, C.c_uint, C.POINTER(C.c_uint64), C.c_size_t, C.c_void_p)
+
+
 class _Info(C.Structure):
     _fields_ = [("p", C.c_uint64), ("omega", C.c_uint64), ("omega_inv", C.c_uint64),
                 ("n_inv", C.c_uint64), ("n_inv_hat", C.c_uint64), ("mu", C.c_uint64),
@@ -128,7 +131,8 @@ EXPORTS = (
     "nttk_basemul", "nttk_polymul", "nttk_ntt_forward_host", "nttk_intt_inverse_host",
     "nttk_roundtrip_host", "nttk_pointwise_multiply_host", "nttk_polymul_host",
     "nttk_modmul_sweep", "nttk_make_reduction_context", "nttk_reduce", "nttk_reduce_host",
-    "nttk_butterfly", "nttk_butterfly_host",
+    "nttk_butterfly", "nttk_butterfly_host", "nttk_ntt_forward_observed",
+    "nttk_intt_inverse_observed",
     "nttk_last_error", "nttk_launch_count", "nttk_device_available", "nttk_version",
 )
 
@@ -170,6 +174,8 @@ def lib() -> C.CDLL:
             extra = [vp] if f == "nttk_butterfly" else []
             getattr(L, f).argtypes = ([C.c_int, C.POINTER(ReductionContext), C.c_uint32, C.c_uint32]
                                       + [vp] * 6 + [sz] + extra)
+        for f in ("nttk_ntt_forward_observed", "nttk_intt_inverse_observed"):
+            getattr(L, f).argtypes = [vp, C.c_int, vp, vp, _OBSERVER, vp]
         L.nttk_last_error.restype = C.c_char_p
         L.nttk_launch_count.restype = C.c_uint64
         L.nttk_version.restype = C.c_char_p
@@ -752,3 +758,42 @@ def gs_inverse_plain_twiddles(N: int, omega: int, p: int) -> list:
             out.append(pow(omega, N - e if e else 0, p))
         ln *= 2
     return out
+
+
+# ---------------------------------------------------------------------------
+# observed transforms (transform.hpp:207-217, 233-337): observer(layer, state) per layer
+
+def _observed(fn, P: NttParams, kind, words, observer):
+    a = np.ascontiguousarray(np.array(words, dtype=np.uint64).reshape(-1))
+    if a.size != P.size:
+        raise ContractViolation(("ntt_forward" if fn.endswith("forward_observed") else "intt_inverse")
+                                + ": wrong input length")
+    out = np.empty_like(a)
+    err = []
+
+    def cb(layer, state, n, user):
+        if err or observer is None:
+            return
+        try:
+            observer(int(layer), [int(state[i]) for i in range(n)])
+        except BaseException as e:  # re-raised after the call: never unwind through C
+            err.append(e)
+
+    cfn = _OBSERVER(cb)
+    st = getattr(lib(), fn)(P.handle, int(kind), a.ctypes.data, out.ctypes.data, cfn, None)
+    if err:
+        raise err[0]
+    _check(st)
+    return [int(v) for v in out]
+
+
+def ntt_forward_observed(f, P: NttParams, kind, observer) -> Spectrum:
+    """transform.hpp:207-217."""
+    return Spectrum(_observed("nttk_ntt_forward_observed", P, kind, f, observer), Ordering.bit_reversed)
+
+
+def intt_inverse_observed(s: Spectrum, P: NttParams, kind, observer) -> list:
+    """transform.hpp:233-337."""
+    if s.ordering != Ordering.bit_reversed:
+        raise ContractViolation("intt_inverse: spectrum must be in butterfly order")
+    return _observed("nttk_intt_inverse_observed", P, kind, s.values, observer)

@@ -262,6 +262,25 @@ int main() {
     CHECK(preset_spec("falcon1024").size == 1024);
     CHECK(throws_with([] { (void)preset_spec("nope"); }, "unknown preset"));
   }
+  // observed transforms: one callback per layer, the last forward state is the spectrum,
+  // the inverse's states end in the scaled polynomial's pre-scaling sums
+  {
+    const auto P = preset("toy13");
+    const Polynomial f{1, 2, 3, 4};
+    for (auto k : all_butterfly_kinds()) {
+      std::vector<std::vector<uint64_t>> states;
+      const auto s = ntt_forward_observed(f, P, k, [&](unsigned layer, const std::vector<uint64_t>& v) {
+        CHECK(layer == states.size() + 1);
+        states.push_back(v);
+      });
+      CHECK(states.size() == 2 && states.back() == s.values && s.values == ntt_forward(f, P, k).values);
+      unsigned layers = 0;
+      const auto g = intt_inverse_observed(s, P, k, [&](unsigned, const std::vector<uint64_t>&) { ++layers; });
+      CHECK(layers == 2 && g == f);
+    }
+    CHECK(throws_with([&] { (void)ntt_forward_observed({13, 0, 0, 0}, P, ButterflyKind::ntl, nullptr); },
+                      "coefficients must be canonical"));
+  }
   std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }

@@ -427,3 +427,30 @@ def test_launch_counter_moves():
     x = torch.zeros(64, 256, dtype=torch.int16, device="cuda")
     nttk.forward(P, IMPROVED, x)
     assert nttk.launch_count() == before + 1
+
+
+@pytest.mark.parametrize("name", ["toy13", "kyber256", "falcon512"])
+def test_observed_transforms_match_reference_layer_by_layer(name):
+    """ntt_forward_observed / intt_inverse_observed: every intermediate layer state equals the
+    unmodified reference's (transform.hpp:77-116 observer calls), every kind."""
+    from oracle.oracle import Oracle, Reference, reference_available
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    P = nttk.preset(name)
+    R = Reference().params(P.p, P.size, P.n_bits, (NTL, HARVEY, SCOTT, IMPROVED))
+    L = P.size.bit_length() - 1
+    f = Oracle().rng(17, P.p, P.size)
+    for k in (NTL, HARVEY, SCOTT, IMPROVED):
+        got = []
+        spec = nttk.ntt_forward_observed(f, P, k, lambda layer, st: got.append((layer, st)))
+        want_states, want_out = R.observed(k, 0, f, L)
+        assert [g[0] for g in got] == list(range(1, L + 1))
+        for (layer, st), w in zip(got, want_states):
+            assert st == [int(x) for x in w], (name, k, layer)
+        assert spec.values == [int(x) for x in want_out]
+        got_i = []
+        back = nttk.intt_inverse_observed(spec, P, k, lambda layer, st: got_i.append(st))
+        want_states, want_out = R.observed(k, 1, spec.values, L)
+        assert got_i == [[int(x) for x in w] for w in want_states], (name, k)
+        assert back == [int(x) for x in f]
