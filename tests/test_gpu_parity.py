@@ -454,3 +454,30 @@ def test_observed_transforms_match_reference_layer_by_layer(name):
         want_states, want_out = R.observed(k, 1, spec.values, L)
         assert got_i == [[int(x) for x in w] for w in want_states], (name, k)
         assert back == [int(x) for x in f]
+
+
+@pytest.mark.parametrize("p,N,n,tree,layers", [(40961, 4096, 32, CYCLIC, 0), (65537, 8192, 32, CYCLIC, 0),
+                                               (65537, 16384, 32, CYCLIC, 0),
+                                               (40961, 4096, 32, NEGA, 10)])
+def test_generic_large_n_vs_oracle(oracle, p, N, n, tree, layers):
+    """The generic kernel at large N: one CTA per polynomial up to N = 4096, one launch per
+    layer beyond (generic.cu) -- every admitted kind, forward words and round trips."""
+    kinds = (NTL, HARVEY, SCOTT, IMPROVED) if tree == CYCLIC else (HARVEY, IMPROVED, SMONT)
+    admitted = []
+    for k in kinds:
+        try:
+            engine_params(p, N, n, [k], tree=tree, layers=layers, exact=True)
+            admitted.append(k)
+        except nttk.ContractViolation:
+            pass
+    assert admitted
+    B = 3
+    f = oracle.rng(N + p, p, B * N).reshape(B, N)
+    for k in admitted:
+        P = engine_params(p, N, n, [k], tree=tree, layers=layers, exact=True)
+        Q = oracle.params(p, N, n, (k,), tree=tree, layers=layers, exact=True)
+        assert k not in P.fast_path
+        sgn = k == SMONT
+        y = nttk.forward(P, k, to_dev(f, 8, sgn))
+        assert (from_dev(y, sgn).astype(np.int64) == Q.forward(k, f).astype(np.int64)).all(), k
+        assert (from_dev(nttk.inverse(P, k, y)) == f).all(), k
