@@ -116,6 +116,8 @@ int check_canonical_storage(const HostParams& P, int elem, const char* who) {
   return NTTK_OK;
 }
 
+bool aligned16(const void* p) { return !(reinterpret_cast<uintptr_t>(p) & 15); }
+
 bool use_fast(const HostParams& P, int kind) {
   if (!((P.fast_mask >> kind) & 1u)) return false;
   if (P.N != 256) return true;  // fastn_tma.cu (N = 512 / 1024, full trees; fast_eligible)
@@ -152,7 +154,9 @@ int run_transform(const HostParams& P, int kind, int dir, const void* in, void* 
     if (!tab) return fail(NTTK_CUDA, err);
     e = nttk_b200::fastn_launch(P, kind, dir, in, out, batch, elem, tab, st);
     g_launches += batch ? 1 : 0;
-  } else if (P.N == 256 && use_fast(P, kind)) {
+  } else if (P.N == 256 && use_fast(P, kind) && aligned16(in) && aligned16(out)) {
+    // both N = 256 kernels read and write 16-byte vectors: misaligned buffers take the
+    // generic kernel
     // NTTK_KERNEL=v1 selects the register-prefetch kernels (A/B comparisons)
     static const bool v1 = [] {
       const char* k = std::getenv("NTTK_KERNEL");

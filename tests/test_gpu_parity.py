@@ -481,3 +481,45 @@ def test_generic_large_n_vs_oracle(oracle, p, N, n, tree, layers):
         y = nttk.forward(P, k, to_dev(f, 8, sgn))
         assert (from_dev(y, sgn).astype(np.int64) == Q.forward(k, f).astype(np.int64)).all(), k
         assert (from_dev(nttk.inverse(P, k, y)) == f).all(), k
+
+
+def test_randomized_dispatch_sweep(oracle):
+    """Seeded random (kind, N, tree, storage width, batch, buffer offset) cases across every
+    dispatch path (TMA N=256 / N=512/1024 kernels, the register-prefetch u64 kernel, the
+    generic kernel for misaligned buffers): forward vs oracle, round trip."""
+    rng = np.random.default_rng(2402)
+    cases = 0
+    while cases < 40:
+        N = int(rng.choice([256, 512, 1024]))
+        p = {256: int(rng.choice([3329, 7681, 8380417])), 512: 12289, 1024: 12289}[N]
+        n = 16 if (p == 3329 and rng.random() < 0.5) else 32
+        tree = CYCLIC if (N > 256 or rng.random() < 0.6) else NEGA
+        kinds = [IMPROVED, HARVEY, SMONT] + ([NTL, SCOTT] if tree == CYCLIC else [])
+        k = int(rng.choice(kinds))
+        layers = 0 if tree == CYCLIC else (7 if p == 3329 else 8)
+        try:
+            P = engine_params(p, N, n, [k], tree=tree, layers=layers, exact=True)
+            Q = oracle.params(p, N, n, (k,), tree=tree, layers=layers, exact=True)
+        except (nttk.ContractViolation, Exception):
+            continue
+        sgn = k == SMONT
+        L = N.bit_length() - 1 if not layers else layers
+        bound = {NTL: p, HARVEY: 2 * p, SCOTT: N * p, IMPROVED: (L + 1) * p, SMONT: (L + 2) * p}[k]
+        lim = {2: 1 << 15, 4: 1 << 31, 8: 1 << 63} if sgn else {2: 1 << 16, 4: 1 << 32, 8: 1 << 64}
+        elems = [e for e in (2, 4, 8) if bound <= lim[e]]
+        if not elems:
+            continue
+        elem = int(rng.choice(elems))
+        B = int(rng.integers(1, 70))
+        off = int(rng.choice([0, 0, 1, 8]))  # 1: not 16-byte aligned -> fallback path
+        f = oracle.rng(int(rng.integers(1 << 30)), p, B * N).reshape(B, N)
+        dt = (SDT if sgn else DT)[elem]
+        tdt = TDT[elem]
+        buf = torch.zeros(B * N + off, dtype=tdt, device="cuda")
+        x = buf[off:].view(B, N)
+        x.copy_(torch.from_numpy(np.ascontiguousarray(f.astype(dt)).view(SDT[elem])).cuda())
+        y = nttk.forward(P, k, x)
+        want = Q.forward(k, f)
+        assert (from_dev(y, sgn).astype(np.int64) == want.astype(np.int64)).all(), (p, N, n, tree, k, elem, B, off)
+        assert (from_dev(nttk.inverse(P, k, y)) == f).all(), (p, N, n, tree, k, elem, B, off)
+        cases += 1
