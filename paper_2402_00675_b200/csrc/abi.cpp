@@ -81,7 +81,14 @@ void spectrum_range(const HostParams& P, int kind, int64_t& lo, uint64_t& hi) {
   switch (kind) {
     case NTTK_NTL: hi = P.p; break;
     case NTTK_HARVEY: hi = 2ull * P.p; break;
-    case NTTK_SCOTT: hi = uint64_t(P.N) * P.p; break;
+    case NTTK_SCOTT:
+      // N p when no T = X + (N/L) p - Y underflows (offset >= 2^{layers-1} p); otherwise the
+      // reference's uint64 words wrap (e.g. Kyber at n = 16) and only
+      // 64-bit storage holds them
+      hi = P.scott_L && uint64_t(P.N / P.scott_L) * P.p >= (uint64_t(P.p) << (P.layers - 1))
+               ? uint64_t(P.N) * P.p
+               : ~uint64_t(0);
+      break;
     case NTTK_IMPROVED: hi = uint64_t(P.layers + 1) * P.p; break;
     default:  // smont: X + t / X - t growth from [0, p)
       hi = uint64_t(P.layers + 1) * P.p;
@@ -277,8 +284,8 @@ int host_pipeline(const HostParams& P, int elem, size_t batch, const std::vector
       e = cudaMemcpyAsync(W->buf[s][i], static_cast<const char*>(h_in[i]) + done * poly_bytes,
                           n * poly_bytes, cudaMemcpyHostToDevice, st);
       if (e != cudaSuccess) return cuda_fail(e, who);
-      if (check_input_bound && i == 0) {
-        e = nttk_b200::check_canonical(W->buf[s][0], n * P.N, elem, bound, W->d_flag, st);
+      if (check_input_bound) {  // every input (both polymul operands, transform.hpp:372-379)
+        e = nttk_b200::check_canonical(W->buf[s][i], n * P.N, elem, bound, W->d_flag, st);
         ++g_launches;
         if (e != cudaSuccess) return cuda_fail(e, who);
       }
@@ -432,30 +439,73 @@ int nttk_basemul(nttk_params_t h, int kind, const void* d_l, const void* d_r, vo
   return run_product(h->P, kind, d_l, d_r, d_out, batch, elem, static_cast<cudaStream_t>(stream));
 }
 
+}  // extern "C"
+
+namespace {
+// forward(a), forward(b), product, inverse: the fused kernel when eligible, else four
+// passes at the storage width, else -- when only canonical words fit the width (e.g. the
+// improved spectrum of q = 12289 in 16 bits) -- the same passes on u64 copies
+int run_polymul(const HostParams& P, int kind, const void* a, const void* b, void* out,
+                size_t batch, int elem, cudaStream_t st) {
+  if (use_fused_polymul(P, kind, elem, a, b, out)) {
+    cudaError_t e = nttk_b200::polymul256_launch(P, kind, a, b, out, batch, elem, st);
+    ++g_launches;
+    return e == cudaSuccess ? int(NTTK_OK) : cuda_fail(e, "polymul");
+  }
+  const std::string keep = g_err;
+  const bool narrow_ok = check_storage(P, kind, elem, "polymul") == NTTK_OK;
+  g_err = keep;  // a failed width probe is not an error of this call
+  const int w = narrow_ok ? elem : 8;
+  const size_t n = batch * P.N;
+  char* tmp = nullptr;
+  cudaError_t e = cudaMallocAsync(&tmp, n * size_t(w) * (narrow_ok ? 1 : 3), st);
+  if (e != cudaSuccess) return cuda_fail(e, "polymul");
+  const void* A = a;
+  const void* Bv = b;
+  void* O = out;
+  void* T = tmp;
+  if (!narrow_ok) {  // u64 copies: a -> O (in place), b -> B64, temp
+    uint64_t* o64 = reinterpret_cast<uint64_t*>(tmp);
+    uint64_t* b64 = o64 + n;
+    e = nttk_b200::widen_to_u64(a, elem, o64, n, st);
+    if (e == cudaSuccess) e = nttk_b200::widen_to_u64(b, elem, b64, n, st);
+    g_launches += 2;
+    if (e != cudaSuccess) {
+      cudaFreeAsync(tmp, st);
+      return cuda_fail(e, "polymul");
+    }
+    A = o64;
+    Bv = b64;
+    O = o64;
+    T = b64 + n;
+  }
+  int rc = run_transform(P, kind, 0, Bv, T, batch, w, st);
+  if (!rc) rc = run_transform(P, kind, 0, A, O, batch, w, st);
+  if (!rc) rc = run_product(P, kind, O, T, O, batch, w, st);
+  if (!rc) rc = run_transform(P, kind, 1, O, O, batch, w, st);
+  if (!rc && !narrow_ok) {
+    e = nttk_b200::narrow_from_u64(reinterpret_cast<const uint64_t*>(O), out, elem, n, st);
+    ++g_launches;
+    if (e != cudaSuccess) rc = cuda_fail(e, "polymul");
+  }
+  cudaFreeAsync(tmp, st);
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
 int nttk_polymul(nttk_params_t h, int kind, const void* d_a, const void* d_b, void* d_out,
                  size_t batch, int elem, void* stream) {
   if (!h) return fail(NTTK_CONTRACT, "polymul: null params");
   const HostParams& P = h->P;
   if (int s = check_kind(P, kind, "polymul")) return s;
-  if (int s = check_storage(P, kind, elem, "polymul")) return s;
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, "polymul: elem_bytes must be 2, 4 or 8");
+  if (int s = check_canonical_storage(P, elem, "polymul")) return s;
   if (int s = need_device("polymul")) return s;
   if (!batch) return NTTK_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (use_fused_polymul(P, kind, elem, d_a, d_b, d_out)) {
-    cudaError_t e = nttk_b200::polymul256_launch(P, kind, d_a, d_b, d_out, batch, elem, st);
-    ++g_launches;
-    return e == cudaSuccess ? NTTK_OK : cuda_fail(e, "polymul");
-  }
-  void* tmp = nullptr;
-  const size_t bytes = batch * P.N * size_t(elem);
-  cudaError_t e = cudaMallocAsync(&tmp, bytes, st);
-  if (e != cudaSuccess) return cuda_fail(e, "polymul");
-  int rc = run_transform(P, kind, 0, d_b, tmp, batch, elem, st);
-  if (!rc) rc = run_transform(P, kind, 0, d_a, d_out, batch, elem, st);
-  if (!rc) rc = run_product(P, kind, d_out, tmp, d_out, batch, elem, st);
-  if (!rc) rc = run_transform(P, kind, 1, d_out, d_out, batch, elem, st);
-  cudaFreeAsync(tmp, st);
-  return rc;
+  return run_polymul(P, kind, d_a, d_b, d_out, batch, elem, static_cast<cudaStream_t>(stream));
 }
 
 // ---- host entry points ----------------------------------------------------------
@@ -528,20 +578,13 @@ int nttk_polymul_host(nttk_params_t h, int kind, const void* h_a, const void* h_
   if (!h) return fail(NTTK_CONTRACT, "polymul: null params");
   const HostParams& P = h->P;
   if (int s = check_kind(P, kind, "polymul")) return s;
-  if (int s = check_storage(P, kind, elem, "polymul")) return s;
+  if (elem != 2 && elem != 4 && elem != 8)
+    return fail(NTTK_CONTRACT, "polymul: elem_bytes must be 2, 4 or 8");
+  if (int s = check_canonical_storage(P, elem, "polymul")) return s;
   const int rc = host_pipeline(
       P, elem, batch, {h_a, h_b}, {{h_out, 2}},
       [&](cudaStream_t st, void** b, size_t n) {
-        if (use_fused_polymul(P, kind, elem, b[0], b[1], b[2])) {
-          cudaError_t e = nttk_b200::polymul256_launch(P, kind, b[0], b[1], b[2], n, elem, st);
-          ++g_launches;
-          return e == cudaSuccess ? int(NTTK_OK) : cuda_fail(e, "polymul");
-        }
-        int r = run_transform(P, kind, 0, b[0], b[0], n, elem, st);
-        if (!r) r = run_transform(P, kind, 0, b[1], b[1], n, elem, st);
-        if (!r) r = run_product(P, kind, b[0], b[1], b[2], n, elem, st);
-        if (!r) r = run_transform(P, kind, 1, b[2], b[2], n, elem, st);
-        return r;
+        return run_polymul(P, kind, b[0], b[1], b[2], n, elem, st);
       },
       "polymul", true, P.p);
   if (rc == NTTK_PROPERTY) return fail(NTTK_CONTRACT, "ntt_forward: coefficients must be canonical");

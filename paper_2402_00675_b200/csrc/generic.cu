@@ -419,6 +419,45 @@ cudaError_t generic_transform(const HostParams& P, const DeviceTables& T, int ki
   }
 }
 
+namespace {
+// storage-width conversions for the wide product composition (canonical words only)
+template <class IO>
+__global__ void widen_kernel(const IO* __restrict__ src, uint64_t* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<uint64_t>(src[i]);
+}
+template <class IO>
+__global__ void narrow_kernel(const uint64_t* __restrict__ src, IO* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<IO>(src[i]);
+}
+
+}  // namespace
+
+cudaError_t widen_to_u64(const void* src, int elem, uint64_t* dst, size_t n, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  if (elem == 2)
+    widen_kernel<uint16_t><<<grid_for(n, 256), 256, 0, st>>>(static_cast<const uint16_t*>(src), dst, n);
+  else if (elem == 4)
+    widen_kernel<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(static_cast<const uint32_t*>(src), dst, n);
+  else
+    return cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, st);
+  return cudaGetLastError();
+}
+
+cudaError_t narrow_from_u64(const uint64_t* src, void* dst, int elem, size_t n, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  if (elem == 2)
+    narrow_kernel<uint16_t><<<grid_for(n, 256), 256, 0, st>>>(src, static_cast<uint16_t*>(dst), n);
+  else if (elem == 4)
+    narrow_kernel<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(src, static_cast<uint32_t*>(dst), n);
+  else
+    return cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, st);
+  return cudaGetLastError();
+}
+
 // ntt_forward_observed / intt_inverse_observed (transform.hpp:77-116, 207-337): one
 // polynomial, one launch per layer; after each layer the u64 state is read back and
 // observe(layer, state) runs on the host (layers numbered as the reference's

@@ -12,6 +12,9 @@ namespace nttk_b200 {
 cudaError_t generic_transform(const HostParams& P, const DeviceTables& T, int kind, int dir,
                               const void* in, void* out, size_t batch, int elem_bytes,
                               cudaStream_t st);
+// canonical words between a storage width (2/4/8 bytes) and u64 (wide product path)
+cudaError_t widen_to_u64(const void* src, int elem, uint64_t* dst, size_t n, cudaStream_t st);
+cudaError_t narrow_from_u64(const uint64_t* src, void* dst, int elem, size_t n, cudaStream_t st);
 // one polynomial, layer by layer, observe(layer) after each (state copied to h_state)
 cudaError_t generic_transform_observed(const HostParams& P, const DeviceTables& T, int kind,
                                        int dir, uint64_t* d_io, uint64_t* h_state,

@@ -523,3 +523,68 @@ def test_randomized_dispatch_sweep(oracle):
         assert (from_dev(y, sgn).astype(np.int64) == want.astype(np.int64)).all(), (p, N, n, tree, k, elem, B, off)
         assert (from_dev(nttk.inverse(P, k, y)) == f).all(), (p, N, n, tree, k, elem, B, off)
         cases += 1
+
+
+def test_randomized_products_and_host_calls(oracle):
+    """Seeded random cases for the product paths (fused polymul when aligned, the four-kernel
+    composition otherwise, pointwise / basemul) and the host entry points, vs the oracle."""
+    rng = np.random.default_rng(675)
+    done = 0
+    while done < 30:
+        N = int(rng.choice([256, 256, 512, 1024]))
+        p = {256: int(rng.choice([3329, 8380417])), 512: 12289, 1024: 12289}[N]
+        n = 16 if (p == 3329 and rng.random() < 0.6) else 32
+        tree = NEGA if (N == 256 and rng.random() < 0.5) else CYCLIC
+        layers = (7 if p == 3329 else 8) if tree == NEGA else 0
+        k = int(rng.choice([IMPROVED, HARVEY, SMONT] + ([NTL, SCOTT] if tree == CYCLIC else [])))
+        try:
+            P = engine_params(p, N, n, [k], tree=tree, layers=layers, exact=True)
+            Q = oracle.params(p, N, n, (k,), tree=tree, layers=layers, exact=True)
+        except Exception:
+            continue
+        B = int(rng.integers(1, 40))
+        a = oracle.rng(int(rng.integers(1 << 30)), p, B * N).reshape(B, N)
+        b = oracle.rng(int(rng.integers(1 << 30)), p, B * N).reshape(B, N)
+        elem = 2 if p < (1 << 16) and rng.random() < 0.5 else (4 if rng.random() < 0.7 else 8)
+        off = int(rng.choice([0, 0, 1]))
+        tdt = TDT[elem]
+
+        def dev(v):
+            buf = torch.zeros(B * N + off, dtype=tdt, device="cuda")
+            x = buf[off:].view(B, N)
+            x.copy_(torch.from_numpy(np.ascontiguousarray(v.astype(DT[elem])).view(SDT[elem])).cuda())
+            return x
+        got = from_dev(nttk.polymul(P, k, dev(a), dev(b)))
+        assert (got == Q.polymul(k, a, b)).all(), (p, N, n, tree, k, elem, B, off)
+        # host forward at a width that holds the kind's spectrum (narrower ones are refused)
+        L = N.bit_length() - 1 if not layers else layers
+        bound = {NTL: p, HARVEY: 2 * p, SCOTT: N * p, IMPROVED: (L + 1) * p, SMONT: (L + 2) * p}[k]
+        # (scott at n = 16 wraps in the reference: only 64-bit words hold it, and the engine
+        # refuses the narrower ones -- SURVEY §0 item 6)
+        host = None
+        for hel in (e for e in (2, 4, 8) if bound <= (1 << (8 * e - (1 if k == SMONT else 0)))):
+            try:
+                host = nttk.ntt_forward_batch(a.astype({2: np.uint16, 4: np.uint32, 8: np.uint64}[hel]), P, k)
+                break
+            except nttk.ContractViolation as e:
+                assert "cannot hold" in str(e) and k == SCOTT and n == 16, e
+        host = np.asarray(host).astype({2: np.int16, 4: np.int32, 8: np.int64}[hel]).astype(np.int64) \
+            if k == SMONT else np.asarray(host).astype(np.int64)
+        assert (host == Q.forward(k, a).astype(np.int64)).all(), (p, N, k, hel)
+        done += 1
+
+
+def test_scott_n16_refuses_narrow_storage(oracle):
+    """scott at Kyber n = 16 wraps uint64 in the reference; only 64-bit
+    storage holds those words, so the engine refuses 16/32-bit storage instead of
+    truncating -- and its 64-bit results (and polymul at any width) match the oracle."""
+    P = engine_params(KYBER, 256, 16, [SCOTT])
+    Q = oracle.params(KYBER, 256, 16, (SCOTT,))
+    f = oracle.rng(8, KYBER, 5 * 256).reshape(5, 256)
+    g = oracle.rng(9, KYBER, 5 * 256).reshape(5, 256)
+    for elem in (2, 4):
+        with pytest.raises(nttk.ContractViolation, match="cannot hold the scott spectrum bound"):
+            nttk.forward(P, SCOTT, to_dev(f, elem))
+        assert (from_dev(nttk.polymul(P, SCOTT, to_dev(f, elem), to_dev(g, elem))) ==
+                Q.polymul(SCOTT, f, g)).all(), elem
+    assert (from_dev(nttk.forward(P, SCOTT, to_dev(f, 8))) == Q.forward(SCOTT, f)).all()
