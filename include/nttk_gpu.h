@@ -115,7 +115,7 @@ int nttk_pointwise_multiply(nttk_params_t P, int kind, const void* d_lhs, const 
 int nttk_basemul(nttk_params_t P, int kind, const void* d_lhs, const void* d_rhs, void* d_out,
                  size_t batch, int elem_bytes, void* stream);
 /* cyclic_convolution_via_ntt (transform.hpp:372-379) and its negacyclic twin:
- * forward(a), forward(b), pointwise/basemul, inverse.  d_out may alias d_a. */
+ * forward(a), forward(b), pointwise/basemul, inverse.  d_out may alias d_a or d_b. */
 int nttk_polymul(nttk_params_t P, int kind, const void* d_a, const void* d_b, void* d_out,
                  size_t batch, int elem_bytes, void* stream);
 

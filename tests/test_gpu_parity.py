@@ -588,3 +588,34 @@ def test_scott_n16_refuses_narrow_storage(oracle):
         assert (from_dev(nttk.polymul(P, SCOTT, to_dev(f, elem), to_dev(g, elem))) ==
                 Q.polymul(SCOTT, f, g)).all(), elem
     assert (from_dev(nttk.forward(P, SCOTT, to_dev(f, 8))) == Q.forward(SCOTT, f)).all()
+
+
+def test_randomized_pointwise_basemul_and_aliasing(oracle):
+    """pointwise / basemul on real forward spectra (lazy words) at random sizes and widths,
+    and polymul with its output aliasing either operand."""
+    rng = np.random.default_rng(2024)
+    for case in range(16):
+        p, n = (KYBER, 16) if case % 2 else (DILITHIUM, 32)
+        tree = NEGA if case % 4 < 2 else CYCLIC
+        layers = (7 if p == KYBER else 8) if tree == NEGA else 0
+        k = int(rng.choice([IMPROVED, HARVEY, SMONT]))
+        P = engine_params(p, 256, n, [k], tree=tree, layers=layers, exact=True)
+        Q = oracle.params(p, 256, n, (k,), tree=tree, layers=layers, exact=True)
+        B = int(rng.integers(1, 50))
+        a = oracle.rng(100 + case, p, B * 256).reshape(B, 256)
+        b = oracle.rng(200 + case, p, B * 256).reshape(B, 256)
+        sgn = k == SMONT
+        elem = 4 if p == DILITHIUM else int(rng.choice([2, 4]))
+        fa, fb = nttk.forward(P, k, to_dev(a, elem)), nttk.forward(P, k, to_dev(b, elem))
+        Fa, Fb = Q.forward(k, a), Q.forward(k, b)
+        if tree == NEGA and layers == 7:
+            assert (from_dev(nttk.basemul(P, k, fa, fb)) == Q.basemul(k, Fa, Fb)).all(), case
+        else:
+            assert (from_dev(nttk.pointwise(P, k, fa, fb)) == Q.pointwise(k, Fa, Fb)).all(), case
+        want = Q.polymul(k, a, b)
+        xa, xb = to_dev(a, elem), to_dev(b, elem)
+        nttk.polymul(P, k, xa, xb, out=xb)  # out aliases b
+        assert (from_dev(xb) == want).all(), case
+        xa, xb = to_dev(a, elem), to_dev(b, elem)
+        nttk.polymul(P, k, xa, xb, out=xa)  # out aliases a
+        assert (from_dev(xa) == want).all(), case
