@@ -301,3 +301,41 @@ def test_canonicalize_on_device():
     v = np.array([0, 7680, 7681, 7682, 2**63 + 5, 2**64 - 1], dtype=np.uint64)
     got = nttk.canonicalize(v, 7681)
     assert got.tolist() == [int(x) % 7681 for x in v.tolist()]
+
+
+def test_randomized_reduction_contexts(oracle):
+    """Random (p, n, alpha, ell), valid or not: context validation accepts/refuses exactly as
+    the oracle does, and every admitted op agrees with it on random in-range operands."""
+    rng = np.random.default_rng(90)
+    for _ in range(60):
+        n = int(rng.integers(2, 33))
+        p = int(rng.integers(2, min(1 << n, 1 << 31) + 3))
+        alpha, ell = int(rng.integers(0, n + 1)), int(rng.integers(0, n + 1))
+        try:
+            o = oracle.ctx(p, n, alpha, ell)
+        except OracleError:
+            with pytest.raises(nttk.ContractViolation, match="reduction context"):
+                nttk.make_reduction_context(p, n, alpha, ell)
+            continue
+        c = nttk.make_reduction_context(p, n, alpha, ell)
+        m = 2000
+        ops = [("mont", lambda: (rng.integers(0, p * p, m, dtype=np.uint64),), nttk.mont_redc,
+                oracle.mont_redc, True)]
+        if c.fits_signed_montgomery_bound():
+            lim = p << (n - 1) >> 1
+            ops.append(("smont", lambda: (rng.integers(-lim + 1, lim, m, dtype=np.int64),),
+                        nttk.signed_mont_redc, oracle.signed_mont_redc, True))
+        if c.fits_plantard_bound():
+            ops.append(("plantard", lambda: (rng.integers(0, p + 1, m, dtype=np.uint64),
+                                             rng.integers(0, p + 1, m, dtype=np.uint64)),
+                        nttk.plantard_redc, oracle.plantard_redc, True))
+        if c.fits_lazy_plantard_bound():
+            ops.append(("mplantard", lambda: (rng.integers(0, p, m, dtype=np.uint64),
+                                              rng.integers(0, p << ell, m, dtype=np.uint64)),
+                        nttk.modified_plantard_mul, oracle.modified_plantard_mul, True))
+        for name, gen, fn, ref, _ in ops:
+            args = gen()
+            got = fn(*args, c)
+            for i in range(0, m, 97):
+                want = ref(*[int(a[i]) for a in args], o)
+                assert int(got[i]) == want, (name, p, n, alpha, ell)
