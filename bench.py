@@ -414,14 +414,22 @@ def run_extras(dev):
             else:
                 A = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
                 Bv = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
+            want = nttk.modmul_sweep(v, q, n, ell, A, Bv)  # synchronous form: the checksum
+            cs = torch.zeros(1, dtype=torch.int64, device=dev)
             for _ in range(3):  # warm-up (module load, occupancy query, clocks)
-                nttk.modmul_sweep(v, q, n, ell, A, Bv)
-            torch.cuda.synchronize()
+                nttk.modmul_sweep_device(v, q, n, ell, A, Bv, cs)
             reps = 20
-            t0 = time.perf_counter()
-            for _ in range(reps):
-                nttk.modmul_sweep(v, q, n, ell, A, Bv)  # synchronises (returns the checksum)
-            sec = (time.perf_counter() - t0) / reps
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            cs.zero_()
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):  # device form: queued back to back, one checksum word
+                nttk.modmul_sweep_device(v, q, n, ell, A, Bv, cs)
+            e1.record()
+            torch.cuda.synchronize()
+            sec = e0.elapsed_time(e1) / 1e3 / reps
+            if (int(cs.item()) & (2**64 - 1)) != (want * reps) & (2**64 - 1):
+                raise RuntimeError(f"config5 sweep checksum mismatch (variant {v}, q {q})")
             rate = (1 << 30) / sec
             roof = n_sm * 1965e6 / cost[(n, v)]
             c5[f"q{q}_{names[v]}"] = {"mults_per_s": rate, "imad_roof_mults_per_s": roof,

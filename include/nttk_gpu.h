@@ -152,6 +152,12 @@ enum nttk_redc {
 int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, const int64_t* d_A,
                       size_t na, const int64_t* d_B, size_t nb, int64_t* d_r,
                       uint64_t* h_checksum, void* stream);
+/* Device form of nttk_modmul_sweep: atomically ADDS the wrapping sum into the device
+ * word *d_checksum (the caller zeroes it) and returns without synchronising, so sweeps
+ * can be queued back to back or captured in a CUDA graph. */
+int nttk_modmul_sweep_device(int variant, uint64_t p, uint32_t n_bits, uint32_t ell,
+                             const int64_t* d_A, size_t na, const int64_t* d_B, size_t nb,
+                             int64_t* d_r, uint64_t* d_checksum, void* stream);
 /* ---- observed transforms (transform.hpp:207-217, 233-337) ------------------------ */
 /* One polynomial (u64 words), run one layer per launch; after every layer the state is
  * copied back and observer(layer, state, N, user) runs on the calling thread, with layers

@@ -593,9 +593,7 @@ int nttk_polymul_host(nttk_params_t h, int kind, const void* h_a, const void* h_
 
 // ---- reductions -------------------------------------------------------------------
 
-int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, const int64_t* d_A,
-                      size_t na, const int64_t* d_B, size_t nb, int64_t* d_r,
-                      uint64_t* h_checksum, void* stream) {
+static int sweep_check(int variant, uint64_t p, uint32_t n_bits, uint32_t ell) {
   if (variant < NTTK_REDC_MONT || variant > NTTK_REDC_MPLANTARD)
     return fail(NTTK_CONTRACT, "modmul_sweep: unknown reduction variant");
   if (n_bits < 2 || n_bits > 32)
@@ -603,7 +601,6 @@ int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, co
   if (p < 3 || !(p & 1)) return fail(NTTK_CONTRACT, "reduction context: p must be odd and >= 3");
   if (p >= (uint64_t(1) << n_bits)) return fail(NTTK_CONTRACT, "reduction context: p must be < 2^n");
   if (ell >= n_bits) return fail(NTTK_CONTRACT, "reduction context: ell must be < n");
-  const nttk_b200::Ctx c = nttk_b200::make_ctx(p, n_bits, ell);
   using nttk_b200::u128;
   // per-variant context bounds (reduction.hpp:64-77)
   if (variant == NTTK_REDC_SMONT && !(u128(2) * p < (u128(1) << n_bits)))
@@ -615,7 +612,28 @@ int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, co
   if (variant == NTTK_REDC_MPLANTARD &&
       !(ell + 2 < n_bits && u128(p) < (u128(1) << (n_bits - ell - 2))))
     return fail(NTTK_CONTRACT, "modified_plantard_mul: requires p < 2^{n-ell-2}");
-  if (int s = need_device("modmul_sweep")) return s;
+  return need_device("modmul_sweep");
+}
+
+int nttk_modmul_sweep_device(int variant, uint64_t p, uint32_t n_bits, uint32_t ell,
+                             const int64_t* d_A, size_t na, const int64_t* d_B, size_t nb,
+                             int64_t* d_r, uint64_t* d_checksum, void* stream) {
+  if (int s = sweep_check(variant, p, n_bits, ell)) return s;
+  if (!d_checksum) return fail(NTTK_CONTRACT, "modmul_sweep: null checksum accumulator");
+  const nttk_b200::Ctx c = nttk_b200::make_ctx(p, n_bits, ell);
+  cudaError_t e = nttk_b200::sweep_launch(variant, c, d_A, na, d_B, nb, d_r,
+                                          reinterpret_cast<unsigned long long*>(d_checksum),
+                                          static_cast<cudaStream_t>(stream));
+  ++g_launches;
+  if (e != cudaSuccess) return cuda_fail(e, "modmul_sweep");
+  return NTTK_OK;
+}
+
+int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, const int64_t* d_A,
+                      size_t na, const int64_t* d_B, size_t nb, int64_t* d_r,
+                      uint64_t* h_checksum, void* stream) {
+  if (int s = sweep_check(variant, p, n_bits, ell)) return s;
+  const nttk_b200::Ctx c = nttk_b200::make_ctx(p, n_bits, ell);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned long long* d_sum = nullptr;
   cudaError_t e = cudaMallocAsync(&d_sum, sizeof(unsigned long long), st);

@@ -4,22 +4,31 @@
 // pair (A[i], B[j]) of an operand grid: mont_redc(a b), signed_mont_redc(a b),
 // plantard_redc(a, b) and modified_plantard_mul(a, b).  Bit-exact with the reference
 // bodies; the operand that plays the twiddle role (a) is premultiplied per row, so the
-// per-pair cost is the reduction itself (2 IMAD for modified Plantard at n = 16).
-// Each thread keeps 8 columns in registers and walks a block of rows; results are
-// optionally stored (int64, row-major) and always folded into a wrapping u64 checksum.
+// per-pair cost is the reduction itself (IMAD + IMAD.HI for modified Plantard at n = 16).
+// A block stages up to 256 premultiplied rows at a time in shared memory (read back as broadcasts),
+// each thread keeps 16 columns in registers and walks the rows; results are optionally
+// stored (int64, row-major) and always folded into a wrapping u64 checksum.
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "arith.cuh"
+#include "launch_cache.hpp"
 #include "sweep.hpp"
 
 namespace nttk_b200 {
 namespace {
 
-constexpr int kCols = 8;       // columns per thread
-constexpr int kThreads = 256;  // threads per block -> 2048 columns per block
-constexpr int kRows = 64;      // rows per block
+#ifndef NTTK_SWEEP_COLS
+#define NTTK_SWEEP_COLS 16
+#endif
+#ifndef NTTK_SWEEP_ROWS
+#define NTTK_SWEEP_ROWS 256
+#endif
+constexpr int kCols = NTTK_SWEEP_COLS;   // columns per thread
+constexpr int kThreads = 256;            // threads per block -> 4096 columns per block
+constexpr int kRows = NTTK_SWEEP_ROWS;   // rows staged per chunk
+static_assert(kCols % 8 == 0 && kRows * kCols <= 16384, "sweep tile shape");
 
 struct SweepArgs {
   uint64_t p, beta_mask, r2n_mask, p_inv_beta, neg_p_inv_beta, mu;
@@ -43,41 +52,39 @@ struct Redc {
       r.am = static_cast<uint64_t>(a) * S.neg_p_inv_beta & S.beta_mask;  // a k mod 2^n
     return r;
   }
+  // The n = 16 / 32 bodies stay in 32-bit registers; each is exact against the
+  // reference's 64-bit statement (reduction.hpp lines cited per variant).
   __device__ static int64_t pair(const Row& R, int64_t b, const SweepArgs& S) {
     const uint32_t p = static_cast<uint32_t>(S.p);
+    const uint32_t b32 = static_cast<uint32_t>(b);
+    const uint32_t lo = static_cast<uint32_t>(R.am), hi = static_cast<uint32_t>(R.am >> 32);
     if (VAR == NTTK_REDC_MPLANTARD) {  // reduction.hpp:252-258
-      if (NB == 16) return mp_n16<false>(static_cast<uint32_t>(b), static_cast<uint32_t>(R.am), p);
-      if (NB == 32)
-        return mp_n32(static_cast<uint32_t>(b), static_cast<uint32_t>(R.am),
-                      static_cast<uint32_t>(R.am >> 32), p);
+      if (NB == 16) return mp_n16<false>(b32, lo, p);
+      // r = hi32((h_hi + 1) p); the output is canonical, so h_hi + 1 never wraps
+      if (NB == 32) return __umulhi(hi * b32 + __umulhi(lo, b32) + 1u, p);
       const uint64_t h = (R.am * static_cast<uint64_t>(b)) & S.r2n_mask;
       return static_cast<int64_t>((((h >> S.n_bits) + 1) * S.p) >> S.n_bits);
     }
     if (VAR == NTTK_REDC_PLANTARD) {  // reduction.hpp:178-191: paper form + r == p corner
-      uint32_t r;
-      if (NB == 16) {
-        r = mp_n16<true>(static_cast<uint32_t>(b), static_cast<uint32_t>(R.am), p);
-      } else if (NB == 32) {
-        r = mp_n32(static_cast<uint32_t>(b), static_cast<uint32_t>(R.am),
-                   static_cast<uint32_t>(R.am >> 32), p);
-        // mp_n32 wraps h_hi + 1 = 2^32 to 0; the reference then returns p -> 0 as well
-      } else {
-        const uint64_t h = (R.am * static_cast<uint64_t>(b)) & S.r2n_mask;
-        r = static_cast<uint32_t>((((h >> S.n_bits) + 1) * S.p) >> S.n_bits);
-      }
-      return r == p ? 0 : r;
+      // r == p exactly when h_hi = 2^n - 1; letting h_hi + 1 wrap to 0 in n bits returns
+      // the reference's corrected 0 with no compare
+      if (NB == 16) return (((b32 * lo + 0x10000u) >> 16) * p) >> 16;
+      if (NB == 32) return __umulhi(hi * b32 + __umulhi(lo, b32) + 1u, p);
+      const uint64_t h = (R.am * static_cast<uint64_t>(b)) & S.r2n_mask;
+      const uint64_t r = (((h >> S.n_bits) + 1) * S.p) >> S.n_bits;
+      return static_cast<int64_t>(r == S.p ? 0 : r);
     }
     if (VAR == NTTK_REDC_MONT) {  // reduction.hpp:125-135
       if (NB == 16) {
-        const uint32_t T = static_cast<uint32_t>(R.a) * static_cast<uint32_t>(b);
-        const uint32_t m = (static_cast<uint32_t>(R.am) * static_cast<uint32_t>(b)) & 0xffffu;
+        const uint32_t T = static_cast<uint32_t>(R.a) * b32;
+        const uint32_t m = (lo * b32) & 0xffffu;
         const uint32_t t = (T + m * p) >> 16;
         return umin32(t, t - p);
       }
-      if (NB == 32) {
-        const uint64_t T = R.a * static_cast<uint64_t>(b);
-        const uint32_t m = static_cast<uint32_t>(R.am) * static_cast<uint32_t>(b);
-        const uint32_t t = static_cast<uint32_t>((T + static_cast<uint64_t>(m) * p) >> 32);
+      if (NB == 32) {  // t = hi32(m p + T): one IMAD.WIDE with the 64-bit addend T
+        const uint64_t T = static_cast<uint64_t>(static_cast<uint32_t>(R.a)) * b32;
+        const uint32_t m = lo * b32;
+        const uint32_t t = static_cast<uint32_t>((static_cast<uint64_t>(m) * p + T) >> 32);
         return umin32(t, t - p);
       }
       const uint64_t T = R.a * static_cast<uint64_t>(b);
@@ -89,14 +96,13 @@ struct Redc {
     // signed Montgomery, reduction.hpp:141-165: r = (A - m p) / 2^n
     if (NB == 16) {
       const int32_t A = static_cast<int32_t>(R.a) * static_cast<int32_t>(b);
-      const int32_t m =
-          static_cast<int32_t>((static_cast<uint32_t>(R.am) << 16) * static_cast<uint32_t>(b)) >> 16;
+      const int32_t m = static_cast<int32_t>((lo << 16) * b32) >> 16;
       return (A - m * static_cast<int32_t>(p)) >> 16;
     }
-    if (NB == 32) {
-      const int64_t A = static_cast<int64_t>(R.a) * b;
-      const int32_t m = static_cast<int32_t>(static_cast<uint32_t>(R.am) * static_cast<uint32_t>(b));
-      return static_cast<int32_t>((A - static_cast<int64_t>(m) * p) >> 32);
+    if (NB == 32) {  // A and m p agree in their low words: r = hi(A) - hi(m p), signed
+      const int32_t m = static_cast<int32_t>(lo * b32);
+      return __mulhi(static_cast<int32_t>(R.a), static_cast<int32_t>(b32)) -
+             __mulhi(m, static_cast<int32_t>(p));
     }
     const int64_t A = static_cast<int64_t>(R.a) * b;
     const int64_t a1 = A >> S.n_bits;
@@ -108,37 +114,76 @@ struct Redc {
   }
 };
 
+// Every variant maps b = 0 to 0 (all four bodies are linear in b before the final
+// shift / reduction and the +1 Plantard offsets vanish under >> n for p < 2^n), so the
+// out-of-range columns are zero-padded instead of masked per pair.
 template <int VAR, int NB, bool STORE>
 __global__ void __launch_bounds__(kThreads)
     sweep_kernel(const int64_t* __restrict__ A, size_t na, const int64_t* __restrict__ B, size_t nb,
-                 int64_t* __restrict__ r, unsigned long long* __restrict__ sum, SweepArgs S) {
+                 int64_t* __restrict__ r, unsigned long long* __restrict__ sum, SweepArgs S,
+                 unsigned row_split) {
+  using Row = typename Redc<VAR, NB>::Row;
+  __shared__ Row rows[kRows];
+  // work split: gridDim.x = col_tiles * row_split when the column tiles do not fill the
+  // grid (each CTA owns one column tile and an even 1/row_split share of the rows, so the
+  // last wave is never partial); otherwise row_split = 1 and CTAs stride over column tiles
   const size_t col_tiles = (nb + kThreads * kCols - 1) / (kThreads * kCols);
-  const size_t row_tiles = (na + kRows - 1) / kRows;
+  const unsigned rs = blockIdx.x / static_cast<unsigned>(col_tiles < gridDim.x ? col_tiles : gridDim.x);
+  const size_t ra = na * rs / row_split, rb = na * (rs + 1) / row_split;
   unsigned long long acc = 0;
-  for (size_t t = blockIdx.x; t < col_tiles * row_tiles; t += gridDim.x) {
-    const size_t ct = t % col_tiles, rt = t / col_tiles;
+  for (size_t ct = blockIdx.x % col_tiles; ct < col_tiles; ct += row_split == 1 ? gridDim.x : col_tiles)
+   for (size_t r0 = ra; r0 < rb; r0 += kRows) {
     const size_t c0 = ct * kThreads * kCols + threadIdx.x;
+    const int nrows = static_cast<int>(r0 + kRows < rb ? kRows : rb - r0);
+    __syncthreads();  // previous chunk's rows consumed
+    for (int i = threadIdx.x; i < nrows; i += kThreads) rows[i] = Redc<VAR, NB>::row(A[r0 + i], S);
     int64_t b[kCols];
-    bool ok[kCols];
 #pragma unroll
     for (int k = 0; k < kCols; ++k) {
       const size_t c = c0 + size_t(k) * kThreads;
-      ok[k] = c < nb;
-      b[k] = ok[k] ? B[c] : 0;
+      b[k] = c < nb ? B[c] : 0;
     }
-    const size_t r0 = rt * kRows, r1 = r0 + kRows < na ? r0 + kRows : na;
-    for (size_t i = r0; i < r1; ++i) {
-      const auto R = Redc<VAR, NB>::row(A[i], S);
-      int32_t part = 0;  // |result| < p < 2^31 / kCols: no overflow inside one row
-      int64_t part64 = 0;
+    __syncthreads();
+    if (NB) {
+      // |result| < p < 2^27: 8 results fit an int32 partial, 16-bit words a whole chunk.
+      // Partials are summed as u32 bit patterns (two's complement) so ptxas sees plain
+      // 32-bit adds, then sign-extended.
+      uint32_t tile = 0;
+#pragma unroll 2
+      for (int i = 0; i < nrows; ++i) {
+        const Row R = rows[i];
+        uint32_t h[kCols / 8] = {};
 #pragma unroll
-      for (int k = 0; k < kCols; ++k) {
-        const int64_t v = Redc<VAR, NB>::pair(R, b[k], S);
-        if (NB) part += ok[k] ? static_cast<int32_t>(v) : 0;
-        else part64 += ok[k] ? v : 0;
-        if (STORE && ok[k]) r[i * nb + c0 + size_t(k) * kThreads] = v;
+        for (int k = 0; k < kCols; ++k) {
+          const uint32_t v = static_cast<uint32_t>(Redc<VAR, NB>::pair(R, b[k], S));
+          h[k / 8] += v;
+          if (STORE) {
+            const size_t c = c0 + size_t(k) * kThreads;
+            if (c < nb) r[(r0 + i) * nb + c] = static_cast<int32_t>(v);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kCols / 8; ++j) {
+          if (NB == 16) tile += h[j];
+          else acc += static_cast<unsigned long long>(static_cast<int64_t>(static_cast<int32_t>(h[j])));
+        }
       }
-      acc += static_cast<unsigned long long>(NB ? static_cast<int64_t>(part) : part64);
+      if (NB == 16) acc += static_cast<unsigned long long>(static_cast<int64_t>(static_cast<int32_t>(tile)));
+    } else {
+      for (int i = 0; i < nrows; ++i) {
+        const Row R = rows[i];
+        int64_t part = 0;
+#pragma unroll
+        for (int k = 0; k < kCols; ++k) {
+          const int64_t v = Redc<VAR, NB>::pair(R, b[k], S);
+          part += v;
+          if (STORE) {
+            const size_t c = c0 + size_t(k) * kThreads;
+            if (c < nb) r[(r0 + i) * nb + c] = v;
+          }
+        }
+        acc += static_cast<unsigned long long>(part);
+      }
     }
   }
   // warp reduce, one atomic per warp
@@ -150,21 +195,20 @@ __global__ void __launch_bounds__(kThreads)
 template <int VAR, int NB>
 cudaError_t launch_var(const int64_t* A, size_t na, const int64_t* B, size_t nb, int64_t* r,
                        unsigned long long* sum, const SweepArgs& S, cudaStream_t st) {
-  int dev = 0, sms = 148, occ = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t tiles = ((nb + kThreads * kCols - 1) / (kThreads * kCols)) * ((na + kRows - 1) / kRows);
-  if (r) {
-    auto k = sweep_kernel<VAR, NB, true>;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
-    const size_t g = tiles < size_t(sms) * occ ? tiles : size_t(sms) * occ;
-    k<<<static_cast<unsigned>(g ? g : 1), kThreads, 0, st>>>(A, na, B, nb, r, sum, S);
-  } else {
-    auto k = sweep_kernel<VAR, NB, false>;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
-    const size_t g = tiles < size_t(sms) * occ ? tiles : size_t(sms) * occ;
-    k<<<static_cast<unsigned>(g ? g : 1), kThreads, 0, st>>>(A, na, B, nb, r, sum, S);
+  static OccCache occ_store, occ_sum;
+  const int sms = sm_count_current();
+  auto k = r ? sweep_kernel<VAR, NB, true> : sweep_kernel<VAR, NB, false>;
+  const size_t cap = size_t(sms) * occupancy_current(k, kThreads, 0, r ? occ_store : occ_sum);
+  const size_t col_tiles = (nb + kThreads * kCols - 1) / (kThreads * kCols);
+  const size_t row_chunks = (na + kRows - 1) / kRows;
+  size_t row_split = 1, g = col_tiles < cap ? col_tiles : cap;
+  if (col_tiles < cap) {  // split the rows evenly across cap / col_tiles CTAs per column tile
+    row_split = cap / col_tiles;
+    if (row_split > row_chunks) row_split = row_chunks;
+    g = col_tiles * row_split;
   }
+  k<<<static_cast<unsigned>(g), kThreads, 0, st>>>(A, na, B, nb, r, sum, S,
+                                                    static_cast<unsigned>(row_split));
   return cudaGetLastError();
 }
 

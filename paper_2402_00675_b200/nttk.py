@@ -130,7 +130,7 @@ EXPORTS = (
     "nttk_params_table", "nttk_ntt_forward", "nttk_intt_inverse", "nttk_pointwise_multiply",
     "nttk_basemul", "nttk_polymul", "nttk_ntt_forward_host", "nttk_intt_inverse_host",
     "nttk_roundtrip_host", "nttk_pointwise_multiply_host", "nttk_polymul_host",
-    "nttk_modmul_sweep", "nttk_make_reduction_context", "nttk_reduce", "nttk_reduce_host",
+    "nttk_modmul_sweep", "nttk_modmul_sweep_device", "nttk_make_reduction_context", "nttk_reduce", "nttk_reduce_host",
     "nttk_butterfly", "nttk_butterfly_host", "nttk_ntt_forward_observed",
     "nttk_intt_inverse_observed",
     "nttk_last_error", "nttk_launch_count", "nttk_device_available", "nttk_version",
@@ -166,6 +166,8 @@ def lib() -> C.CDLL:
             getattr(L, f).argtypes = [vp, C.c_int, vp, vp, vp, sz, C.c_int]
         L.nttk_modmul_sweep.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, vp, sz, vp,
                                         sz, vp, C.POINTER(C.c_uint64), vp]
+        L.nttk_modmul_sweep_device.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, vp,
+                                               sz, vp, sz, vp, vp, vp]
         L.nttk_make_reduction_context.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                                   C.POINTER(ReductionContext)]
         L.nttk_reduce.argtypes = [C.c_int, C.POINTER(ReductionContext), vp, vp, vp, sz, vp]
@@ -511,6 +513,19 @@ def modmul_sweep(variant, p: int, n_bits: int, ell: int, A, B, r=None, stream=No
                                    B.data_ptr(), B.numel(), r.data_ptr() if r is not None else None,
                                    C.byref(s), _stream_ptr(stream)))
     return int(s.value)
+
+
+def modmul_sweep_device(variant, p: int, n_bits: int, ell: int, A, B, checksum, r=None,
+                        stream=None) -> None:
+    """Device form of :func:`modmul_sweep`: adds the wrapping sum into ``checksum`` (a
+    one-element int64 CUDA tensor the caller zeroes) without synchronising."""
+    import torch
+    if checksum.dtype != torch.int64 or checksum.numel() < 1 or not checksum.is_cuda:
+        raise ContractViolation("modmul_sweep: checksum must be a CUDA int64 tensor")
+    _check(lib().nttk_modmul_sweep_device(int(variant), p, n_bits, ell, A.data_ptr(), A.numel(),
+                                          B.data_ptr(), B.numel(),
+                                          r.data_ptr() if r is not None else None,
+                                          checksum.data_ptr(), _stream_ptr(stream)))
 
 
 # ---------------------------------------------------------------------------

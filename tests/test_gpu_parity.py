@@ -421,6 +421,30 @@ def test_sweep_vs_oracle_grid(oracle):
             assert nttk.modmul_sweep(variant, p, n, ell, dA, dB) == s
 
 
+@pytest.mark.gpu
+def test_sweep_device_form_ragged(oracle):
+    """nttk_modmul_sweep_device: queued, accumulating; ragged rows/columns around the
+    64-row x 4096-column tile, every word-size path (n = 16, 32 and the any-n form)."""
+    rng = np.random.default_rng(11)
+    for p, n, ell in ((KYBER, 16, 2), (DILITHIUM, 32, 7), (12289, 24, 3), (257, 12, 1)):
+        ctx = oracle.ctx(p, n, 0, ell)
+        for variant in range(4):
+            if variant == 2 and not 5 * p * p < ((1 << (n + 1)) - p) ** 2:
+                continue  # plantard_redc context bound
+            for na, nb in ((1, 1), (65, 4097), (130, 4095), (3, 8193)):
+                A = rng.integers(0, p, na)
+                B = rng.integers(0, p, nb)
+                want, s = oracle.sweep(variant, ctx, A, B)
+                dA = torch.tensor(A, dtype=torch.int64, device="cuda")
+                dB = torch.tensor(B, dtype=torch.int64, device="cuda")
+                cs = torch.zeros(1, dtype=torch.int64, device="cuda")
+                r = torch.empty(na * nb, dtype=torch.int64, device="cuda")
+                nttk.modmul_sweep_device(variant, p, n, ell, dA, dB, cs, r)
+                nttk.modmul_sweep_device(variant, p, n, ell, dA, dB, cs)
+                assert (int(cs.item()) & (2**64 - 1)) == (2 * s) & (2**64 - 1), (p, variant, na, nb)
+                assert (r.cpu().numpy() == want).all(), (p, variant, na, nb)
+
+
 def test_launch_counter_moves():
     before = nttk.launch_count()
     P = engine_params(KYBER, 256, 16, [IMPROVED], exact=True)
