@@ -394,7 +394,7 @@ def run_extras(dev):
     # config 5: reduction sweep, 2^30 operand pairs (2^15 x 2^15 grid) per (q, variant);
     # IMAD roof = SM-cycles per mult of the variant's multiplies (IMAD 1/64, IMAD.HI and
     # IMAD.WIDE 1/32 per lane-op, measured)
-    cost = {(16, 0): 3 / 64, (16, 1): 3 / 64, (16, 2): 2 / 64, (16, 3): 3 / 64,
+    cost = {(16, 0): 3 / 64, (16, 1): 3 / 64, (16, 2): 2 / 64, (16, 3): 2 / 64,
             (32, 0): 5 / 64, (32, 1): 5 / 64, (32, 2): 5 / 64, (32, 3): 5 / 64}
     names = ["mont_redc", "signed_mont_redc", "plantard_redc", "modified_plantard_mul"]
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count

@@ -59,7 +59,12 @@ struct Redc {
     const uint32_t b32 = static_cast<uint32_t>(b);
     const uint32_t lo = static_cast<uint32_t>(R.am), hi = static_cast<uint32_t>(R.am >> 32);
     if (VAR == NTTK_REDC_MPLANTARD) {  // reduction.hpp:252-258
-      if (NB == 16) return mp_n16<false>(b32, lo, p);
+      // r = ((h_hi + 1) p) >> 16 in the shift form with the +1 folded into the IMAD
+      // addend (h + 2^16; the output is canonical, so h_hi + 1 never wraps): 2 IMAD + 2 SHF.
+      // Alone in a sweep this beats the umulhi form (IMAD + IMAD.HI: the IMAD.HI holds the
+      // fma-heavy pipe for 4 cycles); inside a butterfly the add/sub already load the ALU
+      // pipe, which is why the NTT kernels keep the umulhi form (arith.cuh).
+      if (NB == 16) return (((b32 * lo + 0x10000u) >> 16) * p) >> 16;
       // r = hi32((h_hi + 1) p); the output is canonical, so h_hi + 1 never wraps
       if (NB == 32) return __umulhi(hi * b32 + __umulhi(lo, b32) + 1u, p);
       const uint64_t h = (R.am * static_cast<uint64_t>(b)) & S.r2n_mask;

@@ -66,6 +66,20 @@ def test_reductions_exhaustive_toy(oracle, p, n, ell, variant):
     assert gs == s and (got == want).all()
 
 
+@pytest.mark.parametrize("variant", [MONT, SMONT_R, PLANTARD, MPLANTARD])
+def test_reductions_exhaustive_kyber_n16(oracle, variant):
+    """Every operand pair of the variant's domain at Kyber's q = 3329, n = 16 (the
+    specialised 32-bit sweep bodies), in row blocks of <= 2^24 pairs."""
+    p, n, ell = 3329, 16, 2
+    (a0, a1), (b0, b1) = operand_ranges(variant, p, n, ell)
+    B = np.arange(b0, b1, dtype=np.int64)
+    rows = max(1, (1 << 24) // B.size)
+    for r0 in range(a0, a1, rows):
+        A = np.arange(r0, min(a1, r0 + rows), dtype=np.int64)
+        want, s, got, gs = run_sweep(oracle, variant, p, n, ell, A, B)
+        assert gs == s and (got == want).all(), (variant, r0)
+
+
 @pytest.mark.parametrize("p,n,ell", [(3329, 16, 2), (8380417, 32, 7)])
 @pytest.mark.parametrize("variant", [MONT, SMONT_R, PLANTARD, MPLANTARD])
 def test_reductions_random_production(oracle, p, n, ell, variant):

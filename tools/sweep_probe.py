@@ -8,7 +8,7 @@ import torch  # noqa: E402
 
 import paper_2402_00675_b200.nttk as nttk  # noqa: E402
 
-COST = {(16, 0): 3 / 64, (16, 1): 3 / 64, (16, 2): 2 / 64, (16, 3): 3 / 64,
+COST = {(16, 0): 3 / 64, (16, 1): 3 / 64, (16, 2): 2 / 64, (16, 3): 2 / 64,
         (32, 0): 5 / 64, (32, 1): 5 / 64, (32, 2): 5 / 64, (32, 3): 5 / 64}
 NAMES = ["mont_redc", "signed_mont_redc", "plantard_redc", "modified_plantard_mul"]
 
