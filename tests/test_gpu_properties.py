@@ -80,6 +80,34 @@ def test_reductions_exhaustive_kyber_n16(oracle, variant):
         assert gs == s and (got == want).all(), (variant, r0)
 
 
+def boundary_operands(lo, hi, p, ell, signed):
+    """SURVEY §8(d) config 5 boundary set: {0, 1, q-1, q, 2^k q - 1, 2^k q (k <= ell + 1),
+    range max - 1, range max - 2}, plus the negative mirrors for the signed operand;
+    clipped to [lo, hi)."""
+    v = {0, 1, p - 1, p, hi - 1, hi - 2}
+    for k in range(ell + 2):
+        v |= {(p << k) - 1, p << k}
+    if signed:
+        v |= {-x for x in list(v)} | {lo, lo + 1}
+    return np.array(sorted(x for x in v if lo <= x < hi), dtype=np.int64)
+
+
+@pytest.mark.parametrize("p,n,ell", [(3329, 16, 2), (8380417, 32, 7)])
+@pytest.mark.parametrize("variant", [MONT, SMONT_R, PLANTARD, MPLANTARD])
+def test_reductions_boundary_grid(oracle, p, n, ell, variant):
+    """Boundary x boundary, boundary x random and random x boundary grids (config 5's
+    boundary values) through the sweep kernel, bit-exact against the reference."""
+    rng = np.random.default_rng(777 + 7 * variant + n)
+    (a0, a1), (b0, b1) = operand_ranges(variant, p, n, ell)
+    Ab = boundary_operands(a0, a1, p, ell, False)
+    Bb = boundary_operands(b0, b1, p, ell, variant == SMONT_R)
+    Ar = rng.integers(a0, a1, 4099, dtype=np.int64)
+    Br = rng.integers(b0, b1, 4099, dtype=np.int64)
+    for A, B in ((Ab, Bb), (Ab, Br), (Ar, Bb)):
+        want, s, got, gs = run_sweep(oracle, variant, p, n, ell, A, B)
+        assert gs == s and (got == want).all(), (variant, A.size, B.size)
+
+
 @pytest.mark.parametrize("p,n,ell", [(3329, 16, 2), (8380417, 32, 7)])
 @pytest.mark.parametrize("variant", [MONT, SMONT_R, PLANTARD, MPLANTARD])
 def test_reductions_random_production(oracle, p, n, ell, variant):
