@@ -23,6 +23,7 @@
 #include "arith.cuh"
 #include "fast256.hpp"
 #include "launch_cache.hpp"
+#include "tensor_map.hpp"
 #include "tma_common.cuh"
 
 namespace nttk_b200 {
@@ -136,15 +137,19 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
 template <class K, class IO, int L, int MODE>
 __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     inv256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
-                      const __grid_constant__ FastArgs A) {
+                      const __grid_constant__ FastArgs A, const __grid_constant__ CUtensorMap tmap) {
   using G = Geo<IO>;
-  extern __shared__ __align__(128) uint8_t smem[];
+  using GS = GeoSwz<IO>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // SWIZZLE_128B destinations must be 1024-byte aligned (GS::kSmem carries the slack)
+  uint8_t* smem = inv_swz<IO>() ? smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u) : smem_raw;
+  constexpr int kStageBytes = inv_swz<IO>() ? GS::kStageBytes : G::kStageBytes;
   uint8_t* stages = smem;
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + G::kStages * G::kStageBytes);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + G::kStages * kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + kConsumers * kScratchWords);
   uint64_t* empty = full + G::kStages;
   using Tw = typename K::Tw;
-  Tw* tws = reinterpret_cast<Tw*>(smem + G::kSmem);  // lane twiddles (tws_on)
+  Tw* tws = reinterpret_cast<Tw*>(empty + G::kStages);  // lane twiddles (tws_on)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if constexpr (tws_on<IO, 1>()) {
     if (threadIdx.x < 16) {
@@ -156,13 +161,25 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
   }
   init_barriers(full, empty, G::kStages);  // __syncthreads: table visible
   if (warp == kConsumers) {
-    if (lane == 0) produce<IO>(in, batch, stages, full, empty);
+    if (lane == 0) {
+      if constexpr (inv_swz<IO>())
+        produce_rows<GS::kBoxRows, G::kStages>(&tmap, static_cast<uint32_t>((batch + kTile - 1) / kTile),
+                                               stages, full, empty);
+      else
+        produce<IO>(in, batch, stages, full, empty);
+    }
     return;
   }
   const int j = lane & 15, half = lane >> 4;
   uint32_t* S = scratch + warp * kScratchWords + half * 272;
   Xpose X;
   X.init(S, j);
+  // swizzled stage: polynomial half * 8 + warp of the tile, lane segment j (16 coefficients)
+  uint32_t soff[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    soff[c] = swz128(uint32_t((half * kConsumers + warp) * G::kPolyBytes + j * 16 * int(sizeof(IO)) + 16 * c));
+  const uint32_t sbase = smem_addr(stages);
   auto run = [&](const auto& twl) {
     const uint32_t ntiles = static_cast<uint32_t>((batch + kTile - 1) / kTile);
     const uint32_t nb = static_cast<uint32_t>(batch), pstep = gridDim.x * kTile;
@@ -172,8 +189,11 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       mbar_wait(&full[s], phase);
       uint32_t v[16];
-      load_contiguous<IO, K::kSigned>(
-          v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
+      if constexpr (inv_swz<IO>())
+        load_contiguous_swz<IO, K::kSigned>(v, sbase + s * kStageBytes, soff);
+      else
+        load_contiguous<IO, K::kSigned>(
+            v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
       release_stage(&empty[s], lane);
       constexpr int CM = MODE & 3;
       if (CM != 2) {
@@ -233,9 +253,16 @@ cudaError_t inv_launch_mode(const void* in, void* out, size_t batch, const FastA
                             cudaStream_t st) {
   static OccCache occ;
   auto kern = inv256_tma_kernel<K, IO, L, MODE>;
-  constexpr int smem = Geo<IO>::kSmem + (tws_on<IO, 1>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  constexpr int smem = (inv_swz<IO>() ? GeoSwz<IO>::kSmem : Geo<IO>::kSmem) +
+                       (tws_on<IO, 1>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  CUtensorMap map{};
+  if constexpr (inv_swz<IO>()) {
+    const cudaError_t e = make_rows128_map(&map, in, uint64_t(batch) * GeoSwz<IO>::kRowsPerPoly,
+                                           GeoSwz<IO>::kBoxRows);
+    if (e != cudaSuccess) return e;
+  }
   const int blocks = grid_for(kern, smem, occ, batch);
-  kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
+  kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A, map);
   return cudaGetLastError();
 }
 
@@ -288,11 +315,12 @@ bool fast256_tma_supports(int elem_bytes, const void* in, const void* out) {
 cudaError_t fast256_tma_launch_one(const HostParams& P, int kind, int dir, const void* in,
                                    void* out, size_t batch, int elem_bytes, cudaStream_t st);
 
-// the kernels count polynomials in 32 bits: split batches of 2^31 or more (more than any
-// B200 holds at N = 256, kept for safety)
+// the kernels count polynomials in 32 bits and the inverse addresses its input through a
+// tensor map of at most kMaxMapRows 128-byte rows (8 per u32 polynomial): launches of at
+// most 2^27 polynomials (more than any B200 holds at N = 256, kept for safety)
 cudaError_t fast256_tma_launch(const HostParams& P, int kind, int dir, const void* in, void* out,
                                size_t batch, int elem_bytes, cudaStream_t st) {
-  constexpr size_t kMax = size_t(1) << 30;
+  constexpr size_t kMax = size_t(1) << 27;
   const size_t bytes = size_t(256) * elem_bytes;
   for (size_t done = 0; done < batch;) {
     const size_t n = batch - done < kMax ? batch - done : kMax;

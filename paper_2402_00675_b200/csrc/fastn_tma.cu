@@ -21,6 +21,7 @@
 #include "arith.cuh"
 #include "fastn.hpp"
 #include "launch_cache.hpp"
+#include "tensor_map.hpp"
 #include "tma_common.cuh"
 
 namespace nttk_b200 {
@@ -46,6 +47,13 @@ struct GeoN {
   __device__ static constexpr int poly_offset(int w, int h) {
     return h * (kHalfBytes + kPad) + w * kPolyBytes;
   }
+  // inverse with 128B-swizzled tensor-map stages (tma_common.cuh inv_swz): one box of
+  // kTileN polynomials, 1024-byte aligned, no pad
+  static constexpr int kRowsPerPoly = kPolyBytes / 128;
+  static constexpr int kBoxRows = kTileN * kRowsPerPoly;  // <= 256
+  static constexpr int kSwzStageBytes = kBoxRows * 128;
+  static constexpr int kSwzSmem = 1024 + kStages * kSwzStageBytes + kConsumers * kScratchWords * 4 +
+                                  N * 8 + 2 * kStages * 8;
 };
 
 // Transpose tile of one polynomial: 32-word rows, 16-byte chunk c of row r stored at chunk
@@ -176,6 +184,34 @@ __device__ __forceinline__ void load_contiguous_n(uint32_t (&v)[32], const IO* p
       v[4 * c + 2] = a.z;
       v[4 * c + 3] = a.w;
     }
+  }
+}
+
+// contiguous read from a 128B-swizzled stage: chunk c of the lane's segment at stage + off[c]
+template <class IO, bool SGN>
+__device__ __forceinline__ void load_contiguous_n_swz(uint32_t (&v)[32], uint32_t stage,
+                                                      const uint32_t (&off)[8]) {
+  if constexpr (sizeof(IO) == 2) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t w[4];
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                   : "r"(stage + off[c])
+                   : "memory");
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[8 * c + 2 * e] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] & 0xffffu));
+        v[8 * c + 2 * e + 1] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] >> 16));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[4 * c]), "=r"(v[4 * c + 1]), "=r"(v[4 * c + 2]), "=r"(v[4 * c + 3])
+                   : "r"(stage + off[c])
+                   : "memory");
   }
 }
 
@@ -435,11 +471,15 @@ __global__ void __launch_bounds__(kThreads)
 template <class K, class IO, int LOGN, int MODE>
 __global__ void __launch_bounds__(kThreads)
     invn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
-                    const uint32_t* __restrict__ tab, const __grid_constant__ FastArgs A) {
+                    const uint32_t* __restrict__ tab, const __grid_constant__ FastArgs A,
+                    const __grid_constant__ CUtensorMap tmap) {
   using GN = GeoN<LOGN, IO>;
-  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr bool SWZ = inv_swz<IO>();
+  constexpr int kStageBytes = SWZ ? GN::kSwzStageBytes : GN::kStageBytes;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = SWZ ? smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u) : smem_raw;
   uint8_t* stages = smem;
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + GN::kStages * GN::kStageBytes);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + GN::kStages * kStageBytes);
   uint2* tws = reinterpret_cast<uint2*>(scratch + kConsumers * GN::kScratchWords);
   uint64_t* full = reinterpret_cast<uint64_t*>(tws + GN::N);
   uint64_t* empty = full + GN::kStages;
@@ -447,13 +487,24 @@ __global__ void __launch_bounds__(kThreads)
   init_barriers(full, empty, GN::kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kConsumers) {
-    if (lane == 0) produce_n<LOGN, IO>(in, batch, stages, full, empty);
+    if (lane == 0) {
+      if constexpr (SWZ)
+        produce_rows<GN::kBoxRows, GN::kStages>(
+            &tmap, static_cast<uint32_t>((batch + GN::kTileN - 1) / GN::kTileN), stages, full, empty);
+      else
+        produce_n<LOGN, IO>(in, batch, stages, full, empty);
+    }
     return;
   }
   constexpr int G = GN::G;
   const int j = lane & (G - 1), half = GN::PPW == 2 ? lane >> 4 : 0;
   XposeN<G> X;
   X.init(scratch + warp * GN::kScratchWords + half * GN::kRegionWords, j);
+  uint32_t soff[8];  // swizzled stage: polynomial half * 8 + warp, lane segment j
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    soff[c] = swz128(uint32_t((half * kConsumers + warp) * GN::kPolyBytes + j * 32 * int(sizeof(IO)) + 16 * c));
+  const uint32_t sbase = smem_addr(stages);
   const size_t ntiles = (batch + GN::kTileN - 1) / GN::kTileN;
   int it = 0;
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -461,8 +512,11 @@ __global__ void __launch_bounds__(kThreads)
     const size_t poly = t * GN::kTileN + half * kConsumers + warp;
     mbar_wait(&full[s], (it / GN::kStages) & 1);
     uint32_t v[32];
-    load_contiguous_n<IO, K::kSigned>(
-        v, reinterpret_cast<const IO*>(stages + s * GN::kStageBytes + GN::poly_offset(warp, half)), j);
+    if constexpr (SWZ)
+      load_contiguous_n_swz<IO, K::kSigned>(v, sbase + s * kStageBytes, soff);
+    else
+      load_contiguous_n<IO, K::kSigned>(
+          v, reinterpret_cast<const IO*>(stages + s * GN::kStageBytes + GN::poly_offset(warp, half)), j);
     release_stage(&empty[s], lane);
 #pragma unroll
     for (int k = 0; k < 32; ++k) v[k] = canon<IO, K::kSigned, (MODE & 3) == 1>(v[k], A);
@@ -496,10 +550,25 @@ cudaError_t inv_n_mode(const void* in, void* out, size_t batch, const uint32_t* 
   using GN = GeoN<LOGN, IO>;
   static OccCache occ;
   auto kern = invn_tma_kernel<K, IO, LOGN, MODE>;
-  const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN);
-  kern<<<blocks, kThreads, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,
-                                            tab, A);
-  return cudaGetLastError();
+  constexpr bool SWZ = inv_swz<IO>();
+  constexpr int smem = SWZ ? GN::kSwzSmem : GN::kSmem;
+  // the swizzled input is addressed through a tensor map of <= kMaxMapRows rows
+  constexpr size_t kMaxBatch = SWZ ? size_t(kMaxMapRows / GN::kRowsPerPoly) : ~size_t(0);
+  for (size_t done = 0; done < batch;) {
+    const size_t n = batch - done < kMaxBatch ? batch - done : kMaxBatch;
+    const IO* src = static_cast<const IO*>(in) + done * GN::N;
+    CUtensorMap map{};
+    if constexpr (SWZ) {
+      const cudaError_t e = make_rows128_map(&map, src, uint64_t(n) * GN::kRowsPerPoly, GN::kBoxRows);
+      if (e != cudaSuccess) return e;
+    }
+    const int blocks = grid_n(kern, smem, occ, (n + GN::kTileN - 1) / GN::kTileN);
+    kern<<<blocks, kThreads, smem, st>>>(src, static_cast<IO*>(out) + done * GN::N, n, tab, A, map);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    done += n;
+  }
+  return cudaSuccess;
 }
 
 template <class K, class IO, int LOGN, int LZ>

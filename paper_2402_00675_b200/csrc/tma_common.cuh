@@ -3,6 +3,7 @@
 // release, the swizzled transpose tile, and the producer loop.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -43,6 +44,27 @@ struct Geo {
   }
 };
 
+// Inverse kernels: the stage is one TMA tensor box of kTile polynomials (128-byte rows,
+// SWIZZLE_128B, tensor_map.hpp) instead of two padded linear bulk copies.  A/B switch.
+#ifndef NTTK_INV_SWZ
+#define NTTK_INV_SWZ 0x2  // bit 0: u16 stages, bit 1: u32 stages (measured: u32 -3.3 %, u16 +0.4 %)
+#endif
+template <class IO>
+constexpr bool inv_swz() {
+  return (NTTK_INV_SWZ >> (sizeof(IO) == 4 ? 1 : 0)) & 1;
+}
+
+template <class IO>
+struct GeoSwz {
+  static constexpr int kPolyBytes = 256 * int(sizeof(IO));
+  static constexpr int kRowsPerPoly = kPolyBytes / 128;
+  static constexpr int kBoxRows = kTile * kRowsPerPoly;  // 64 (u16) / 128 (u32) <= 256
+  static constexpr int kStageBytes = kBoxRows * 128;     // multiple of 1024
+  static constexpr int kUsed = Geo<IO>::kStages * kStageBytes + kConsumers * kScratchWords * 4 +
+                               2 * Geo<IO>::kStages * 8;
+  static constexpr int kSmem = kUsed + 1024;  // + alignment slack for the 1024-byte base
+};
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -76,6 +98,42 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(b))
       : "memory");
+}
+
+// 2-D tiled tensor copy global -> shared through a TMA tensor map (tensor_map.hpp): box
+// origin (x, y) in elements; the full box is written (rows past the tensor end are
+// zero-filled) and counted on the mbarrier.
+__device__ __forceinline__ void bulk_tensor_g2s(void* dst, const CUtensorMap* map, int x, int y,
+                                                uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(b))
+      : "memory");
+}
+
+// Byte offset of linear offset L inside a CU_TENSOR_MAP_SWIZZLE_128B destination (1024-byte
+// aligned): 16-byte chunk c of 128-byte row r sits at chunk c ^ (r & 7).
+__host__ __device__ constexpr uint32_t swz128(uint32_t L) {
+  return (L & ~127u) | ((((L >> 4) & 7u) ^ ((L >> 7) & 7u)) << 4);
+}
+
+// producer over 128-byte-row tensor boxes: tile t = rows [t BOX_ROWS, (t+1) BOX_ROWS)
+template <int BOX_ROWS, int STAGES>
+__device__ __forceinline__ void produce_rows(const CUtensorMap* map, uint32_t ntiles, uint8_t* stages,
+                                             uint64_t* full, uint64_t* empty) {
+  constexpr uint32_t kBytes = BOX_ROWS * 128;
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+  uint32_t s = 0, phase = 0, k = 0;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    if (k >= uint32_t(STAGES)) mbar_wait(&empty[s], phase ^ 1);
+    mbar_expect_tx(&full[s], kBytes);
+    bulk_tensor_g2s(stages + s * kBytes, map, 0, int(t * BOX_ROWS), &full[s]);
+    if (++s == uint32_t(STAGES)) {
+      s = 0;
+      phase ^= 1;
+    }
+  }
 }
 
 // shared -> global bulk store (bulk-group completion), its commit and the wait that makes
@@ -639,6 +697,35 @@ __device__ __forceinline__ void load_contiguous(uint32_t (&v)[16], const IO* pol
 }
 
 // barrier setup shared by every TMA kernel
+// contiguous read v[r] = a[16 j + r] from a 128B-swizzled stage: chunk c of the lane's
+// segment at stage + off[c] (off = swz128 of its linear offset, hoisted per lane)
+template <class IO, bool SGN>
+__device__ __forceinline__ void load_contiguous_swz(uint32_t (&v)[16], uint32_t stage,
+                                                    const uint32_t (&off)[4]) {
+  if constexpr (sizeof(IO) == 2) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t w[4];
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                   : "r"(stage + off[c])
+                   : "memory");
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[8 * c + 2 * e] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] & 0xffffu));
+        v[8 * c + 2 * e + 1] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] >> 16));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[4 * c]), "=r"(v[4 * c + 1]), "=r"(v[4 * c + 2]), "=r"(v[4 * c + 3])
+                   : "r"(stage + off[c])
+                   : "memory");
+  }
+}
+
 __device__ __forceinline__ void init_barriers(uint64_t* full, uint64_t* empty, int stages) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
