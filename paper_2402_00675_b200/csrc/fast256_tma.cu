@@ -133,7 +133,9 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
 // ---------------------------------------------------------------------------
 // MODE bits 0-1 -- 0: generic canonicalisation; 1: host-validated fast canonicalisation
 // (A.flags bits 0/1); 2: u16 input with the fused first merge layer (A.flags bit 2,
-// improved n=16).  MODE bit 2: lazy merge outputs (A.flags bit 3, improved n=16).
+// improved n=16).  MODE bit 2: lazy merge outputs (A.flags bit 3, improved).  Bit 3: TW1
+// multiply-free block-0 merges (A.flags bit 5); bit 4: DEFER, no input canonicalisation
+// (A.flags bit 6, u16 improved n=16) -- see inv_body_lazy.
 template <class K, class IO, int L, int MODE>
 __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     inv256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
       }
-      inv_body<K, L, CM == 2, (MODE & 4) != 0>(v, twl, A, X);
+      inv_body<K, L, CM == 2, (MODE & 4) != 0, (MODE & 8) != 0, (MODE & 16) != 0>(v, twl, A, X);
       store_strided<IO>(optr, j, v, S, X, poly < nb);
       poly += pstep;
       optr += ostep;
@@ -279,7 +281,17 @@ cudaError_t inv_launch_canon(const void* in, void* out, size_t batch, const Fast
 template <class K, class IO, int L>
 cudaError_t inv_launch(const void* in, void* out, size_t batch, const FastArgs& A, cudaStream_t st) {
   if constexpr (lazy_of<K>::value) {
-    if (A.flags & 8) return inv_launch_canon<K, IO, L, 4>(in, out, batch, A, st);
+    if (A.flags & 8) {
+      if constexpr (L == 8) {
+        // DEFER: u16 improved n = 16 with the fused first layer (flags 4 | 64)
+        constexpr bool kDefer = sizeof(IO) == 2 && std::is_same<K, ImprovedN16<false>>::value;
+        if (kDefer && (A.flags & 64) && (A.flags & 4))
+          return (A.flags & 32) ? inv_launch_mode<K, IO, L, kDefer ? (2 | 4 | 8 | 16) : 4>(in, out, batch, A, st)
+                                : inv_launch_mode<K, IO, L, kDefer ? (2 | 4 | 16) : 4>(in, out, batch, A, st);
+        if (A.flags & 32) return inv_launch_canon<K, IO, L, 4 | 8>(in, out, batch, A, st);
+      }
+      return inv_launch_canon<K, IO, L, 4>(in, out, batch, A, st);
+    }
   }
   return inv_launch_canon<K, IO, L, 0>(in, out, batch, A, st);
 }

@@ -195,6 +195,27 @@ void fill_fast(HostParams& P, int kind) {
     }
     // n = 32: lo32(h' p) < 2p for every fast-path operand (ImprovedN32 lazy merge)
     if (kind == NTTK_IMPROVED && !n16 && u128(4) * p < (u128(1) << 32)) A.flags |= 8;
+    // inverse TW1 (inv_body_lazy): block 0 of merge layers len = 16, 32, 64 has twiddle
+    // 1 (index 2^L - 2^s of the merge table, s = 4, 3, 2).  Every value of merge depth d
+    // stays below 2^d p, the bound the lazy / exact-bound checks already assume.
+    if (kind == NTTK_IMPROVED && dir == 1 && P.layers == 8 && P.N == 256 && (A.flags & 8) &&
+        P.gs_plain.size() >= 256 - 4 && P.gs_plain[256 - 16] == 1 && P.gs_plain[256 - 8] == 1 &&
+        P.gs_plain[256 - 4] == 1)
+      A.flags |= 32;
+    // inverse DEFER (u16 input, no canonicalisation): sum-chain products h K p + h (2^16 - 1)
+    // for h <= 8 inside Prop. 4's range, lazily consumed ones (h <= 4) pairwise below 2^32,
+    // and v0 < 16 (2^16 - 1) reducible by MP(1^, v0)
+    if (kind == NTTK_IMPROVED && n16 && dir == 1 && P.layers == 8 && P.N == 256 &&
+        (A.flags & 4) && (A.flags & 8)) {
+      const u128 t1 = (uint64_t(1) << 16) - 1 + A.kp, lim = u128(c.beta) * (c.beta - p);
+      const u128 tl = std::max<u128>(u128(p) << (P.layers - 1), 4 * t1);
+      if (u128(p - 1) * 8 * t1 < lim && 2 * u128(p - 1) * tl < (u128(1) << 32) &&
+          u128(p - 1) * 16 * ((uint64_t(1) << 16) - 1) < lim) {
+        for (int m = 0; m < 4; ++m) A.skp[m] = A.kp << m;
+        A.one_lo = static_cast<uint32_t>(to_plantard(1, c) * c.mu);
+        A.flags |= 64;
+      }
+    }
     // forward block 0 of layers 1..4 has twiddle 1 (cyclic tree): multiply-free
     // Plantard products (fwd_body W1)
     if (kind == NTTK_IMPROVED && dir == 0 && P.layers >= 4 && P.ct_plain.size() >= 8 &&

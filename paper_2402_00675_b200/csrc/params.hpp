@@ -61,9 +61,13 @@ struct FastArgs {
   uint32_t cb_m = 0, cb_s = 0;  // x mod p = x - ((x cb_m) >> cb_s) p, exact for x < 2^17
   uint32_t cs_s = 0;       // x mod p = min(r, r - p), r = x - (x >> cs_s) p, exact for x < 2^32
   uint32_t kp = 0;         // K p >= 2^16 - 1: fused first inverse layer offset (u16 input)
+  uint32_t skp[4] = {};    // kp << m: inverse sum-chain offsets without canonicalisation
+  uint32_t one_lo = 0;     // Plantard encoding of 1 times mu mod 2^32 (n = 16)
   uint32_t flags = 0;      // bit0: cb valid; bit1: cs valid; bit2: fused first layer valid;
                            // bit3: lazy merge valid (improved n = 16);
-                           // bit4: forward block-0 twiddles are 1 (cyclic, improved)
+                           // bit4: forward block-0 twiddles are 1 (cyclic, improved);
+                           // bit5: inverse phase-2 block-0 twiddles are 1 (TW1, L = 8);
+                           // bit6: u16 inverse without canonicalisation (DEFER)
   uint32_t fold_lo = 0, fold_hi = 0;  // last merge twiddle times N^{-1}, kind encoding
   uint32_t soff = 0;       // scott: butterfly offset (N/L) p (butterfly.hpp:172-184)
   uint32_t lo[256] = {};   // twiddle words in reference table order

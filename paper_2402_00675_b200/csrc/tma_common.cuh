@@ -433,11 +433,29 @@ struct w1_of<K, std::void_t<decltype(&K::fwd_w1)>> {
 // layer of half-span h the words at (r & h) hold pre-quotient h-values; the next layer
 // (span 2h) pairs them with each other, so "both inputs lazy" is the compile-time test
 // r & (h_prev).  Lazy words are materialised before the transpose.
-template <class K, int L, bool FUSE, class TWL>
+//
+// The inverse output is canonical (hence unique), so its intermediate words are free as
+// long as every value stays exact mod p inside the multiplies' valid ranges.  Two
+// host-validated options use that freedom:
+//   TW1   (A.flags bit 5, cyclic tree, L = 8): block 0 of merge layers len = 16, 32, 64
+//         has twiddle omega^0 = 1, so Y' = X + off - Y is kept unreduced instead of
+//         MP(1^, T) -- 7 of the 72 products per lane disappear.  Every value of merge
+//         depth d stays < 2^d p (T < X + off with off = 2^{d-1} p), the standard bound.
+//   DEFER (A.flags bit 6, u16 input, improved n = 16, L = 8): no input canonicalisation.
+//         Raw words (< 2^16) flow through phase 1; only the "sum chain" (the positions
+//         whose X input is a sum of 2^m raw words: r & (h - 1) == 0) needs the larger
+//         offset h K p (A.skp), and its single survivor v[0] (< 16 (2^16 - 1)) is reduced
+//         with one Plantard product by 1^ before the transpose.  Replaces 8 Barrett
+//         reductions per lane by one product.
+// Phase 2 tracks which words are lazy at compile time (lz[], constant-folded by the full
+// unroll): TW1 outputs are materialised, and a pair with one lazy word materialises it.
+template <class K, int L, bool FUSE, bool TW1 = false, bool DEFER = false, class TWL>
 __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                               const Xpose& X) {
   using Tw = typename K::Tw;
   constexpr int TL = 1 << L;
+  static_assert(!DEFER || (FUSE && L == 8), "DEFER needs the fused u16 first layer at L = 8");
+  static_assert(!TW1 || L == 8, "TW1 needs the full 8-layer tree");
 #pragma unroll
   for (int sl = 8; sl >= 5; --sl) {  // phase 1: merge layers s = L..5
     if (sl > L) continue;
@@ -450,7 +468,10 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl,
       const Tw w = twl[base + (r >> (9 - sl))];
       if (sl == L) {  // first merge layer: materialised (raw u16 if FUSE) inputs
         const uint32_t x = v[r], y = v[r + h];
-        if constexpr (FUSE) {
+        if constexpr (DEFER) {
+          v[r] = x + y + A.zero;
+          v[r + h] = (x + A.kp - y) * w;
+        } else if constexpr (FUSE) {
           v[r] = mod_cb(x + y + A.zero, A);
           v[r + h] = (x + A.kp - y) * w;
         } else {
@@ -458,6 +479,8 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl,
         }
       } else if (r & (h >> 1)) {
         K::inv_hh(v[r], v[r + h], w, off, A);
+      } else if (DEFER && (r & (h - 1)) == 0) {  // sum chain: inputs < h (2^16 - 1)
+        K::inv_h(v[r], v[r + h], w, A.skp[sl == 7 ? 1 : sl == 6 ? 2 : 3], A);
       } else {
         K::inv_h(v[r], v[r + h], w, off, A);
       }
@@ -466,12 +489,16 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl,
 #pragma unroll
   for (int r = 0; r < 16; ++r)
     if (r & 8) v[r] = K::materialize(v[r], A);
+  if constexpr (DEFER) v[0] = __umulhi(v[0] * A.one_lo, A.p);  // MP(1^, v0): canonical
   __syncwarp();
 #pragma unroll
   for (int c = 0; c < 4; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = X.get(r);
+  bool lz[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) lz[r] = false;
 #pragma unroll
   for (int sl = 4; sl >= 1; --sl) {  // phase 2: merge layers s = 4..1, materialised start
     const int h = 1 << (4 - sl);
@@ -479,14 +506,34 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl,
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
-      const bool lazy = sl < 4 && (r & (h >> 1));
+      bool lx = lz[r], ly = lz[r + h];
+      if (lx != ly) {  // mixed pair (after a TW1 block): materialise the lazy word
+        if (lx) v[r] = K::materialize(v[r], A);
+        else v[r + h] = K::materialize(v[r + h], A);
+        lx = ly = false;
+      }
       if (sl == 1) {  // N^{-1} folded into the last merge layer
-        if (lazy) K::inv_last_hh(v[r], v[r + h], off, A);
+        if (lx) K::inv_last_hh(v[r], v[r + h], off, A);
         else K::inv_last(v[r], v[r + h], off, A);
+        lz[r] = lz[r + h] = false;
+      } else if (TW1 && (r >> (5 - sl)) == 0) {  // twiddle 1: Y' = T unreduced
+        uint32_t x = v[r], y = v[r + h];
+        if (lx) {
+          uint32_t Xm;
+          const uint32_t S = K::sum_hh(x, y, Xm, A);
+          v[r] = S;
+          v[r + h] = Xm + Xm + off - S + A.zero;
+        } else {
+          v[r] = x + y + A.zero;
+          v[r + h] = x + off - y;
+        }
+        lz[r] = lz[r + h] = false;
       } else {
         const Tw w = K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl)));
-        if (lazy) K::inv_hh(v[r], v[r + h], w, off, A);
+        if (lx) K::inv_hh(v[r], v[r + h], w, off, A);
         else K::inv_h(v[r], v[r + h], w, off, A);
+        lz[r] = false;
+        lz[r + h] = true;
       }
     }
   }
@@ -546,13 +593,14 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl
   }
 }
 
-// LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3).
-template <class K, int L, bool FUSE, bool LAZY = false, class TWL>
+// LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3); TW1 / DEFER: see there.
+template <class K, int L, bool FUSE, bool LAZY = false, bool TW1 = false, bool DEFER = false,
+          class TWL>
 __device__ __forceinline__ void inv_body(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                          const Xpose& X) {
   if constexpr (LAZY) {
     static_assert(lazy_of<K>::value, "policy has no lazy merge");
-    inv_body_lazy<K, L, FUSE>(v, twl, A, X);
+    inv_body_lazy<K, L, FUSE, TW1, DEFER>(v, twl, A, X);
   } else {
     inv_body_eager<K, L, FUSE>(v, twl, A, X);
   }

@@ -643,3 +643,42 @@ def test_randomized_pointwise_basemul_and_aliasing(oracle):
         xa, xb = to_dev(a, elem), to_dev(b, elem)
         nttk.polymul(P, k, xa, xb, out=xa)  # out aliases a
         assert (from_dev(xa) == want).all(), case
+
+
+def _extreme_words(p, bits, B, seed):
+    """Inverse inputs that drive the merge bounds: all-max words, max/zero patterns that
+    maximise T = X + off - Y, and random draws from boundary values (words need not be
+    canonical: the inverse canonicalises, transform.hpp:243)."""
+    top = (1 << bits) - 1
+    rs = np.random.RandomState(seed)
+    pts = np.array([0, 1, p - 1, p, 2 * p - 1, 9 * p - 1, top - p, top - 1, top], dtype=np.uint64)
+    pts = pts[pts <= top]
+    w = pts[rs.randint(0, len(pts), size=(B, 256))]
+    w[0] = top
+    w[1] = 0
+    w[2, ::2], w[2, 1::2] = top, 0
+    w[3, :128], w[3, 128:] = top, 0
+    idx = np.arange(256)
+    for k in range(4):  # X max / Y zero at every merge span 2^k .. 2^(k+4)
+        w[4 + k] = np.where((idx >> k) & 1, 0, top)
+        w[8 + k] = np.where((idx >> (k + 4)) & 1, 0, top)
+    return w
+
+
+@pytest.mark.parametrize("p,n,elem,tree,layers", [(KYBER, 16, 2, CYCLIC, 8),
+                                                   (KYBER, 16, 2, NEGA, 7), (DILITHIUM, 32, 4, CYCLIC, 8),
+                                                   (DILITHIUM, 32, 4, NEGA, 8), (7681, 32, 4, CYCLIC, 8),
+                                                   (12289, 32, 4, CYCLIC, 8)])
+def test_inverse_extreme_words(oracle, p, n, elem, tree, layers):
+    """Worst-case words through the fast inverse (TW1 multiply-free block-0 merges and the
+    u16 DEFER path without input canonicalisation) vs the oracle, bit-exact."""
+    P = engine_params(p, 256, n, [IMPROVED], tree=tree, layers=layers, exact=True)
+    Q = oracle.params(p, 256, n, (IMPROVED,), tree=tree, layers=layers, exact=True)
+    assert IMPROVED in P.fast_path
+    w = _extreme_words(p, 8 * elem, 515, 7 + p + layers)
+    got = from_dev(nttk.inverse(P, IMPROVED, to_dev(w, elem)))
+    assert (got == Q.inverse(IMPROVED, w)).all()
+    # and the round trip of their forward images
+    f = np.asarray(Q.inverse(IMPROVED, w))
+    y = nttk.forward(P, IMPROVED, to_dev(f, elem))
+    assert (from_dev(nttk.inverse(P, IMPROVED, y)) == f).all()
