@@ -36,7 +36,7 @@ template <class K, class IO, int L, bool PER_INDEX, bool W1>
 __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
-  using G = Geo<IO>;
+  using G = Geo<IO, 0>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + G::kStages * G::kStageBytes);
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
   }
   init_barriers(full, empty, G::kStages);  // __syncthreads: table visible
   if (warp == kConsumers) {
-    if (lane == 0) produce<IO>(in, batch, stages, full, empty);
+    if (lane == 0) produce<IO, 0>(in, batch, stages, full, empty);
     return;
   }
   const int j = lane & 15, half = lane >> 4;
@@ -140,8 +140,8 @@ template <class K, class IO, int L, int MODE>
 __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
     inv256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A, const __grid_constant__ CUtensorMap tmap) {
-  using G = Geo<IO>;
-  using GS = GeoSwz<IO>;
+  using G = Geo<IO, 1>;
+  using GS = GeoSwz<IO, 1>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // SWIZZLE_128B destinations must be 1024-byte aligned (GS::kSmem carries the slack)
   uint8_t* smem = inv_swz<IO>() ? smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u) : smem_raw;
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
         produce_rows<GS::kBoxRows, G::kStages>(&tmap, static_cast<uint32_t>((batch + kTile - 1) / kTile),
                                                stages, full, empty);
       else
-        produce<IO>(in, batch, stages, full, empty);
+        produce<IO, 1>(in, batch, stages, full, empty);
     }
     return;
   }
@@ -236,7 +236,7 @@ cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs
                          cudaStream_t st) {
   static OccCache occ;
   auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1>;
-  constexpr int smem = Geo<IO>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  constexpr int smem = Geo<IO, 0>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
   const int blocks = grid_for(kern, smem, occ, batch);
   kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
   return cudaGetLastError();
@@ -255,12 +255,12 @@ cudaError_t inv_launch_mode(const void* in, void* out, size_t batch, const FastA
                             cudaStream_t st) {
   static OccCache occ;
   auto kern = inv256_tma_kernel<K, IO, L, MODE>;
-  constexpr int smem = (inv_swz<IO>() ? GeoSwz<IO>::kSmem : Geo<IO>::kSmem) +
+  constexpr int smem = (inv_swz<IO>() ? GeoSwz<IO, 1>::kSmem : Geo<IO, 1>::kSmem) +
                        (tws_on<IO, 1>() ? 240 * int(sizeof(typename K::Tw)) : 0);
   CUtensorMap map{};
   if constexpr (inv_swz<IO>()) {
-    const cudaError_t e = make_rows128_map(&map, in, uint64_t(batch) * GeoSwz<IO>::kRowsPerPoly,
-                                           GeoSwz<IO>::kBoxRows);
+    const cudaError_t e = make_rows128_map(&map, in, uint64_t(batch) * GeoSwz<IO, 1>::kRowsPerPoly,
+                                           GeoSwz<IO, 1>::kBoxRows);
     if (e != cudaSuccess) return e;
   }
   const int blocks = grid_for(kern, smem, occ, batch);

@@ -23,18 +23,37 @@ constexpr int kScratchWords = 2 * 272;         // per-warp transpose scratch (u3
 // each: polynomials 0..7 and 8..15 of the tile).  Consumer warp w owns polynomial w of
 // the first half and polynomial w of the second; the second half starts kPad bytes
 // later so the two polynomials of a warp sit on disjoint bank halves.
-template <class IO>
-struct Geo {
-  static constexpr int kPolyBytes = 256 * int(sizeof(IO));
-  static constexpr int kPad = sizeof(IO) == 2 ? 32 : 64;
-  static constexpr int kHalfBytes = kConsumers * kPolyBytes;
+// Stage counts per use (DIR 0 forward, 1 inverse, 2 fused polymul).  Fewer bytes in flight
+// per SM can be faster: a TMA -> STG copy peaks at 48-64 KiB per SM (tools/copy_probe.cu:
+// 6.59 TB/s at 1 CTA x 3 stages vs 6.16 at 3 CTAs x 3 stages).  Measured (B200, 3 CTAs/SM):
+// u32 forward 2 stages 0.806 -> 0.776 ms, u16 inverse 2 stages 1.152 -> 1.123 ms; the u16
+// forward keeps 4 (2: +1.5 %), the u32 inverse 3 (profiles/r02_stage_sweep.txt).
 #ifndef NTTK_STAGES16
 #define NTTK_STAGES16 4
 #endif
 #ifndef NTTK_STAGES32
 #define NTTK_STAGES32 3
 #endif
-  static constexpr int kStages = sizeof(IO) == 2 ? NTTK_STAGES16 : NTTK_STAGES32;
+#ifndef NTTK_FWD_STAGES16
+#define NTTK_FWD_STAGES16 4
+#endif
+#ifndef NTTK_FWD_STAGES32
+#define NTTK_FWD_STAGES32 2
+#endif
+#ifndef NTTK_INV_STAGES16
+#define NTTK_INV_STAGES16 2
+#endif
+#ifndef NTTK_INV_STAGES32
+#define NTTK_INV_STAGES32 3
+#endif
+template <class IO, int DIR = 2>
+struct Geo {
+  static constexpr int kPolyBytes = 256 * int(sizeof(IO));
+  static constexpr int kPad = sizeof(IO) == 2 ? 32 : 64;
+  static constexpr int kHalfBytes = kConsumers * kPolyBytes;
+  static constexpr int kStages = DIR == 0   ? (sizeof(IO) == 2 ? NTTK_FWD_STAGES16 : NTTK_FWD_STAGES32)
+                                 : DIR == 1 ? (sizeof(IO) == 2 ? NTTK_INV_STAGES16 : NTTK_INV_STAGES32)
+                                            : (sizeof(IO) == 2 ? NTTK_STAGES16 : NTTK_STAGES32);
   static constexpr int kStageBytes = 2 * kHalfBytes + kPad + 64;  // keep stages 128B-aligned
   static constexpr int kSmem = kStages * kStageBytes + kConsumers * kScratchWords * 4 +
                                2 * kStages * 8;
@@ -54,14 +73,14 @@ constexpr bool inv_swz() {
   return (NTTK_INV_SWZ >> (sizeof(IO) == 4 ? 1 : 0)) & 1;
 }
 
-template <class IO>
+template <class IO, int DIR = 2>
 struct GeoSwz {
   static constexpr int kPolyBytes = 256 * int(sizeof(IO));
   static constexpr int kRowsPerPoly = kPolyBytes / 128;
   static constexpr int kBoxRows = kTile * kRowsPerPoly;  // 64 (u16) / 128 (u32) <= 256
   static constexpr int kStageBytes = kBoxRows * 128;     // multiple of 1024
-  static constexpr int kUsed = Geo<IO>::kStages * kStageBytes + kConsumers * kScratchWords * 4 +
-                               2 * Geo<IO>::kStages * 8;
+  static constexpr int kUsed = Geo<IO, DIR>::kStages * kStageBytes + kConsumers * kScratchWords * 4 +
+                               2 * Geo<IO, DIR>::kStages * 8;
   static constexpr int kSmem = kUsed + 1024;  // + alignment slack for the 1024-byte base
 };
 
@@ -278,10 +297,10 @@ __host__ __device__ constexpr bool tws_on() {
 }
 
 // producer: stream tiles of kTile polynomials into the stage ring
-template <class IO>
+template <class IO, int DIR = 2>
 __device__ __forceinline__ void produce(const IO* in, size_t batch, uint8_t* stages, uint64_t* full,
                                         uint64_t* empty) {
-  using G = Geo<IO>;
+  using G = Geo<IO, DIR>;
   const size_t ntiles = (batch + kTile - 1) / kTile;
   int k = 0;
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
