@@ -38,8 +38,12 @@ for part in re.split(r"\n\s+Function : ", txt)[1:]:
         t = re.search(r"0x([0-9a-f]+)", rest)
         if op.startswith("BRA") and t and int(t.group(1), 16) < a:
             lo = int(t.group(1), 16)
+            if any(lo <= x <= a and o == "EXIT" for x, o, _ in ins):
+                continue  # a retry stub branching back over the producer / kernel exits
             n = sum(1 for x, o, _ in ins if lo <= x <= a and o.startswith("IMAD"))
-            if n > best_n:
+            # the most IMADs; among equal counts the tightest region (the retry stubs of
+            # mbarrier waits branch back from the end of the kernel over everything)
+            if n > best_n or (n == best_n and a - lo < best[1] - best[0]):
                 best, best_n = (lo, a), n
     if not best:
         continue
