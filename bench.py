@@ -438,6 +438,43 @@ def run_extras(dev):
     return ex
 
 
+def run_e2e(a, torch, dist, nttk, Pk, Pd, IMP, xk, xd, nk, nd, world, dev, polys_per_step):
+    """The same step end to end through the C ABI host entry point (nttk_roundtrip_host:
+    pinned host buffers, H2D + kernels + D2H inside the timed region).  The pinned
+    allocation is agreed on by all ranks first, so a rank that cannot pin fails the e2e
+    leg everywhere instead of leaving the others in a collective."""
+    err, okf = None, torch.ones(1, device=dev)
+    try:
+        hk = torch.empty((nk, 256), dtype=torch.int16, pin_memory=True)
+        hd = torch.empty((nd, 256), dtype=torch.int32, pin_memory=True)
+        ohk, ohd = torch.empty_like(hk, pin_memory=True), torch.empty_like(hd, pin_memory=True)
+    except Exception as ex:
+        err = f"{type(ex).__name__}: {ex}"
+        okf.zero_()
+    if world > 1:
+        dist.all_reduce(okf, op=dist.ReduceOp.MIN)
+    if okf.item() == 0:
+        raise RuntimeError(err or "pinned host allocation failed on another rank")
+    hk.copy_(xk)
+    hd.copy_(xd)
+    nttk.roundtrip_host(Pk, IMP, hk, None, ohk)
+    nttk.roundtrip_host(Pd, IMP, hd, None, ohd)
+    if world > 1:
+        dist.barrier()
+    te = time.perf_counter()
+    for _ in range(a.e2e_steps):
+        nttk.roundtrip_host(Pk, IMP, hk, None, ohk)
+        nttk.roundtrip_host(Pd, IMP, hd, None, ohd)
+    dt = torch.tensor([time.perf_counter() - te], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    assert torch.equal(ohk, hk) and torch.equal(ohd, hd), "e2e round trip mismatch"
+    return {"value": polys_per_step * a.e2e_steps / float(dt.item()), "unit": UNIT,
+            "h2d_bytes_per_step": nk * 512 + nd * 1024,
+            "d2h_bytes_per_step": nk * 512 + nd * 1024,
+            "path": "nttk_roundtrip_host (C ABI, pinned host buffers, 3-stream pipeline)"}
+
+
 def run_engine_arm(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -541,29 +578,10 @@ def run_engine_arm(a, rank, world, local_rank):
     # end-to-end through the C ABI host entry point (pinned host buffers, copies timed)
     e2e = None
     if not a.no_e2e:
-        hk = torch.empty((nk, 256), dtype=torch.int16, pin_memory=True)
-        hd = torch.empty((nd, 256), dtype=torch.int32, pin_memory=True)
-        hk.copy_(xk)
-        hd.copy_(xd)
-        ohk, ohd = torch.empty_like(hk, pin_memory=True), torch.empty_like(hd, pin_memory=True)
-        for _ in range(1):
-            nttk.roundtrip_host(Pk, IMP, hk, None, ohk)
-            nttk.roundtrip_host(Pd, IMP, hd, None, ohd)
-        if world > 1:
-            dist.barrier()
-        te = time.perf_counter()
-        for _ in range(a.e2e_steps):
-            nttk.roundtrip_host(Pk, IMP, hk, None, ohk)
-            nttk.roundtrip_host(Pd, IMP, hd, None, ohd)
-        dt = torch.tensor([time.perf_counter() - te], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        assert torch.equal(ohk, hk) and torch.equal(ohd, hd), "e2e round trip mismatch"
-        e2e = {"value": polys_per_step * a.e2e_steps / float(dt.item()), "unit": UNIT,
-               "h2d_bytes_per_step": nk * 512 + nd * 1024,
-               "d2h_bytes_per_step": nk * 512 + nd * 1024,
-               "path": "nttk_roundtrip_host (C ABI, pinned host buffers, 3-stream pipeline)"}
-
+        try:
+            e2e = run_e2e(a, torch, dist, nttk, Pk, Pd, IMP, xk, xd, nk, nd, world, dev, polys_per_step)
+        except Exception as ex:  # e.g. pinned host memory exhausted with many ranks per host
+            e2e = {"value": None, "unit": UNIT, "error": f"{type(ex).__name__}: {ex}"[:300]}
     digest = None
     if a.gather and world > 1:  # NCCL only to gather results when asked, outside timing
         d = torch.stack([sk.view(-1)[:1024].to(torch.int64).sum(), sd.view(-1)[:1024].to(torch.int64).sum()])

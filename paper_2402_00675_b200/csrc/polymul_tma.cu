@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "arith.cuh"
 #include "fast256.hpp"
@@ -67,19 +68,63 @@ __device__ __forceinline__ void produce2(const IO* a, const IO* b, size_t batch,
   }
 }
 
+// Lane twiddles of the forward (bit 0) / inverse (bit 1) transform read from shared
+// memory (TwSmem) instead of 15 pinned registers each, and the register cap that buys
+// (minimum CTAs per SM, u16 storage, n = 16 kinds, 7 layers).  Measured (B200, config 2, tools/polymul_probe.py):
+// both tables in shared memory at 3 CTAs/SM (96 -> 72 registers, no spills) lifts improved
+// 1.05 -> 1.07, harvey 0.666 -> 0.680, smont 0.695 -> 0.726 G products/s; 3 CTAs with the
+// tables in registers spills (0.99 G).  u32 storage keeps the allocator's choice (its
+// stages admit 2 CTAs/SM).
+#ifndef NTTK_PM_TWS
+#define NTTK_PM_TWS 0x3
+#endif
+template <class K>
+struct pm_n16 : std::false_type {};
+template <bool F>
+struct pm_n16<ImprovedN16<F>> : std::true_type {};
+template <bool C>
+struct pm_n16<Harvey<16, C>> : std::true_type {};
+template <>
+struct pm_n16<Smont<16>> : std::true_type {};
+#ifndef NTTK_PM_MINB  // 3 CTAs/SM where the 72-register cap does not spill
+#define NTTK_PM_MINB(K, IO, L) (sizeof(IO) == 2 && L == 7 && pm_n16<K>::value ? 3 : sizeof(IO) == 4 ? 2 : 1)
+#endif
+
+template <class K, int DIR>
+struct PmTw {
+  static constexpr bool kSmem = (NTTK_PM_TWS >> DIR) & 1;
+};
+
 template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, NTTK_PM_MINB(K, IO, L))
     polymul256_tma_kernel(const IO* __restrict__ a, const IO* __restrict__ b, IO* __restrict__ out,
                           size_t batch, const __grid_constant__ PolymulArgs PA) {
   using G = Geo2<IO>;
   using Enc = typename K::Enc;
+  using Tw = typename K::Tw;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + G::kStages * G::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + kConsumers * kScratchWords);
   uint64_t* empty = full + G::kStages;
+  Tw* tws = reinterpret_cast<Tw*>(empty + G::kStages);  // [2][240] lane twiddles (PmTw)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  init_barriers(full, empty, G::kStages);
+  if constexpr (PmTw<K, 0>::kSmem || PmTw<K, 1>::kSmem) {
+    if (threadIdx.x < 16) {
+      Tw t[15];
+      if constexpr (PmTw<K, 0>::kSmem) {
+        fwd_twiddles<K, L, PER_INDEX>(t, PA.fwd, threadIdx.x);
+#pragma unroll
+        for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
+      }
+      if constexpr (PmTw<K, 1>::kSmem) {
+        inv_twiddles<K, L>(t, PA.inv, threadIdx.x);
+#pragma unroll
+        for (int i = 0; i < 15; ++i) tws[240 + 16 * i + threadIdx.x] = t[i];
+      }
+    }
+  }
+  init_barriers(full, empty, G::kStages);  // __syncthreads: tables visible
   if (warp == kConsumers) {
     if (lane == 0) produce2<IO>(a, b, batch, stages, full, empty);
     return;
@@ -90,9 +135,14 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t* S = scratch + warp * kScratchWords + half * 272;
   Xpose X;
   X.init(S, j);
-  typename K::Tw twf[15], twi[15];
-  fwd_twiddles<K, L, PER_INDEX>(twf, AF, j);
-  inv_twiddles<K, L>(twi, AI, j);
+  using TwF = std::conditional_t<PmTw<K, 0>::kSmem, TwSmem<Tw>, Tw[15]>;
+  using TwI = std::conditional_t<PmTw<K, 1>::kSmem, TwSmem<Tw>, Tw[15]>;
+  TwF twf;
+  TwI twi;
+  if constexpr (PmTw<K, 0>::kSmem) twf = TwSmem<Tw>{tws + j};
+  else fwd_twiddles<K, L, PER_INDEX>(twf, AF, j);
+  if constexpr (PmTw<K, 1>::kSmem) twi = TwSmem<Tw>{tws + 240 + j};
+  else inv_twiddles<K, L>(twi, AI, j);
   // basemul moduli of this lane's 8 pairs (k = 8 j + q)
   Enc gam[8];
   if (PA.prod.basemul) {
@@ -148,7 +198,7 @@ cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, con
                       cudaStream_t st) {
   static OccCache occ;
   auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY, W1>;
-  constexpr int smem = Geo2<IO>::kSmem;
+  constexpr int smem = Geo2<IO>::kSmem + ((NTTK_PM_TWS & 3) ? 480 * int(sizeof(typename K::Tw)) : 0);
   const int g_sms2 = sm_count_current();
   const int o = occupancy_current(kern, kThreads, smem, occ);
   const size_t tiles = (batch + kTile - 1) / kTile;

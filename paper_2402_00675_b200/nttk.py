@@ -423,11 +423,22 @@ def _torch_elem(t) -> int:
     return _TORCH_ELEM[t.dtype]
 
 
-def _stream_ptr(stream) -> int:
+_RAW_STREAM = None
+
+
+def _stream_ptr(stream, t=None) -> int:
+    """cudaStream_t of `stream`, else torch's current stream on t's device (raw getter:
+    building a torch.cuda.Stream object per call costs microseconds)."""
+    global _RAW_STREAM
+    if stream is not None:
+        return stream.cuda_stream
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if _RAW_STREAM is None:
+        _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", False)
+    if _RAW_STREAM and t is not None:
+        return _RAW_STREAM(t.device.index)
+    return torch.cuda.current_stream().cuda_stream
 
 
 def _batch_of(t, N: int) -> int:
@@ -443,7 +454,7 @@ def forward(P: NttParams, kind, x, out=None, stream=None):
     e = _torch_elem(x)
     out = torch.empty_like(x) if out is None else out
     _check(lib().nttk_ntt_forward(P.handle, int(kind), x.data_ptr(), out.data_ptr(),
-                                  _batch_of(x, P.size), e, _stream_ptr(stream)))
+                                  _batch_of(x, P.size), e, _stream_ptr(stream, x)))
     return out
 
 
@@ -454,7 +465,7 @@ def inverse(P: NttParams, kind, x, out=None, stream=None):
     e = _torch_elem(x)
     out = torch.empty_like(x) if out is None else out
     _check(lib().nttk_intt_inverse(P.handle, int(kind), x.data_ptr(), out.data_ptr(),
-                                   _batch_of(x, P.size), e, _stream_ptr(stream)))
+                                   _batch_of(x, P.size), e, _stream_ptr(stream, x)))
     return out
 
 
