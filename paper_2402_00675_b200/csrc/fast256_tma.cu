@@ -31,12 +31,32 @@ namespace {
 
 using namespace tma;
 
+// Consumer warps per CTA.  Measured (B200, round 1, profiles/r02_consumer_sweep.txt): 12
+// consumers (2 CTAs/SM: 24 consumer warps, 2 producer warps instead of 3) beat 8 for the
+// improved u16 forward (0.994 -> 0.983 ms), u16 inverse (1.123 -> 1.088) and u32 inverse
+// (0.872 -> 0.862); the u32 forward keeps 8 at 3 CTAs/SM (12: 0.776 -> 0.826).  The other
+// kinds keep 8: most of them use 79-128 registers, where 12 consumers would leave one CTA
+// (12 warps) per SM.
+template <class K, class IO, int DIR>
+struct cons_of {
+  static constexpr int value =
+      (std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2) ||
+              (std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1)
+          ? 12
+          : kConsumers;
+};
+template <class K, class IO, int DIR>
+using GeoK = Geo<IO, DIR, cons_of<K, IO, DIR>::value>;
+template <class K, class IO, int DIR>
+using GeoSwzK = GeoSwz<IO, DIR, cons_of<K, IO, DIR>::value>;
+
 // ---------------------------------------------------------------------------
 template <class K, class IO, int L, bool PER_INDEX, bool W1>
-__global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
+__global__ void __launch_bounds__(GeoK<K, IO, 0>::kThreadsP, NTTK_FWD_MINB(IO))
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
-  using G = Geo<IO, 0>;
+  using G = GeoK<K, IO, 0>;
+  constexpr int kConsumers = G::kC, kTile = G::kTileP;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + G::kStages * G::kStageBytes);
@@ -53,9 +73,9 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
       for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
     }
   }
-  init_barriers(full, empty, G::kStages);  // __syncthreads: table visible
+  init_barriers(full, empty, G::kStages, kConsumers);  // __syncthreads: table visible
   if (warp == kConsumers) {
-    if (lane == 0) produce<IO, 0>(in, batch, stages, full, empty);
+    if (lane == 0) produce<IO, 0, kConsumers>(in, batch, stages, full, empty);
     return;
   }
   const int j = lane & 15, half = lane >> 4;
@@ -137,11 +157,12 @@ __global__ void __launch_bounds__(kThreads, NTTK_FWD_MINB(IO))
 // multiply-free block-0 merges (A.flags bit 5); bit 4: DEFER, no input canonicalisation
 // (A.flags bit 6, u16 improved n=16) -- see inv_body_lazy.
 template <class K, class IO, int L, int MODE>
-__global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
+__global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, NTTK_MINB(IO))
     inv256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A, const __grid_constant__ CUtensorMap tmap) {
-  using G = Geo<IO, 1>;
-  using GS = GeoSwz<IO, 1>;
+  using G = GeoK<K, IO, 1>;
+  using GS = GeoSwzK<K, IO, 1>;
+  constexpr int kConsumers = G::kC, kTile = G::kTileP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // SWIZZLE_128B destinations must be 1024-byte aligned (GS::kSmem carries the slack)
   uint8_t* smem = inv_swz<IO>() ? smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u) : smem_raw;
@@ -161,14 +182,14 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
       for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
     }
   }
-  init_barriers(full, empty, G::kStages);  // __syncthreads: table visible
+  init_barriers(full, empty, G::kStages, kConsumers);  // __syncthreads: table visible
   if (warp == kConsumers) {
     if (lane == 0) {
       if constexpr (inv_swz<IO>())
         produce_rows<GS::kBoxRows, G::kStages>(&tmap, static_cast<uint32_t>((batch + kTile - 1) / kTile),
                                                stages, full, empty);
       else
-        produce<IO, 1>(in, batch, stages, full, empty);
+        produce<IO, 1, kConsumers>(in, batch, stages, full, empty);
     }
     return;
   }
@@ -223,10 +244,10 @@ __global__ void __launch_bounds__(kThreads, NTTK_MINB(IO))
 
 // ---------------------------------------------------------------------------
 template <class Kern>
-int grid_for(Kern kern, int smem, OccCache& occ, size_t batch) {
-  const int o = occupancy_current(kern, kThreads, smem, occ);
+int grid_for(Kern kern, int threads, int tile, int smem, OccCache& occ, size_t batch) {
+  const int o = occupancy_current(kern, threads, smem, occ);
   const int g_sms = sm_count_current();
-  const size_t tiles = (batch + kTile - 1) / kTile;
+  const size_t tiles = (batch + tile - 1) / tile;
   const size_t full = size_t(g_sms) * o;
   return static_cast<int>(tiles < full ? tiles : full);
 }
@@ -236,9 +257,10 @@ cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs
                          cudaStream_t st) {
   static OccCache occ;
   auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1>;
-  constexpr int smem = Geo<IO, 0>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
-  const int blocks = grid_for(kern, smem, occ, batch);
-  kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
+  constexpr int smem = GeoK<K, IO, 0>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  using G = GeoK<K, IO, 0>;
+  const int blocks = grid_for(kern, G::kThreadsP, G::kTileP, smem, occ, batch);
+  kern<<<blocks, G::kThreadsP, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
   return cudaGetLastError();
 }
 
@@ -255,16 +277,17 @@ cudaError_t inv_launch_mode(const void* in, void* out, size_t batch, const FastA
                             cudaStream_t st) {
   static OccCache occ;
   auto kern = inv256_tma_kernel<K, IO, L, MODE>;
-  constexpr int smem = (inv_swz<IO>() ? GeoSwz<IO, 1>::kSmem : Geo<IO, 1>::kSmem) +
+  constexpr int smem = (inv_swz<IO>() ? GeoSwzK<K, IO, 1>::kSmem : GeoK<K, IO, 1>::kSmem) +
                        (tws_on<IO, 1>() ? 240 * int(sizeof(typename K::Tw)) : 0);
   CUtensorMap map{};
   if constexpr (inv_swz<IO>()) {
-    const cudaError_t e = make_rows128_map(&map, in, uint64_t(batch) * GeoSwz<IO, 1>::kRowsPerPoly,
-                                           GeoSwz<IO, 1>::kBoxRows);
+    const cudaError_t e = make_rows128_map(&map, in, uint64_t(batch) * GeoSwzK<K, IO, 1>::kRowsPerPoly,
+                                           GeoSwzK<K, IO, 1>::kBoxRows);
     if (e != cudaSuccess) return e;
   }
-  const int blocks = grid_for(kern, smem, occ, batch);
-  kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A, map);
+  using G = GeoK<K, IO, 1>;
+  const int blocks = grid_for(kern, G::kThreadsP, G::kTileP, smem, occ, batch);
+  kern<<<blocks, G::kThreadsP, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A, map);
   return cudaGetLastError();
 }
 

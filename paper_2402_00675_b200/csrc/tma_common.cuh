@@ -14,7 +14,10 @@
 namespace nttk_b200 {
 namespace tma {
 
-constexpr int kConsumers = 8;                  // consumer warps per CTA
+#ifndef NTTK_CONSUMERS
+#define NTTK_CONSUMERS 8
+#endif
+constexpr int kConsumers = NTTK_CONSUMERS;     // consumer warps per CTA
 constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr int kTile = 2 * kConsumers;          // polynomials per stage
 constexpr int kScratchWords = 2 * 272;         // per-warp transpose scratch (u32)
@@ -46,17 +49,20 @@ constexpr int kScratchWords = 2 * 272;         // per-warp transpose scratch (u3
 #ifndef NTTK_INV_STAGES32
 #define NTTK_INV_STAGES32 3
 #endif
-template <class IO, int DIR = 2>
+// C = consumer warps per CTA (fast256_tma.cu picks it per kernel, see cons_of there)
+template <class IO, int DIR = 2, int C = kConsumers>
 struct Geo {
+  static constexpr int kC = C;
+  static constexpr int kTileP = 2 * kC;              // polynomials per stage
+  static constexpr int kThreadsP = (kC + 1) * 32;    // + the producer warp
   static constexpr int kPolyBytes = 256 * int(sizeof(IO));
   static constexpr int kPad = sizeof(IO) == 2 ? 32 : 64;
-  static constexpr int kHalfBytes = kConsumers * kPolyBytes;
+  static constexpr int kHalfBytes = kC * kPolyBytes;
   static constexpr int kStages = DIR == 0   ? (sizeof(IO) == 2 ? NTTK_FWD_STAGES16 : NTTK_FWD_STAGES32)
                                  : DIR == 1 ? (sizeof(IO) == 2 ? NTTK_INV_STAGES16 : NTTK_INV_STAGES32)
                                             : (sizeof(IO) == 2 ? NTTK_STAGES16 : NTTK_STAGES32);
   static constexpr int kStageBytes = 2 * kHalfBytes + kPad + 64;  // keep stages 128B-aligned
-  static constexpr int kSmem = kStages * kStageBytes + kConsumers * kScratchWords * 4 +
-                               2 * kStages * 8;
+  static constexpr int kSmem = kStages * kStageBytes + kC * kScratchWords * 4 + 2 * kStages * 8;
   // byte offset of the polynomial of warp w, half h inside a stage
   __device__ static constexpr int poly_offset(int w, int h) {
     return h * (kHalfBytes + kPad) + w * kPolyBytes;
@@ -73,14 +79,14 @@ constexpr bool inv_swz() {
   return (NTTK_INV_SWZ >> (sizeof(IO) == 4 ? 1 : 0)) & 1;
 }
 
-template <class IO, int DIR = 2>
+template <class IO, int DIR = 2, int C = kConsumers>
 struct GeoSwz {
+  using G = Geo<IO, DIR, C>;
   static constexpr int kPolyBytes = 256 * int(sizeof(IO));
   static constexpr int kRowsPerPoly = kPolyBytes / 128;
-  static constexpr int kBoxRows = kTile * kRowsPerPoly;  // 64 (u16) / 128 (u32) <= 256
+  static constexpr int kBoxRows = G::kTileP * kRowsPerPoly;  // <= 256
   static constexpr int kStageBytes = kBoxRows * 128;     // multiple of 1024
-  static constexpr int kUsed = Geo<IO, DIR>::kStages * kStageBytes + kConsumers * kScratchWords * 4 +
-                               2 * Geo<IO, DIR>::kStages * 8;
+  static constexpr int kUsed = G::kStages * kStageBytes + G::kC * kScratchWords * 4 + 2 * G::kStages * 8;
   static constexpr int kSmem = kUsed + 1024;  // + alignment slack for the 1024-byte base
 };
 
@@ -297,10 +303,11 @@ __host__ __device__ constexpr bool tws_on() {
 }
 
 // producer: stream tiles of kTile polynomials into the stage ring
-template <class IO, int DIR = 2>
+template <class IO, int DIR = 2, int C = kConsumers>
 __device__ __forceinline__ void produce(const IO* in, size_t batch, uint8_t* stages, uint64_t* full,
                                         uint64_t* empty) {
-  using G = Geo<IO, DIR>;
+  using G = Geo<IO, DIR, C>;
+  constexpr int kTile = G::kTileP, kConsumers = G::kC;
   const size_t ntiles = (batch + kTile - 1) / kTile;
   int k = 0;
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
@@ -793,11 +800,12 @@ __device__ __forceinline__ void load_contiguous_swz(uint32_t (&v)[16], uint32_t 
   }
 }
 
-__device__ __forceinline__ void init_barriers(uint64_t* full, uint64_t* empty, int stages) {
+__device__ __forceinline__ void init_barriers(uint64_t* full, uint64_t* empty, int stages,
+                                              int consumers = kConsumers) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers);
+      mbar_init(&empty[s], consumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
