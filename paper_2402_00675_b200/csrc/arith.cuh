@@ -114,6 +114,12 @@ __device__ __forceinline__ uint32_t mp_n32(uint32_t t, uint32_t lo, uint32_t hi,
 //   scale(v)            final N^{-1} pass (transform.hpp:323-335), canonical
 //   inv_last(x, y, off) last merge layer with the N^{-1} pass folded in (kFold)
 
+// Form of the X-side product of the last (N^{-1}-folded) merge layer: 1 = paper form
+// (IMAD + 2 shifts, ALU-balanced), 0 = umulhi form (IMAD + IMAD.HI, 2 fewer instructions)
+#ifndef NTTK_LAST_PAPER
+#define NTTK_LAST_PAPER 1
+#endif
+
 template <bool PAPER_FORM = false>
 struct ImprovedN16 {
   using Tw = uint32_t;
@@ -159,7 +165,7 @@ struct ImprovedN16 {
   // result equals scale() applied after the last merge (canonical outputs are unique)
   __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
-    x = mp_n16<true>(x + y + A.zero, A.scale_lo, A.p);
+    x = mp_n16<NTTK_LAST_PAPER != 0>(x + y + A.zero, A.scale_lo, A.p);
     y = mp_n16<PAPER_FORM>(t, A.fold_lo, A.p);
   }
   // ---- lazy merge (inv_body_lazy, umulhi form only) ----
@@ -199,7 +205,7 @@ struct ImprovedN16 {
     uint32_t X;
     const uint32_t S = sum_hh(x, y, X, A);
     const uint32_t t = X + X + off - S + A.zero;
-    x = mp_n16<true>(S, A.scale_lo, A.p);
+    x = mp_n16<NTTK_LAST_PAPER != 0>(S, A.scale_lo, A.p);
     y = mp_n16<PAPER_FORM>(t, A.fold_lo, A.p);
   }
   // product stage (fused polymul): x -> (x (-2^{2n}) mod p) mu, then MP(.., y) = x y mod p

@@ -150,6 +150,11 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0>::kThreadsP, NTTK_FWD_MINB(IO))
   }
 }
 
+// u16 DEFER inverse: first merge layer from packed words with dp2a (A/B switch)
+#ifndef NTTK_DEFER_IDP
+#define NTTK_DEFER_IDP 1  // measured: Kyber inverse 1.088 -> 1.040 ms (profiles/r02_idp.txt)
+#endif
+
 // ---------------------------------------------------------------------------
 // MODE bits 0-1 -- 0: generic canonicalisation; 1: host-validated fast canonicalisation
 // (A.flags bits 0/1); 2: u16 input with the fused first merge layer (A.flags bit 2,
@@ -212,18 +217,24 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, NTTK_MINB(IO))
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       mbar_wait(&full[s], phase);
       uint32_t v[16];
-      if constexpr (inv_swz<IO>())
+      constexpr bool kPacked = NTTK_DEFER_IDP && (MODE & 16) && sizeof(IO) == 2 && !inv_swz<IO>();
+      if constexpr (kPacked) {  // raw packed words in v[8..15] (inv_body_lazy PACKED)
+        const uint4* src = reinterpret_cast<const uint4*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)) + 2 * j;
+        const uint4 a = src[0], b = src[1];
+        v[8] = a.x, v[9] = a.y, v[10] = a.z, v[11] = a.w, v[12] = b.x, v[13] = b.y, v[14] = b.z, v[15] = b.w;
+      } else if constexpr (inv_swz<IO>()) {
         load_contiguous_swz<IO, K::kSigned>(v, sbase + s * kStageBytes, soff);
-      else
+      } else {
         load_contiguous<IO, K::kSigned>(
             v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
+      }
       release_stage(&empty[s], lane);
       constexpr int CM = MODE & 3;
       if (CM != 2) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
       }
-      inv_body<K, L, CM == 2, (MODE & 4) != 0, (MODE & 8) != 0, (MODE & 16) != 0>(v, twl, A, X);
+      inv_body<K, L, CM == 2, (MODE & 4) != 0, (MODE & 8) != 0, (MODE & 16) != 0, kPacked>(v, twl, A, X);
       store_strided<IO>(optr, j, v, S, X, poly < nb);
       poly += pstep;
       optr += ostep;

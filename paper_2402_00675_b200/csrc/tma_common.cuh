@@ -475,7 +475,11 @@ struct w1_of<K, std::void_t<decltype(&K::fwd_w1)>> {
 //         reductions per lane by one product.
 // Phase 2 tracks which words are lazy at compile time (lz[], constant-folded by the full
 // unroll): TW1 outputs are materialised, and a pair with one lazy word materialises it.
-template <class K, int L, bool FUSE, bool TW1 = false, bool DEFER = false, class TWL>
+// PACKED (DEFER only): the caller leaves the 8 raw packed u16 words of the lane in v[8..15];
+// the first merge layer pairs the two halves of one word, so X + Y and X + Kp - Y come from
+// two dp2a dot products (IDP.2A) with byte vectors (1, 1) and (1, -1) instead of two
+// unpack ops and two adds.
+template <class K, int L, bool FUSE, bool TW1 = false, bool DEFER = false, bool PACKED = false, class TWL>
 __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                               const Xpose& X) {
   using Tw = typename K::Tw;
@@ -493,6 +497,16 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl,
       const int base = sl == 5 ? 0 : sl == 6 ? 1 : sl == 7 ? 3 : 7;
       const Tw w = twl[base + (r >> (9 - sl))];
       if (sl == L) {  // first merge layer: materialised (raw u16 if FUSE) inputs
+        if constexpr (PACKED) {
+          static_assert(DEFER, "PACKED input needs DEFER");
+          const uint32_t pw = v[8 + r / 2];
+          uint32_t sum, dif;
+          asm("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(sum) : "r"(pw), "r"(0x0101u), "r"(0u));
+          asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(dif) : "r"(pw), "r"(0xff01u), "r"(A.kp));
+          v[r] = sum;
+          v[r + h] = dif * w;
+          continue;
+        }
         const uint32_t x = v[r], y = v[r + h];
         if constexpr (DEFER) {
           v[r] = x + y + A.zero;
@@ -621,12 +635,12 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl
 
 // LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3); TW1 / DEFER: see there.
 template <class K, int L, bool FUSE, bool LAZY = false, bool TW1 = false, bool DEFER = false,
-          class TWL>
+          bool PACKED = false, class TWL>
 __device__ __forceinline__ void inv_body(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                          const Xpose& X) {
   if constexpr (LAZY) {
     static_assert(lazy_of<K>::value, "policy has no lazy merge");
-    inv_body_lazy<K, L, FUSE, TW1, DEFER>(v, twl, A, X);
+    inv_body_lazy<K, L, FUSE, TW1, DEFER, PACKED>(v, twl, A, X);
   } else {
     inv_body_eager<K, L, FUSE>(v, twl, A, X);
   }

@@ -35,6 +35,20 @@ __global__ void bench(uint32_t* out, uint32_t a, uint32_t b, long long* cycles) 
       } else if (OP == 4) {  // LOP3 / shift (alu)
         asm volatile("shr.u32 %0, %0, 1;" : "+r"(v[c]));
         asm volatile("xor.b32 %0, %0, %1;" : "+r"(v[c]) : "r"(b));
+      } else if (OP == 6) {  // IDP.2A (dp2a)
+        asm volatile("dp2a.lo.u32.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(b), "r"(a));
+      } else if (OP >= 7 && OP <= 9) {  // even chains IDP.2A, odd chains IMAD / IMAD.HI / IADD3
+        if (c & 1) {
+          if (OP == 7) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(a), "r"(b));
+          if (OP == 8) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(a), "r"(b));
+          if (OP == 9) asm volatile("add.u32 %0, %0, %1;" : "+r"(v[c]) : "r"(a));
+        } else {
+          asm volatile("dp2a.lo.u32.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(b), "r"(a));
+        }
+      } else if (OP == 10 || OP == 11) {  // even chains IADD3 (10) / IMAD.HI (11), odd IMAD
+        if (c & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(a), "r"(b));
+        else if (OP == 10) asm volatile("add.u32 %0, %0, %1;" : "+r"(v[c]) : "r"(a));
+        else asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(v[c]) : "r"(a), "r"(b));
       } else if (OP == 5) {  // Plantard n=16 tail: IMAD + IMAD.HI + 2 adds (a butterfly)
         uint32_t h = v[c] * a;
         uint32_t r = __umulhi(h, b);
@@ -92,5 +106,11 @@ int main() {
   run<3>("IADD3 (add.u32)", 1, sms);
   run<4>("SHF+LOP3", 2, sms);
   run<5>("plantard16 bfly (~5 instr)", 5, sms);
+  run<6>("IDP.2A (dp2a)", 1, sms);
+  run<7>("IDP.2A | IMAD (1:1)", 1, sms);
+  run<8>("IDP.2A | IMAD.HI (1:1)", 1, sms);
+  run<9>("IDP.2A | IADD3 (1:1)", 1, sms);
+  run<10>("IADD3 | IMAD (1:1)", 1, sms);
+  run<11>("IMAD.HI | IMAD (1:1)", 1, sms);
   return 0;
 }
