@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0>::kThreadsP, NTTK_FWD_MINB(IO))
 // ---------------------------------------------------------------------------
 // MODE bits 0-1 -- 0: generic canonicalisation; 1: host-validated fast canonicalisation
 // (A.flags bits 0/1); 2: u16 input with the fused first merge layer (A.flags bit 2,
-// improved n=16).  MODE bit 2: lazy merge outputs (A.flags bit 3, improved).  Bit 3: TW1
+// improved n=16); 3: u32 partial canonicalisation to [0, 2p) with doubled merge offsets
+// (A.flags bit 7, lazy improved n=32).  MODE bit 2: lazy merge outputs (A.flags bit 3, improved).  Bit 3: TW1
 // multiply-free block-0 merges (A.flags bit 5); bit 4: DEFER, no input canonicalisation
 // (A.flags bit 6, u16 improved n=16) -- see inv_body_lazy.
 template <class K, class IO, int L, int MODE>
@@ -230,11 +231,15 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, NTTK_MINB(IO))
       }
       release_stage(&empty[s], lane);
       constexpr int CM = MODE & 3;
-      if (CM != 2) {
+      if constexpr (CM == 3) {  // partial: [0, 2p) without the conditional subtraction
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = v[r] + (v[r] >> A.cs_s) * A.negp;
+      } else if (CM != 2) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
       }
-      inv_body<K, L, CM == 2, (MODE & 4) != 0, (MODE & 8) != 0, (MODE & 16) != 0, kPacked>(v, twl, A, X);
+      inv_body<K, L, CM == 2, (MODE & 4) != 0, (MODE & 8) != 0, (MODE & 16) != 0, kPacked, CM == 3 ? 1 : 0>(
+          v, twl, A, X);
       store_strided<IO>(optr, j, v, S, X, poly < nb);
       poly += pstep;
       optr += ostep;
@@ -308,6 +313,9 @@ cudaError_t inv_launch_canon(const void* in, void* out, size_t batch, const Fast
   constexpr bool kCanFuse = sizeof(IO) == 2 && std::is_same<K, ImprovedN16<false>>::value;
   const unsigned fast_bit = sizeof(IO) == 2 ? 1u : 2u;
   if (kCanFuse && (A.flags & 4)) return inv_launch_mode<K, IO, L, (kCanFuse ? 2 : 1) | LZ>(in, out, batch, A, st);
+  // partial canonicalisation (lazy improved n = 32 on u32, A.flags bit 7)
+  constexpr bool kPartial = sizeof(IO) == 4 && std::is_same<K, ImprovedN32>::value && (LZ & 4);
+  if (kPartial && (A.flags & 128)) return inv_launch_mode<K, IO, L, (kPartial ? 3 : 1) | LZ>(in, out, batch, A, st);
   if (!K::kSigned && (A.flags & fast_bit)) return inv_launch_mode<K, IO, L, 1 | LZ>(in, out, batch, A, st);
   return inv_launch_mode<K, IO, L, 0 | LZ>(in, out, batch, A, st);
 }

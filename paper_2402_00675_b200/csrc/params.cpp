@@ -202,6 +202,14 @@ void fill_fast(HostParams& P, int kind) {
         P.gs_plain.size() >= 256 - 4 && P.gs_plain[256 - 16] == 1 && P.gs_plain[256 - 8] == 1 &&
         P.gs_plain[256 - 4] == 1)
       A.flags |= 32;
+    // inverse partial canonicalisation (u32, lazy improved n = 32): inputs reduced to [0, 2p)
+    // by the shift reduction without its conditional subtraction; every merge bound doubles,
+    // so the last layer's X + Y < 2^{L+1} p must fit 32 bits (Prop. 4's range at n = 32 is
+    // far larger)
+    if (kind == NTTK_IMPROVED && !n16 && dir == 1 && P.N == 256 && (A.flags & 2) && (A.flags & 8) &&
+        (u128(p) << (P.layers + 1)) < (u128(1) << 32) &&
+        u128(p - 1) * (u128(p) << (P.layers + 1)) < u128(c.beta) * (c.beta - p))
+      A.flags |= 128;
     // inverse DEFER (u16 input, no canonicalisation): sum-chain products h K p + h (2^16 - 1)
     // for h <= 8 inside Prop. 4's range, lazily consumed ones (h <= 4) pairwise below 2^32,
     // and v0 < 16 (2^16 - 1) reducible by MP(1^, v0)

@@ -67,7 +67,8 @@ struct FastArgs {
                            // bit3: lazy merge valid (improved n = 16);
                            // bit4: forward block-0 twiddles are 1 (cyclic, improved);
                            // bit5: inverse phase-2 block-0 twiddles are 1 (TW1, L = 8);
-                           // bit6: u16 inverse without canonicalisation (DEFER)
+                           // bit6: u16 inverse without canonicalisation (DEFER);
+                           // bit7: u32 inverse with partial canonicalisation to [0, 2p)
   uint32_t fold_lo = 0, fold_hi = 0;  // last merge twiddle times N^{-1}, kind encoding
   uint32_t soff = 0;       // scott: butterfly offset (N/L) p (butterfly.hpp:172-184)
   uint32_t lo[256] = {};   // twiddle words in reference table order

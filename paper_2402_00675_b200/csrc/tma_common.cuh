@@ -479,7 +479,10 @@ struct w1_of<K, std::void_t<decltype(&K::fwd_w1)>> {
 // the first merge layer pairs the two halves of one word, so X + Y and X + Kp - Y come from
 // two dp2a dot products (IDP.2A) with byte vectors (1, 1) and (1, -1) instead of two
 // unpack ops and two adds.
-template <class K, int L, bool FUSE, bool TW1 = false, bool DEFER = false, bool PACKED = false, class TWL>
+// OSH = 1: inputs only partially reduced to [0, 2p) (u32 inverse, A.flags bit 7), every
+// bound doubles, so merge depth d takes the offset of depth d + 1.
+template <class K, int L, bool FUSE, bool TW1 = false, bool DEFER = false, bool PACKED = false,
+          int OSH = 0, class TWL>
 __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                               const Xpose& X) {
   using Tw = typename K::Tw;
@@ -490,7 +493,7 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl,
   for (int sl = 8; sl >= 5; --sl) {  // phase 1: merge layers s = L..5
     if (sl > L) continue;
     const int h = 1 << (8 - sl);
-    const uint32_t off = A.off[L - sl + 1];
+    const uint32_t off = A.off[L - sl + 1 + OSH];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
@@ -542,7 +545,7 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl,
 #pragma unroll
   for (int sl = 4; sl >= 1; --sl) {  // phase 2: merge layers s = 4..1, materialised start
     const int h = 1 << (4 - sl);
-    const uint32_t off = A.off[L - sl + 1];
+    const uint32_t off = A.off[L - sl + 1 + OSH];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
@@ -635,13 +638,14 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl
 
 // LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3); TW1 / DEFER: see there.
 template <class K, int L, bool FUSE, bool LAZY = false, bool TW1 = false, bool DEFER = false,
-          bool PACKED = false, class TWL>
+          bool PACKED = false, int OSH = 0, class TWL>
 __device__ __forceinline__ void inv_body(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                          const Xpose& X) {
   if constexpr (LAZY) {
     static_assert(lazy_of<K>::value, "policy has no lazy merge");
-    inv_body_lazy<K, L, FUSE, TW1, DEFER, PACKED>(v, twl, A, X);
+    inv_body_lazy<K, L, FUSE, TW1, DEFER, PACKED, OSH>(v, twl, A, X);
   } else {
+    static_assert(OSH == 0, "partial canonicalisation needs the lazy body");
     inv_body_eager<K, L, FUSE>(v, twl, A, X);
   }
 }
