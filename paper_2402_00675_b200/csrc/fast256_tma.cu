@@ -37,25 +37,30 @@ using namespace tma;
 // (0.872 -> 0.862); the u32 forward keeps 8 at 3 CTAs/SM (12: 0.776 -> 0.826).  The other
 // kinds keep 8: most of them use 79-128 registers, where 12 consumers would leave one CTA
 // (12 warps) per SM.
-template <class K, class IO, int DIR>
+#ifndef NTTK_CONS_IMPROVED
+#define NTTK_CONS_IMPROVED 12
+#endif
+// (W1 = the cyclic forward with twiddle-1 blocks.)  The 7-layer negacyclic forward keeps 8 at
+// every batch size (tools/c1_probe.py: 4096 polys 5.5 -> 4.2 us, 2^21 493 -> 488 us with 8).
+template <class K, class IO, int DIR, int L = 8, bool W1 = true>
 struct cons_of {
   static constexpr int value =
-      (std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2) ||
+      (std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2 && (DIR == 1 || (L == 8 && W1))) ||
               (std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1)
-          ? 12
+          ? NTTK_CONS_IMPROVED
           : kConsumers;
 };
-template <class K, class IO, int DIR>
-using GeoK = Geo<IO, DIR, cons_of<K, IO, DIR>::value>;
+template <class K, class IO, int DIR, int L = 8, bool W1 = true>
+using GeoK = Geo<IO, DIR, cons_of<K, IO, DIR, L, W1>::value>;
 template <class K, class IO, int DIR>
 using GeoSwzK = GeoSwz<IO, DIR, cons_of<K, IO, DIR>::value>;
 
 // ---------------------------------------------------------------------------
 template <class K, class IO, int L, bool PER_INDEX, bool W1>
-__global__ void __launch_bounds__(GeoK<K, IO, 0>::kThreadsP, NTTK_FWD_MINB(IO))
+__global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP, NTTK_FWD_MINB(IO))
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
-  using G = GeoK<K, IO, 0>;
+  using G = GeoK<K, IO, 0, L, W1>;
   constexpr int kConsumers = G::kC, kTile = G::kTileP;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
@@ -273,8 +278,8 @@ cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs
                          cudaStream_t st) {
   static OccCache occ;
   auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1>;
-  constexpr int smem = GeoK<K, IO, 0>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
-  using G = GeoK<K, IO, 0>;
+  constexpr int smem = GeoK<K, IO, 0, L, W1>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  using G = GeoK<K, IO, 0, L, W1>;
   const int blocks = grid_for(kern, G::kThreadsP, G::kTileP, smem, occ, batch);
   kern<<<blocks, G::kThreadsP, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
   return cudaGetLastError();
