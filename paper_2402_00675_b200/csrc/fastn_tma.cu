@@ -361,7 +361,10 @@ __device__ __forceinline__ void inv_body_n(uint32_t (&v)[32], const uint2* tws, 
 // inv_body_lazy): after a layer of register half-span h the words at (k & h) hold
 // pre-quotient values, paired with each other by the next layer; materialised before the
 // transpose, and phase 2 starts materialised.
-template <class K, int LOGN>
+// TW1 (A.flags bit 5, cyclic full tree): block 0 of the phase-2 merge layers (len >= N/32)
+// has twiddle 1 and is uniform across lanes; Y' = X + off - Y stays unreduced (every value
+// of merge depth d < 2^d p, as in tma_common.cuh inv_body_lazy).
+template <class K, int LOGN, bool TW1 = false>
 __device__ __forceinline__ void inv_body_n_lazy(uint32_t (&v)[32], const uint2* tws,
                                                 const FastArgs& A,
                                                 const XposeN<(1 << LOGN) / 32>& X, int j) {
@@ -389,6 +392,9 @@ __device__ __forceinline__ void inv_body_n_lazy(uint32_t (&v)[32], const uint2* 
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 32; ++k) v[k] = X.get(k);
+  bool lz[32];  // lazy words of phase 2 (compile-time after the unroll; see inv_body_lazy)
+#pragma unroll
+  for (int k = 0; k < 32; ++k) lz[k] = false;
 #pragma unroll
   for (int s = 5; s >= 1; --s) {  // phase 2: strided, h = 2^{5-s}, materialised start
     const int h = 1 << (5 - s);
@@ -396,14 +402,34 @@ __device__ __forceinline__ void inv_body_n_lazy(uint32_t (&v)[32], const uint2* 
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       if (k & h) continue;
-      const bool lazy = s < 5 && (k & (h >> 1));
+      bool lx = lz[k], ly = lz[k + h];
+      if (lx != ly) {  // mixed pair after a TW1 block: materialise the lazy word
+        if (lx) v[k] = K::materialize(v[k], A);
+        else v[k + h] = K::materialize(v[k + h], A);
+        lx = ly = false;
+      }
       if (s == 1) {
-        if (lazy) K::inv_last_hh(v[k], v[k + h], off, A);
+        if (lx) K::inv_last_hh(v[k], v[k + h], off, A);
         else K::inv_last(v[k], v[k + h], off, A);
+        lz[k] = lz[k + h] = false;
+      } else if (TW1 && (k >> (6 - s)) == 0) {  // block 0: twiddle 1, Y' = T unreduced
+        const uint32_t x = v[k], y = v[k + h];
+        if (lx) {
+          uint32_t Xm;
+          const uint32_t S = K::sum_hh(x, y, Xm, A);
+          v[k] = S;
+          v[k + h] = Xm + Xm + off - S + A.zero;
+        } else {
+          v[k] = x + y + A.zero;
+          v[k + h] = x + off - y;
+        }
+        lz[k] = lz[k + h] = false;
       } else {
         const Tw w = K::tw(A, 32 - (2 << (s - 1)) + (k >> (6 - s)));
-        if (lazy) K::inv_hh(v[k], v[k + h], w, off, A);
+        if (lx) K::inv_hh(v[k], v[k + h], w, off, A);
         else K::inv_h(v[k], v[k + h], w, off, A);
+        lz[k] = false;
+        lz[k + h] = true;
       }
     }
   }
@@ -467,7 +493,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // MODE bits 0-1 -- 0: generic canonicalisation of the input words; 1: host-validated fast
-// form.  MODE bit 2: lazy merge (policy kLazy, A.flags bit 3).
+// form.  MODE bit 2: lazy merge (policy kLazy, A.flags bit 3); bit 3: TW1 (A.flags bit 5).
 template <class K, class IO, int LOGN, int MODE>
 __global__ void __launch_bounds__(kThreads)
     invn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
@@ -520,7 +546,7 @@ __global__ void __launch_bounds__(kThreads)
     release_stage(&empty[s], lane);
 #pragma unroll
     for (int k = 0; k < 32; ++k) v[k] = canon<IO, K::kSigned, (MODE & 3) == 1>(v[k], A);
-    if constexpr ((MODE & 4) != 0) inv_body_n_lazy<K, LOGN>(v, tws, A, X, j);
+    if constexpr ((MODE & 4) != 0) inv_body_n_lazy<K, LOGN, (MODE & 8) != 0>(v, tws, A, X, j);
     else inv_body_n<K, LOGN>(v, tws, A, X, j);
     store_strided_n<IO, G>(out + poly * GN::N, j, v, X, poly < batch);
   }
@@ -584,7 +610,10 @@ template <class K, class IO, int LOGN>
 cudaError_t inv_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
                   cudaStream_t st) {
   if constexpr (lazy_of<K>::value) {
-    if (A.flags & 8) return inv_n_canon<K, IO, LOGN, 4>(in, out, batch, tab, A, st);
+    if (A.flags & 8) {
+      if (A.flags & 32) return inv_n_canon<K, IO, LOGN, 4 | 8>(in, out, batch, tab, A, st);
+      return inv_n_canon<K, IO, LOGN, 4>(in, out, batch, tab, A, st);
+    }
   }
   return inv_n_canon<K, IO, LOGN, 0>(in, out, batch, tab, A, st);
 }

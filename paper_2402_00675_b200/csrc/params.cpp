@@ -198,10 +198,16 @@ void fill_fast(HostParams& P, int kind) {
     // inverse TW1 (inv_body_lazy): block 0 of merge layers len = 16, 32, 64 has twiddle
     // 1 (index 2^L - 2^s of the merge table, s = 4, 3, 2).  Every value of merge depth d
     // stays below 2^d p, the bound the lazy / exact-bound checks already assume.
-    if (kind == NTTK_IMPROVED && dir == 1 && P.layers == 8 && P.N == 256 && (A.flags & 8) &&
-        P.gs_plain.size() >= 256 - 4 && P.gs_plain[256 - 16] == 1 && P.gs_plain[256 - 8] == 1 &&
-        P.gs_plain[256 - 4] == 1)
-      A.flags |= 32;
+    // N = 512 / 1024 (fastn_tma.cu, full trees): the phase-2 layers are s = 5..2, the same
+    // table positions 2^L - 2^s.
+    if (kind == NTTK_IMPROVED && dir == 1 && (A.flags & 8) &&
+        ((P.N == 256 && P.layers == 8) || ((P.N == 512 || P.N == 1024) && (1u << P.layers) == P.N))) {
+      const unsigned smax = P.N == 256 ? 4 : 5;
+      bool ones = P.gs_plain.size() >= (size_t(1) << P.layers) - 4;
+      for (unsigned st = 2; ones && st <= smax; ++st)
+        ones = P.gs_plain[(size_t(1) << P.layers) - (size_t(1) << st)] == 1;
+      if (ones) A.flags |= 32;
+    }
     // inverse partial canonicalisation (u32, lazy improved n = 32): inputs reduced to [0, 2p)
     // by the shift reduction without its conditional subtraction; every merge bound doubles,
     // so the last layer's X + Y < 2^{L+1} p must fit 32 bits (Prop. 4's range at n = 32 is

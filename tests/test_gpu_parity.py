@@ -645,7 +645,7 @@ def test_randomized_pointwise_basemul_and_aliasing(oracle):
         assert (from_dev(xa) == want).all(), case
 
 
-def _extreme_words(p, bits, B, seed):
+def _extreme_words(p, bits, B, seed, N=256):
     """Inverse inputs that drive the merge bounds: all-max words, max/zero patterns that
     maximise T = X + off - Y, and random draws from boundary values (words need not be
     canonical: the inverse canonicalises, transform.hpp:243)."""
@@ -653,15 +653,15 @@ def _extreme_words(p, bits, B, seed):
     rs = np.random.RandomState(seed)
     pts = np.array([0, 1, p - 1, p, 2 * p - 1, 9 * p - 1, top - p, top - 1, top], dtype=np.uint64)
     pts = pts[pts <= top]
-    w = pts[rs.randint(0, len(pts), size=(B, 256))]
+    w = pts[rs.randint(0, len(pts), size=(B, N))]
     w[0] = top
     w[1] = 0
     w[2, ::2], w[2, 1::2] = top, 0
-    w[3, :128], w[3, 128:] = top, 0
-    idx = np.arange(256)
-    for k in range(4):  # X max / Y zero at every merge span 2^k .. 2^(k+4)
+    w[3, :N // 2], w[3, N // 2:] = top, 0
+    idx = np.arange(N)
+    L = N.bit_length() - 1
+    for k in range(L):  # X max / Y zero at every merge span 2^k
         w[4 + k] = np.where((idx >> k) & 1, 0, top)
-        w[8 + k] = np.where((idx >> (k + 4)) & 1, 0, top)
     return w
 
 
@@ -682,3 +682,17 @@ def test_inverse_extreme_words(oracle, p, n, elem, tree, layers):
     f = np.asarray(Q.inverse(IMPROVED, w))
     y = nttk.forward(P, IMPROVED, to_dev(f, elem))
     assert (from_dev(nttk.inverse(P, IMPROVED, y)) == f).all()
+
+
+@pytest.mark.parametrize("N", [512, 1024])
+@pytest.mark.parametrize("n,elem", [(32, 4), (32, 8)])
+def test_fastn_inverse_extreme_words(oracle, N, n, elem):
+    """Worst-case words through the N = 512 / 1024 inverse (TW1 multiply-free block-0
+    merges of the phase-2 layers) vs the oracle, bit-exact."""
+    p = 12289
+    P = engine_params(p, N, n, [IMPROVED])
+    Q = oracle.params(p, N, n, (IMPROVED,))
+    assert IMPROVED in P.fast_path
+    w = _extreme_words(p, 8 * elem if elem < 8 else 40, 131, 3 + N + n, N)
+    got = from_dev(nttk.inverse(P, IMPROVED, to_dev(w, elem)))
+    assert (got == Q.inverse(IMPROVED, w)).all()
