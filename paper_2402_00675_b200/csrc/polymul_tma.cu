@@ -27,6 +27,14 @@ namespace {
 
 using namespace tma;
 
+// consumer warps per CTA of the fused polymul (shadows tma::kConsumers here; A/B switch)
+#ifndef NTTK_PM_CONS
+#define NTTK_PM_CONS 8
+#endif
+constexpr int kConsumers = NTTK_PM_CONS;
+constexpr int kThreads = (kConsumers + 1) * 32;
+constexpr int kTile = 2 * kConsumers;
+
 // stage = a-tile and b-tile, each two halves of 8 polynomials (one bulk copy per half)
 template <class IO>
 struct Geo2 {
@@ -86,8 +94,11 @@ template <bool C>
 struct pm_n16<Harvey<16, C>> : std::true_type {};
 template <>
 struct pm_n16<Smont<16>> : std::true_type {};
-#ifndef NTTK_PM_MINB  // 3 CTAs/SM where the 72-register cap does not spill
-#define NTTK_PM_MINB(K, IO, L) (sizeof(IO) == 2 && L == 7 && pm_n16<K>::value ? 3 : sizeof(IO) == 4 ? 2 : 1)
+#ifndef NTTK_PM_MINB16  // 3 CTAs/SM where the 72-register cap does not spill
+#define NTTK_PM_MINB16 3
+#endif
+#ifndef NTTK_PM_MINB
+#define NTTK_PM_MINB(K, IO, L) (sizeof(IO) == 2 && L == 7 && pm_n16<K>::value ? NTTK_PM_MINB16 : sizeof(IO) == 4 ? 2 : 1)
 #endif
 
 template <class K, int DIR>
@@ -124,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, NTTK_PM_MINB(K, IO, L))
       }
     }
   }
-  init_barriers(full, empty, G::kStages);  // __syncthreads: tables visible
+  init_barriers(full, empty, G::kStages, kConsumers);  // __syncthreads: tables visible
   if (warp == kConsumers) {
     if (lane == 0) produce2<IO>(a, b, batch, stages, full, empty);
     return;
