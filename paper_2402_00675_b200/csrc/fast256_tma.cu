@@ -42,11 +42,15 @@ using namespace tma;
 #endif
 // (W1 = the cyclic forward with twiddle-1 blocks.)  The 7-layer negacyclic forward keeps 8 at
 // every batch size (tools/c1_probe.py: 4096 polys 5.5 -> 4.2 us, 2^21 493 -> 488 us with 8).
+#ifndef NTTK_CONS_FWD16
+#define NTTK_CONS_FWD16 NTTK_CONS_IMPROVED
+#endif
 template <class K, class IO, int DIR, int L = 8, bool W1 = true>
 struct cons_of {
+  static constexpr bool kN16 = std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2;
   static constexpr int value =
-      (std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2 && (DIR == 1 || (L == 8 && W1))) ||
-              (std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1)
+      kN16 && DIR == 0 && L == 8 && W1 ? NTTK_CONS_FWD16
+      : (kN16 && DIR == 1) || (std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1)
           ? NTTK_CONS_IMPROVED
           : kConsumers;
 };
