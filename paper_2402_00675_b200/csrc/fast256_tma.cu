@@ -37,6 +37,14 @@ using namespace tma;
 // (0.872 -> 0.862); the u32 forward keeps 8 at 3 CTAs/SM (12: 0.776 -> 0.826).  The other
 // kinds keep 8: most of them use 79-128 registers, where 12 consumers would leave one CTA
 // (12 warps) per SM.
+// forward output through the transpose tile with coalesced stores.  Measured (B200, round
+// 1): u32 Dilithium forward 0.777 -> 0.748 ms (profiles/r02_store_variants.txt); u16 A/B below
+#ifndef NTTK_FWD_CSTORE
+#define NTTK_FWD_CSTORE 1
+#endif
+#ifndef NTTK_FWD_CSTORE16
+#define NTTK_FWD_CSTORE16 0
+#endif
 #ifndef NTTK_CONS_IMPROVED
 #define NTTK_CONS_IMPROVED 12
 #endif
@@ -137,7 +145,14 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP, NTTK_FWD_MIN
         if (j == 0 && poly < nb) bulk_s2g(optr, T, 256 * sizeof(IO));
       }
 #else
-      if (poly < nb) store_contiguous<IO>(optr, j, v);
+      if constexpr (NTTK_FWD_CSTORE && sizeof(IO) == 4)
+        store_contiguous_coalesced(reinterpret_cast<uint32_t*>(optr), j, v, X,
+                                   scratch + warp * kScratchWords + half * 272, poly < nb);
+      else if constexpr (NTTK_FWD_CSTORE16 && sizeof(IO) == 2)
+        store_contiguous_coalesced16(reinterpret_cast<uint16_t*>(optr), j, v,
+                                     scratch + warp * kScratchWords + half * 272, poly < nb);
+      else if (poly < nb)
+        store_contiguous<IO>(optr, j, v);
 #endif
       poly += pstep;
       optr += ostep;

@@ -674,6 +674,61 @@ __device__ __forceinline__ void store_contiguous(IO* out_poly, int j, const uint
   }
 }
 
+// u32 contiguous ownership -> coalesced stores through the half-warp's transpose tile: 4
+// swizzled 16-byte chunk writes per lane (Xpose::put4), then lane j stores chunks j + 16 k,
+// so each store instruction writes 256 contiguous bytes instead of 16 chunks 64 B apart
+__device__ __forceinline__ void store_contiguous_coalesced(uint32_t* out_poly, int j, const uint32_t (&v)[16],
+                                                           const Xpose& X, const uint32_t* tile,
+                                                           bool valid) {
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+  if (!valid) return;
+  const uint32_t b = smem_addr(tile);
+  uint4* dst = reinterpret_cast<uint4*>(out_poly);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int row = (j >> 2) + 4 * k, ch = (j & 3) ^ ((row >> 1) & 3);
+    uint4 w;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                 : "r"(b + 64u * row + 16u * ch)
+                 : "memory");
+    __stcs(dst + j + 16 * k, w);
+  }
+}
+
+// u16 twin: the lane's two packed chunks (slots 16 j .. 16 j + 15) go to chunk slots
+// q ^ ((j >> 2) & 1), q = 2 j + c (each 16-byte bank group hit twice per instruction), and
+// lane j stores chunks j and j + 16
+__device__ __forceinline__ void store_contiguous_coalesced16(uint16_t* out_poly, int j, const uint32_t (&v)[16],
+                                                             const uint32_t* tile, bool valid) {
+  const uint32_t b = smem_addr(tile);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const uint32_t q = uint32_t(2 * j + c) ^ uint32_t((j >> 2) & 1);
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(b + 16u * q),
+                 "r"(__byte_perm(v[8 * c], v[8 * c + 1], 0x5410)), "r"(__byte_perm(v[8 * c + 2], v[8 * c + 3], 0x5410)),
+                 "r"(__byte_perm(v[8 * c + 4], v[8 * c + 5], 0x5410)), "r"(__byte_perm(v[8 * c + 6], v[8 * c + 7], 0x5410))
+                 : "memory");
+  }
+  __syncwarp();
+  if (!valid) return;
+  uint4* dst = reinterpret_cast<uint4*>(out_poly);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t m = uint32_t(j + 16 * k), q = m ^ ((m >> 3) & 1u);
+    uint4 w;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                 : "r"(b + 16u * q)
+                 : "memory");
+    __stcs(dst + m, w);
+  }
+}
+
 // strided ownership -> coalesced 128-bit stores through the transpose tile
 template <class IO>
 __device__ __forceinline__ void store_strided(IO* out_poly, int j, const uint32_t (&v)[16],
