@@ -215,6 +215,11 @@ __device__ __forceinline__ void load_contiguous_n_swz(uint32_t (&v)[32], uint32_
   }
 }
 
+// forward output through the transpose tile (bit 0: u16, bit 1: u32), A/B switch
+#ifndef NTTK_FASTN_CSTORE
+#define NTTK_FASTN_CSTORE 0x2
+#endif
+
 // contiguous ownership -> global (lane j writes its 32 consecutive coefficients)
 template <class IO>
 __device__ __forceinline__ void store_contiguous_n(IO* out_poly, int j, const uint32_t (&v)[32]) {
@@ -233,16 +238,10 @@ __device__ __forceinline__ void store_contiguous_n(IO* out_poly, int j, const ui
   }
 }
 
-// strided ownership -> natural-order coalesced 128-bit stores through the transpose tile
+// natural-order coalesced 128-bit stores of the transpose tile (lane j: chunks j + G t)
 template <class IO, int G>
-__device__ __forceinline__ void store_strided_n(IO* out_poly, int j, const uint32_t (&v)[32],
-                                                const XposeN<G>& X, bool valid) {
+__device__ __forceinline__ void store_tile_n(IO* out_poly, int j, const XposeN<G>& X) {
   constexpr int N = 32 * G;
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 32; ++k) X.put(k, v[k]);
-  __syncwarp();
-  if (!valid) return;
   uint4* dst = reinterpret_cast<uint4*>(out_poly);
   if constexpr (sizeof(IO) == 2) {  // 8 coefficients per 16-byte vector
 #pragma unroll
@@ -259,6 +258,29 @@ __device__ __forceinline__ void store_strided_n(IO* out_poly, int j, const uint3
       __stcs(dst + q, X.chunk(q));
     }
   }
+}
+
+// strided ownership -> natural-order coalesced 128-bit stores through the transpose tile
+template <class IO, int G>
+__device__ __forceinline__ void store_strided_n(IO* out_poly, int j, const uint32_t (&v)[32],
+                                                const XposeN<G>& X, bool valid) {
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) X.put(k, v[k]);
+  __syncwarp();
+  if (valid) store_tile_n<IO, G>(out_poly, j, X);
+}
+
+// contiguous ownership (forward output) -> the same coalesced stores: 8 conflict-free
+// 16-byte row writes per lane instead of 8 stores whose lanes sit 64 / 128 B apart
+template <class IO, int G>
+__device__ __forceinline__ void store_contiguous_n_coalesced(IO* out_poly, int j, const uint32_t (&v)[32],
+                                                             const XposeN<G>& X, bool valid) {
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+  if (valid) store_tile_n<IO, G>(out_poly, j, X);
 }
 
 // Stage the direction table into shared memory.  The lane-dependent segments (per-block
@@ -488,7 +510,10 @@ __global__ void __launch_bounds__(kThreads)
         v, reinterpret_cast<const IO*>(stages + s * GN::kStageBytes + GN::poly_offset(warp, half)), j);
     release_stage(&empty[s], lane);
     fwd_body_n<K, LOGN, PER_INDEX>(v, tws, A, X, j);
-    if (poly < batch) store_contiguous_n<IO>(out + poly * GN::N, j, v);
+    if constexpr ((NTTK_FASTN_CSTORE >> (sizeof(IO) == 4 ? 1 : 0)) & 1)
+      store_contiguous_n_coalesced<IO, G>(out + poly * GN::N, j, v, X, poly < batch);
+    else if (poly < batch)
+      store_contiguous_n<IO>(out + poly * GN::N, j, v);
   }
 }
 
