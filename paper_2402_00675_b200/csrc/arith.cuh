@@ -348,6 +348,13 @@ struct Harvey {
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
     dif(x, y, w, A);
   }
+  // merge butterfly whose twiddle is 1 (TW1): Y' = X - Y mod 2p, any representative in
+  // [0, 2p) keeps the canonical inverse output bit-exact
+  __device__ static void inv_w1(uint32_t& x, uint32_t& y, const FastArgs& A) {
+    const uint32_t s = x + y + A.zero, t = x + A.two_p - y;
+    x = umin32(s, s - A.two_p);
+    y = umin32(t, t - A.two_p);
+  }
   __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
     inv(x, y, w, off, A);
   }
@@ -404,6 +411,12 @@ struct Scott32 {
   }
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
     fwd(x, y, w, A);
+  }
+  // twiddle 1 (TW1): canonical X - Y mod p without the Shoup product
+  __device__ static void inv_w1(uint32_t& x, uint32_t& y, const FastArgs& A) {
+    const uint32_t s = x + y + A.zero, t = x + A.p - y;
+    x = umin32(s, s - A.p);
+    y = umin32(t, t - A.p);
   }
   __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
     inv(x, y, w, off, A);

@@ -359,6 +359,9 @@ cudaError_t inv_launch(const void* in, void* out, size_t batch, const FastArgs& 
       return inv_launch_canon<K, IO, L, 4>(in, out, batch, A, st);
     }
   }
+  if constexpr (inv_w1_of<K>::value && L == 8) {  // harvey / ntl: TW1 on the eager body
+    if (A.flags & 32) return inv_launch_canon<K, IO, L, 8>(in, out, batch, A, st);
+  }
   return inv_launch_canon<K, IO, L, 0>(in, out, batch, A, st);
 }
 

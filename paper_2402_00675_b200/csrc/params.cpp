@@ -200,7 +200,10 @@ void fill_fast(HostParams& P, int kind) {
     // stays below 2^d p, the bound the lazy / exact-bound checks already assume.
     // N = 512 / 1024 (fastn_tma.cu, full trees): the phase-2 layers are s = 5..2, the same
     // table positions 2^L - 2^s.
-    if (kind == NTTK_IMPROVED && dir == 1 && (A.flags & 8) &&
+    // harvey / ntl (eager merge, N = 256): inv_w1 keeps their [0, 2p) / canonical invariants
+    const bool tw1_kind = (kind == NTTK_IMPROVED && (A.flags & 8)) ||
+                          ((kind == NTTK_HARVEY || kind == NTTK_NTL) && P.N == 256);
+    if (tw1_kind && dir == 1 &&
         ((P.N == 256 && P.layers == 8) || ((P.N == 512 || P.N == 1024) && (1u << P.layers) == P.N))) {
       const unsigned smax = P.N == 256 ? 4 : 5;
       bool ones = P.gs_plain.size() >= (size_t(1) << P.layers) - 4;

@@ -585,7 +585,18 @@ __device__ __forceinline__ void inv_body_lazy(uint32_t (&v)[16], const TWL& twl,
 // run_merge_layers + final N^{-1} (transform.hpp:99-116, 323-335): contiguous in
 // (canonical unless FUSE) -> strided out (canonical).  FUSE: u16 raw input, fused first
 // merge layer (A.flags bit 2, improved n = 16 only).
-template <class K, int L, bool FUSE, class TWL>
+// TW1 (policies with inv_w1: harvey, ntl; A.flags bit 5): phase-2 block-0 merges without
+// a product, as in inv_body_lazy.
+template <class K, class = void>
+struct inv_w1_of {
+  static constexpr bool value = false;
+};
+template <class K>
+struct inv_w1_of<K, std::void_t<decltype(&K::inv_w1)>> {
+  static constexpr bool value = true;
+};
+
+template <class K, int L, bool FUSE, bool TW1 = false, class TWL>
 __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                                const Xpose& X) {
   using Tw = typename K::Tw;
@@ -624,9 +635,13 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
-      if (K::kFold && sl == 1)  // N^{-1} folded into the last merge layer
+      if (K::kFold && sl == 1) {  // N^{-1} folded into the last merge layer
         K::inv_last(v[r], v[r + h], off, A);
-      else
+      } else if constexpr (TW1) {
+        static_assert(inv_w1_of<K>::value && L == 8, "TW1 needs inv_w1 and the 8-layer tree");
+        if ((r >> (5 - sl)) == 0) K::inv_w1(v[r], v[r + h], A);
+        else inv_bf<K>(sl, v[r], v[r + h], K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl))), off, A);
+      } else
         inv_bf<K>(sl, v[r], v[r + h], K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl))), off, A);
     }
   }
@@ -646,7 +661,7 @@ __device__ __forceinline__ void inv_body(uint32_t (&v)[16], const TWL& twl, cons
     inv_body_lazy<K, L, FUSE, TW1, DEFER, PACKED, OSH>(v, twl, A, X);
   } else {
     static_assert(OSH == 0, "partial canonicalisation needs the lazy body");
-    inv_body_eager<K, L, FUSE>(v, twl, A, X);
+    inv_body_eager<K, L, FUSE, TW1>(v, twl, A, X);
   }
 }
 

@@ -669,19 +669,23 @@ def _extreme_words(p, bits, B, seed, N=256):
                                                    (KYBER, 16, 2, NEGA, 7), (DILITHIUM, 32, 4, CYCLIC, 8),
                                                    (DILITHIUM, 32, 4, NEGA, 8), (7681, 32, 4, CYCLIC, 8),
                                                    (12289, 32, 4, CYCLIC, 8)])
-def test_inverse_extreme_words(oracle, p, n, elem, tree, layers):
-    """Worst-case words through the fast inverse (TW1 multiply-free block-0 merges and the
-    u16 DEFER path without input canonicalisation) vs the oracle, bit-exact."""
-    P = engine_params(p, 256, n, [IMPROVED], tree=tree, layers=layers, exact=True)
-    Q = oracle.params(p, 256, n, (IMPROVED,), tree=tree, layers=layers, exact=True)
-    assert IMPROVED in P.fast_path
+@pytest.mark.parametrize("kind", [IMPROVED, HARVEY, NTL])
+def test_inverse_extreme_words(oracle, p, n, elem, tree, layers, kind):
+    """Worst-case words through the fast inverse (TW1 multiply-free block-0 merges for the
+    improved / harvey / ntl kinds, the u16 DEFER path without input canonicalisation, the
+    u32 partial canonicalisation) vs the oracle, bit-exact."""
+    if kind == NTL and tree == NEGA:
+        pytest.skip("ntl is a DIF kind: cyclic tree only")
+    P = engine_params(p, 256, n, [kind], tree=tree, layers=layers, exact=True)
+    Q = oracle.params(p, 256, n, (kind,), tree=tree, layers=layers, exact=True)
+    assert kind in P.fast_path
     w = _extreme_words(p, 8 * elem, 515, 7 + p + layers)
-    got = from_dev(nttk.inverse(P, IMPROVED, to_dev(w, elem)))
-    assert (got == Q.inverse(IMPROVED, w)).all()
+    got = from_dev(nttk.inverse(P, kind, to_dev(w, elem)))
+    assert (got == Q.inverse(kind, w)).all()
     # and the round trip of their forward images
-    f = np.asarray(Q.inverse(IMPROVED, w))
-    y = nttk.forward(P, IMPROVED, to_dev(f, elem))
-    assert (from_dev(nttk.inverse(P, IMPROVED, y)) == f).all()
+    f = np.asarray(Q.inverse(kind, w))
+    y = nttk.forward(P, kind, to_dev(f, elem))
+    assert (from_dev(nttk.inverse(P, kind, y)) == f).all()
 
 
 @pytest.mark.parametrize("N", [512, 1024])
