@@ -92,6 +92,12 @@ int nttk_build_params(const nttk_params_desc* desc, nttk_params_t* out);
 int nttk_preset(const char* name, nttk_params_t* out);
 int nttk_params_destroy(nttk_params_t P);
 int nttk_params_get_info(nttk_params_t P, nttk_params_info* out);
+/* extension (introspection): the host-validated fast-kernel option bits of (kind, dir)
+ * (dir 0 forward, 1 inverse): 1/2 fast canonicalisation (u16 Barrett / u32 shift), 4 fused
+ * u16 first merge layer, 8 lazy merge, 16 forward twiddle-1 blocks, 32 inverse twiddle-1
+ * blocks (TW1), 64 u16 inverse without canonicalisation (DEFER), 128 u32 inverse partial
+ * canonicalisation.  Status 2 if the kind is not built into P. */
+int nttk_params_fast_flags(nttk_params_t P, int kind, int dir, uint32_t* flags);
 /* read back a host table (names: dif_w dif_wq dif_mont ct_plain ct_plantard ct_mont
  * ct_smont gs_plain gs_wq gs_mont gs_plantard gs_smont); returns its length */
 size_t nttk_params_table(nttk_params_t P, const char* name, uint64_t* out, size_t cap);

@@ -368,6 +368,14 @@ int nttk_params_get_info(nttk_params_t h, nttk_params_info* o) {
   return NTTK_OK;
 }
 
+int nttk_params_fast_flags(nttk_params_t h, int kind, int dir, uint32_t* flags) {
+  if (!h || !flags) return fail(NTTK_CONTRACT, "params_fast_flags: null argument");
+  if (dir != 0 && dir != 1) return fail(NTTK_CONTRACT, "params_fast_flags: dir must be 0 or 1");
+  if (int s = check_kind(h->P, kind, "params_fast_flags")) return s;
+  *flags = h->P.fast[kind][dir].flags;
+  return NTTK_OK;
+}
+
 size_t nttk_params_table(nttk_params_t h, const char* name, uint64_t* out, size_t cap) {
   if (!h || !name) return 0;
   const HostParams& P = h->P;

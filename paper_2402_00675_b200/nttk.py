@@ -127,6 +127,7 @@ class _Info(C.Structure):
 
 EXPORTS = (
     "nttk_build_params", "nttk_preset", "nttk_params_destroy", "nttk_params_get_info",
+    "nttk_params_fast_flags",
     "nttk_params_table", "nttk_ntt_forward", "nttk_intt_inverse", "nttk_pointwise_multiply",
     "nttk_basemul", "nttk_polymul", "nttk_ntt_forward_host", "nttk_intt_inverse_host",
     "nttk_roundtrip_host", "nttk_pointwise_multiply_host", "nttk_polymul_host",
@@ -153,6 +154,7 @@ def lib() -> C.CDLL:
         L.nttk_preset.argtypes = [C.c_char_p, C.POINTER(vp)]
         L.nttk_params_destroy.argtypes = [vp]
         L.nttk_params_get_info.argtypes = [vp, C.POINTER(_Info)]
+        L.nttk_params_fast_flags.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_uint32)]
         L.nttk_params_table.restype = sz
         L.nttk_params_table.argtypes = [vp, C.c_char_p, vp, sz]
         for f in ("nttk_ntt_forward", "nttk_intt_inverse"):
@@ -243,6 +245,13 @@ class NttParams:
 
     def has(self, kind) -> bool:
         return ButterflyKind(kind) in self.kinds
+
+    def fast_flags(self, kind, direction: int) -> int:
+        """Host-validated fast-kernel option bits of (kind, direction) -- see
+        nttk_params_fast_flags in include/nttk_gpu.h (introspection, no device needed)."""
+        f = C.c_uint32(0)
+        _check(lib().nttk_params_fast_flags(self.handle, int(kind), int(direction), C.byref(f)))
+        return f.value
 
     def table(self, name: str) -> np.ndarray:
         n = lib().nttk_params_table(self._h, name.encode(), None, 0)

@@ -149,3 +149,43 @@ def test_params_helpers_match_engine_tables(engine):
     assert engine.to_natural_order(engine.Spectrum([0, 1, 2, 3])) == [0, 2, 1, 3]
     with pytest.raises(engine.ContractViolation, match="unknown preset"):
         engine.preset_spec("nope")
+
+
+# ---------------------------------------------------------------------------
+# host validation of the fast-kernel options (params.cpp fill_fast): the bounds that make the
+# inverse shortcuts exact must be checked on the host, per parameter set
+FWD_W1, CANON16, CANON32, FUSE16, LAZY, TW1, DEFER, PARTIAL = 16, 1, 2, 4, 8, 32, 64, 128
+
+
+def test_fast_flags_kyber_dilithium(engine):
+    K = engine.ButterflyKind
+    Pk = engine.build_params(3329, 256, 16, [K.improved, K.harvey, K.ntl], exact_bound=True)
+    fi = Pk.fast_flags(K.improved, 1)
+    assert fi & (FUSE16 | LAZY | TW1 | DEFER) == FUSE16 | LAZY | TW1 | DEFER
+    assert not fi & PARTIAL
+    assert Pk.fast_flags(K.improved, 0) & FWD_W1
+    assert Pk.fast_flags(K.harvey, 1) & TW1 and Pk.fast_flags(K.ntl, 1) & TW1
+    Pd = engine.build_params(8380417, 256, 32, [K.improved], exact_bound=True)
+    fd = Pd.fast_flags(K.improved, 1)
+    # 2^9 p = 4 290 773 504 < 2^32: the doubled bounds of the partial canonicalisation fit
+    assert fd & (CANON32 | LAZY | TW1 | PARTIAL) == CANON32 | LAZY | TW1 | PARTIAL
+    assert not fd & (DEFER | FUSE16)
+
+
+def test_fast_flags_refused_where_bounds_fail(engine):
+    K = engine.ButterflyKind
+    # 2^9 p >= 2^32: no partial canonicalisation (X + Y would overflow 32 bits), TW1 stays
+    P = engine.build_params(8392193, 256, 32, [K.improved], exact_bound=True)
+    f = P.fast_flags(K.improved, 1)
+    assert f & TW1 and not f & PARTIAL
+    # negacyclic / 7-layer trees: no twiddle-1 blocks, no DEFER (8 layers only)
+    Pn = engine.build_params(3329, 256, 16, [K.improved], tree=engine.Tree.negacyclic, layers=7,
+                             exact_bound=True)
+    fn = Pn.fast_flags(K.improved, 1)
+    assert not fn & (TW1 | DEFER)
+    assert not Pn.fast_flags(K.improved, 0) & FWD_W1
+    # N = 1024 full tree: TW1 on the phase-2 layers of fastn_tma.cu
+    P10 = engine.build_params(12289, 1024, 32, [K.improved])
+    assert P10.fast_flags(K.improved, 1) & TW1
+    with pytest.raises(engine.ContractViolation):
+        P10.fast_flags(K.harvey, 1)  # kind not built into these params
