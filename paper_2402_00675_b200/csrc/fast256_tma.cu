@@ -53,14 +53,17 @@ using namespace tma;
 #ifndef NTTK_CONS_FWD16
 #define NTTK_CONS_FWD16 NTTK_CONS_IMPROVED
 #endif
+#ifndef NTTK_CONS_INV32
+#define NTTK_CONS_INV32 16  // measured: 0.836 -> 0.824 ms vs 12 (14: 0.918), profiles/r02_consumer_sweep.txt
+#endif
 template <class K, class IO, int DIR, int L = 8, bool W1 = true>
 struct cons_of {
   static constexpr bool kN16 = std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2;
   static constexpr int value =
-      kN16 && DIR == 0 && L == 8 && W1 ? NTTK_CONS_FWD16
-      : (kN16 && DIR == 1) || (std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1)
-          ? NTTK_CONS_IMPROVED
-          : kConsumers;
+      kN16 && DIR == 0 && L == 8 && W1                                         ? NTTK_CONS_FWD16
+      : kN16 && DIR == 1                                                         ? NTTK_CONS_IMPROVED
+      : std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1 ? NTTK_CONS_INV32
+                                                                               : kConsumers;
 };
 template <class K, class IO, int DIR, int L = 8, bool W1 = true>
 using GeoK = Geo<IO, DIR, cons_of<K, IO, DIR, L, W1>::value>;
