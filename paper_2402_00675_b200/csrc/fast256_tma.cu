@@ -31,12 +31,14 @@ namespace {
 
 using namespace tma;
 
-// Consumer warps per CTA.  Measured (B200, round 1, profiles/r02_consumer_sweep.txt): 12
-// consumers (2 CTAs/SM: 24 consumer warps, 2 producer warps instead of 3) beat 8 for the
-// improved u16 forward (0.994 -> 0.983 ms), u16 inverse (1.123 -> 1.088) and u32 inverse
-// (0.872 -> 0.862); the u32 forward keeps 8 at 3 CTAs/SM (12: 0.776 -> 0.826).  The other
-// kinds keep 8: most of them use 79-128 registers, where 12 consumers would leave one CTA
-// (12 warps) per SM.
+// Consumer warps per CTA (cons_of below).  Measured (B200, round 1,
+// profiles/r02_consumer_sweep.txt, r02_consumer_batch.txt): 12 consumers (2 CTAs/SM: 24
+// consumer warps, 2 producer warps instead of 3) beat 8 for the improved u16 cyclic forward
+// (0.994 -> 0.983 ms); one CTA of 16 consumers per SM beats both for the improved inverses
+// (u16 1.123 -> 1.088 -> 1.026 ms, u32 0.872 -> 0.862 -> 0.824 ms; the u32 tile is then one
+// 256-row tensor box).  The u32 forward keeps 8 at 3 CTAs/SM (12: 0.776 -> 0.826), the
+// 7-layer negacyclic forward keeps 8 at every batch size (4096 polys 5.5 -> 4.2 us), and the
+// other kinds keep 8: most use 79-128 registers, where more consumers leave fewer warps.
 // forward output through the transpose tile with coalesced stores.  Measured (B200, round
 // 1): u32 Dilithium forward 0.777 -> 0.748 ms (profiles/r02_store_variants.txt); u16 A/B below
 #ifndef NTTK_FWD_CSTORE
@@ -45,23 +47,21 @@ using namespace tma;
 #ifndef NTTK_FWD_CSTORE16
 #define NTTK_FWD_CSTORE16 0
 #endif
-#ifndef NTTK_CONS_IMPROVED
-#define NTTK_CONS_IMPROVED 12
+#ifndef NTTK_CONS_FWD16  // improved u16 cyclic W1 forward
+#define NTTK_CONS_FWD16 12
 #endif
-// (W1 = the cyclic forward with twiddle-1 blocks.)  The 7-layer negacyclic forward keeps 8 at
-// every batch size (tools/c1_probe.py: 4096 polys 5.5 -> 4.2 us, 2^21 493 -> 488 us with 8).
-#ifndef NTTK_CONS_FWD16
-#define NTTK_CONS_FWD16 NTTK_CONS_IMPROVED
+#ifndef NTTK_CONS_INV16  // improved u16 inverse: 1.039 -> 1.026 ms vs 12 (20 equal, 24 / 26 slower)
+#define NTTK_CONS_INV16 16
 #endif
-#ifndef NTTK_CONS_INV32
-#define NTTK_CONS_INV32 16  // measured: 0.836 -> 0.824 ms vs 12 (14: 0.918), profiles/r02_consumer_sweep.txt
+#ifndef NTTK_CONS_INV32  // improved u32 inverse: 0.836 -> 0.824 ms vs 12 (14: 0.918)
+#define NTTK_CONS_INV32 16
 #endif
 template <class K, class IO, int DIR, int L = 8, bool W1 = true>
 struct cons_of {
   static constexpr bool kN16 = std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2;
   static constexpr int value =
       kN16 && DIR == 0 && L == 8 && W1                                         ? NTTK_CONS_FWD16
-      : kN16 && DIR == 1                                                         ? NTTK_CONS_IMPROVED
+      : kN16 && DIR == 1                                                         ? NTTK_CONS_INV16
       : std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1 ? NTTK_CONS_INV32
                                                                                : kConsumers;
 };
