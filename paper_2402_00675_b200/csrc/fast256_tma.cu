@@ -50,6 +50,9 @@ using namespace tma;
 #ifndef NTTK_CONS_FWD16  // improved u16 cyclic W1 forward
 #define NTTK_CONS_FWD16 12
 #endif
+#ifndef NTTK_CONS_FWD32  // improved u32 cyclic W1 forward
+#define NTTK_CONS_FWD32 16  // one 94-register CTA per SM: 0.748 -> 0.695 ms (12: 0.743, 20: 0.743)
+#endif
 #ifndef NTTK_CONS_INV16  // improved u16 inverse: 1.039 -> 1.026 ms vs 12 (20 equal, 24 / 26 slower)
 #define NTTK_CONS_INV16 16
 #endif
@@ -61,6 +64,8 @@ struct cons_of {
   static constexpr bool kN16 = std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2;
   static constexpr int value =
       kN16 && DIR == 0 && L == 8 && W1                                         ? NTTK_CONS_FWD16
+      : std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 0 && L == 8 && W1
+          ? NTTK_CONS_FWD32
       : kN16 && DIR == 1                                                         ? NTTK_CONS_INV16
       : std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1 ? NTTK_CONS_INV32
                                                                                : kConsumers;
@@ -72,7 +77,8 @@ using GeoSwzK = GeoSwz<IO, DIR, cons_of<K, IO, DIR>::value>;
 
 // ---------------------------------------------------------------------------
 template <class K, class IO, int L, bool PER_INDEX, bool W1>
-__global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP, NTTK_FWD_MINB(IO))
+__global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
+                                  GeoK<K, IO, 0, L, W1>::kC >= 16 ? 1 : NTTK_FWD_MINB(IO))
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
   using G = GeoK<K, IO, 0, L, W1>;
