@@ -53,6 +53,9 @@ using namespace tma;
 #ifndef NTTK_CONS_FWD32  // improved u32 cyclic W1 forward
 #define NTTK_CONS_FWD32 16  // one 94-register CTA per SM: 0.748 -> 0.695 ms (12: 0.743, 20: 0.743)
 #endif
+#ifndef NTTK_CONS_FWD32_ALL  // the u32 forward geometry for every kind and tree
+#define NTTK_CONS_FWD32_ALL 0
+#endif
 #ifndef NTTK_CONS_INV16  // improved u16 inverse: 1.039 -> 1.026 ms vs 12 (20 equal, 24 / 26 slower)
 #define NTTK_CONS_INV16 16
 #endif
@@ -64,7 +67,7 @@ struct cons_of {
   static constexpr bool kN16 = std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2;
   static constexpr int value =
       kN16 && DIR == 0 && L == 8 && W1                                         ? NTTK_CONS_FWD16
-      : std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 0 && L == 8 && W1
+      : sizeof(IO) == 4 && DIR == 0 && (NTTK_CONS_FWD32_ALL || (std::is_same<K, ImprovedN32>::value && L == 8 && W1))
           ? NTTK_CONS_FWD32
       : kN16 && DIR == 1                                                         ? NTTK_CONS_INV16
       : std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1 ? NTTK_CONS_INV32
