@@ -27,19 +27,27 @@ namespace {
 
 using namespace tma;
 
-// consumer warps per CTA of the fused polymul (shadows tma::kConsumers here; A/B switch)
-#ifndef NTTK_PM_CONS
-#define NTTK_PM_CONS 8
+// Consumer warps per CTA of the fused polymul, per storage width (shadow tma::kConsumers in
+// this file).  Measured (B200, config 2, tools/polymul_probe.py): one CTA of 16 consumers
+// per SM for u16 lifts improved 1.07 -> 1.12, harvey 0.68 -> 0.71, smont 0.73 -> 0.78 G
+// products/s; u32 keeps 8 (16 would cap its registers at 60 and spill).
+#ifndef NTTK_PM_CONS16
+#define NTTK_PM_CONS16 16
 #endif
-constexpr int kConsumers = NTTK_PM_CONS;
-constexpr int kThreads = (kConsumers + 1) * 32;
-constexpr int kTile = 2 * kConsumers;
+#ifndef NTTK_PM_CONS32
+#define NTTK_PM_CONS32 8
+#endif
+template <class IO>
+constexpr int pm_cons() {
+  return sizeof(IO) == 2 ? NTTK_PM_CONS16 : NTTK_PM_CONS32;
+}
 
 // stage = a-tile and b-tile, each two halves of 8 polynomials (one bulk copy per half)
 template <class IO>
 struct Geo2 {
   static constexpr int kPolyBytes = 256 * int(sizeof(IO));
   static constexpr int kPad = sizeof(IO) == 2 ? 32 : 64;
+  static constexpr int kConsumers = pm_cons<IO>();
   static constexpr int kHalfBytes = kConsumers * kPolyBytes;
   static constexpr int kTileBytes = 2 * kHalfBytes + kPad + 64;
   static constexpr int kStages = sizeof(IO) == 2 ? 3 : 2;
@@ -55,6 +63,7 @@ template <class IO>
 __device__ __forceinline__ void produce2(const IO* a, const IO* b, size_t batch, uint8_t* stages,
                                          uint64_t* full, uint64_t* empty) {
   using G = Geo2<IO>;
+  constexpr int kConsumers = G::kConsumers, kTile = 2 * kConsumers;
   const size_t ntiles = (batch + kTile - 1) / kTile;
   int k = 0;
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
@@ -94,8 +103,8 @@ template <bool C>
 struct pm_n16<Harvey<16, C>> : std::true_type {};
 template <>
 struct pm_n16<Smont<16>> : std::true_type {};
-#ifndef NTTK_PM_MINB16  // 3 CTAs/SM where the 72-register cap does not spill
-#define NTTK_PM_MINB16 3
+#ifndef NTTK_PM_MINB16  // u16, n = 16, 7 layers: 1 with 16 consumers (3 with 8: 72 registers)
+#define NTTK_PM_MINB16 (NTTK_PM_CONS16 >= 16 ? 1 : 3)
 #endif
 #ifndef NTTK_PM_MINB
 #define NTTK_PM_MINB(K, IO, L) (sizeof(IO) == 2 && L == 7 && pm_n16<K>::value ? NTTK_PM_MINB16 : sizeof(IO) == 4 ? 2 : 1)
@@ -107,10 +116,11 @@ struct PmTw {
 };
 
 template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
-__global__ void __launch_bounds__(kThreads, NTTK_PM_MINB(K, IO, L))
+__global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, NTTK_PM_MINB(K, IO, L))
     polymul256_tma_kernel(const IO* __restrict__ a, const IO* __restrict__ b, IO* __restrict__ out,
                           size_t batch, const __grid_constant__ PolymulArgs PA) {
   using G = Geo2<IO>;
+  constexpr int kConsumers = G::kConsumers, kTile = 2 * kConsumers;
   using Enc = typename K::Enc;
   using Tw = typename K::Tw;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -210,6 +220,7 @@ cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, con
   static OccCache occ;
   auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY, W1>;
   constexpr int smem = Geo2<IO>::kSmem + ((NTTK_PM_TWS & 3) ? 480 * int(sizeof(typename K::Tw)) : 0);
+  constexpr int kThreads = (Geo2<IO>::kConsumers + 1) * 32, kTile = 2 * Geo2<IO>::kConsumers;
   const int g_sms2 = sm_count_current();
   const int o = occupancy_current(kern, kThreads, smem, occ);
   const size_t tiles = (batch + kTile - 1) / kTile;
