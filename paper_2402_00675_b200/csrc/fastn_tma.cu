@@ -29,8 +29,12 @@ namespace {
 
 using namespace tma;
 
-template <int LOGN, class IO>
+// C = consumer warps per CTA (the forward may use more than the inverse, whose swizzled
+// tensor box of kTileN polynomials is limited to 256 rows)
+template <int LOGN, class IO, int C = kConsumers>
 struct GeoN {
+  static constexpr int kConsumers = C;
+  static constexpr int kThreadsN = (C + 1) * 32;
   static constexpr int N = 1 << LOGN;
   static constexpr int G = N / 32;                  // lanes per polynomial
   static constexpr int PPW = 32 / G;                // polynomials per warp (2 or 1)
@@ -119,10 +123,11 @@ __device__ __forceinline__ Tw tw_smem(const uint2* tws, int idx) {
   return mk_tw<Tw>(tws[idx]);
 }
 
-template <int LOGN, class IO>
+template <int LOGN, class IO, int C = kConsumers>
 __device__ __forceinline__ void produce_n(const IO* in, size_t batch, uint8_t* stages, uint64_t* full,
                                           uint64_t* empty) {
-  using GN = GeoN<LOGN, IO>;
+  using GN = GeoN<LOGN, IO, C>;
+  constexpr int kConsumers = C;
   const size_t ntiles = (batch + GN::kTileN - 1) / GN::kTileN;
   int k = 0;
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
@@ -477,11 +482,16 @@ __device__ __forceinline__ void stage_table(uint2* tws, const uint32_t* tab) {
   }
 }
 
+#ifndef NTTK_FASTN_FWD_CONS  // consumer warps of the N = 512 / 1024 forward (A/B switch)
+#define NTTK_FASTN_FWD_CONS 16  // falcon512 improved -3 %, falcon1024 harvey -12 %, improved +0.7 % (profiles/r02_fastn_store.txt)
+#endif
+
 template <class K, class IO, int LOGN, bool PER_INDEX>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(GeoN<LOGN, IO, NTTK_FASTN_FWD_CONS>::kThreadsN)
     fwdn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                     const uint32_t* __restrict__ tab, const __grid_constant__ FastArgs A) {
-  using GN = GeoN<LOGN, IO>;
+  using GN = GeoN<LOGN, IO, NTTK_FASTN_FWD_CONS>;
+  constexpr int kConsumers = GN::kConsumers;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + GN::kStages * GN::kStageBytes);
@@ -489,10 +499,10 @@ __global__ void __launch_bounds__(kThreads)
   uint64_t* full = reinterpret_cast<uint64_t*>(tws + GN::N);
   uint64_t* empty = full + GN::kStages;
   stage_table<LOGN, !PER_INDEX, false>(tws, tab);
-  init_barriers(full, empty, GN::kStages);  // __syncthreads: table visible
+  init_barriers(full, empty, GN::kStages, kConsumers);  // __syncthreads: table visible
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kConsumers) {
-    if (lane == 0) produce_n<LOGN, IO>(in, batch, stages, full, empty);
+    if (lane == 0) produce_n<LOGN, IO, kConsumers>(in, batch, stages, full, empty);
     return;
   }
   constexpr int G = GN::G;
@@ -578,19 +588,19 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <class Kern>
-int grid_n(Kern kern, int smem, OccCache& occ, size_t tiles) {
-  const size_t full = size_t(sm_count_current()) * occupancy_current(kern, kThreads, smem, occ);
+int grid_n(Kern kern, int smem, OccCache& occ, size_t tiles, int threads = kThreads) {
+  const size_t full = size_t(sm_count_current()) * occupancy_current(kern, threads, smem, occ);
   return static_cast<int>(tiles < full ? tiles : full);
 }
 
 template <class K, class IO, int LOGN, bool PER_INDEX>
 cudaError_t fwd_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
                   cudaStream_t st) {
-  using GN = GeoN<LOGN, IO>;
+  using GN = GeoN<LOGN, IO, NTTK_FASTN_FWD_CONS>;
   static OccCache occ;
   auto kern = fwdn_tma_kernel<K, IO, LOGN, PER_INDEX>;
-  const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN);
-  kern<<<blocks, kThreads, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,
+  const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN, GN::kThreadsN);
+  kern<<<blocks, GN::kThreadsN, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,
                                             tab, A);
   return cudaGetLastError();
 }
