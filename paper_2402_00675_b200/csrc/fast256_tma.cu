@@ -56,6 +56,9 @@ using namespace tma;
 #ifndef NTTK_CONS_FWD32_ALL  // the u32 forward geometry for every kind and tree
 #define NTTK_CONS_FWD32_ALL 0
 #endif
+#ifndef NTTK_CONS_INV_ALL  // the wide inverse geometry for every kind (A/B switch)
+#define NTTK_CONS_INV_ALL 1  // comparison kinds gain 2-11 % (profiles/r02_consumer_sweep.txt)
+#endif
 #ifndef NTTK_CONS_INV16  // improved u16 inverse: 1.039 -> 1.026 ms vs 12 (20 equal, 24 / 26 slower)
 #define NTTK_CONS_INV16 16
 #endif
@@ -69,8 +72,9 @@ struct cons_of {
       kN16 && DIR == 0 && L == 8 && W1                                         ? NTTK_CONS_FWD16
       : sizeof(IO) == 4 && DIR == 0 && (NTTK_CONS_FWD32_ALL || (std::is_same<K, ImprovedN32>::value && L == 8 && W1))
           ? NTTK_CONS_FWD32
-      : kN16 && DIR == 1                                                         ? NTTK_CONS_INV16
-      : std::is_same<K, ImprovedN32>::value && sizeof(IO) == 4 && DIR == 1 ? NTTK_CONS_INV32
+      : (kN16 || (NTTK_CONS_INV_ALL && sizeof(IO) == 2)) && DIR == 1            ? NTTK_CONS_INV16
+      : (std::is_same<K, ImprovedN32>::value || NTTK_CONS_INV_ALL) && sizeof(IO) == 4 && DIR == 1
+          ? NTTK_CONS_INV32
                                                                                : kConsumers;
 };
 template <class K, class IO, int DIR, int L = 8, bool W1 = true>
