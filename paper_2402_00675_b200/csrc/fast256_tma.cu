@@ -56,6 +56,9 @@ using namespace tma;
 #ifndef NTTK_CONS_FWD32_ALL  // the u32 forward geometry for every kind and tree
 #define NTTK_CONS_FWD32_ALL 0
 #endif
+#ifndef NTTK_CONS_FWD16_ALL  // the u16 forward geometry for every kind's 8-layer tree (A/B)
+#define NTTK_CONS_FWD16_ALL 0
+#endif
 #ifndef NTTK_CONS_INV_ALL  // the wide inverse geometry for every kind (A/B switch)
 #define NTTK_CONS_INV_ALL 1  // comparison kinds gain 2-11 % (profiles/r02_consumer_sweep.txt)
 #endif
@@ -69,7 +72,8 @@ template <class K, class IO, int DIR, int L = 8, bool W1 = true>
 struct cons_of {
   static constexpr bool kN16 = std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2;
   static constexpr int value =
-      kN16 && DIR == 0 && L == 8 && W1                                         ? NTTK_CONS_FWD16
+      ((kN16 && W1) || (NTTK_CONS_FWD16_ALL && sizeof(IO) == 2 && !kN16)) && DIR == 0 && L == 8
+          ? NTTK_CONS_FWD16
       : sizeof(IO) == 4 && DIR == 0 && (NTTK_CONS_FWD32_ALL || (std::is_same<K, ImprovedN32>::value && L == 8 && W1))
           ? NTTK_CONS_FWD32
       : (kN16 || (NTTK_CONS_INV_ALL && sizeof(IO) == 2)) && DIR == 1            ? NTTK_CONS_INV16
