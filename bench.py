@@ -391,30 +391,32 @@ def run_extras(dev):
         t2[name] = row
         del xp, sp, op
     ex["table2_presets_2^16"] = t2
-    # config 5: reduction sweep, 2^30 operand pairs (2^15 x 2^15 grid) per (q, variant);
-    # IMAD roof = SM-cycles per mult of the variant's multiplies (IMAD 1/64, IMAD.HI and
-    # IMAD.WIDE 1/32 per lane-op, measured)
+    # config 5: reduction sweep, 2^30 operand pairs (2^15 x 2^15 grid) per (q, variant) from
+    # tests/golden/sweep_inputs.py; every checksum must equal the unmodified reference's over
+    # the same full grid (tests/golden/sweep_2p30.json) or the bench line fails.  "mults" are
+    # grid pairs: the row operand's premultiplication (a mu, a k, a p^-1) is done once per
+    # row, so each pair costs the reduction's remaining multiplies (IMAD 1/64, IMAD.HI and
+    # IMAD.WIDE 1/32 SM-cycles per lane-op, measured)
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from sweep_inputs import CONFIGS, NAMES, grid
+
+    with open(os.path.join(ROOT, "tests", "golden", "sweep_2p30.json")) as fh:
+        ref_sums = {(r["q"], r["variant"]): r["checksum"] for r in json.load(fh)["rows"]}
     cost = {(16, 0): 3 / 64, (16, 1): 3 / 64, (16, 2): 2 / 64, (16, 3): 2 / 64,
             (32, 0): 5 / 64, (32, 1): 5 / 64, (32, 2): 5 / 64, (32, 3): 5 / 64}
-    names = ["mont_redc", "signed_mont_redc", "plantard_redc", "modified_plantard_mul"]
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    c5 = {}
-    for q, n, ell in ((KYBER_Q, 16, 2), (DIL_Q, 32, 7)):
+    c5 = {"grid": "2^15 rows x 2^15 columns per (q, reduction), tests/golden/sweep_inputs.py",
+          "validated": "checksum == the reference's checked reductions over the full grid "
+                       "(tests/golden/sweep_2p30.json)"}
+    for q, n, ell in CONFIGS:
         for v in range(4):
-            if v == 1:
-                A = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
-                Bv = torch.randint(-(1 << (n - 1)), 1 << (n - 1), (1 << 15,), generator=g, device=dev,
-                                   dtype=torch.int64)
-            elif v == 2:
-                A = torch.randint(0, q + 1, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
-                Bv = torch.randint(0, q + 1, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
-            elif v == 3:
-                A = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
-                Bv = torch.randint(0, q << ell, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
-            else:
-                A = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
-                Bv = torch.randint(0, q, (1 << 15,), generator=g, device=dev, dtype=torch.int64)
-            want = nttk.modmul_sweep(v, q, n, ell, A, Bv)  # synchronous form: the checksum
+            Ah, Bh = grid(q, n, ell, v)
+            A, Bv = torch.from_numpy(Ah).to(dev), torch.from_numpy(Bh).to(dev)
+            got = "%016x" % nttk.modmul_sweep(v, q, n, ell, A, Bv)  # synchronous form
+            if got != ref_sums[(q, v)]:
+                raise RuntimeError(f"config5 sweep checksum {got} != reference {ref_sums[(q, v)]} "
+                                   f"(variant {NAMES[v]}, q {q})")
+            want = int(got, 16)
             cs = torch.zeros(1, dtype=torch.int64, device=dev)
             for _ in range(3):  # warm-up (module load, occupancy query, clocks)
                 nttk.modmul_sweep_device(v, q, n, ell, A, Bv, cs)
@@ -429,11 +431,11 @@ def run_extras(dev):
             torch.cuda.synchronize()
             sec = e0.elapsed_time(e1) / 1e3 / reps
             if (int(cs.item()) & (2**64 - 1)) != (want * reps) & (2**64 - 1):
-                raise RuntimeError(f"config5 sweep checksum mismatch (variant {v}, q {q})")
+                raise RuntimeError(f"config5 timed sweep checksum mismatch (variant {v}, q {q})")
             rate = (1 << 30) / sec
             roof = n_sm * 1965e6 / cost[(n, v)]
-            c5[f"q{q}_{names[v]}"] = {"mults_per_s": rate, "imad_roof_mults_per_s": roof,
-                                      "frac": rate / roof}
+            c5[f"q{q}_{NAMES[v]}"] = {"grid_pairs_per_s": rate, "imad_roof_pairs_per_s": roof,
+                                      "frac": rate / roof, "checksum": got}
     ex["config5_sweep_2^30"] = c5
     return ex
 

@@ -321,6 +321,8 @@ class Reference:
             L.ref_run_all_suites.argtypes = [C.c_uint64, C.c_char_p, C.c_size_t,
                                              C.POINTER(C.c_uint64)]
             L.ref_observed.argtypes = [C.c_void_p, C.c_int, C.c_int, u64p, u64p, u64p]
+            L.ref_tree_run.argtypes = [C.c_uint64, C.c_uint32, C.c_uint, C.c_int, C.c_uint32,
+                                       C.c_int, C.c_int, u64p, C.c_void_p, C.c_size_t]
             if hasattr(L, "ref_run_bench"):
                 L.ref_run_bench.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int,
                                             C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
@@ -368,6 +370,28 @@ class Reference:
         out = np.empty(count, dtype=np.uint64)
         self.lib.ref_rng_fill(seed, bound, out, count)
         return out
+
+    def tree(self, p, N, n_bits, tree, layers, kind, direction, a, b=None):
+        """Extension trees on the reference's unmodified cores (ref_shim.cpp
+        ref_tree_run): direction 0 forward, 1 inverse, 2 polymul (fwd a, fwd b, basemul, inv).
+        Signed (smont) words come back as two's complement uint64."""
+        a = np.array(a, dtype=np.int64).astype(np.uint64).reshape(-1, N).copy()
+        bp = None
+        if b is not None:
+            b = np.ascontiguousarray(np.array(b, dtype=np.int64).astype(np.uint64).reshape(-1, N))
+            bp = b.ctypes.data
+        self._check(self.lib.ref_tree_run(p, N, n_bits, tree, layers, kind, direction, a, bp,
+                                          a.shape[0]))
+        return a
+
+    def sweep_checksum(self, variant, p, n, ell, A, B) -> int:
+        """Wrapping u64 sum of the reference's checked reduction over the grid A x B,
+        without materialising the results (ctypes drops the GIL: threads may split A)."""
+        A = np.ascontiguousarray(A, dtype=np.int64)
+        B = np.ascontiguousarray(B, dtype=np.int64)
+        s = C.c_uint64()
+        self._check(self.lib.ref_sweep(variant, p, n, ell, A, A.size, B, B.size, None, C.byref(s)))
+        return s.value
 
     def sweep(self, variant, p, n, ell, A, B):
         A = np.ascontiguousarray(A, dtype=np.int64)

@@ -307,6 +307,220 @@ int ref_observed(void* hv, int kind, int dir, const uint64_t* in, uint64_t* stat
   });
 }
 
+// ---- extension trees driven by the reference's UNMODIFIED cores ----
+// The reference has no negacyclic / 7-layer driver, basemul or signed-Montgomery transform.
+// These drivers reproduce the split/merge loop shape of run_split_layers / run_merge_layers
+// (transform.hpp:77-116) on the a22 schedule -- layer s, block b uses zeta^{br_L(2^{s-1}+b)}
+// (negacyclic) or omega^{(N >> s) br_{s-1}(b)} (cyclic, params.hpp:60-88) -- and compute
+// every product with the reference's own functions:
+//   improved  improved_ct_core / improved_gs_core (butterfly.hpp:224-243) on twiddles
+//             encoded by to_plantard_domain (reduction.hpp:279-283), final scale by
+//             modified_plantard_core with the encoded 2^{-L} (transform.hpp:323-330 pattern)
+//   harvey    the Montgomery product of harvey_core (butterfly.hpp:92-106, its Y output with
+//             X = Y, Y = 2p, i.e. t = Y) on to_montgomery_domain twiddles; the CT-form sums
+//             (X + t, X + 2p - t) mod 2p are the extension's own
+//   smont     signed_mont_redc (reduction.hpp:141-165, checked entry) on centered
+//             Montgomery twiddles; the GS sum uses the extension's signed Barrett
+// Words of the forward transform are the reference-run words the GPU kernels must equal;
+// the inverse and basemul outputs are canonical.
+namespace tree {
+
+enum { kNtl = 0, kHarvey = 1, kScott = 2, kImproved = 3, kSmont = 4 };
+
+struct Sched {
+  ReductionContext ctx;
+  uint32_t N = 0, L = 0;
+  int nega = 0;
+  uint64_t root = 0, order = 0, scale = 0;  // scale = N^{-1} (cyclic) or 2^{-L} (nega)
+  std::vector<uint64_t> ct, gs;             // plain twiddles, driver order (layer, block)
+};
+
+Sched make(uint64_t p, uint32_t N, unsigned n_bits, int nega, uint32_t L) {
+  Sched S;
+  S.ctx = make_reduction_context(p, n_bits);
+  S.N = N;
+  S.L = L;
+  S.nega = nega;
+  S.order = nega ? (uint64_t(2) << L) : N;
+  S.root = find_primitive_root(p, static_cast<uint32_t>(S.order));
+  for (unsigned s = 1; s <= L; ++s)
+    for (uint64_t b = 0; b < (uint64_t(1) << (s - 1)); ++b) {
+      const uint64_t e = nega ? bit_reverse((uint64_t(1) << (s - 1)) + b, L) % S.order
+                              : (uint64_t(N >> s) * bit_reverse(b, s - 1)) % S.order;
+      S.ct.push_back(pow_mod(S.root, e, p));
+    }
+  for (unsigned s = L; s >= 1; --s)
+    for (uint64_t b = 0; b < (uint64_t(1) << (s - 1)); ++b) {
+      const uint64_t e = nega ? bit_reverse((uint64_t(1) << (s - 1)) + b, L) % S.order
+                              : (uint64_t(N >> s) * bit_reverse(b, s - 1)) % S.order;
+      S.gs.push_back(pow_mod(S.root, e == 0 ? 0 : S.order - e, p));
+    }
+  S.scale = static_cast<uint64_t>(mod_inverse((nega ? (uint64_t(1) << L) : N) % p, p));
+  return S;
+}
+
+int64_t signed_twiddle(uint64_t w, const ReductionContext& c) {  // centered w 2^n mod p
+  const uint64_t m = to_montgomery_domain(w, c);
+  return m > c.p / 2 ? int64_t(m) - int64_t(c.p) : int64_t(m);
+}
+
+int64_t signed_barrett(int64_t a, const ReductionContext& c) {  // extension, S = n + 10
+  const unsigned S = c.n_bits + 10;
+  const int64_t V = static_cast<int64_t>(((u128(1) << S) + (c.p >> 1)) / c.p);
+  const int64_t q = static_cast<int64_t>((i128(a) * V + (i128(1) << (S - 1))) >> S);
+  return a - q * int64_t(c.p);
+}
+
+uint64_t harvey_mul(uint64_t t, uint64_t w_mont, const ReductionContext& c) {
+  return harvey_core(t, 2 * uint64_t(c.p), w_mont, c.p_inv_beta, c.p, c.n_bits, c.beta_mask).y;
+}
+
+void forward(const Sched& S, int kind, uint64_t* a) {
+  const auto& c = S.ctx;
+  const uint64_t p = c.p;
+  size_t cursor = 0;
+  for (unsigned s = 1; s <= S.L; ++s) {
+    const uint32_t len = S.N >> s, blocks = 1u << (s - 1);
+    for (uint32_t b = 0; b < blocks; ++b) {
+      const uint64_t w = S.ct[cursor + b];
+      const uint64_t w_hat = kind == kImproved ? to_plantard_domain(w, c) : 0;
+      const uint64_t w_mont = kind == kHarvey ? to_montgomery_domain(w, c) : 0;
+      const int64_t w_s = kind == kSmont ? signed_twiddle(w, c) : 0;
+      for (uint32_t j = 0; j < len; ++j) {
+        uint64_t& X = a[size_t(b) * 2 * len + j];
+        uint64_t& Y = a[size_t(b) * 2 * len + j + len];
+        if (kind == kImproved) {
+          const auto o = improved_ct_core<uint64_t>(X, Y, w_hat, c.mu, p, c.n_bits, c.r2n_mask);
+          X = o.x, Y = o.y;
+        } else if (kind == kHarvey) {
+          const uint64_t r = harvey_mul(Y, w_mont, c);
+          uint64_t u = X + r, v = X + 2 * p - r;
+          if (u >= 2 * p) u -= 2 * p;
+          if (v >= 2 * p) v -= 2 * p;
+          X = u, Y = v;
+        } else {
+          const int64_t t = signed_mont_redc(w_s * int64_t(Y), c);
+          const int64_t x = int64_t(X);
+          X = uint64_t(x + t), Y = uint64_t(x - t);
+        }
+      }
+    }
+    cursor += blocks;
+  }
+}
+
+void inverse(const Sched& S, int kind, uint64_t* a) {
+  const auto& c = S.ctx;
+  const uint64_t p = c.p;
+  for (uint32_t i = 0; i < S.N; ++i) {  // canonicalize (transform.hpp:243)
+    if (kind == kSmont) {
+      const int64_t v = int64_t(a[i]) % int64_t(p);
+      a[i] = uint64_t(v < 0 ? v + int64_t(p) : v);
+    } else {
+      a[i] %= p;
+    }
+  }
+  size_t cursor = 0;
+  unsigned m = 0;
+  for (unsigned s = S.L; s >= 1; --s) {
+    ++m;
+    const uint32_t len = S.N >> s, blocks = 1u << (s - 1);
+    for (uint32_t b = 0; b < blocks; ++b) {
+      const uint64_t w = S.gs[cursor + b];
+      const uint64_t w_hat = kind == kImproved ? to_plantard_domain(w, c) : 0;
+      const uint64_t w_mont = kind == kHarvey ? to_montgomery_domain(w, c) : 0;
+      const int64_t w_s = kind == kSmont ? signed_twiddle(w, c) : 0;
+      for (uint32_t j = 0; j < len; ++j) {
+        uint64_t& X = a[size_t(b) * 2 * len + j];
+        uint64_t& Y = a[size_t(b) * 2 * len + j + len];
+        if (kind == kImproved) {
+          const auto o = improved_gs_core<uint64_t>(X, Y, p << (m - 1), w_hat, c.mu, p, c.n_bits,
+                                                    c.r2n_mask);
+          X = o.x, Y = o.y;
+        } else if (kind == kHarvey) {
+          const auto o = harvey_core(X, Y, w_mont, c.p_inv_beta, p, c.n_bits, c.beta_mask);
+          X = o.x, Y = o.y;
+        } else {
+          const int64_t x = int64_t(X), y = int64_t(Y);
+          X = uint64_t(signed_barrett(x + y, c));
+          Y = uint64_t(signed_mont_redc(w_s * (x - y), c));
+        }
+      }
+    }
+    cursor += blocks;
+  }
+  const uint64_t s_hat = kind == kImproved ? to_plantard_domain(S.scale, c) : 0;
+  const int64_t s_s = kind == kSmont ? signed_twiddle(S.scale, c) : 0;
+  for (uint32_t i = 0; i < S.N; ++i) {
+    if (kind == kImproved) {
+      a[i] = modified_plantard_core<uint64_t>(s_hat, a[i], c.mu, p, c.n_bits, c.r2n_mask);
+    } else if (kind == kSmont) {
+      const int64_t v = signed_mont_redc(s_s * int64_t(a[i]), c);
+      a[i] = uint64_t(v < 0 ? v + int64_t(p) : v);
+    } else {
+      a[i] = static_cast<uint64_t>(u128(a[i] % p) * S.scale % p);
+    }
+  }
+}
+
+// canonical product of canonical a, b: modified_plantard_core(to_plantard_domain(a), b)
+uint64_t mulc(uint64_t a, uint64_t b, const ReductionContext& c) {
+  return modified_plantard_core<uint64_t>(to_plantard_domain(a, c), b, c.mu, c.p, c.n_bits,
+                                          c.r2n_mask);
+}
+
+// degree-2 basemul mod (x^2 - gamma), gamma = +-(last-layer twiddle), canonical output
+void basemul(const Sched& S, int kind, const uint64_t* l, const uint64_t* r, uint64_t* o) {
+  const auto& c = S.ctx;
+  const uint64_t p = c.p;
+  auto canon = [&](uint64_t v) {
+    if (kind == kSmont) {
+      const int64_t s = int64_t(v) % int64_t(p);
+      return uint64_t(s < 0 ? s + int64_t(p) : s);
+    }
+    return v % p;
+  };
+  const size_t last = (size_t(1) << (S.L - 1)) - 1;
+  for (uint32_t k = 0; k < S.N / 2; ++k) {
+    const uint64_t z = S.ct[last + k / 2];
+    const uint64_t g = (k & 1) ? (p - z) % p : z;
+    const uint64_t a0 = canon(l[2 * k]), a1 = canon(l[2 * k + 1]);
+    const uint64_t b0 = canon(r[2 * k]), b1 = canon(r[2 * k + 1]);
+    o[2 * k] = (mulc(a0, b0, c) + mulc(mulc(a1, b1, c), g, c)) % p;
+    o[2 * k + 1] = (mulc(a0, b1, c) + mulc(a1, b0, c)) % p;
+  }
+}
+
+}  // namespace tree
+
+// dir 0 forward, 1 inverse, 2 polymul (forward a, forward b, basemul, inverse; `b` used)
+int ref_tree_run(uint64_t p, uint32_t N, unsigned n_bits, int nega, uint32_t layers, int kind,
+                 int dir, uint64_t* a, const uint64_t* b, size_t batch) {
+  return guarded([&] {
+    NTTK_REQUIRE(kind == tree::kImproved || kind == tree::kHarvey || kind == tree::kSmont,
+                 "ref_tree_run: kind must be improved, harvey or smont");
+    NTTK_REQUIRE(layers >= 1 && (N >> layers) >= 1, "ref_tree_run: bad layer count");
+    const tree::Sched S = tree::make(p, N, n_bits, nega, layers);
+    std::vector<uint64_t> fb(N), prod(N);
+    for (size_t i = 0; i < batch; ++i) {
+      uint64_t* x = a + i * N;
+      if (dir == 0) {
+        tree::forward(S, kind, x);
+      } else if (dir == 1) {
+        tree::inverse(S, kind, x);
+      } else {
+        NTTK_REQUIRE((N >> layers) == 2, "ref_tree_run: polymul needs degree-2 leaves");
+        std::memcpy(fb.data(), b + i * N, N * 8);
+        tree::forward(S, kind, x);
+        tree::forward(S, kind, fb.data());
+        tree::basemul(S, kind, x, fb.data(), prod.data());
+        tree::inverse(S, kind, prod.data());
+        std::memcpy(x, prod.data(), N * 8);
+      }
+    }
+  });
+}
+
 // The reference's own property suites (verify.hpp:576-584 run_all_suites): writes one line
 // "name cases failures" per suite into out; returns the total failure count in *failures.
 int ref_run_all_suites(uint64_t random_cases, char* out, size_t cap, uint64_t* failures) {

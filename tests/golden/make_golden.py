@@ -83,6 +83,43 @@ for p, N, n, kinds, seed in ((7681, 256, 32, (NTL, HARVEY, SCOTT, IMPROVED), 313
                      "conv_first": [int(v) for v in cv[0][:16]]})
 out["products"] = prod
 
+# extension trees: the reference's unmodified cores driven on the
+# negacyclic / 7-layer schedules (oracle/ref_shim.cpp ref_tree_run) -- the Kyber 7-layer
+# forward, degree-2 basemul polymul, the Dilithium 8-layer negacyclic tree and the
+# signed-Montgomery transform, at the storage words the GPU keeps (u16 Kyber, u32 Dilithium)
+from oracle.oracle import CYCLIC, NEGA, SMONT  # noqa: E402
+
+trees = []
+TREES = [
+    # (label, p, N, n, tree, layers, polys, seed)
+    ("kyber_nega7_n16", 3329, 256, 16, NEGA, 7, 16, 4242),
+    ("kyber_nega7_n32", 3329, 256, 32, NEGA, 7, 8, 4243),
+    ("dilithium_nega8_n32", 8380417, 256, 32, NEGA, 8, 16, 4244),
+    ("kyber_cyclic8_n16", 3329, 256, 16, CYCLIC, 8, 8, 4245),
+    ("dilithium_cyclic8_n32", 8380417, 256, 32, CYCLIC, 8, 8, 4246),
+]
+for label, p, N, n, tree, L, polys, seed in TREES:
+    f = ref.rng(seed, p, polys * N).reshape(polys, N)
+    g = ref.rng(seed + 1, 1 << 15, polys * N).reshape(polys, N)  # arbitrary inverse input
+    h = ref.rng(seed + 2, p, polys * N).reshape(polys, N)
+    for kind in ((IMPROVED, HARVEY, SMONT) if tree == NEGA else (SMONT,)):
+        fwd = ref.tree(p, N, n, tree, L, kind, 0, f)
+        inv = ref.tree(p, N, n, tree, L, kind, 1, fwd)
+        assert (inv == f).all(), (label, kind)
+        gi = g.astype(np.int64) - (1 << 14) if kind == SMONT else g  # signed words for smont
+        inv_g = ref.tree(p, N, n, tree, L, kind, 1, gi)
+        row = {"label": label, "p": p, "N": N, "n_bits": n, "tree": tree, "layers": L,
+               "kind": kind, "polys": polys, "seed": seed,
+               "fwd_fnv": fnv(fwd), "inv_g_fnv": fnv(inv_g),
+               "fwd_poly0": [int(np.int64(v)) if kind == SMONT else int(v) for v in fwd[0]],
+               "inv_g_poly0": [int(v) for v in inv_g[0]]}
+        if (N >> L) == 2:
+            pm = ref.tree(p, N, n, tree, L, kind, 2, f, h)
+            row["polymul_fnv"] = fnv(pm)
+            row["polymul_poly0"] = [int(v) for v in pm[0]]
+        trees.append(row)
+out["trees"] = trees
+
 # reductions over operand grids incl. boundary values (reduction.hpp:125-273)
 def grid(p, n, variant, ell):
     rng_a = ref.rng(777 + variant, 1 << 62, 64)

@@ -93,6 +93,35 @@ def test_golden_products(oracle, golden):
         assert fnv(oracle, host) == c["conv_fnv"]
 
 
+def test_golden_trees(oracle, golden):
+    """Extension trees (Kyber 7-layer negacyclic, basemul polymul, Dilithium
+    negacyclic, signed Montgomery) against reference-run words (tests/golden: the
+    reference's unmodified cores on the a22 schedule), at every storage width that holds
+    the kind's words: fast u16/u32 kernels, the fused polymul, the u64 generic kernel."""
+    for c in golden["trees"]:
+        p, N, n, kind, L, tree = c["p"], c["N"], c["n_bits"], c["kind"], c["layers"], c["tree"]
+        sg = kind == SMONT
+        P = engine_params(p, N, n, [kind], tree=tree, layers=L, exact=True)
+        f = oracle.rng(c["seed"], p, c["polys"] * N).reshape(c["polys"], N)
+        g = oracle.rng(c["seed"] + 1, 1 << 15, c["polys"] * N).reshape(c["polys"], N)
+        if sg:
+            g = g.astype(np.int64) - (1 << 14)
+        h = oracle.rng(c["seed"] + 2, p, c["polys"] * N).reshape(c["polys"], N)
+        widths = (2, 4, 8) if p < (1 << 15) else (4, 8)
+        for elem in widths:
+            y = nttk.forward(P, kind, to_dev(f, elem, sg))
+            fwd = from_dev(y, sg)
+            assert fnv(oracle, fwd) == c["fwd_fnv"], (c["label"], kind, elem)
+            assert [int(v) for v in fwd[0]] == c["fwd_poly0"], (c["label"], kind, elem)
+            assert (from_dev(nttk.inverse(P, kind, y)) == f).all(), (c["label"], kind, elem)
+            inv_g = from_dev(nttk.inverse(P, kind, to_dev(g, elem, sg)))
+            assert fnv(oracle, inv_g) == c["inv_g_fnv"], (c["label"], kind, elem)
+            if "polymul_fnv" in c:
+                pm = from_dev(nttk.polymul(P, kind, to_dev(f, elem), to_dev(h, elem)))
+                assert fnv(oracle, pm) == c["polymul_fnv"], (c["label"], kind, elem)
+                assert [int(v) for v in pm[0]] == c["polymul_poly0"], (c["label"], kind, elem)
+
+
 def test_golden_reductions(golden):
     for c in golden["reductions"]:
         A = torch.tensor(c["A"], dtype=torch.int64, device="cuda")
@@ -700,3 +729,23 @@ def test_fastn_inverse_extreme_words(oracle, N, n, elem):
     w = _extreme_words(p, 8 * elem if elem < 8 else 40, 131, 3 + N + n, N)
     got = from_dev(nttk.inverse(P, IMPROVED, to_dev(w, elem)))
     assert (got == Q.inverse(IMPROVED, w)).all()
+
+
+def test_sweep_full_grid_vs_reference_checksums():
+    """BASELINE config 5 at its stated size: every 2^15 x 2^15 = 2^30-pair grid of
+    tests/golden/sweep_inputs.py (boundary values first) on the GPU reproduces the checksum
+    of the reference's checked reductions over the same grid (tests/golden/sweep_2p30.json)."""
+    import json
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from sweep_inputs import grid
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sweep_2p30.json")) as fh:
+        rows = json.load(fh)["rows"]
+    for row in rows:
+        A, B = grid(row["q"], row["n_bits"], row["ell"], row["variant"])
+        s = nttk.modmul_sweep(row["variant"], row["q"], row["n_bits"], row["ell"],
+                              torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+        assert "%016x" % s == row["checksum"], row

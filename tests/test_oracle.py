@@ -215,7 +215,50 @@ def test_golden_reductions(oracle, golden):
     assert golden["plantard_fires"] == 0
 
 
-# ---- extension rows (parity unpinned by any reference test): naive evaluation ------
+def test_golden_trees(oracle, golden):
+    """Extension trees pinned to reference-run words: the golden rows come from
+    the reference's unmodified cores driven on the negacyclic / 7-layer schedules
+    (oracle/ref_shim.cpp ref_tree_run); the C restatement must reproduce every word."""
+    assert len(golden["trees"]) >= 11
+    for c in golden["trees"]:
+        p, N, n, kind, L, tree = c["p"], c["N"], c["n_bits"], c["kind"], c["layers"], c["tree"]
+        P = oracle.params(p, N, n, (kind,), tree=tree, layers=L, exact=True)
+        f = oracle.rng(c["seed"], p, c["polys"] * N).reshape(c["polys"], N)
+        fwd = P.forward(kind, f)
+        assert "%016x" % oracle.fnv(fwd) == c["fwd_fnv"], c["label"]
+        got0 = fwd[0].astype(np.int64) if kind == SMONT else fwd[0]
+        assert [int(v) for v in got0] == c["fwd_poly0"], c["label"]
+        g = oracle.rng(c["seed"] + 1, 1 << 15, c["polys"] * N).reshape(c["polys"], N)
+        if kind == SMONT:
+            g = (g.astype(np.int64) - (1 << 14)).astype(np.uint64)
+        assert "%016x" % oracle.fnv(P.inverse(kind, g)) == c["inv_g_fnv"], c["label"]
+        if "polymul_fnv" in c:
+            h = oracle.rng(c["seed"] + 2, p, c["polys"] * N).reshape(c["polys"], N)
+            pm = P.polymul(kind, f, h)
+            assert "%016x" % oracle.fnv(pm) == c["polymul_fnv"], c["label"]
+            assert (pm[0] == oracle.schoolbook_negacyclic(f[0], h[0], p)).all()
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("p,N,n,L", [(3329, 256, 16, 7), (3329, 256, 32, 7), (8380417, 256, 32, 8),
+                                     (12289, 1024, 32, 9), (17, 8, 16, 2)])
+def test_live_trees_against_reference_cores(oracle, p, N, n, L):
+    """Live cross-check of the restated extension trees against the reference's own cores
+    on fresh seeds (forward words, inverse of arbitrary words, polymul)."""
+    ref = Reference()
+    for kind in (IMPROVED, HARVEY, SMONT):
+        P = oracle.params(p, N, n, (kind,), tree=NEGA, layers=L, exact=True)
+        f = oracle.rng(9000 + kind, p, 4 * N).reshape(4, N)
+        fwd = P.forward(kind, f)
+        assert (fwd == ref.tree(p, N, n, NEGA, L, kind, 0, f)).all(), (p, kind)
+        g = oracle.rng(9100 + kind, min(1 << 15, 8 * p), 4 * N).reshape(4, N)
+        assert (P.inverse(kind, g) == ref.tree(p, N, n, NEGA, L, kind, 1, g)).all(), (p, kind)
+        if (N >> L) == 2:
+            h = oracle.rng(9200 + kind, p, 4 * N).reshape(4, N)
+            assert (P.polymul(kind, f, h) == ref.tree(p, N, n, NEGA, L, kind, 2, f, h)).all()
+
+
+# ---- extension rows: also checked against naive evaluation ---------------------------
 
 @pytest.mark.parametrize("p,N,n,L,root", [(3329, 256, 16, 7, 0), (8380417, 256, 32, 8, 0),
                                           (3329, 256, 32, 7, 0), (17, 8, 16, 2, 0)])
@@ -270,3 +313,26 @@ def test_reference_self_verification_suites():
             "transform"} <= names
     assert failures == 0, rows
     assert all(c > 0 for _, c, _ in rows)
+
+
+def test_sweep_full_grid_checksums_match_reference(oracle):
+    """BASELINE config 5 at its stated size: the restated reductions over every 2^30-pair
+    grid of tests/golden/sweep_inputs.py reproduce the reference's checksums
+    (tests/golden/sweep_2p30.json, generated by the reference's checked reductions)."""
+    import json
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from sweep_inputs import grid
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sweep_2p30.json")) as fh:
+        rows = json.load(fh)["rows"]
+    assert len(rows) == 8
+    threads = max(1, len(os.sched_getaffinity(0)))
+    for row in rows:
+        A, B = grid(row["q"], row["n_bits"], row["ell"], row["variant"])
+        assert A.size * B.size == row["pairs"] == 1 << 30
+        ctx = oracle.ctx(row["q"], row["n_bits"], 0, row["ell"])
+        _, s = oracle.sweep(row["variant"], ctx, A, B, want_results=False, threads=threads)
+        assert "%016x" % s == row["checksum"], row
