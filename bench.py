@@ -569,7 +569,7 @@ def run_engine_arm(a, rank, world, local_rank):
                          "peak_modmul_per_s": n_sm * sm_hz / cyc[dom],
                          "frac": imad_roof_ms[dom] / per_kernel[dom],
                          "definition": "fmaheavy cycles of the modmul's IMAD/IMAD.HI (measured "
-                                       "rates, profiles/r01_imad_microbench.txt) x modmuls/poly"},
+                                       "rates, profiles/r1a_imad_microbench.txt) x modmuls/poly"},
                 "step_frac_of_roofline": sum(roof_ms) / sum(per_kernel),
                 "per_kernel_ms": dict(zip(names, [round(x, 4) for x in per_kernel])),
                 "per_kernel_roof_ms": dict(zip(names, [round(x, 4) for x in roof_ms])),

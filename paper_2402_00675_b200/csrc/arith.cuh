@@ -13,8 +13,8 @@
 //                               (extension)
 //   Scott32, Ntl<16|32>         Alg. 9 / Alg. 7 (butterfly.hpp:172-184, 60-71)
 //
-// Issue-slot economy (measured on B200, profiles/r01_imad_microbench.txt and
-// r02_bf_microbench*.txt): IMAD runs at 64 lanes/clk/SM on the fmaheavy pipe, IMAD.HI and
+// Issue-slot economy (measured on B200, profiles/r1a_imad_microbench.txt and
+// r1b_bf_microbench*.txt): IMAD runs at 64 lanes/clk/SM on the fmaheavy pipe, IMAD.HI and
 // IMAD.WIDE at half that, the ALU pipe at 64; mixed into a butterfly stream every non-FMA
 // instruction costs about 0.8 cycles on top of the FMA cycles.  So:
 //   * plain additions are written x + y + A.zero (A.zero == 0 at run time, opaque to
@@ -24,7 +24,7 @@
 //     ops, multiply-free twiddle-1 blocks), and the umulhi form is used everywhere by
 //     default (the paper form trades 2 FMA cycles for 2 shifts, measured slower).
 //
-// SASS per Plantard multiply (census: profiles/r02_sass_census.txt):
+// SASS per Plantard multiply (census: profiles/r1b_sass_census.txt):
 //   n=16: IMAD (h = t * w_hat mu) + IMAD.HI (r = hi32(h p))        [umulhi form]
 //         IMAD + SHF + IMAD + SHF (r = (((h >> 16) + 1) p) >> 16)  [paper form]
 //   n=32: IMAD + IMAD.HI (h_hi) + IMAD.HI/IMAD.WIDE (r = hi32(h_hi p + p))
@@ -68,12 +68,7 @@ __device__ __forceinline__ uint32_t mod_cs(uint32_t x, const FastArgs& A) {
 // the preceding IMAD.HI as an addend -- it then re-issues a second IMAD.HI for the other
 // use of the same product, doubling the most expensive instruction.  One ALU op instead.
 __device__ __forceinline__ uint32_t fence_val(uint32_t r, const FastArgs& A) {
-#ifdef NTTK_NO_FENCE
-  (void)A;
-  return r;
-#else
   return r ^ A.zero;
-#endif
 }
 // canonical residue of a two's complement 32-bit value
 __device__ __forceinline__ uint32_t mod_s32(uint32_t x, const FastArgs& A) {
@@ -109,16 +104,14 @@ __device__ __forceinline__ uint32_t mp_n32(uint32_t t, uint32_t lo, uint32_t hi,
 // ---------------------------------------------------------------------------
 // Policies.  Values live in 32-bit registers (signed kinds: two's complement).
 //   fwd(x, y, w)        forward butterfly (CT form unless noted)
-//   fwd_alt(x, y, w)    same result, alternative pipe mix (n = 16 Plantard only)
 //   inv(x, y, w, off)   GS form, off = 2^{layer-1} p
 //   scale(v)            final N^{-1} pass (transform.hpp:323-335), canonical
 //   inv_last(x, y, off) last merge layer with the N^{-1} pass folded in (kFold)
 
-// Form of the X-side product of the last (N^{-1}-folded) merge layer: 1 = paper form
-// (IMAD + 2 shifts, ALU-balanced), 0 = umulhi form (IMAD + IMAD.HI, 2 fewer instructions)
-#ifndef NTTK_LAST_PAPER
-#define NTTK_LAST_PAPER 1
-#endif
+// The X-side product of the last (N^{-1}-folded) merge layer uses the paper form (IMAD + 2
+// shifts, ALU-balanced); the umulhi form there (2 fewer instructions, +16 FMA cycles)
+// measured neutral.
+constexpr bool kLastPaper = true;
 
 template <bool PAPER_FORM = false>
 struct ImprovedN16 {
@@ -129,11 +122,6 @@ struct ImprovedN16 {
   // Alg. 11 (butterfly.hpp:224-230)
   __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
     const uint32_t r = mp_n16<PAPER_FORM>(y, w, A.p);
-    y = x + A.p - r;
-    x = x + r + A.zero;
-  }
-  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
-    const uint32_t r = mp_n16<!PAPER_FORM>(y, w, A.p);
     y = x + A.p - r;
     x = x + r + A.zero;
   }
@@ -153,11 +141,6 @@ struct ImprovedN16 {
     x = x + y + A.zero;
     y = fence_val(mp_n16<PAPER_FORM>(t, w, A.p), A);
   }
-  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
-    const uint32_t t = x + off - y;
-    x = x + y + A.zero;
-    y = mp_n16<!PAPER_FORM>(t, w, A.p);
-  }
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return mp_n16<PAPER_FORM>(v, A.scale_lo, A.p);
   }
@@ -165,7 +148,7 @@ struct ImprovedN16 {
   // result equals scale() applied after the last merge (canonical outputs are unique)
   __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
     const uint32_t t = x + off - y;
-    x = mp_n16<NTTK_LAST_PAPER != 0>(x + y + A.zero, A.scale_lo, A.p);
+    x = mp_n16<kLastPaper>(x + y + A.zero, A.scale_lo, A.p);
     y = mp_n16<PAPER_FORM>(t, A.fold_lo, A.p);
   }
   // ---- lazy merge (inv_body_lazy, umulhi form only) ----
@@ -205,7 +188,7 @@ struct ImprovedN16 {
     uint32_t X;
     const uint32_t S = sum_hh(x, y, X, A);
     const uint32_t t = X + X + off - S + A.zero;
-    x = mp_n16<NTTK_LAST_PAPER != 0>(S, A.scale_lo, A.p);
+    x = mp_n16<kLastPaper>(S, A.scale_lo, A.p);
     y = mp_n16<PAPER_FORM>(t, A.fold_lo, A.p);
   }
   // product stage (fused polymul): x -> (x (-2^{2n}) mod p) mu, then MP(.., y) = x y mod p
@@ -229,9 +212,6 @@ struct ImprovedN32 {
     y = x + A.p - r;
     x = x + r + A.zero;
   }
-  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
-    fwd(x, y, w, A);
-  }
   __device__ static void fwd_w1(uint32_t& x, uint32_t& y, int layer, const FastArgs& A) {
     uint32_t r = y;  // see ImprovedN16::fwd_w1
     if (layer >= 3) r = umin32(r, r - A.two_p);
@@ -243,9 +223,6 @@ struct ImprovedN32 {
     const uint32_t t = x + off - y;
     x = x + y + A.zero;
     y = fence_val(mp_n32(t, w.x, w.y, A.p), A);
-  }
-  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
-    inv(x, y, w, off, A);
   }
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return mp_n32(v, A.scale_lo, A.scale_hi, A.p);
@@ -335,9 +312,6 @@ struct Harvey {
       dif(x, y, w, A);
     }
   }
-  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
-    fwd(x, y, w, A);
-  }
   // harvey_core (butterfly.hpp:92-106): X' = X + Y mod 2p (branchless), Y' lazy
   __device__ static void dif(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
     const uint32_t s = x + y + A.zero;
@@ -354,9 +328,6 @@ struct Harvey {
     const uint32_t s = x + y + A.zero, t = x + A.two_p - y;
     x = umin32(s, s - A.two_p);
     y = umin32(t, t - A.two_p);
-  }
-  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
-    inv(x, y, w, off, A);
   }
   // v in [0, 2p) -> v n^{-1} mod p, canonical (the reference's mul_mod,
   // transform.hpp:331-335; any exact method is bit-identical)
@@ -406,9 +377,6 @@ struct Scott32 {
     x = x + y + A.zero;
     y = scott_mul(t, w, A);
   }
-  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
-    fwd(x, y, w, A);
-  }
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
     fwd(x, y, w, A);
   }
@@ -417,9 +385,6 @@ struct Scott32 {
     const uint32_t s = x + y + A.zero, t = x + A.p - y;
     x = umin32(s, s - A.p);
     y = umin32(t, t - A.p);
-  }
-  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
-    inv(x, y, w, off, A);
   }
   // canonical v n^{-1} mod p (transform.hpp:331-335; any exact method is bit-identical)
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
@@ -460,14 +425,8 @@ struct Ntl {
     x = umin32(s, s - A.p);
     y = shoup_mul<N_BITS>(t, w.x, w.y, A);
   }
-  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
-    fwd(x, y, w, A);
-  }
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
     fwd(x, y, w, A);
-  }
-  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
-    inv(x, y, w, off, A);
   }
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return shoup_mul<N_BITS>(v, A.scale_lo, A.scale_hi, A);
@@ -519,16 +478,10 @@ struct Smont {
     y = static_cast<uint32_t>(static_cast<int32_t>(x) - t);
     x = static_cast<uint32_t>(static_cast<int32_t>(x) + t) + A.zero;
   }
-  __device__ static void fwd_alt(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
-    fwd(x, y, w, A);
-  }
   __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
     const int32_t xs = static_cast<int32_t>(x), ys = static_cast<int32_t>(y);
     x = static_cast<uint32_t>(sbarrett<N_BITS>(xs + ys, A));
     y = static_cast<uint32_t>(smont_mul<N_BITS>(xs - ys, static_cast<int32_t>(w.x), w.y, A));
-  }
-  __device__ static void inv_alt(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
-    inv(x, y, w, off, A);
   }
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     const int32_t r = smont_mul<N_BITS>(static_cast<int32_t>(v), static_cast<int32_t>(A.scale_lo),

@@ -32,54 +32,28 @@ namespace {
 using namespace tma;
 
 // Consumer warps per CTA (cons_of below).  Measured (B200, round 1,
-// profiles/r02_consumer_sweep.txt, r02_consumer_batch.txt): 12 consumers (2 CTAs/SM: 24
+// profiles/r1b_consumer_sweep.txt, r1b_consumer_batch.txt): 12 consumers (2 CTAs/SM: 24
 // consumer warps, 2 producer warps instead of 3) beat 8 for the improved u16 cyclic forward
 // (0.994 -> 0.983 ms); one CTA of 16 consumers per SM beats both for the improved inverses
 // (u16 1.123 -> 1.088 -> 1.026 ms, u32 0.872 -> 0.862 -> 0.824 ms; the u32 tile is then one
 // 256-row tensor box).  The u32 forward keeps 8 at 3 CTAs/SM (12: 0.776 -> 0.826), the
 // 7-layer negacyclic forward keeps 8 at every batch size (4096 polys 5.5 -> 4.2 us), and the
 // other kinds keep 8: most use 79-128 registers, where more consumers leave fewer warps.
-// forward output through the transpose tile with coalesced stores.  Measured (B200, round
-// 1): u32 Dilithium forward 0.777 -> 0.748 ms (profiles/r02_store_variants.txt); u16 A/B below
-#ifndef NTTK_FWD_CSTORE
-#define NTTK_FWD_CSTORE 1
-#endif
-#ifndef NTTK_FWD_CSTORE16
-#define NTTK_FWD_CSTORE16 0
-#endif
-#ifndef NTTK_CONS_FWD16  // improved u16 cyclic W1 forward
-#define NTTK_CONS_FWD16 12
-#endif
-#ifndef NTTK_CONS_FWD32  // improved u32 cyclic W1 forward
-#define NTTK_CONS_FWD32 16  // one 94-register CTA per SM: 0.748 -> 0.695 ms (12: 0.743, 20: 0.743)
-#endif
-#ifndef NTTK_CONS_FWD32_ALL  // the u32 forward geometry for every kind and tree
-#define NTTK_CONS_FWD32_ALL 0
-#endif
-#ifndef NTTK_CONS_FWD16_ALL  // the u16 forward geometry for every kind's 8-layer tree (A/B)
-#define NTTK_CONS_FWD16_ALL 0
-#endif
-#ifndef NTTK_CONS_INV_ALL  // the wide inverse geometry for every kind (A/B switch)
-#define NTTK_CONS_INV_ALL 1  // comparison kinds gain 2-11 % (profiles/r02_consumer_sweep.txt)
-#endif
-#ifndef NTTK_CONS_INV16  // improved u16 inverse: 1.039 -> 1.026 ms vs 12 (20 equal, 24 / 26 slower)
-#define NTTK_CONS_INV16 16
-#endif
-#ifndef NTTK_CONS_INV32  // improved u32 inverse: 0.836 -> 0.824 ms vs 12 (14: 0.918)
-#define NTTK_CONS_INV32 16
-#endif
+// The u32 forward writes its output through the transpose tile with coalesced stores
+// (Dilithium forward 0.777 -> 0.748 ms, profiles/r1b_store_variants.txt); the compute-bound
+// u16 forward stores straight from registers (its coalesced twin measured 0.982 -> 0.999 ms).
+// Consumer counts: 12 for the improved u16 cyclic W1 forward, 16 (one 94-register CTA per
+// SM: 0.748 -> 0.695 ms; 12 or 20: 0.743) for the improved u32 cyclic W1 forward, 16 for
+// every inverse (improved u16 1.039 -> 1.026 ms vs 12, 20 equal, 24 / 26 slower; u32 0.836
+// -> 0.824 ms vs 12, 14: 0.918; the comparison kinds gain 2-11 %), 8 otherwise.
 template <class K, class IO, int DIR, int L = 8, bool W1 = true>
 struct cons_of {
   static constexpr bool kN16 = std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 2;
   static constexpr int value =
-      ((kN16 && W1) || (NTTK_CONS_FWD16_ALL && sizeof(IO) == 2 && !kN16)) && DIR == 0 && L == 8
-          ? NTTK_CONS_FWD16
-      : sizeof(IO) == 4 && DIR == 0 && (NTTK_CONS_FWD32_ALL || (std::is_same<K, ImprovedN32>::value && L == 8 && W1))
-          ? NTTK_CONS_FWD32
-      : (kN16 || (NTTK_CONS_INV_ALL && sizeof(IO) == 2)) && DIR == 1            ? NTTK_CONS_INV16
-      : (std::is_same<K, ImprovedN32>::value || NTTK_CONS_INV_ALL) && sizeof(IO) == 4 && DIR == 1
-          ? NTTK_CONS_INV32
-                                                                               : kConsumers;
+      kN16 && W1 && DIR == 0 && L == 8                                                   ? 12
+      : sizeof(IO) == 4 && DIR == 0 && std::is_same<K, ImprovedN32>::value && L == 8 && W1 ? 16
+      : DIR == 1                                                                         ? 16
+                                                                                         : kConsumers;
 };
 template <class K, class IO, int DIR, int L = 8, bool W1 = true>
 using GeoK = Geo<IO, DIR, cons_of<K, IO, DIR, L, W1>::value>;
@@ -89,7 +63,7 @@ using GeoSwzK = GeoSwz<IO, DIR, cons_of<K, IO, DIR>::value>;
 // ---------------------------------------------------------------------------
 template <class K, class IO, int L, bool PER_INDEX, bool W1>
 __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
-                                  GeoK<K, IO, 0, L, W1>::kC >= 16 ? 1 : NTTK_FWD_MINB(IO))
+                                  GeoK<K, IO, 0, L, W1>::kC >= 16 ? 1 : fwd_minb<IO>())
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A) {
   using G = GeoK<K, IO, 0, L, W1>;
@@ -100,17 +74,8 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + kConsumers * kScratchWords);
   uint64_t* empty = full + G::kStages;
   using Tw = typename K::Tw;
-  Tw* tws = reinterpret_cast<Tw*>(smem + G::kSmem);  // lane twiddles (tws_on)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if constexpr (tws_on<IO, 0>()) {
-    if (threadIdx.x < 16) {
-      Tw t[15];
-      fwd_twiddles<K, L, PER_INDEX>(t, A, threadIdx.x);
-#pragma unroll
-      for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
-    }
-  }
-  init_barriers(full, empty, G::kStages, kConsumers);  // __syncthreads: table visible
+  init_barriers(full, empty, G::kStages, kConsumers);
   if (warp == kConsumers) {
     if (lane == 0) produce<IO, 0, kConsumers>(in, batch, stages, full, empty);
     return;
@@ -132,48 +97,12 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
       load_strided<IO, K::kSigned>(
           v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
       release_stage(&empty[s], lane);
-#ifdef NTTK_BULK_STORE
-      if (j == 0) bulk_wait_read();  // previous tile's bulk store has read the tile
-      __syncwarp();
-#endif
-#ifndef NTTK_COPY_ONLY  // A/B: the pipeline alone (loads, stores; no butterflies)
       fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
-#else
-      (void)twl;
-#endif
-#ifdef NTTK_BULK_STORE
-      // A/B: natural-order poly into this half-warp's transpose tile, one 256-coefficient
-      // bulk store (async proxy) instead of per-lane 16-byte stores.  Measured (round 2):
-      // lifts the copy-only u32 pipeline 5.56 -> 5.72 TB/s, but with the butterflies the
-      // extra shared stores and waits make the forward 5-9 % slower -- off by default.
-      {
-        uint32_t* T = scratch + warp * kScratchWords + half * 272;
-        __syncwarp();
-        if constexpr (sizeof(IO) == 4) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            reinterpret_cast<uint4*>(T)[4 * j + c] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-            reinterpret_cast<uint4*>(T)[2 * j + c] =
-                make_uint4(__byte_perm(v[8 * c], v[8 * c + 1], 0x5410), __byte_perm(v[8 * c + 2], v[8 * c + 3], 0x5410),
-                           __byte_perm(v[8 * c + 4], v[8 * c + 5], 0x5410), __byte_perm(v[8 * c + 6], v[8 * c + 7], 0x5410));
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (j == 0 && poly < nb) bulk_s2g(optr, T, 256 * sizeof(IO));
-      }
-#else
-      if constexpr (NTTK_FWD_CSTORE && sizeof(IO) == 4)
+      if constexpr (sizeof(IO) == 4)
         store_contiguous_coalesced(reinterpret_cast<uint32_t*>(optr), j, v, X,
                                    scratch + warp * kScratchWords + half * 272, poly < nb);
-      else if constexpr (NTTK_FWD_CSTORE16 && sizeof(IO) == 2)
-        store_contiguous_coalesced16(reinterpret_cast<uint16_t*>(optr), j, v,
-                                     scratch + warp * kScratchWords + half * 272, poly < nb);
       else if (poly < nb)
         store_contiguous<IO>(optr, j, v);
-#endif
       poly += pstep;
       optr += ostep;
       if (++s == G::kStages) {
@@ -181,23 +110,14 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
         phase ^= 1;
       }
     }
-#ifdef NTTK_BULK_STORE
-    if (j == 0) bulk_wait_all();
-#endif
   };
-  if constexpr (tws_on<IO, 0>()) {
-    run(TwSmem<Tw>{tws + j});
-  } else {
-    Tw twl[15];
-    fwd_twiddles<K, L, PER_INDEX>(twl, A, j);
-    run(twl);
-  }
+  Tw twl[15];
+  fwd_twiddles<K, L, PER_INDEX>(twl, A, j);
+  run(twl);
 }
 
-// u16 DEFER inverse: first merge layer from packed words with dp2a (A/B switch)
-#ifndef NTTK_DEFER_IDP
-#define NTTK_DEFER_IDP 1  // measured: Kyber inverse 1.088 -> 1.040 ms (profiles/r02_idp.txt)
-#endif
+// u16 DEFER inverse: first merge layer from packed words with dp2a (Kyber inverse 1.088 ->
+// 1.040 ms, profiles/r1b_idp.txt)
 
 // ---------------------------------------------------------------------------
 // MODE bits 0-1 -- 0: generic canonicalisation; 1: host-validated fast canonicalisation
@@ -207,7 +127,7 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
 // multiply-free block-0 merges (A.flags bit 5); bit 4: DEFER, no input canonicalisation
 // (A.flags bit 6, u16 improved n=16) -- see inv_body_lazy.
 template <class K, class IO, int L, int MODE>
-__global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, NTTK_MINB(IO))
+__global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
     inv256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                       const __grid_constant__ FastArgs A, const __grid_constant__ CUtensorMap tmap) {
   using G = GeoK<K, IO, 1>;
@@ -222,17 +142,8 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, NTTK_MINB(IO))
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + kConsumers * kScratchWords);
   uint64_t* empty = full + G::kStages;
   using Tw = typename K::Tw;
-  Tw* tws = reinterpret_cast<Tw*>(empty + G::kStages);  // lane twiddles (tws_on)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if constexpr (tws_on<IO, 1>()) {
-    if (threadIdx.x < 16) {
-      Tw t[15];
-      inv_twiddles<K, L>(t, A, threadIdx.x);
-#pragma unroll
-      for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
-    }
-  }
-  init_barriers(full, empty, G::kStages, kConsumers);  // __syncthreads: table visible
+  init_barriers(full, empty, G::kStages, kConsumers);
   if (warp == kConsumers) {
     if (lane == 0) {
       if constexpr (inv_swz<IO>())
@@ -262,7 +173,7 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, NTTK_MINB(IO))
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       mbar_wait(&full[s], phase);
       uint32_t v[16];
-      constexpr bool kPacked = NTTK_DEFER_IDP && (MODE & 16) && sizeof(IO) == 2 && !inv_swz<IO>();
+      constexpr bool kPacked = (MODE & 16) && sizeof(IO) == 2 && !inv_swz<IO>();
       if constexpr (kPacked) {  // raw packed words in v[8..15] (inv_body_lazy PACKED)
         const uint4* src = reinterpret_cast<const uint4*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)) + 2 * j;
         const uint4 a = src[0], b = src[1];
@@ -293,13 +204,9 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, NTTK_MINB(IO))
       }
     }
   };
-  if constexpr (tws_on<IO, 1>()) {
-    run(TwSmem<Tw>{tws + j});
-  } else {
-    Tw twl[15];
-    inv_twiddles<K, L>(twl, A, j);
-    run(twl);
-  }
+  Tw twl[15];
+  inv_twiddles<K, L>(twl, A, j);
+  run(twl);
 }
 
 // ---------------------------------------------------------------------------
@@ -317,7 +224,7 @@ cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs
                          cudaStream_t st) {
   static OccCache occ;
   auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1>;
-  constexpr int smem = GeoK<K, IO, 0, L, W1>::kSmem + (tws_on<IO, 0>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  constexpr int smem = GeoK<K, IO, 0, L, W1>::kSmem;
   using G = GeoK<K, IO, 0, L, W1>;
   const int blocks = grid_for(kern, G::kThreadsP, G::kTileP, smem, occ, batch);
   kern<<<blocks, G::kThreadsP, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
@@ -337,8 +244,7 @@ cudaError_t inv_launch_mode(const void* in, void* out, size_t batch, const FastA
                             cudaStream_t st) {
   static OccCache occ;
   auto kern = inv256_tma_kernel<K, IO, L, MODE>;
-  constexpr int smem = (inv_swz<IO>() ? GeoSwzK<K, IO, 1>::kSmem : GeoK<K, IO, 1>::kSmem) +
-                       (tws_on<IO, 1>() ? 240 * int(sizeof(typename K::Tw)) : 0);
+  constexpr int smem = inv_swz<IO>() ? GeoSwzK<K, IO, 1>::kSmem : GeoK<K, IO, 1>::kSmem;
   CUtensorMap map{};
   if constexpr (inv_swz<IO>()) {
     const cudaError_t e = make_rows128_map(&map, in, uint64_t(batch) * GeoSwzK<K, IO, 1>::kRowsPerPoly,

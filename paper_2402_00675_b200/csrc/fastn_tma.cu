@@ -220,10 +220,8 @@ __device__ __forceinline__ void load_contiguous_n_swz(uint32_t (&v)[32], uint32_
   }
 }
 
-// forward output through the transpose tile (bit 0: u16, bit 1: u32), A/B switch
-#ifndef NTTK_FASTN_CSTORE
-#define NTTK_FASTN_CSTORE 0x2
-#endif
+// The u32 forward writes its output through the transpose tile (coalesced stores, +10-11 %,
+// profiles/r1b_fastn_store.txt); u16 stores straight from registers.
 
 // contiguous ownership -> global (lane j writes its 32 consecutive coefficients)
 template <class IO>
@@ -356,7 +354,7 @@ __device__ __forceinline__ void inv_body_n(uint32_t (&v)[32], const uint2* tws, 
     for (int k = 0; k < 32; ++k) {
       if (k & h) continue;
       const Tw w = tw_smem<Tw>(tws, seg_base<LOGN, true>(s) + (k >> (LOGN - s + 1)) * G + j);
-      inv_bf<K>(s, v[k], v[k + h], w, off, A);
+      K::inv(v[k], v[k + h], w, off, A);
     }
   }
   __syncwarp();
@@ -375,7 +373,7 @@ __device__ __forceinline__ void inv_body_n(uint32_t (&v)[32], const uint2* tws, 
       if (K::kFold && s == 1)
         K::inv_last(v[k], v[k + h], off, A);
       else  // block k >> (6 - s), compact merge order 32 - 2^s + b (constant bank)
-        inv_bf<K>(s, v[k], v[k + h], K::tw(A, 32 - (2 << (s - 1)) + (k >> (6 - s))), off, A);
+        K::inv(v[k], v[k + h], K::tw(A, 32 - (2 << (s - 1)) + (k >> (6 - s))), off, A);
     }
   }
   if (!K::kFold) {
@@ -482,15 +480,15 @@ __device__ __forceinline__ void stage_table(uint2* tws, const uint32_t* tab) {
   }
 }
 
-#ifndef NTTK_FASTN_FWD_CONS  // consumer warps of the N = 512 / 1024 forward (A/B switch)
-#define NTTK_FASTN_FWD_CONS 16  // falcon512 improved -3 %, falcon1024 harvey -12 %, improved +0.7 % (profiles/r02_fastn_store.txt)
-#endif
+// consumer warps of the N = 512 / 1024 forward: 16 (falcon512 improved -3 %, falcon1024
+// harvey -12 %, improved +0.7 % vs 8, profiles/r1b_fastn_store.txt)
+constexpr int kFwdConsN = 16;
 
 template <class K, class IO, int LOGN, bool PER_INDEX>
-__global__ void __launch_bounds__(GeoN<LOGN, IO, NTTK_FASTN_FWD_CONS>::kThreadsN)
+__global__ void __launch_bounds__(GeoN<LOGN, IO, kFwdConsN>::kThreadsN)
     fwdn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                     const uint32_t* __restrict__ tab, const __grid_constant__ FastArgs A) {
-  using GN = GeoN<LOGN, IO, NTTK_FASTN_FWD_CONS>;
+  using GN = GeoN<LOGN, IO, kFwdConsN>;
   constexpr int kConsumers = GN::kConsumers;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
@@ -520,7 +518,7 @@ __global__ void __launch_bounds__(GeoN<LOGN, IO, NTTK_FASTN_FWD_CONS>::kThreadsN
         v, reinterpret_cast<const IO*>(stages + s * GN::kStageBytes + GN::poly_offset(warp, half)), j);
     release_stage(&empty[s], lane);
     fwd_body_n<K, LOGN, PER_INDEX>(v, tws, A, X, j);
-    if constexpr ((NTTK_FASTN_CSTORE >> (sizeof(IO) == 4 ? 1 : 0)) & 1)
+    if constexpr (sizeof(IO) == 4)
       store_contiguous_n_coalesced<IO, G>(out + poly * GN::N, j, v, X, poly < batch);
     else if (poly < batch)
       store_contiguous_n<IO>(out + poly * GN::N, j, v);
@@ -596,7 +594,7 @@ int grid_n(Kern kern, int smem, OccCache& occ, size_t tiles, int threads = kThre
 template <class K, class IO, int LOGN, bool PER_INDEX>
 cudaError_t fwd_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
                   cudaStream_t st) {
-  using GN = GeoN<LOGN, IO, NTTK_FASTN_FWD_CONS>;
+  using GN = GeoN<LOGN, IO, kFwdConsN>;
   static OccCache occ;
   auto kern = fwdn_tma_kernel<K, IO, LOGN, PER_INDEX>;
   const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN, GN::kThreadsN);

@@ -31,15 +31,9 @@ using namespace tma;
 // this file).  Measured (B200, config 2, tools/polymul_probe.py): one CTA of 16 consumers
 // per SM for u16 lifts improved 1.07 -> 1.12, harvey 0.68 -> 0.71, smont 0.73 -> 0.78 G
 // products/s; u32 keeps 8 (16 would cap its registers at 60 and spill).
-#ifndef NTTK_PM_CONS16
-#define NTTK_PM_CONS16 16
-#endif
-#ifndef NTTK_PM_CONS32
-#define NTTK_PM_CONS32 8
-#endif
 template <class IO>
 constexpr int pm_cons() {
-  return sizeof(IO) == 2 ? NTTK_PM_CONS16 : NTTK_PM_CONS32;
+  return sizeof(IO) == 2 ? 16 : 8;
 }
 
 // stage = a-tile and b-tile, each two halves of 8 polynomials (one bulk copy per half)
@@ -85,38 +79,18 @@ __device__ __forceinline__ void produce2(const IO* a, const IO* b, size_t batch,
   }
 }
 
-// Lane twiddles of the forward (bit 0) / inverse (bit 1) transform read from shared
-// memory (TwSmem) instead of 15 pinned registers each, and the register cap that buys
-// (minimum CTAs per SM, u16 storage, n = 16 kinds, 7 layers).  Measured (B200, config 2, tools/polymul_probe.py):
-// both tables in shared memory at 3 CTAs/SM (96 -> 72 registers, no spills) lifts improved
-// 1.05 -> 1.07, harvey 0.666 -> 0.680, smont 0.695 -> 0.726 G products/s; 3 CTAs with the
-// tables in registers spills (0.99 G).  u32 storage keeps the allocator's choice (its
-// stages admit 2 CTAs/SM).
-#ifndef NTTK_PM_TWS
-#define NTTK_PM_TWS 0x3
-#endif
-template <class K>
-struct pm_n16 : std::false_type {};
-template <bool F>
-struct pm_n16<ImprovedN16<F>> : std::true_type {};
-template <bool C>
-struct pm_n16<Harvey<16, C>> : std::true_type {};
-template <>
-struct pm_n16<Smont<16>> : std::true_type {};
-#ifndef NTTK_PM_MINB16  // u16, n = 16, 7 layers: 1 with 16 consumers (3 with 8: 72 registers)
-#define NTTK_PM_MINB16 (NTTK_PM_CONS16 >= 16 ? 1 : 3)
-#endif
-#ifndef NTTK_PM_MINB
-#define NTTK_PM_MINB(K, IO, L) (sizeof(IO) == 2 && L == 7 && pm_n16<K>::value ? NTTK_PM_MINB16 : sizeof(IO) == 4 ? 2 : 1)
-#endif
-
-template <class K, int DIR>
-struct PmTw {
-  static constexpr bool kSmem = (NTTK_PM_TWS >> DIR) & 1;
-};
+// Lane twiddles of both directions are read from shared memory (TwSmem) instead of 15
+// pinned registers each.  Measured (B200, config 2, tools/polymul_probe.py): both tables in
+// shared memory (96 -> 72 registers, no spills) lifts improved 1.05 -> 1.07, harvey 0.666 ->
+// 0.680, smont 0.695 -> 0.726 G products/s; with the tables in registers a register cap
+// spills (0.99 G).  u32 storage caps registers for 2 CTAs per SM (its stages admit 2).
+template <class IO>
+constexpr int pm_minb() {
+  return sizeof(IO) == 4 ? 2 : 1;
+}
 
 template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
-__global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, NTTK_PM_MINB(K, IO, L))
+__global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, pm_minb<IO>())
     polymul256_tma_kernel(const IO* __restrict__ a, const IO* __restrict__ b, IO* __restrict__ out,
                           size_t batch, const __grid_constant__ PolymulArgs PA) {
   using G = Geo2<IO>;
@@ -128,22 +102,16 @@ __global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, NTTK_PM_MINB(K, IO, 
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + G::kStages * G::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch + kConsumers * kScratchWords);
   uint64_t* empty = full + G::kStages;
-  Tw* tws = reinterpret_cast<Tw*>(empty + G::kStages);  // [2][240] lane twiddles (PmTw)
+  Tw* tws = reinterpret_cast<Tw*>(empty + G::kStages);  // [2][240] lane twiddles
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if constexpr (PmTw<K, 0>::kSmem || PmTw<K, 1>::kSmem) {
-    if (threadIdx.x < 16) {
-      Tw t[15];
-      if constexpr (PmTw<K, 0>::kSmem) {
-        fwd_twiddles<K, L, PER_INDEX>(t, PA.fwd, threadIdx.x);
+  if (threadIdx.x < 16) {
+    Tw t[15];
+    fwd_twiddles<K, L, PER_INDEX>(t, PA.fwd, threadIdx.x);
 #pragma unroll
-        for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
-      }
-      if constexpr (PmTw<K, 1>::kSmem) {
-        inv_twiddles<K, L>(t, PA.inv, threadIdx.x);
+    for (int i = 0; i < 15; ++i) tws[16 * i + threadIdx.x] = t[i];
+    inv_twiddles<K, L>(t, PA.inv, threadIdx.x);
 #pragma unroll
-        for (int i = 0; i < 15; ++i) tws[240 + 16 * i + threadIdx.x] = t[i];
-      }
-    }
+    for (int i = 0; i < 15; ++i) tws[240 + 16 * i + threadIdx.x] = t[i];
   }
   init_barriers(full, empty, G::kStages, kConsumers);  // __syncthreads: tables visible
   if (warp == kConsumers) {
@@ -156,14 +124,7 @@ __global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, NTTK_PM_MINB(K, IO, 
   uint32_t* S = scratch + warp * kScratchWords + half * 272;
   Xpose X;
   X.init(S, j);
-  using TwF = std::conditional_t<PmTw<K, 0>::kSmem, TwSmem<Tw>, Tw[15]>;
-  using TwI = std::conditional_t<PmTw<K, 1>::kSmem, TwSmem<Tw>, Tw[15]>;
-  TwF twf;
-  TwI twi;
-  if constexpr (PmTw<K, 0>::kSmem) twf = TwSmem<Tw>{tws + j};
-  else fwd_twiddles<K, L, PER_INDEX>(twf, AF, j);
-  if constexpr (PmTw<K, 1>::kSmem) twi = TwSmem<Tw>{tws + 240 + j};
-  else inv_twiddles<K, L>(twi, AI, j);
+  const TwSmem<Tw> twf{tws + j}, twi{tws + 240 + j};
   // basemul moduli of this lane's 8 pairs (k = 8 j + q)
   Enc gam[8];
   if (PA.prod.basemul) {
@@ -219,7 +180,7 @@ cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, con
                       cudaStream_t st) {
   static OccCache occ;
   auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY, W1>;
-  constexpr int smem = Geo2<IO>::kSmem + ((NTTK_PM_TWS & 3) ? 480 * int(sizeof(typename K::Tw)) : 0);
+  constexpr int smem = Geo2<IO>::kSmem + 480 * int(sizeof(typename K::Tw));
   constexpr int kThreads = (Geo2<IO>::kConsumers + 1) * 32, kTile = 2 * Geo2<IO>::kConsumers;
   const int g_sms2 = sm_count_current();
   const int o = occupancy_current(kern, kThreads, smem, occ);

@@ -19,15 +19,9 @@
 namespace nttk_b200 {
 namespace {
 
-#ifndef NTTK_SWEEP_COLS
-#define NTTK_SWEEP_COLS 16
-#endif
-#ifndef NTTK_SWEEP_ROWS
-#define NTTK_SWEEP_ROWS 256
-#endif
-constexpr int kCols = NTTK_SWEEP_COLS;   // columns per thread
+constexpr int kCols = 16;                // columns per thread
 constexpr int kThreads = 256;            // threads per block -> 4096 columns per block
-constexpr int kRows = NTTK_SWEEP_ROWS;   // rows staged per chunk
+constexpr int kRows = 256;               // rows staged per chunk
 static_assert(kCols % 8 == 0 && kRows * kCols <= 16384, "sweep tile shape");
 
 struct SweepArgs {

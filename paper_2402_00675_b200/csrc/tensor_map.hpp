@@ -5,7 +5,7 @@
 // tile of rows with CU_TENSOR_MAP_SWIZZLE_128B: 16-byte chunk c of row r lands at chunk
 // c ^ (r & 7) of its 128-byte shared-memory row, so the lanes' contiguous-ownership reads
 // (lane j reads its own 32..128-byte segment) hit distinct banks -- the linear bulk copy
-// left them 2-way (u16) / 4-way (u32) conflicted (profiles/r02_ncu_full: 16 wavefronts per
+// left them 2-way (u16) / 4-way (u32) conflicted (profiles/r1b_ncu_full: 16 wavefronts per
 // LDS.128 against an ideal 4).
 #pragma once
 

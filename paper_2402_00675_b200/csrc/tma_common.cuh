@@ -14,10 +14,7 @@
 namespace nttk_b200 {
 namespace tma {
 
-#ifndef NTTK_CONSUMERS
-#define NTTK_CONSUMERS 8
-#endif
-constexpr int kConsumers = NTTK_CONSUMERS;     // consumer warps per CTA
+constexpr int kConsumers = 8;                 // default consumer warps per CTA
 constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr int kTile = 2 * kConsumers;          // polynomials per stage
 constexpr int kScratchWords = 2 * 272;         // per-warp transpose scratch (u32)
@@ -30,25 +27,11 @@ constexpr int kScratchWords = 2 * 272;         // per-warp transpose scratch (u3
 // per SM can be faster: a TMA -> STG copy peaks at 48-64 KiB per SM (tools/copy_probe.cu:
 // 6.59 TB/s at 1 CTA x 3 stages vs 6.16 at 3 CTAs x 3 stages).  Measured (B200, 3 CTAs/SM):
 // u32 forward 2 stages 0.806 -> 0.776 ms, u16 inverse 2 stages 1.152 -> 1.123 ms; the u16
-// forward keeps 4 (2: +1.5 %), the u32 inverse 3 (profiles/r02_stage_sweep.txt).
-#ifndef NTTK_STAGES16
-#define NTTK_STAGES16 4
-#endif
-#ifndef NTTK_STAGES32
-#define NTTK_STAGES32 3
-#endif
-#ifndef NTTK_FWD_STAGES16
-#define NTTK_FWD_STAGES16 4
-#endif
-#ifndef NTTK_FWD_STAGES32
-#define NTTK_FWD_STAGES32 2
-#endif
-#ifndef NTTK_INV_STAGES16
-#define NTTK_INV_STAGES16 2
-#endif
-#ifndef NTTK_INV_STAGES32
-#define NTTK_INV_STAGES32 3
-#endif
+// forward keeps 4 (2: +1.5 %), the u32 inverse 3 (profiles/r1b_stage_sweep.txt).
+template <int DIR, int BYTES>
+constexpr int stages_of() {
+  return DIR == 0 ? (BYTES == 2 ? 4 : 2) : DIR == 1 ? (BYTES == 2 ? 2 : 3) : (BYTES == 2 ? 4 : 3);
+}
 // C = consumer warps per CTA (fast256_tma.cu picks it per kernel, see cons_of there)
 template <class IO, int DIR = 2, int C = kConsumers>
 struct Geo {
@@ -58,9 +41,7 @@ struct Geo {
   static constexpr int kPolyBytes = 256 * int(sizeof(IO));
   static constexpr int kPad = sizeof(IO) == 2 ? 32 : 64;
   static constexpr int kHalfBytes = kC * kPolyBytes;
-  static constexpr int kStages = DIR == 0   ? (sizeof(IO) == 2 ? NTTK_FWD_STAGES16 : NTTK_FWD_STAGES32)
-                                 : DIR == 1 ? (sizeof(IO) == 2 ? NTTK_INV_STAGES16 : NTTK_INV_STAGES32)
-                                            : (sizeof(IO) == 2 ? NTTK_STAGES16 : NTTK_STAGES32);
+  static constexpr int kStages = stages_of<DIR, int(sizeof(IO))>();
   static constexpr int kStageBytes = 2 * kHalfBytes + kPad + 64;  // keep stages 128B-aligned
   static constexpr int kSmem = kStages * kStageBytes + kC * kScratchWords * 4 + 2 * kStages * 8;
   // byte offset of the polynomial of warp w, half h inside a stage
@@ -69,14 +50,12 @@ struct Geo {
   }
 };
 
-// Inverse kernels: the stage is one TMA tensor box of kTile polynomials (128-byte rows,
-// SWIZZLE_128B, tensor_map.hpp) instead of two padded linear bulk copies.  A/B switch.
-#ifndef NTTK_INV_SWZ
-#define NTTK_INV_SWZ 0x2  // bit 0: u16 stages, bit 1: u32 stages (measured: u32 -3.3 %, u16 +0.4 %)
-#endif
+// Inverse kernels on u32 words: the stage is one TMA tensor box of kTile polynomials
+// (128-byte rows, SWIZZLE_128B, tensor_map.hpp) instead of two padded linear bulk copies
+// (measured: u32 -3.3 %; u16 +0.4 %, so u16 keeps the linear copies).
 template <class IO>
 constexpr bool inv_swz() {
-  return (NTTK_INV_SWZ >> (sizeof(IO) == 4 ? 1 : 0)) & 1;
+  return sizeof(IO) == 4;
 }
 
 template <class IO, int DIR = 2, int C = kConsumers>
@@ -161,29 +140,12 @@ __device__ __forceinline__ void produce_rows(const CUtensorMap* map, uint32_t nt
   }
 }
 
-// shared -> global bulk store (bulk-group completion), its commit and the wait that makes
-// the shared source reusable
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(smem_addr(src)), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
 // Hand a consumed stage back to the producer.  The stage was read through the generic
 // proxy (LDS) and will be overwritten by the async proxy (the next bulk copy): the
 // proxy fence orders this warp's reads before the refill (WAR across proxies), the
 // warp barrier collects all lanes, one lane arrives.
 __device__ __forceinline__ void release_stage(uint64_t* empty, int lane) {
-#ifndef NTTK_NO_PROXY_FENCE  // A/B only: without it the refill races the reads (stress test)
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tools/stress_fwd.py
   __syncwarp();
   if (lane == 0) mbar_arrive(empty);
 }
@@ -256,51 +218,26 @@ __device__ __forceinline__ uint32_t canon(uint32_t x, const FastArgs& A) {
   return FAST ? mod_cs(x, A) : mod_u32(x, A);
 }
 
-#ifndef NTTK_ALT_MASK
-#define NTTK_ALT_MASK 0x0  // forward layers (bit s) using the alternative Plantard form
-// (measured: 0x22 balanced FMA/ALU at 378/358 cycles and ran 6% slower than 0x0 at 410/294)
-#endif
-#ifndef NTTK_INV_ALT_MASK
-#define NTTK_INV_ALT_MASK 0x0  // inverse merge layers (bit s) using the alternative form
-#endif
-
-// Minimum CTAs per SM for the register allocator (shared memory admits 4 for u16 and 3
-// for u32 stages).  Measured on B200 (round 2): capping the u32 forward to 3 CTAs (72
-// regs, was 2 CTAs at 92) is 3.5% faster; the same cap on the u32 inverse is 1.7% slower
-// and capping the u16 kernels to 4 CTAs (56 regs) is 2-6% slower.
-#ifndef NTTK_MINB
-#define NTTK_MINB(IO) 1
-#endif
-#ifndef NTTK_FWD_MINB
-#define NTTK_FWD_MINB(IO) (sizeof(IO) == 4 ? 3 : 1)
-#endif
-
-template <class K, class Tw>
-__device__ __forceinline__ void inv_bf(int sl, uint32_t& x, uint32_t& y, Tw w, uint32_t off,
-                                       const FastArgs& A) {
-  if ((NTTK_INV_ALT_MASK >> sl) & 1) K::inv_alt(x, y, w, off, A);
-  else K::inv(x, y, w, off, A);
+// Minimum CTAs per SM for the forward's register allocator (shared memory admits 4 for u16
+// and 3 for u32 stages).  Measured on B200: capping the u32 forward to 3 CTAs (72 regs, was
+// 2 CTAs at 92) is 3.5% faster; the same cap on the u32 inverse is 1.7% slower and capping
+// the u16 kernels to 4 CTAs (56 regs) is 2-6% slower.  Lane twiddles stay in registers:
+// staging them in shared memory (fewer registers, more CTAs) measured slower everywhere
+// (u32 inverse 1.032 -> 1.050 ms at 3 CTAs/SM): these kernels are bound by FMA/ALU pipe
+// scheduling, not by occupancy.
+template <class IO>
+constexpr int fwd_minb() {
+  return sizeof(IO) == 4 ? 3 : 1;
 }
 
-// Lane-dependent twiddles read from shared memory instead of 15 registers per lane
-// (NTTK_TWS_MASK): entry i of lane j at S[16 i + j] -- consecutive lanes, consecutive
-// words, the two half-warps broadcast.  Frees 15 (n = 16) or 30 (n = 32) registers.
+// Lane-dependent twiddles read from shared memory (the fused polymul keeps both directions'
+// tables there): entry i of lane j at S[16 i + j] -- consecutive lanes, consecutive words,
+// the two half-warps broadcast.
 template <class Tw>
 struct TwSmem {
   const Tw* base;  // S + j
   __device__ __forceinline__ Tw operator[](int i) const { return base[16 * i]; }
 };
-
-// Measured (B200, round 2): every combination is slower than registers -- e.g. the u32
-// inverse drops from 96 to 70 registers (2 -> 3 CTAs/SM) yet runs 1.7 % slower (1.032 ->
-// 1.050 ms): these kernels are bound by FMA/ALU pipe scheduling, not by occupancy.
-#ifndef NTTK_TWS_MASK
-#define NTTK_TWS_MASK 0x0  // bit0 fwd u16, bit1 fwd u32, bit2 inv u16, bit3 inv u32
-#endif
-template <class IO, int DIR>
-__host__ __device__ constexpr bool tws_on() {
-  return (NTTK_TWS_MASK >> (2 * DIR + (sizeof(IO) == 4 ? 1 : 0))) & 1;
-}
 
 // producer: stream tiles of kTile polynomials into the stage ring
 template <class IO, int DIR = 2, int C = kConsumers>
@@ -372,12 +309,10 @@ __device__ __forceinline__ void inv_twiddles(typename K::Tw (&twl)[15], const Fa
   }
 }
 
-// Forward layers whose block-0 product is multiply-free (1..4).  Measured (round 2): 2 is
-// best for Kyber (0.996 ms vs 1.014 at 3 or 4 -- the extra min ops and the changed
-// schedule cost more than the 3 saved multiplies); Dilithium is flat within noise.
-#ifndef NTTK_W1_LAYERS
-#define NTTK_W1_LAYERS 2
-#endif
+// Forward layers whose block-0 product is multiply-free (1..4).  Measured: 2 is best for
+// Kyber (0.996 ms vs 1.014 at 3 or 4 -- the extra min ops and the changed schedule cost
+// more than the 3 saved multiplies); Dilithium is flat within noise.
+constexpr int kW1Layers = 2;
 
 // run_split_layers (transform.hpp:77-96): strided in -> contiguous out.
 // W1 (A.flags bit 4, improved kinds on the cyclic tree): block 0 of layers 1..4 has
@@ -395,7 +330,7 @@ __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const TWL& twl, cons
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
       if constexpr (W1 && !PER_INDEX) {
-        if (sl <= NTTK_W1_LAYERS && (r >> (5 - sl)) == 0) {
+        if (sl <= kW1Layers && (r >> (5 - sl)) == 0) {
           K::fwd_w1(v[r], v[r + h], sl, A);
           continue;
         }
@@ -407,8 +342,7 @@ __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const TWL& twl, cons
       } else {
         w = K::tw(A, (1 << (sl - 1)) - 1 + (r >> (5 - sl)));
       }
-      if ((NTTK_ALT_MASK >> sl) & 1) K::fwd_alt(v[r], v[r + h], w, A);
-      else K::fwd(v[r], v[r + h], w, A);
+      K::fwd(v[r], v[r + h], w, A);
     }
   }
   __syncwarp();  // the tile is free (previous readers done)
@@ -431,8 +365,7 @@ __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const TWL& twl, cons
         const int base = sl == 5 ? 0 : sl == 6 ? 1 : sl == 7 ? 3 : 7;
         w = twl[base + (r >> (9 - sl))];
       }
-      if ((NTTK_ALT_MASK >> sl) & 1) K::fwd_alt(v[r], v[r + h], w, A);
-      else K::fwd(v[r], v[r + h], w, A);
+      K::fwd(v[r], v[r + h], w, A);
     }
   }
 }
@@ -619,7 +552,7 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl
           continue;
         }
       }
-      inv_bf<K>(sl, v[r], v[r + h], w, off, A);
+      K::inv(v[r], v[r + h], w, off, A);
     }
   }
   __syncwarp();
@@ -640,9 +573,9 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl
       } else if constexpr (TW1) {
         static_assert(inv_w1_of<K>::value && L == 8, "TW1 needs inv_w1 and the 8-layer tree");
         if ((r >> (5 - sl)) == 0) K::inv_w1(v[r], v[r + h], A);
-        else inv_bf<K>(sl, v[r], v[r + h], K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl))), off, A);
+        else K::inv(v[r], v[r + h], K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl))), off, A);
       } else
-        inv_bf<K>(sl, v[r], v[r + h], K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl))), off, A);
+        K::inv(v[r], v[r + h], K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl))), off, A);
     }
   }
   if (!K::kFold) {
@@ -711,36 +644,6 @@ __device__ __forceinline__ void store_contiguous_coalesced(uint32_t* out_poly, i
                  : "r"(b + 64u * row + 16u * ch)
                  : "memory");
     __stcs(dst + j + 16 * k, w);
-  }
-}
-
-// u16 twin: the lane's two packed chunks (slots 16 j .. 16 j + 15) go to chunk slots
-// q ^ ((j >> 2) & 1), q = 2 j + c (each 16-byte bank group hit twice per instruction), and
-// lane j stores chunks j and j + 16
-__device__ __forceinline__ void store_contiguous_coalesced16(uint16_t* out_poly, int j, const uint32_t (&v)[16],
-                                                             const uint32_t* tile, bool valid) {
-  const uint32_t b = smem_addr(tile);
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const uint32_t q = uint32_t(2 * j + c) ^ uint32_t((j >> 2) & 1);
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(b + 16u * q),
-                 "r"(__byte_perm(v[8 * c], v[8 * c + 1], 0x5410)), "r"(__byte_perm(v[8 * c + 2], v[8 * c + 3], 0x5410)),
-                 "r"(__byte_perm(v[8 * c + 4], v[8 * c + 5], 0x5410)), "r"(__byte_perm(v[8 * c + 6], v[8 * c + 7], 0x5410))
-                 : "memory");
-  }
-  __syncwarp();
-  if (!valid) return;
-  uint4* dst = reinterpret_cast<uint4*>(out_poly);
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const uint32_t m = uint32_t(j + 16 * k), q = m ^ ((m >> 3) & 1u);
-    uint4 w;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-                 : "r"(b + 16u * q)
-                 : "memory");
-    __stcs(dst + m, w);
   }
 }
 
@@ -823,21 +726,6 @@ template <class IO, bool SGN>
 __device__ __forceinline__ void load_contiguous(uint32_t (&v)[16], const IO* poly, int j) {
   const uint4* src = reinterpret_cast<const uint4*>(poly) + j * (16 * int(sizeof(IO)) / 16);
   if constexpr (sizeof(IO) == 2) {
-#ifdef NTTK_U16_SCALAR_LOAD
-    // 16 scalar 16-bit loads instead of 2 vector loads + 16 unpack ops: measured slower
-    // (4-way bank conflicts on the MIO pipe outweigh the ALU saving), kept as an option
-
-    const uint32_t base = smem_addr(poly) + 32u * j;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      uint32_t x;
-      if (SGN)
-        asm volatile("ld.shared.s16 %0, [%1];" : "=r"(x) : "r"(base + 2u * r) : "memory");
-      else
-        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(base + 2u * r) : "memory");
-      v[r] = x;
-    }
-#else
     const uint4 a = src[0], b = src[1];
     const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
@@ -845,7 +733,6 @@ __device__ __forceinline__ void load_contiguous(uint32_t (&v)[16], const IO* pol
       v[2 * e] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] & 0xffffu));
       v[2 * e + 1] = widen<uint16_t, SGN>(static_cast<uint16_t>(w[e] >> 16));
     }
-#endif
   } else {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {

@@ -5,7 +5,7 @@ For every kernel it finds the hottest loop (the backward-branch region with the 
 IMAD-family instructions), counts opcodes there, and derives per-butterfly costs:
 one loop iteration of a fast256 consumer warp transforms 2 polynomials, i.e. 64
 butterflies per thread (8 layers x 8) or 56 (7 layers).  The fmaheavy estimate uses the
-measured issue costs (profiles/r01_imad_microbench.txt): IMAD 2 cycles, IMAD.HI /
+measured issue costs (profiles/r1a_imad_microbench.txt): IMAD 2 cycles, IMAD.HI /
 IMAD.WIDE 4 cycles per warp instruction on one SM sub-partition.
 Usage: python tools/sass_census.py [lib.so] [name-regex] [--ops]   (--ops: opcode breakdown)
 """
