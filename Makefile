@@ -7,7 +7,7 @@ NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC,-Wall --expt-relaxe
 CSRC    := paper_2402_00675_b200/csrc
 LIB     := paper_2402_00675_b200/libnttk_gpu.so
 OBJDIR  := build/obj
-CU      := $(CSRC)/fast256.cu $(CSRC)/fast256_tma.cu $(CSRC)/fastn_tma.cu $(CSRC)/polymul_tma.cu $(CSRC)/generic.cu $(CSRC)/sweep.cu $(CSRC)/reduce.cu
+CU      := $(CSRC)/fast256.cu $(CSRC)/fast256_tma.cu $(CSRC)/fastn_tma.cu $(CSRC)/polymul_tma.cu $(CSRC)/generic.cu $(CSRC)/sweep.cu $(CSRC)/reduce.cu $(CSRC)/product.cu
 CPP     := $(CSRC)/params.cpp $(CSRC)/abi.cpp $(CSRC)/tensor_map.cpp
 HDR     := $(wildcard $(CSRC)/*.hpp $(CSRC)/*.cuh) include/nttk_gpu.h
 OBJS    := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU)) $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CPP))

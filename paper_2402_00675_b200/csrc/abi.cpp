@@ -21,6 +21,7 @@
 #include "fast256.hpp"
 #include "fastn.hpp"
 #include "generic.hpp"
+#include "product.hpp"
 #include "params.hpp"
 #include "reduce.hpp"
 #include "sweep.hpp"
@@ -188,7 +189,9 @@ int run_transform(const HostParams& P, int kind, int dir, const void* in, void* 
 int run_product(const HostParams& P, int kind, const void* l, const void* r, void* out,
                 size_t batch, int elem, cudaStream_t st) {
   cudaError_t e;
-  if ((P.N >> P.layers) == 2) {
+  if (nttk_b200::product_supports(P, kind, elem, l, r, out)) {
+    e = nttk_b200::product_launch(P, kind, l, r, out, batch, elem, st);
+  } else if ((P.N >> P.layers) == 2) {
     std::string err;
     const nttk_b200::DeviceTables* T = P.device_tables(current_device(), err);
     if (!T) return fail(NTTK_CUDA, err);
@@ -255,11 +258,12 @@ int ensure_cap(Workspace& W, size_t bytes) {
 constexpr size_t kChunkBytes = size_t(64) << 20;
 
 // compute(stream, dev bufs[3], chunk polys) issues the kernels for one chunk;
-// inputs land in bufs[0..n_in), outputs are read from out_slot[i]
+// inputs land in bufs[0..n_in), outputs are read from out_slot[i]; input i is checked
+// against `bound` on the device when bit i of check_mask is set
 template <class F>
 int host_pipeline(const HostParams& P, int elem, size_t batch, const std::vector<const void*>& h_in,
                   const std::vector<std::pair<void*, int>>& h_out, F compute, const char* who,
-                  bool check_input_bound, uint64_t bound) {
+                  unsigned check_mask, uint64_t bound) {
   if (int s = need_device(who)) return s;
   Workspace* W = workspace(current_device());
   if (!W) return fail(NTTK_CUDA, std::string(who) + ": workspace setup failed");
@@ -284,7 +288,7 @@ int host_pipeline(const HostParams& P, int elem, size_t batch, const std::vector
       e = cudaMemcpyAsync(W->buf[s][i], static_cast<const char*>(h_in[i]) + done * poly_bytes,
                           n * poly_bytes, cudaMemcpyHostToDevice, st);
       if (e != cudaSuccess) return cuda_fail(e, who);
-      if (check_input_bound) {  // every input (both polymul operands, transform.hpp:372-379)
+      if ((check_mask >> i) & 1) {  // bound-checked inputs (check_mask bit i = input i)
         e = nttk_b200::check_canonical(W->buf[s][i], n * P.N, elem, bound, W->d_flag, st);
         ++g_launches;
         if (e != cudaSuccess) return cuda_fail(e, who);
@@ -527,7 +531,7 @@ int nttk_ntt_forward_host(nttk_params_t h, int kind, const void* h_in, void* h_o
   const int rc = host_pipeline(
       P, elem, batch, {h_in}, {{h_out, 1}},
       [&](cudaStream_t st, void** b, size_t n) { return run_transform(P, kind, 0, b[0], b[1], n, elem, st); },
-      "ntt_forward", true, P.p);
+      "ntt_forward", 1u, P.p);
   if (rc == NTTK_PROPERTY) return fail(NTTK_CONTRACT, "ntt_forward: coefficients must be canonical");
   return rc;
 }
@@ -541,7 +545,7 @@ int nttk_intt_inverse_host(nttk_params_t h, int kind, const void* h_in, void* h_
   return host_pipeline(
       P, elem, batch, {h_in}, {{h_out, 1}},
       [&](cudaStream_t st, void** b, size_t n) { return run_transform(P, kind, 1, b[0], b[1], n, elem, st); },
-      "intt_inverse", false, 0);
+      "intt_inverse", 0u, 0);
 }
 
 int nttk_roundtrip_host(nttk_params_t h, int kind, const void* h_in, void* h_spec, void* h_out,
@@ -557,7 +561,7 @@ int nttk_roundtrip_host(nttk_params_t h, int kind, const void* h_in, void* h_spe
         if (!r) r = run_transform(P, kind, 1, b[1], b[2], n, elem, st);
         return r;
       },
-      "roundtrip", true, P.p);
+      "roundtrip", 1u, P.p);
   if (rc == NTTK_PROPERTY) return fail(NTTK_CONTRACT, "ntt_forward: coefficients must be canonical");
   return rc;
 }
@@ -569,8 +573,9 @@ int nttk_pointwise_multiply_host(nttk_params_t h, int kind, const void* h_l, con
   if (int s = check_kind(P, kind, "pointwise_multiply")) return s;
   if (int s = check_canonical_storage(P, elem, "pointwise_multiply")) return s;
   // the improved product consumes a lazy right operand below 2^ell p
-  // (modified_plantard_mul's contract, reduction.hpp:264-273)
-  const bool chk = kind == NTTK_IMPROVED;
+  // (modified_plantard_mul's contract, reduction.hpp:264-273); the left operand is reduced
+  // mod p first (transform.hpp:362-365), so only the right one (input 0) is bound-checked
+  const unsigned chk = kind == NTTK_IMPROVED ? 1u : 0u;
   const uint64_t bound = uint64_t(P.p) << P.log2N;
   const int rc = host_pipeline(
       P, elem, batch, {h_r, h_l}, {{h_out, 2}},
@@ -594,7 +599,7 @@ int nttk_polymul_host(nttk_params_t h, int kind, const void* h_a, const void* h_
       [&](cudaStream_t st, void** b, size_t n) {
         return run_polymul(P, kind, b[0], b[1], b[2], n, elem, st);
       },
-      "polymul", true, P.p);
+      "polymul", 3u, P.p);
   if (rc == NTTK_PROPERTY) return fail(NTTK_CONTRACT, "ntt_forward: coefficients must be canonical");
   return rc;
 }

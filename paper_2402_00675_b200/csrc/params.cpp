@@ -423,6 +423,9 @@ const uint32_t* HostParams::fastn_table(int device, int kind, int dir, std::stri
     uint32_t* buf = nullptr;
     cudaError_t e = cudaMalloc(&buf, host.size() * 4);
     if (e == cudaSuccess) e = cudaMemcpy(buf, host.data(), host.size() * 4, cudaMemcpyHostToDevice);
+    // a pageable cudaMemcpy may return before the DMA lands, and the kernels that read the
+    // table run on non-blocking streams: wait for the legacy stream that carries the copy
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
     if (e != cudaSuccess) {
       if (buf) cudaFree(buf);
       err = std::string("fastn table upload: ") + cudaGetErrorString(e);
@@ -463,6 +466,7 @@ const DeviceTables* HostParams::device_tables(int device, std::string& err) cons
   uint64_t* base = nullptr;
   cudaError_t e = cudaMalloc(&base, std::max<size_t>(host.size(), 1) * 8);
   if (e == cudaSuccess) e = cudaMemcpy(base, host.data(), host.size() * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);  // see fastn_table
   if (e != cudaSuccess) {
     err = std::string("device table upload: ") + cudaGetErrorString(e);
     if (base) cudaFree(base);

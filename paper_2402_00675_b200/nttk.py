@@ -456,57 +456,79 @@ def _batch_of(t, N: int) -> int:
     return t.numel() // N
 
 
-def forward(P: NttParams, kind, x, out=None, stream=None):
-    """Batched ntt_forward on device tensors (natural -> bit-reversed lazy spectrum)."""
+def _match(ref, t, what: str):
+    """A second operand or a caller-supplied output must be a CUDA tensor shaped like the
+    first operand: same dtype, element count, device and contiguity (the C ABI only sees
+    pointers and the first operand's batch)."""
+    _torch_elem(t)
+    if t.dtype != ref.dtype or t.numel() != ref.numel() or t.device != ref.device:
+        raise ContractViolation(f"{what} must match the first operand (dtype {ref.dtype}, "
+                                f"{ref.numel()} elements, {ref.device}); got {t.dtype}, "
+                                f"{t.numel()} elements, {t.device}")
+    return t
+
+
+def _on_device(x, call):
+    """Run `call` with x's device current: the C ABI resolves tables and launches on the
+    current device."""
     import torch
 
+    idx = x.device.index
+    if idx == torch.cuda.current_device():
+        return call()
+    with torch.cuda.device(idx):
+        return call()
+
+
+def _out(x, out):
+    import torch
+
+    return torch.empty_like(x) if out is None else _match(x, out, "out")
+
+
+def forward(P: NttParams, kind, x, out=None, stream=None):
+    """Batched ntt_forward on device tensors (natural -> bit-reversed lazy spectrum)."""
     e = _torch_elem(x)
-    out = torch.empty_like(x) if out is None else out
-    _check(lib().nttk_ntt_forward(P.handle, int(kind), x.data_ptr(), out.data_ptr(),
-                                  _batch_of(x, P.size), e, _stream_ptr(stream, x)))
+    out = _out(x, out)
+    _on_device(x, lambda: _check(lib().nttk_ntt_forward(
+        P.handle, int(kind), x.data_ptr(), out.data_ptr(), _batch_of(x, P.size), e,
+        _stream_ptr(stream, x))))
     return out
 
 
 def inverse(P: NttParams, kind, x, out=None, stream=None):
     """Batched intt_inverse on device tensors (canonical natural-order output)."""
-    import torch
-
     e = _torch_elem(x)
-    out = torch.empty_like(x) if out is None else out
-    _check(lib().nttk_intt_inverse(P.handle, int(kind), x.data_ptr(), out.data_ptr(),
-                                   _batch_of(x, P.size), e, _stream_ptr(stream, x)))
+    out = _out(x, out)
+    _on_device(x, lambda: _check(lib().nttk_intt_inverse(
+        P.handle, int(kind), x.data_ptr(), out.data_ptr(), _batch_of(x, P.size), e,
+        _stream_ptr(stream, x))))
+    return out
+
+
+def _binary(fn, P: NttParams, kind, a, b, out, stream):
+    e = _torch_elem(a)
+    _match(a, b, "b")
+    out = _out(a, out)
+    _on_device(a, lambda: _check(fn(P.handle, int(kind), a.data_ptr(), b.data_ptr(),
+                                    out.data_ptr(), _batch_of(a, P.size), e,
+                                    _stream_ptr(stream, a))))
     return out
 
 
 def pointwise(P: NttParams, kind, a, b, out=None, stream=None):
-    import torch
-
-    e = _torch_elem(a)
-    out = torch.empty_like(a) if out is None else out
-    _check(lib().nttk_pointwise_multiply(P.handle, int(kind), a.data_ptr(), b.data_ptr(),
-                                         out.data_ptr(), _batch_of(a, P.size), e,
-                                         _stream_ptr(stream)))
-    return out
+    """Slotwise spectrum product (transform.hpp:349-370), canonical output."""
+    return _binary(lib().nttk_pointwise_multiply, P, kind, a, b, out, stream)
 
 
 def basemul(P: NttParams, kind, a, b, out=None, stream=None):
-    import torch
-
-    e = _torch_elem(a)
-    out = torch.empty_like(a) if out is None else out
-    _check(lib().nttk_basemul(P.handle, int(kind), a.data_ptr(), b.data_ptr(), out.data_ptr(),
-                              _batch_of(a, P.size), e, _stream_ptr(stream)))
-    return out
+    """Degree-2 basemul of 7-layer negacyclic spectra (extension)."""
+    return _binary(lib().nttk_basemul, P, kind, a, b, out, stream)
 
 
 def polymul(P: NttParams, kind, a, b, out=None, stream=None):
-    import torch
-
-    e = _torch_elem(a)
-    out = torch.empty_like(a) if out is None else out
-    _check(lib().nttk_polymul(P.handle, int(kind), a.data_ptr(), b.data_ptr(), out.data_ptr(),
-                              _batch_of(a, P.size), e, _stream_ptr(stream)))
-    return out
+    """Fused forward(a), forward(b), product, inverse (transform.hpp:372-379)."""
+    return _binary(lib().nttk_polymul, P, kind, a, b, out, stream)
 
 
 def roundtrip_host(P: NttParams, kind, h_in, h_spec, h_out) -> None:
@@ -528,11 +550,25 @@ def modmul_sweep(variant, p: int, n_bits: int, ell: int, A, B, r=None, stream=No
 
     Results go to ``r`` (int64, len(A)*len(B), optional); returns the wrapping u64 sum.
     """
+    _sweep_operands(A, B, r)
     s = C.c_uint64()
-    _check(lib().nttk_modmul_sweep(int(variant), p, n_bits, ell, A.data_ptr(), A.numel(),
-                                   B.data_ptr(), B.numel(), r.data_ptr() if r is not None else None,
-                                   C.byref(s), _stream_ptr(stream)))
+    _on_device(A, lambda: _check(lib().nttk_modmul_sweep(
+        int(variant), p, n_bits, ell, A.data_ptr(), A.numel(), B.data_ptr(), B.numel(),
+        r.data_ptr() if r is not None else None, C.byref(s), _stream_ptr(stream, A))))
     return int(s.value)
+
+
+def _sweep_operands(A, B, r):
+    import torch
+
+    for t, what in ((A, "A"), (B, "B")):
+        if t.dtype != torch.int64 or not t.is_cuda or not t.is_contiguous() or t.device != A.device:
+            raise ContractViolation(f"modmul_sweep: {what} must be a contiguous int64 CUDA "
+                                    f"tensor on {A.device}")
+    if r is not None and (r.dtype != torch.int64 or r.numel() < A.numel() * B.numel()
+                          or not r.is_contiguous() or r.device != A.device):
+        raise ContractViolation("modmul_sweep: r must be a contiguous int64 CUDA tensor of "
+                                "len(A) * len(B) elements on A's device")
 
 
 def modmul_sweep_device(variant, p: int, n_bits: int, ell: int, A, B, checksum, r=None,
@@ -540,12 +576,12 @@ def modmul_sweep_device(variant, p: int, n_bits: int, ell: int, A, B, checksum, 
     """Device form of :func:`modmul_sweep`: adds the wrapping sum into ``checksum`` (a
     one-element int64 CUDA tensor the caller zeroes) without synchronising."""
     import torch
-    if checksum.dtype != torch.int64 or checksum.numel() < 1 or not checksum.is_cuda:
-        raise ContractViolation("modmul_sweep: checksum must be a CUDA int64 tensor")
-    _check(lib().nttk_modmul_sweep_device(int(variant), p, n_bits, ell, A.data_ptr(), A.numel(),
-                                          B.data_ptr(), B.numel(),
-                                          r.data_ptr() if r is not None else None,
-                                          checksum.data_ptr(), _stream_ptr(stream)))
+    if checksum.dtype != torch.int64 or checksum.numel() < 1 or checksum.device != A.device:
+        raise ContractViolation("modmul_sweep: checksum must be an int64 CUDA tensor on A's device")
+    _sweep_operands(A, B, r)
+    _on_device(A, lambda: _check(lib().nttk_modmul_sweep_device(
+        int(variant), p, n_bits, ell, A.data_ptr(), A.numel(), B.data_ptr(), B.numel(),
+        r.data_ptr() if r is not None else None, checksum.data_ptr(), _stream_ptr(stream, A))))
 
 
 # ---------------------------------------------------------------------------
@@ -616,10 +652,14 @@ def reduce(op: int, ctx: ReductionContext, x, y=None, out=None, stream=None):
     are checked on the device like the reference's NTTK_REQUIRE)."""
     import torch
 
-    out = torch.empty_like(x) if out is None else out
-    _check(lib().nttk_reduce(int(op), C.byref(ctx), x.data_ptr(),
-                             y.data_ptr() if y is not None else None, out.data_ptr(), x.numel(),
-                             _stream_ptr(stream)))
+    if x.dtype != torch.int64 or not x.is_cuda or not x.is_contiguous():
+        raise ContractViolation("reduce: x must be a contiguous int64 CUDA tensor")
+    if y is not None:
+        _match(x, y, "y")
+    out = _out(x, out)
+    _on_device(x, lambda: _check(lib().nttk_reduce(
+        int(op), C.byref(ctx), x.data_ptr(), y.data_ptr() if y is not None else None,
+        out.data_ptr(), x.numel(), _stream_ptr(stream, x))))
     return out
 
 

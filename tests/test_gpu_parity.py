@@ -359,6 +359,28 @@ def test_reference_shaped_single_poly_calls():
     out = nttk.pointwise_multiply(lhs, rhs, T, K.improved)
     assert out.values == [l * (r % 13) % 13 for l, r in zip(lhs.values, rhs.values)]
     assert nttk.pointwise_multiply(lhs, rhs, T, K.harvey).values == out.values
+    # the left operand is reduced mod p before encoding (transform.hpp:362-365): only the
+    # right one carries modified_plantard_mul's T < 2^ell p contract
+    big = nttk.Spectrum([52, 1000, 2 ** 40 + 3, 2 ** 63 + 7])
+    got = nttk.pointwise_multiply(big, rhs, T, K.improved)
+    assert got.values == [(l % 13) * (r % 13) % 13 for l, r in zip(big.values, rhs.values)]
+
+
+def test_device_api_operand_checks():
+    """b / out must match the first operand (dtype, element count, device, contiguity)."""
+    P = engine_params(KYBER, 256, 16, [IMPROVED], exact=True)
+    a = torch.zeros((4, 256), dtype=torch.int16, device="cuda")
+    for bad in (torch.zeros((3, 256), dtype=torch.int16, device="cuda"),
+                torch.zeros((4, 256), dtype=torch.int32, device="cuda"),
+                torch.zeros((4, 512), dtype=torch.int16, device="cuda")[:, ::2],
+                torch.zeros((4, 256), dtype=torch.int16)):
+        with pytest.raises(nttk.ContractViolation):
+            nttk.polymul(P, K.improved, a, bad)
+        with pytest.raises(nttk.ContractViolation):
+            nttk.forward(P, K.improved, a, out=bad)
+    A = torch.zeros(8, dtype=torch.int64, device="cuda")
+    with pytest.raises(nttk.ContractViolation):
+        nttk.modmul_sweep(0, 3329, 16, 2, A, A, torch.zeros(8, dtype=torch.int64, device="cuda"))
 
 
 def test_contracts_match_reference_messages():
@@ -749,3 +771,45 @@ def test_sweep_full_grid_vs_reference_checksums():
         s = nttk.modmul_sweep(row["variant"], row["q"], row["n_bits"], row["ell"],
                               torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
         assert "%016x" % s == row["checksum"], row
+
+
+@pytest.mark.parametrize("p,n,tree,layers", [(KYBER, 16, NEGA, 7), (KYBER, 16, CYCLIC, 8),
+                                             (DILITHIUM, 32, NEGA, 8), (DILITHIUM, 32, CYCLIC, 8),
+                                             (12289, 32, CYCLIC, 9)])
+@pytest.mark.parametrize("kind", [IMPROVED, HARVEY, SMONT])
+def test_standalone_products_vs_oracle(oracle, p, n, tree, layers, kind):
+    """Standalone pointwise / basemul (product.cu: 32-bit per-kind reductions, 128-bit I/O)
+    on lazy forward spectra and on arbitrary storage words vs the oracle, every storage
+    width that holds the words; a misaligned view exercises the generic fallback."""
+    N = 1 << layers if tree == CYCLIC else 256
+    P = engine_params(p, N, n, [kind], tree=tree, layers=layers, exact=True)
+    Q = oracle.params(p, N, n, (kind,), tree=tree, layers=layers, exact=True)
+    sg = kind == SMONT
+    B = 37
+    a = oracle.rng(300 + kind, p, B * N).reshape(B, N)
+    b = oracle.rng(400 + kind, p, B * N).reshape(B, N)
+    fa, fb = Q.forward(kind, a), Q.forward(kind, b)
+    prod = Q.basemul if (N >> layers) == 2 else Q.pointwise
+    want = prod(kind, fa, fb)
+    fits16 = max(np.abs(fa.astype(np.int64)).max(), np.abs(fb.astype(np.int64)).max()) < (1 << 15)
+    for elem in ((2, 4) if fits16 else (4,)):
+        xa, xb = to_dev(fa, elem, sg), to_dev(fb, elem, sg)
+        fn = nttk.basemul if (N >> layers) == 2 else nttk.pointwise
+        assert (from_dev(fn(P, kind, xa, xb)) == want).all(), (elem, "spectra")
+        # arbitrary storage words: canonicalised first
+        wa = oracle.rng(500 + kind, 1 << (8 * elem - 1), B * N).reshape(B, N)
+        wb = oracle.rng(600 + kind, 1 << (8 * elem - 1), B * N).reshape(B, N)
+        if sg:
+            wa = wa.astype(np.int64) - (1 << (8 * elem - 2))
+            wb = wb.astype(np.int64) - (1 << (8 * elem - 2))
+        ca = np.array([[int(v) % p for v in row] for row in wa], dtype=np.uint64)
+        cb = np.array([[int(v) % p for v in row] for row in wb], dtype=np.uint64)
+        got = from_dev(fn(P, kind, to_dev(wa, elem, sg), to_dev(wb, elem, sg)))
+        assert (got == prod(kind, ca, cb)).all(), (elem, "words")
+        # misaligned (not 16-byte aligned) buffers: the generic kernel, same result
+        buf_a = torch.zeros(B * N + 1, dtype=TDT[elem], device="cuda")
+        buf_b = torch.zeros(B * N + 1, dtype=TDT[elem], device="cuda")
+        buf_a[1:] = xa.view(-1)
+        buf_b[1:] = xb.view(-1)
+        got = from_dev(fn(P, kind, buf_a[1:], buf_b[1:]))
+        assert (got.reshape(B, N) == want).all(), (elem, "misaligned")
