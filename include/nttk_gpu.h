@@ -237,6 +237,12 @@ int nttk_butterfly_host(int op, const nttk_reduction_ctx* ctx, uint32_t aux0, ui
 const char* nttk_last_error(void);
 /* number of kernel launches issued by this process so far (bench gpu_launches) */
 uint64_t nttk_launch_count(void);
+/* replaces plantard_correction_fires() (reduction.hpp:172-175): how often plantard_redc's
+ * r == p corner (reduction.hpp:186-189) has fired in this process, counted on the device by
+ * nttk_reduce / nttk_reduce_host (NTTK_OP_PLANTARD_REDC) and the synchronous
+ * nttk_modmul_sweep (NTTK_REDC_PLANTARD); the throughput form nttk_modmul_sweep_device does
+ * not count */
+uint64_t nttk_plantard_correction_fires(void);
 /* 1 when a CUDA device is usable, else 0 (the engine has no CPU fallback) */
 int nttk_device_available(void);
 /* version string of the engine */

@@ -36,6 +36,8 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+// plantard_redc's r == p corner, as the reference counts it (reduction.hpp:172-191)
+std::atomic<uint64_t> g_plantard_fires{0};
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -321,6 +323,7 @@ extern "C" {
 
 const char* nttk_last_error(void) { return g_err.c_str(); }
 uint64_t nttk_launch_count(void) { return g_launches.load(); }
+uint64_t nttk_plantard_correction_fires(void) { return g_plantard_fires.load(); }
 int nttk_device_available(void) { return device_count() > 0 ? 1 : 0; }
 const char* nttk_version(void) { return "nttk-b200 0.1 (sm_100a)"; }
 
@@ -648,17 +651,22 @@ int nttk_modmul_sweep(int variant, uint64_t p, uint32_t n_bits, uint32_t ell, co
   if (int s = sweep_check(variant, p, n_bits, ell)) return s;
   const nttk_b200::Ctx c = nttk_b200::make_ctx(p, n_bits, ell);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  unsigned long long* d_sum = nullptr;
-  cudaError_t e = cudaMallocAsync(&d_sum, sizeof(unsigned long long), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), st);
-  if (e == cudaSuccess) e = nttk_b200::sweep_launch(variant, c, d_A, na, d_B, nb, d_r, d_sum, st);
+  unsigned long long* d_sum = nullptr;  // [0] checksum, [1] plantard corner count
+  cudaError_t e = cudaMallocAsync(&d_sum, 2 * sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_sum, 0, 2 * sizeof(unsigned long long), st);
+  // the synchronous form counts plantard_redc's r == p corner (plantard_correction_fires,
+  // reduction.hpp:172-191); the throughput form nttk_modmul_sweep_device does not
+  if (e == cudaSuccess)
+    e = nttk_b200::sweep_launch(variant, c, d_A, na, d_B, nb, d_r, d_sum, st,
+                                variant == NTTK_REDC_PLANTARD ? d_sum + 1 : nullptr);
   ++g_launches;
-  unsigned long long sum = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&sum, d_sum, sizeof sum, cudaMemcpyDeviceToHost, st);
+  unsigned long long sum[2] = {};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(sum, d_sum, sizeof sum, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (d_sum) cudaFreeAsync(d_sum, st);
   if (e != cudaSuccess) return cuda_fail(e, "modmul_sweep");
-  if (h_checksum) *h_checksum = sum;
+  g_plantard_fires += sum[1];
+  if (h_checksum) *h_checksum = sum[0];
   return NTTK_OK;
 }
 
@@ -790,17 +798,20 @@ int nttk_reduce(int op, const nttk_reduction_ctx* ctx, const int64_t* d_x, const
   if (int s = need_device("reduce")) return s;
   if (!n) return NTTK_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  unsigned* d_flag = nullptr;
-  cudaError_t e = cudaMallocAsync(&d_flag, sizeof(unsigned), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(d_flag, 0, sizeof(unsigned), st);
+  unsigned* d_flag = nullptr;  // [0] violation bits, [2..3] plantard corner count
+  cudaError_t e = cudaMallocAsync(&d_flag, 16, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_flag, 0, 16, st);
   if (e == cudaSuccess) e = nttk_b200::reduce_launch(op, *ctx, d_x, d_y, d_out, n, d_flag, st);
   ++g_launches;
-  unsigned flag = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, d_flag, sizeof flag, cudaMemcpyDeviceToHost, st);
+  unsigned flag[4] = {};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(flag, d_flag, sizeof flag, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (d_flag) cudaFreeAsync(d_flag, st);
   if (e != cudaSuccess) return cuda_fail(e, "reduce");
-  if (flag) return reduce_flag_message(op, flag);
+  uint64_t fires;
+  std::memcpy(&fires, flag + 2, sizeof fires);
+  g_plantard_fires += fires;
+  if (flag[0]) return reduce_flag_message(op, flag[0]);
   return NTTK_OK;
 }
 

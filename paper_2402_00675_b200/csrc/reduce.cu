@@ -69,6 +69,10 @@ __global__ void reduce_kernel(const int64_t* __restrict__ x, const int64_t* __re
       }
       const uint64_t h = ((W * T) * R.mu) & R.r2n_mask;
       const uint64_t r = (((h >> R.n_bits) + 1) * p) >> R.n_bits;
+      // the r == p corner counts into plantard_correction_fires (reduction.hpp:172-191):
+      // flag[2..3] is the u64 counter of this launch
+      if (OP == NTTK_OP_PLANTARD_REDC && r == p)
+        atomicAdd(reinterpret_cast<unsigned long long*>(flag + 2), 1ull);
       out[i] = static_cast<int64_t>(OP == NTTK_OP_PLANTARD_REDC && r == p ? 0 : r);
     } else if (OP == NTTK_OP_MOD_P) {  // canonicalize, transform.hpp:38-40
       out[i] = static_cast<int64_t>(static_cast<uint64_t>(x[i]) % p);

@@ -10,7 +10,8 @@
 
 namespace nttk_b200 {
 
-// out[i] = op(x[i] [, y[i]]); operand-range violations OR bits into *d_flag
+// out[i] = op(x[i] [, y[i]]); operand-range violations OR bits into d_flag[0]; d_flag points
+// to 16 zeroed bytes whose second u64 (d_flag + 2) counts plantard_redc's r == p corner
 cudaError_t reduce_launch(int op, const nttk_reduction_ctx& c, const int64_t* x, const int64_t* y,
                           int64_t* out, size_t n, unsigned* d_flag, cudaStream_t st);
 

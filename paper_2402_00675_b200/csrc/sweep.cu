@@ -113,14 +113,27 @@ struct Redc {
   }
 };
 
+// plantard_redc's r == p corner (reduction.hpp:178-191) for the counting kernels: the
+// 32-bit bodies fold it into an n-bit wrap of h_hi + 1, which is 0 exactly when it fires
+template <int NB>
+__device__ __forceinline__ bool plantard_fired(uint64_t am, int64_t b, const SweepArgs& S) {
+  const uint32_t b32 = static_cast<uint32_t>(b);
+  const uint32_t lo = static_cast<uint32_t>(am), hi = static_cast<uint32_t>(am >> 32);
+  if (NB == 16) return ((b32 * lo + 0x10000u) >> 16) == 0;
+  if (NB == 32) return hi * b32 + __umulhi(lo, b32) + 1u == 0;
+  const uint64_t h = (am * static_cast<uint64_t>(b)) & S.r2n_mask;
+  return (((h >> S.n_bits) + 1) * S.p) >> S.n_bits == S.p;
+}
+
 // Every variant maps b = 0 to 0 (all four bodies are linear in b before the final
 // shift / reduction and the +1 Plantard offsets vanish under >> n for p < 2^n), so the
 // out-of-range columns are zero-padded instead of masked per pair.
-template <int VAR, int NB, bool STORE>
+// COUNT (plantard_redc only): also count the r == p corner into *fires.
+template <int VAR, int NB, bool STORE, bool COUNT = false>
 __global__ void __launch_bounds__(kThreads)
     sweep_kernel(const int64_t* __restrict__ A, size_t na, const int64_t* __restrict__ B, size_t nb,
                  int64_t* __restrict__ r, unsigned long long* __restrict__ sum, SweepArgs S,
-                 unsigned row_split) {
+                 unsigned row_split, unsigned long long* __restrict__ fires) {
   using Row = typename Redc<VAR, NB>::Row;
   __shared__ Row rows[kRows];
   // work split: gridDim.x = col_tiles * row_split when the column tiles do not fill the
@@ -130,6 +143,7 @@ __global__ void __launch_bounds__(kThreads)
   const unsigned rs = blockIdx.x / static_cast<unsigned>(col_tiles < gridDim.x ? col_tiles : gridDim.x);
   const size_t ra = na * rs / row_split, rb = na * (rs + 1) / row_split;
   unsigned long long acc = 0;
+  uint32_t nfired = 0;
   for (size_t ct = blockIdx.x % col_tiles; ct < col_tiles; ct += row_split == 1 ? gridDim.x : col_tiles)
    for (size_t r0 = ra; r0 < rb; r0 += kRows) {
     const size_t c0 = ct * kThreads * kCols + threadIdx.x;
@@ -156,6 +170,7 @@ __global__ void __launch_bounds__(kThreads)
         for (int k = 0; k < kCols; ++k) {
           const uint32_t v = static_cast<uint32_t>(Redc<VAR, NB>::pair(R, b[k], S));
           h[k / 8] += v;
+          if (COUNT) nfired += plantard_fired<NB>(R.am, b[k], S) && (c0 + size_t(k) * kThreads < nb);
           if (STORE) {
             const size_t c = c0 + size_t(k) * kThreads;
             if (c < nb) r[(r0 + i) * nb + c] = static_cast<int32_t>(v);
@@ -176,6 +191,7 @@ __global__ void __launch_bounds__(kThreads)
         for (int k = 0; k < kCols; ++k) {
           const int64_t v = Redc<VAR, NB>::pair(R, b[k], S);
           part += v;
+          if (COUNT) nfired += plantard_fired<NB>(R.am, b[k], S) && (c0 + size_t(k) * kThreads < nb);
           if (STORE) {
             const size_t c = c0 + size_t(k) * kThreads;
             if (c < nb) r[(r0 + i) * nb + c] = v;
@@ -189,15 +205,24 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(sum, acc);
+  if (COUNT) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) nfired += __shfl_xor_sync(0xffffffffu, nfired, o);
+    if ((threadIdx.x & 31) == 0 && nfired) atomicAdd(fires, static_cast<unsigned long long>(nfired));
+  }
 }
 
 template <int VAR, int NB>
 cudaError_t launch_var(const int64_t* A, size_t na, const int64_t* B, size_t nb, int64_t* r,
-                       unsigned long long* sum, const SweepArgs& S, cudaStream_t st) {
-  static OccCache occ_store, occ_sum;
+                       unsigned long long* sum, const SweepArgs& S, cudaStream_t st,
+                       unsigned long long* fires) {
+  static OccCache occ_store, occ_sum, occ_count;
   const int sms = sm_count_current();
-  auto k = r ? sweep_kernel<VAR, NB, true> : sweep_kernel<VAR, NB, false>;
-  const size_t cap = size_t(sms) * occupancy_current(k, kThreads, 0, r ? occ_store : occ_sum);
+  constexpr bool kCan = VAR == NTTK_REDC_PLANTARD;
+  const bool count = kCan && fires;
+  auto k = count ? (r ? sweep_kernel<VAR, NB, true, kCan> : sweep_kernel<VAR, NB, false, kCan>)
+                 : (r ? sweep_kernel<VAR, NB, true> : sweep_kernel<VAR, NB, false>);
+  const size_t cap = size_t(sms) * occupancy_current(k, kThreads, 0, count ? occ_count : r ? occ_store : occ_sum);
   const size_t col_tiles = (nb + kThreads * kCols - 1) / (kThreads * kCols);
   const size_t row_chunks = (na + kRows - 1) / kRows;
   size_t row_split = 1, g = col_tiles < cap ? col_tiles : cap;
@@ -207,18 +232,19 @@ cudaError_t launch_var(const int64_t* A, size_t na, const int64_t* B, size_t nb,
     g = col_tiles * row_split;
   }
   k<<<static_cast<unsigned>(g), kThreads, 0, st>>>(A, na, B, nb, r, sum, S,
-                                                    static_cast<unsigned>(row_split));
+                                                    static_cast<unsigned>(row_split), fires);
   return cudaGetLastError();
 }
 
 template <int NB>
 cudaError_t launch_nb(int variant, const int64_t* A, size_t na, const int64_t* B, size_t nb,
-                      int64_t* r, unsigned long long* sum, const SweepArgs& S, cudaStream_t st) {
+                      int64_t* r, unsigned long long* sum, const SweepArgs& S, cudaStream_t st,
+                      unsigned long long* f) {
   switch (variant) {
-    case NTTK_REDC_MONT: return launch_var<NTTK_REDC_MONT, NB>(A, na, B, nb, r, sum, S, st);
-    case NTTK_REDC_SMONT: return launch_var<NTTK_REDC_SMONT, NB>(A, na, B, nb, r, sum, S, st);
-    case NTTK_REDC_PLANTARD: return launch_var<NTTK_REDC_PLANTARD, NB>(A, na, B, nb, r, sum, S, st);
-    case NTTK_REDC_MPLANTARD: return launch_var<NTTK_REDC_MPLANTARD, NB>(A, na, B, nb, r, sum, S, st);
+    case NTTK_REDC_MONT: return launch_var<NTTK_REDC_MONT, NB>(A, na, B, nb, r, sum, S, st, f);
+    case NTTK_REDC_SMONT: return launch_var<NTTK_REDC_SMONT, NB>(A, na, B, nb, r, sum, S, st, f);
+    case NTTK_REDC_PLANTARD: return launch_var<NTTK_REDC_PLANTARD, NB>(A, na, B, nb, r, sum, S, st, f);
+    case NTTK_REDC_MPLANTARD: return launch_var<NTTK_REDC_MPLANTARD, NB>(A, na, B, nb, r, sum, S, st, f);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -226,16 +252,17 @@ cudaError_t launch_nb(int variant, const int64_t* A, size_t na, const int64_t* B
 }  // namespace
 
 cudaError_t sweep_launch(int variant, const Ctx& c, const int64_t* A, size_t na, const int64_t* B,
-                         size_t nb, int64_t* r, unsigned long long* d_sum, cudaStream_t st) {
+                         size_t nb, int64_t* r, unsigned long long* d_sum, cudaStream_t st,
+                         unsigned long long* d_fires) {
   SweepArgs S{c.p, c.beta_mask, c.r2n_mask, c.p_inv_beta, c.neg_p_inv_beta, c.mu, c.n_bits};
   if (!na || !nb) return cudaSuccess;
   // the 32-bit forms need every intermediate inside 32 / 64 bits (checked host-side)
   const uint64_t p = c.p;
   if (c.n_bits == 16 && p * p + (p << 16) < (uint64_t(1) << 32))
-    return launch_nb<16>(variant, A, na, B, nb, r, d_sum, S, st);
+    return launch_nb<16>(variant, A, na, B, nb, r, d_sum, S, st, d_fires);
   if (c.n_bits == 32 && p < (uint64_t(1) << 27))
-    return launch_nb<32>(variant, A, na, B, nb, r, d_sum, S, st);
-  return launch_nb<0>(variant, A, na, B, nb, r, d_sum, S, st);
+    return launch_nb<32>(variant, A, na, B, nb, r, d_sum, S, st, d_fires);
+  return launch_nb<0>(variant, A, na, B, nb, r, d_sum, S, st, d_fires);
 }
 
 }  // namespace nttk_b200

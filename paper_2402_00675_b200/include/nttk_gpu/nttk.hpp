@@ -213,6 +213,16 @@ inline std::vector<Out> reduce(int op, const ReductionContext& ctx, const std::v
   return detail::reduce<uint64_t>(NTTK_OP_TO_MONTGOMERY_DOMAIN, ctx, w);
 }
 
+// reduction.hpp:172-175 returns the std::atomic<uint64_t>& the corner bumps; here the count
+// lives in the engine (device-counted, nttk_plantard_correction_fires), so the drop-in hands
+// back a view with the atomic's read API: plantard_correction_fires().load() as in
+// verify.hpp:132,156.
+struct PlantardFiresView {
+  [[nodiscard]] uint64_t load() const { return nttk_plantard_correction_fires(); }
+  operator uint64_t() const { return load(); }
+};
+[[nodiscard]] inline PlantardFiresView plantard_correction_fires() { return {}; }
+
 // scalar signatures of reduction.hpp
 [[nodiscard]] inline uint64_t mont_redc(uint64_t T, const ReductionContext& ctx) {
   return mont_redc(std::vector<uint64_t>{T}, ctx)[0];

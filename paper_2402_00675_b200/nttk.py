@@ -135,6 +135,7 @@ EXPORTS = (
     "nttk_butterfly", "nttk_butterfly_host", "nttk_ntt_forward_observed",
     "nttk_intt_inverse_observed",
     "nttk_last_error", "nttk_launch_count", "nttk_device_available", "nttk_version",
+    "nttk_plantard_correction_fires",
 )
 
 _lib_handle = None
@@ -182,6 +183,7 @@ def lib() -> C.CDLL:
             getattr(L, f).argtypes = [vp, C.c_int, vp, vp, _OBSERVER, vp]
         L.nttk_last_error.restype = C.c_char_p
         L.nttk_launch_count.restype = C.c_uint64
+        L.nttk_plantard_correction_fires.restype = C.c_uint64
         L.nttk_version.restype = C.c_char_p
         _lib_handle = L
     return _lib_handle
@@ -200,6 +202,12 @@ def _check(status: int) -> None:
 
 def device_available() -> bool:
     return bool(lib().nttk_device_available())
+
+
+def plantard_correction_fires() -> int:
+    """reduction.hpp:172-175: how often plantard_redc's r == p corner fired in this process
+    (counted on the device by the reduce entry points and the synchronous modmul_sweep)."""
+    return int(lib().nttk_plantard_correction_fires())
 
 
 def launch_count() -> int:

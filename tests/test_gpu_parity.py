@@ -813,3 +813,26 @@ def test_standalone_products_vs_oracle(oracle, p, n, tree, layers, kind):
         buf_b[1:] = xb.view(-1)
         got = from_dev(fn(P, kind, buf_a[1:], buf_b[1:]))
         assert (got.reshape(B, N) == want).all(), (elem, "misaligned")
+
+
+def test_plantard_correction_fires_counter():
+    """plantard_correction_fires (reduction.hpp:172-191): within the admitted operand range
+    the r == p corner never fires (the reference's own observation, reduction_test.cpp and
+    Appendix: exhaustive toy radices) -- the counter stays put over a full grid; operands
+    outside the range (the sweep does not check per pair) reach the corner, and the device
+    count equals a numpy count of h_hi == 2^16 - 1."""
+    q, n = 3329, 16
+    before = nttk.plantard_correction_fires()
+    A = torch.arange(0, q + 1, dtype=torch.int64, device="cuda")
+    nttk.modmul_sweep(2, q, n, 0, A, A)
+    assert nttk.plantard_correction_fires() == before
+    # the corner needs W T = 2^32 - k p (k < 2^16): large 16-bit operands
+    W = np.arange(65024, 65536, dtype=np.int64)
+    T = np.arange(0, 1 << 16, dtype=np.int64)
+    mu = pow(q, -1, 1 << 32)
+    wt = (W[:, None] * T[None, :]).astype(np.uint64)  # < 2^32
+    h = (wt * np.uint64(mu)) & np.uint64(0xFFFFFFFF)  # uint64 products wrap mod 2^64
+    want = int(((h >> 16) == 0xFFFF).sum())
+    assert want > 0
+    nttk.modmul_sweep(2, q, n, 0, torch.from_numpy(W).cuda(), torch.from_numpy(T).cuda())
+    assert nttk.plantard_correction_fires() - before == want
