@@ -1,17 +1,23 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 NTT engine (driver contract: one JSON line on rank 0).
 
-Workload (BASELINE.json config 4, the large-batch throughput config), per GPU and step:
+Workload (BASELINE.json config 4, the large-batch throughput config), per step:
   * 2^22 Kyber polynomials  (q = 3329,    N = 256, cyclic 8 layers, int16),
   * 2^21 Dilithium polys    (q = 8380417, N = 256, cyclic 8 layers, int32),
   each run forward then inverse with the paper's modified-Plantard ("improved")
   butterfly: n = 16 (32-bit Plantard constant) for Kyber, n = 32 (64-bit) for Dilithium.
 Inputs are seeded uniform [0, q) synthetic data (no dataset is involved: the reference
 benchmarks seeded random polynomials too, bench.hpp:198-230).  The working set
-(4 GiB in + 4 GiB spectra per GPU) is far above the 126 MB L2, so no flush is needed.
+(4 GiB in + 4 GiB spectra at N = 1) is far above the 126 MB L2, so no flush is needed.
 
-Multi-GPU: one process per GPU (torchrun); every rank transforms its own fixed batch
-(weak scaling, no collective on the compute path); the step time is the max over ranks.
+Multi-GPU: one process per GPU.  `--gpus N` run without torchrun re-launches
+itself through torch.distributed.run (127.0.0.1); under torchrun WORLD_SIZE must equal
+--gpus.  --scaling strong (default, config 4 "sharded evenly"): every rank draws the same
+seeded global batch and paper_2402_00675_b200.shard.Sharder.run hands it its contiguous
+shard -- no collective on the compute path; --scaling weak: each rank transforms the full
+per-GPU sizes.  The step time is the max over ranks.  --gather: the result shards are
+all-gathered with Sharder.gather (NCCL, timed separately) and rank 0 checks sampled
+polynomials against the CPU oracle.
 
 --impl reference times the reference's own CPU path (oracle/_ref: ntt_forward_inplace
 + intt_inverse, transform.hpp:228-231,339-343) on the host cores, same metric/config.
@@ -21,6 +27,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -36,36 +43,95 @@ METRIC = "NTT polys/sec (fwd+inv round trip, modified-Plantard butterfly)"
 UNIT = "polys/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the fixed config-4 batch is sharded over the ranks; "
+                         "weak: every rank transforms the full per-GPU batch")
     ap.add_argument("--kyber-log2", type=int, default=22)
     ap.add_argument("--dil-log2", type=int, default=21)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--gather", action="store_true", help="NCCL-gather per-rank digests")
+    ap.add_argument("--gather", action="store_true",
+                    help="all-gather the result shards (NCCL, timed separately) and check "
+                         "sampled polynomials against the CPU oracle on rank 0")
     ap.add_argument("--no-extras", action="store_true", help="skip BASELINE configs 1/2/3/5")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="print the per-rank shard plan (launcher / sharder check; no GPU work)")
     ap.add_argument("--bench-report", metavar="DIR",
                     help="write the reference BenchReport schema (bench.hpp:365-424) for the GPU "
                          "and for the reference's own run_bench, then exit")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
-def workload_config(a, world):
-    return {
-        "workload": (f"config4: per GPU 2^{a.kyber_log2} Kyber (q=3329,N=256,cyclic 8 layers,"
+def shard_plan(a, rank: int, world: int):
+    """Per-rank (Kyber, Dilithium) polynomial ranges of one step."""
+    from paper_2402_00675_b200.shard import Sharder
+
+    nk, nd = 1 << a.kyber_log2, 1 << a.dil_log2
+    if a.scaling == "weak":
+        return {"kyber": (0, nk), "dilithium": (0, nd), "kyber_total": nk * world,
+                "dilithium_total": nd * world}
+    sh = Sharder(rank, world)
+    return {"kyber": sh.local(nk), "dilithium": sh.local(nd), "kyber_total": nk,
+            "dilithium_total": nd}
+
+
+def workload_config(a, world, shards=None):
+    nk, nd = 1 << a.kyber_log2, 1 << a.dil_log2
+    per = "per GPU " if a.scaling == "weak" else "in total, sharded over the GPUs: "
+    cfg = {
+        "workload": (f"config4: {per}2^{a.kyber_log2} Kyber (q=3329,N=256,cyclic 8 layers,"
                      f"improved n=16,int16) + 2^{a.dil_log2} Dilithium (q=8380417,N=256,cyclic"
                      " 8 layers,improved n=32,int32); step = forward + inverse of both"),
-        "kyber_polys_per_gpu": 1 << a.kyber_log2,
-        "dilithium_polys_per_gpu": 1 << a.dil_log2,
+        "kyber_polys_total": nk * (world if a.scaling == "weak" else 1),
+        "dilithium_polys_total": nd * (world if a.scaling == "weak" else 1),
         "parallelism": f"dp{world} (batch sharding, no collective on the compute path)",
-        "l2": "working set 8 GiB/GPU >> 126 MB L2: no flush needed",
+        "l2": "working set >= 8 GiB / GPU at N = 1 (>> 126 MB L2): no flush needed",
         "storage": "int16 (Kyber) / int32 (Dilithium) words; arithmetic on 32-bit registers",
     }
+    if shards is not None:
+        cfg["shards"] = shards
+    return cfg
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(argv, n):
+    """`bench.py --gpus N` without torchrun: one process per GPU through torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------
@@ -133,24 +199,59 @@ class ClockSampler:
 
 NCU_KERNELS = {"kyber_fwd": "fwd256_tma_kernel<ImprovedN16", "kyber_inv": "inv256_tma_kernel<ImprovedN16",
                "dil_fwd": "fwd256_tma_kernel<ImprovedN32", "dil_inv": "inv256_tma_kernel<ImprovedN32"}
+# the SASS-census instantiations of the bench kernels (MODE 30 = DEFER+dp2a Kyber inverse,
+# 15 = partial-canonicalisation lazy Dilithium inverse; W1 forwards)
+CENSUS_KERNELS = {"kyber_fwd": "fwd256_tma_kernelINS_11ImprovedN16ILb0EEEtLi8ELb0ELb1E",
+                  "kyber_inv": "inv256_tma_kernelINS_11ImprovedN16ILb0EEEtLi8ELi30E",
+                  "dil_fwd": "fwd256_tma_kernelINS_11ImprovedN32EjLi8ELb0ELb1E",
+                  "dil_inv": "inv256_tma_kernelINS_11ImprovedN32EjLi8ELi15E"}
+
+
+def latest_profile(pattern: str):
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern)))
+    return files[-1] if files else None
 
 
 def ncu_traffic(kernel: str, nk: int, nd: int):
     """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full
-    capture of this same bench configuration (profiles/rNN_ncu_full.json), else None."""
-    import glob
-
+    capture of the N = 1 bench configuration (profiles/r*_ncu_full.json), else None."""
     if (nk, nd) != (1 << 22, 1 << 21):
         return None
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full.json")))
-    if not files:
+    path = latest_profile("r*_ncu_full.json")
+    if not path:
         return None
-    with open(files[-1]) as fh:
+    with open(path) as fh:
         caps = json.load(fh)["kernels"]
     for k in caps:
         if NCU_KERNELS[kernel] in k["kernel"].replace("nttk_b200::", "").replace("unnamed>::", ""):
             return k["dram_bytes"]
     return None
+
+
+def sass_census():
+    """Executed fmaheavy cycles per polynomial of the bench kernels from the committed SASS
+    census (tools/sass_census.py --json), flagged stale when the library changed since."""
+    import hashlib
+
+    path = latest_profile("r*_sass_census.json")
+    if not path:
+        return None, None
+    with open(path) as fh:
+        d = json.load(fh)
+    lib = os.path.join(ROOT, "paper_2402_00675_b200", "libnttk_gpu.so")
+    try:
+        with open(lib, "rb") as fh:
+            stale = hashlib.sha256(fh.read()).hexdigest() != d["lib_sha256"]
+    except OSError:
+        stale = True
+    out = {}
+    for key, pat in CENSUS_KERNELS.items():
+        for r in d["rows"]:
+            if pat in r["kernel"]:
+                out[key] = r["fmaheavy_cycles_per_iter"] / r["polys_per_iter"]
+    return out, {"file": os.path.relpath(path, ROOT), "stale": stale}
 
 
 def measured_peaks():
@@ -203,13 +304,6 @@ def cpu_reference_rate(n_kyber: int, n_dil: int, threads: int):
     return (n_kyber + n_dil) / t, "port", t
 
 
-def host_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
-
-
 def run_reference_arm(a, rank, world):
     if rank != 0:
         return 0
@@ -225,15 +319,15 @@ def run_reference_arm(a, rank, world):
         total_polys += per_step_k + per_step_d
     value = total_polys / total_t
     sample = (f"each step: {per_step_k} Kyber + {per_step_d} Dilithium polys, fwd+inv, "
-              f"{threads} host threads")
+              f"{threads} host threads ({cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total_t / a.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (reference Rng, uniform [0,q))",
         "config": workload_config(a, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "cpu": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -256,10 +350,20 @@ def _time_ms(torch, fn, iters, warm=3):
     return e0.elapsed_time(e1) / iters
 
 
-def table2_cpu_reference(name, q, N):
+def _cpu_rate(fn, units, min_s=0.3):
+    """units/s of fn() repeated until at least min_s of wall time."""
+    t, reps = 0.0, 0
+    while t < min_s:
+        t += fn()
+        reps += 1
+    return units * reps / t, t, reps
+
+
+def table2_cpu_reference(q, N):
     """The reference's own path at a Table 2 preset on ONE host thread (the reference is
-    single-threaded), per kind: ntt_forward_inplace, and forward + intt_inverse, over a
-    bounded sample (oracle/_ref, the unmodified reference headers); None if not built."""
+    single-threaded), per kind: ntt_forward_inplace and intt_inverse, each timed directly
+    (transform.hpp:228-231, 339-343) over >= 1 s / >= 2 s of repeated batches
+    (oracle/_ref, the unmodified reference headers); None if not built."""
     from oracle.oracle import HARVEY, IMPROVED, NTL, SCOTT, Oracle, Reference, reference_available
 
     if not reference_available():
@@ -271,13 +375,76 @@ def table2_cpu_reference(name, q, N):
     a = Oracle().rng(77, q, n * N)
     out = {}
     for kname, k in kinds.items():
-        tf = rp.time_batch(k, 0, a.copy(), 1)
-        tr = rp.time_batch(k, 1, a.copy(), 1)
-        out[kname] = {"cpu_ref_fwd_ns_per_poly": tf * 1e9 / n,
-                      "cpu_ref_inv_ns_per_poly": max(tr - tf, 0.0) * 1e9 / n,
-                      "cpu_ref_sample": f"{n} polys, 1 thread"}
+        fwd, tf, rf = _cpu_rate(lambda: rp.time_batch(k, 0, a.copy(), 1), n, 1.0)
+        spec = rp.forward(k, a.reshape(n, N)).ravel()
+        inv, ti, ri = _cpu_rate(lambda: rp.time_batch(k, 2, spec.copy(), 1), n, 2.0)
+        out[kname] = {"cpu_ref_fwd_ns_per_poly": 1e9 / fwd, "cpu_ref_inv_ns_per_poly": 1e9 / inv,
+                      "cpu_ref_sample": f"{n} polys x {rf} (fwd, {tf:.1f} s) / x {ri} (inv, "
+                                        f"{ti:.1f} s), 1 thread"}
     return out
 
+
+def extras_cpu_baselines():
+    """The reference's CPU path beside every BASELINE config (1 thread and all host threads):
+    config 1/2 negacyclic trees through the reference's own cores (oracle/_ref ref_tree_run,
+    restated loop), config 2's reference-pinned twin cyclic_convolution_via_ntt
+    (transform.hpp:372-379), config 3 the Dilithium round trip (ntt_forward_inplace +
+    intt_inverse), config 5 the checked reductions (reduction.hpp:125-273)."""
+    from oracle.oracle import HARVEY, IMPROVED, NEGA, SMONT, Oracle, Reference, reference_available
+
+    if not reference_available():
+        return None
+    ref, o = Reference(), Oracle()
+    thr = host_threads()
+    out = {"cpu": cpu_model(), "threads": thr}
+
+    def both(fn, units):  # (1 thread, all threads) units/s
+        r1, t1, _ = _cpu_rate(lambda: fn(1), units, 0.3)
+        rn, tn, _ = _cpu_rate(lambda: fn(thr), units, 0.3)
+        return {"one_thread": r1, "all_threads": rn}
+
+    B = 8192
+    f = o.rng(101, KYBER_Q, B * 256)
+    g = o.rng(102, KYBER_Q, B * 256)
+    out["config1_kyber7_fwd"] = dict(unit="polys/s", kind="reference cores (ref_tree_run)",
+                                     **both(lambda t: ref.time_tree(KYBER_Q, 256, 16, NEGA, 7, IMPROVED, 0,
+                                                                    f.copy(), threads=t), B))
+    c2 = {"unit": "products/s", "kind": "reference cores (ref_tree_run: 2 fwd + basemul + inv)"}
+    for name, k in (("modified_plantard", IMPROVED), ("montgomery_R2^16", HARVEY),
+                    ("signed_montgomery", SMONT)):
+        c2[name] = both(lambda t, k=k: ref.time_tree(KYBER_Q, 256, 16, NEGA, 7, k, 2, f[:2048 * 256].copy(),
+                                                     g[:2048 * 256], threads=t), 2048)
+    RP = ref.params(KYBER_Q, 256, 32, (IMPROVED, HARVEY))
+    c2["cyclic_convolution_via_ntt_improved_n32"] = both(
+        lambda t: RP.time_convolution(IMPROVED, f[:2048 * 256], g[:2048 * 256], t), 2048)
+    out["config2_kyber_polymul"] = c2
+    dil = o.rng(103, DIL_Q, B * 256)
+    c3 = {"unit": "polys/s", "kind": "reference (ntt_forward_inplace + intt_inverse)"}
+    for name, k, exact in (("modified_plantard_n32", IMPROVED, True), ("montgomery_n32", HARVEY, False)):
+        R3 = ref.params(DIL_Q, 256, 32, (k,), exact=exact)
+        c3[name] = both(lambda t, R3=R3, k=k: R3.time_batch(k, 1, dil.copy(), t), B)
+    out["config3_dilithium_roundtrip"] = c3
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from sweep_inputs import CONFIGS, NAMES, grid
+
+    c5 = {"unit": "mults/s", "kind": "reference checked reductions (ref_sweep)",
+          "sample": "2^10 rows x 2^15 columns of each config-5 grid"}
+    for q, n, ell in CONFIGS:
+        for v in range(4):
+            A, Bv = grid(q, n, ell, v)
+            A = A[:1024]
+
+            def sweep(t, A=A, Bv=Bv, v=v, q=q, n=n, ell=ell):
+                from concurrent.futures import ThreadPoolExecutor
+
+                t0 = time.perf_counter()
+                with ThreadPoolExecutor(t) as ex:
+                    list(ex.map(lambda a: ref.sweep_checksum(v, q, n, ell, a, Bv),
+                                np.array_split(A, t)))
+                return time.perf_counter() - t0
+            c5[f"q{q}_{NAMES[v]}"] = both(sweep, A.size * Bv.size)
+    out["config5_sweep"] = c5
+    return out
 
 def run_extras(dev):
     """The other BASELINE.json configs, device-resident, CUDA events (secondary fields)."""
@@ -325,6 +492,16 @@ def run_extras(dev):
         P2 = nttk.build_params(KYBER_Q, 256, 16, [kind], tree=NEG, layers=7, exact_bound=True)
         ms = _time_ms(torch, lambda: nttk.polymul(P2, kind, xa, xb, xc), 20)
         c2[name] = {"ms": ms, "products_per_s": B / (ms / 1e3)}
+    # the standalone basemul kernel (product.cu) on the same 65536 pairs of forward spectra:
+    # HBM-bound, 3 x 512 B per polynomial pair (two spectra in, one product out)
+    peak, _ = measured_peaks()
+    for name, kind in (("modified_plantard", K.improved), ("montgomery_R2^16", K.harvey),
+                       ("signed_montgomery", K.smont)):
+        P2 = nttk.build_params(KYBER_Q, 256, 16, [kind], tree=NEG, layers=7, exact_bound=True)
+        fa, fb = nttk.forward(P2, kind, xa), nttk.forward(P2, kind, xb)
+        ms = _time_ms(torch, lambda: nttk.basemul(P2, kind, fa, fb, xc), 20)
+        gbs = 3 * B * 512 / (ms / 1e3) / 1e9
+        c2[name]["standalone_basemul"] = {"ms": ms, "GBps": gbs, "frac_of_hbm": gbs / peak}
     ex["config2_kyber_polymul_65536_fused"] = c2
     # config 3: Dilithium round trip, 65536 polys, modified Plantard n=32 vs 32-bit Montgomery
     xd = torch.randint(0, DIL_Q, (B, 256), generator=g, device=dev, dtype=torch.int32)
@@ -384,7 +561,7 @@ def run_extras(dev):
             assert torch.equal(op, xp), (name, kind)
             row[kind.name] = {"fwd_ns_per_poly": fms * 1e6 / Bp, "inv_ns_per_poly": ims * 1e6 / Bp,
                               "fast_path": kind in Pp.fast_path}
-        cpu = table2_cpu_reference(name, qp, Np)
+        cpu = table2_cpu_reference(qp, Np)
         if cpu:
             for kname, v in cpu.items():
                 row[kname].update(v)
@@ -440,15 +617,15 @@ def run_extras(dev):
     return ex
 
 
-def run_e2e(a, torch, dist, nttk, Pk, Pd, IMP, xk, xd, nk, nd, world, dev, polys_per_step):
+def run_e2e(a, torch, dist, nttk, Pk, Pd, IMP, xk, xd, world, dev, polys_per_step):
     """The same step end to end through the C ABI host entry point (nttk_roundtrip_host:
-    pinned host buffers, H2D + kernels + D2H inside the timed region).  The pinned
-    allocation is agreed on by all ranks first, so a rank that cannot pin fails the e2e
-    leg everywhere instead of leaving the others in a collective."""
+    pinned host buffers, H2D + kernels + D2H inside the timed region), each rank on its own
+    shard.  The pinned allocation is agreed on by all ranks first, so a rank that cannot pin
+    fails the e2e leg everywhere instead of leaving the others in a collective."""
     err, okf = None, torch.ones(1, device=dev)
     try:
-        hk = torch.empty((nk, 256), dtype=torch.int16, pin_memory=True)
-        hd = torch.empty((nd, 256), dtype=torch.int32, pin_memory=True)
+        hk = torch.empty(tuple(xk.shape), dtype=torch.int16, pin_memory=True)
+        hd = torch.empty(tuple(xd.shape), dtype=torch.int32, pin_memory=True)
         ohk, ohd = torch.empty_like(hk, pin_memory=True), torch.empty_like(hd, pin_memory=True)
     except Exception as ex:
         err = f"{type(ex).__name__}: {ex}"
@@ -471,10 +648,59 @@ def run_e2e(a, torch, dist, nttk, Pk, Pd, IMP, xk, xd, nk, nd, world, dev, polys
     if world > 1:
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     assert torch.equal(ohk, hk) and torch.equal(ohd, hd), "e2e round trip mismatch"
+    nbytes = torch.tensor([hk.numel() * 2 + hd.numel() * 4], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(nbytes)
     return {"value": polys_per_step * a.e2e_steps / float(dt.item()), "unit": UNIT,
-            "h2d_bytes_per_step": nk * 512 + nd * 1024,
-            "d2h_bytes_per_step": nk * 512 + nd * 1024,
-            "path": "nttk_roundtrip_host (C ABI, pinned host buffers, 3-stream pipeline)"}
+            "h2d_bytes_per_step": int(nbytes.item()), "d2h_bytes_per_step": int(nbytes.item()),
+            "path": "nttk_roundtrip_host (C ABI, pinned host buffers, 3-stream pipeline); "
+                    "wall clock, max over ranks"}
+
+
+def gather_check(a, torch, dist, sh, sk, sd, nk_total, nd_total, seed_k, seed_d, dev):
+    """All-gather the forward-spectrum shards (Sharder.gather: NCCL), timed with CUDA
+    events; rank 0 checks sampled polynomials of the gathered batch against the CPU oracle
+    (the checker, outside every timed region)."""
+    from oracle.oracle import IMPROVED, Oracle
+
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    gk = sh.gather(sk, nk_total)
+    gd = sh.gather(sd, nd_total)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    out = {"gather_ms": float(ms.item()),
+           "bytes": int(gk.numel() * 2 + gd.numel() * 4), "collective": "Sharder.gather "
+           "(torch.distributed all_gather, NCCL)"}
+    if sh.rank == 0:
+        o = Oracle()
+        rs = np.random.RandomState(0)
+        ok = True
+        for P, g, q, n, seed, total in (
+                (o.params(KYBER_Q, 256, 16, (IMPROVED,), exact=True), gk, KYBER_Q, 16, seed_k, nk_total),
+                (o.params(DIL_Q, 256, 32, (IMPROVED,), exact=True), gd, DIL_Q, 32, seed_d, nd_total)):
+            idx = np.sort(rs.choice(total, 16, replace=False))
+            x = global_batch(torch, seed, q, total, torch.int16 if q == KYBER_Q else torch.int32, dev)
+            f = x[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.int64).astype(np.uint64)
+            want = P.forward(IMPROVED, f).astype(np.int64)
+            mask = 0xFFFF if q == KYBER_Q else 0xFFFFFFFF
+            got = g[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.int64) & mask
+            ok &= bool((got == want).all())
+            del x
+        out["sampled_polys_vs_oracle"] = "16 Kyber + 16 Dilithium, bit-exact" if ok else "MISMATCH"
+        if not ok:
+            raise RuntimeError("gathered spectra differ from the oracle")
+    return out
+
+
+def global_batch(torch, seed, q, total, dtype, dev):
+    """The seeded global input batch every rank draws identically (strong scaling)."""
+    g = torch.Generator(device=dev).manual_seed(seed)
+    return torch.randint(0, q, (total, 256), generator=g, device=dev, dtype=torch.int32).to(dtype)
 
 
 def run_engine_arm(a, rank, world, local_rank):
@@ -482,18 +708,28 @@ def run_engine_arm(a, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_2402_00675_b200.nttk as nttk
+    from paper_2402_00675_b200.shard import Sharder
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    nk, nd = 1 << a.kyber_log2, 1 << a.dil_log2
     Pk = nttk.build_params(KYBER_Q, 256, 16, [nttk.ButterflyKind.improved], exact_bound=True)
     Pd = nttk.build_params(DIL_Q, 256, 32, [nttk.ButterflyKind.improved], exact_bound=True)
     IMP = nttk.ButterflyKind.improved
     assert IMP in Pk.fast_path and IMP in Pd.fast_path
 
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    xk = torch.randint(0, KYBER_Q, (nk, 256), generator=g, device=dev, dtype=torch.int32).to(torch.int16)
-    xd = torch.randint(0, DIL_Q, (nd, 256), generator=g, device=dev, dtype=torch.int32)
+    plan = shard_plan(a, rank, world)
+    nk_total, nd_total = plan["kyber_total"], plan["dilithium_total"]
+    seed_k, seed_d = 1234, 4321
+    sh = Sharder(rank, world) if a.scaling == "strong" else Sharder(0, 1)
+    if a.scaling == "strong":  # one global seeded batch, this rank's contiguous shard
+        xk_all = global_batch(torch, seed_k, KYBER_Q, nk_total, torch.int16, dev)
+        xd_all = global_batch(torch, seed_d, DIL_Q, nd_total, torch.int32, dev)
+        xk = sh.run(lambda part: part, xk_all)
+        xd = sh.run(lambda part: part, xd_all)
+    else:  # weak: every rank its own full per-GPU batch
+        xk = global_batch(torch, seed_k + rank, KYBER_Q, 1 << a.kyber_log2, torch.int16, dev)
+        xd = global_batch(torch, seed_d + rank, DIL_Q, 1 << a.dil_log2, torch.int32, dev)
+    nk, nd = xk.shape[0], xd.shape[0]
     sk, sd = torch.empty_like(xk), torch.empty_like(xd)
     ok, od = torch.empty_like(xk), torch.empty_like(xd)
     stream = torch.cuda.current_stream(dev)
@@ -541,55 +777,80 @@ def run_engine_arm(a, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     max_ms = float(tm.item())
-    polys_per_step = (nk + nd) * world
+    polys_per_step = nk_total + nd_total
     value = polys_per_step * a.steps / (max_ms / 1e3)
+    shards = None
+    if world > 1:
+        sizes = torch.tensor([nk, nd], dtype=torch.int64, device=dev)
+        allz = [torch.empty_like(sizes) for _ in range(world)]
+        dist.all_gather(allz, sizes)
+        shards = [{"rank": r, "kyber_polys": int(z[0]), "dilithium_polys": int(z[1])}
+                  for r, z in enumerate(allz)]
 
-    # roofline of the dominant kernel: HBM (bytes in + out) and the IMAD issue roof
-    # (modmuls per poly x measured fmaheavy cost)
+    # roofline of the dominant kernel: HBM (algorithmic bytes in + out) against the measured
+    # copy bandwidth, beside the IMAD issue roof under two cost models:
+    # algorithmic = the reference algorithm's modmuls per polynomial (N/2 log N forward,
+    # + N inverse) x the fmaheavy cost of one modmul (measured IMAD 1/64, IMAD.HI 1/32
+    # SM-cycles per lane-op, profiles/r2_imad_microbench.txt); executed = the fmaheavy cycles
+    # of the kernel's own SASS loop (profiles/r*_sass_census.json)
     dom = int(np.argmax(per_kernel))
     peak, peak_src = measured_peaks()
     achieved = alg_bytes[dom] / (per_kernel[dom] / 1e3) / 1e9
     sm_hz = 1965e6 if not clk.samples else 1e6 * float(np.median([s[0] for s in clk.samples]))
     n_sm = torch.cuda.get_device_properties(local_rank).multi_processor_count
-    # SM-cycles per modmul (fmaheavy: IMAD 1/64, IMAD.HI 1/32 per lane, measured):
-    # n=16 Plantard IMAD + IMAD.HI; n=32 IMAD + 2 IMAD.HI
     cyc = [3 / 64, 3 / 64, 5 / 64, 5 / 64]
-    modmuls = [1024, 1024 + 256, 1024, 1024 + 256]  # fwd N/2 log N; inv + N scaling
+    modmuls = [1024, 1024 + 256, 1024, 1024 + 256]
     polys = [nk, nk, nd, nd]
-    imad_roof_ms = [p_ * m * c / (n_sm * sm_hz) * 1e3 for p_, m, c in zip(polys, modmuls, cyc)]
-    hbm_roof_ms = [b / (peak * 1e9) * 1e3 for b in alg_bytes]
-    roof_ms = [max(a, b) for a, b in zip(imad_roof_ms, hbm_roof_ms)]
+    alg_ms = [p_ * m * c / (n_sm * sm_hz) * 1e3 for p_, m, c in zip(polys, modmuls, cyc)]
+    census, census_src = sass_census()
+    exe_ms = None
+    if census and all(k in census for k in names):
+        # SMSP-cycles per polynomial spread over 4 sub-partitions per SM
+        exe_ms = [p_ * census[k] / (4 * n_sm * sm_hz) * 1e3 for p_, k in zip(polys, names)]
+    hbm_ms = [b / (peak * 1e9) * 1e3 for b in alg_bytes]
     traffic = ncu_traffic(names[dom], nk, nd)
+
+    def bind(imad_ms):
+        return ["imad" if i > h else "hbm" for i, h in zip(imad_ms, hbm_ms)]
+
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": names[dom],
                 "peak_source": peak_src,
-                "binding_roof": "imad" if imad_roof_ms[dom] > hbm_roof_ms[dom] else "hbm",
-                "frac_of_binding_roof": roof_ms[dom] / per_kernel[dom],
-                "imad": {"achieved_modmul_per_s": polys[dom] * modmuls[dom] / (per_kernel[dom] / 1e3),
-                         "peak_modmul_per_s": n_sm * sm_hz / cyc[dom],
-                         "frac": imad_roof_ms[dom] / per_kernel[dom],
-                         "definition": "fmaheavy cycles of the modmul's IMAD/IMAD.HI (measured "
-                                       "rates, profiles/r1a_imad_microbench.txt) x modmuls/poly"},
-                "step_frac_of_roofline": sum(roof_ms) / sum(per_kernel),
                 "per_kernel_ms": dict(zip(names, [round(x, 4) for x in per_kernel])),
-                "per_kernel_roof_ms": dict(zip(names, [round(x, 4) for x in roof_ms])),
                 "per_kernel_GBps": dict(zip(names, [round(b / (t / 1e3) / 1e9, 1)
-                                                    for b, t in zip(alg_bytes, per_kernel)]))}
-    fwd_rate = (nk + nd) * world / (max(per_kernel[0] + per_kernel[2], 1e-9) / 1e3)
+                                                    for b, t in zip(alg_bytes, per_kernel)])),
+                "per_kernel_frac_of_hbm": dict(zip(names, [round(h / t, 3)
+                                                           for h, t in zip(hbm_ms, per_kernel)])),
+                "step_frac_of_hbm": sum(hbm_ms) / sum(per_kernel),
+                "imad_algorithmic": {
+                    "definition": "reference modmuls per poly (fwd 1024, inv 1280) x fmaheavy "
+                                  "cost per modmul (n=16 IMAD+IMAD.HI = 3/64, n=32 IMAD+2 IMAD.HI "
+                                  "= 5/64 SM-cycles per lane-op) at the sampled SM clock",
+                    "roof_ms": dict(zip(names, [round(x, 4) for x in alg_ms])),
+                    "frac": dict(zip(names, [round(r / t, 3) for r, t in zip(alg_ms, per_kernel)])),
+                    "binding_roof": dict(zip(names, bind(alg_ms)))}}
+    if exe_ms is not None:
+        roofline["imad_executed"] = {
+            "definition": "fmaheavy cycles of the kernel's SASS loop (2 x IMAD + 4 x IMAD.HI/WIDE "
+                          "per warp-iteration of 2 polys) at the sampled SM clock",
+            "source": census_src,
+            "roof_ms": dict(zip(names, [round(x, 4) for x in exe_ms])),
+            "frac": dict(zip(names, [round(r / t, 3) for r, t in zip(exe_ms, per_kernel)])),
+            "binding_roof": dict(zip(names, bind(exe_ms)))}
+    fwd_rate = polys_per_step / (max(per_kernel[0] + per_kernel[2], 1e-9) / 1e3)
 
     # end-to-end through the C ABI host entry point (pinned host buffers, copies timed)
     e2e = None
     if not a.no_e2e:
         try:
-            e2e = run_e2e(a, torch, dist, nttk, Pk, Pd, IMP, xk, xd, nk, nd, world, dev, polys_per_step)
+            e2e = run_e2e(a, torch, dist, nttk, Pk, Pd, IMP, xk, xd, world, dev, polys_per_step)
         except Exception as ex:  # e.g. pinned host memory exhausted with many ranks per host
             e2e = {"value": None, "unit": UNIT, "error": f"{type(ex).__name__}: {ex}"[:300]}
-    digest = None
+    gathered = None
     if a.gather and world > 1:  # NCCL only to gather results when asked, outside timing
-        d = torch.stack([sk.view(-1)[:1024].to(torch.int64).sum(), sd.view(-1)[:1024].to(torch.int64).sum()])
-        allv = [torch.empty_like(d) for _ in range(world)]
-        dist.all_gather(allv, d)
-        digest = [v.tolist() for v in allv]
+        if a.scaling != "strong":
+            raise SystemExit("--gather needs --scaling strong (one global batch)")
+        gathered = gather_check(a, torch, dist, sh, sk, sd, nk_total, nd_total, seed_k, seed_d, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -603,7 +864,7 @@ def run_engine_arm(a, rank, world, local_rank):
         rate = reps * (smp_k + smp_d) / tot_t
         # the reference is single-threaded: one core, same workload mix
         _, _, t1 = cpu_reference_rate(16384, 8192, 1)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "cpu": cpu_model(),
                "sample": (f"{reps} x ({smp_k} Kyber + {smp_d} Dilithium) polys fwd+inv, "
                           f"{tot_t:.1f} s wall on {threads} threads"),
                "value_1_core": 24576 / t1,
@@ -612,22 +873,24 @@ def run_engine_arm(a, rank, world, local_rank):
     extras = None
     if rank == 0 and world == 1 and not a.no_extras:  # single-GPU configs: N = 1 runs only
         extras = run_extras(dev)
+        if not a.no_cpu_baseline:
+            extras["cpu_reference_per_config"] = extras_cpu_baselines()
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": max_ms / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "scaling": a.scaling, "vs_baseline": None, "dtype": "u32",
             "data": "synthetic uniform [0,q) (torch.randint, seeded)",
-            "config": workload_config(a, world),
+            "config": workload_config(a, world, shards),
             "fwd_only_polys_per_s": fwd_rate,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }
         if extras is not None:
             line["extras"] = extras
-        if digest is not None:
-            line["gathered_digests"] = digest
+        if gathered is not None:
+            line["gather"] = gathered
         print(json.dumps(line), flush=True)
     return 0
 
@@ -715,17 +978,54 @@ def bench_report(outdir, presets=("kyber256", "falcon512", "falcon1024"), seed=1
     return 0
 
 
-def main():
-    a = parse()
+def plan_only(a, rank, world):
+    """Launcher / sharder check without GPU work: every rank computes its shard plan, the
+    plans are all-gathered (gloo), rank 0 prints one JSON line."""
+    import torch.distributed as dist
+
+    plan = shard_plan(a, rank, world)
+    rows = [None] * world
+    if world > 1:
+        dist.all_gather_object(rows, plan)
+    else:
+        rows = [plan]
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "scaling": a.scaling,
+                          "shards": [{"rank": r, "kyber": list(p["kyber"]),
+                                      "dilithium": list(p["dilithium"])}
+                                     for r, p in enumerate(rows)],
+                          "kyber_total": plan["kyber_total"],
+                          "dilithium_total": plan["dilithium_total"]}), flush=True)
+    return 0
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    a = parse(argv)
     if a.bench_report:
         return bench_report(a.bench_report)
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        return relaunch(argv, a.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if a.impl == "reference":
         if world > 1 and rank != 0:
             return 0
         return run_reference_arm(a, rank, world)
+    if a.plan_only:
+        import torch.distributed as dist
+
+        if world > 1:
+            dist.init_process_group("gloo")
+        try:
+            return plan_only(a, rank, world)
+        finally:
+            if world > 1:
+                dist.destroy_process_group()
     if world > 1:
         import torch
         import torch.distributed as dist

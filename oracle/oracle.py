@@ -323,6 +323,11 @@ class Reference:
             L.ref_observed.argtypes = [C.c_void_p, C.c_int, C.c_int, u64p, u64p, u64p]
             L.ref_tree_run.argtypes = [C.c_uint64, C.c_uint32, C.c_uint, C.c_int, C.c_uint32,
                                        C.c_int, C.c_int, u64p, C.c_void_p, C.c_size_t]
+            L.ref_time_tree.argtypes = [C.c_uint64, C.c_uint32, C.c_uint, C.c_int, C.c_uint32,
+                                        C.c_int, C.c_int, u64p, C.c_void_p, C.c_size_t, C.c_int,
+                                        C.POINTER(C.c_uint64)]
+            L.ref_time_convolution.argtypes = [C.c_void_p, C.c_int, u64p, u64p, u64p, C.c_size_t,
+                                               C.c_int, C.POINTER(C.c_uint64)]
             if hasattr(L, "ref_run_bench"):
                 L.ref_run_bench.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int,
                                             C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
@@ -383,6 +388,17 @@ class Reference:
         self._check(self.lib.ref_tree_run(p, N, n_bits, tree, layers, kind, direction, a, bp,
                                           a.shape[0]))
         return a
+
+    def time_tree(self, p, N, n_bits, tree, layers, kind, direction, a, b=None, threads=1):
+        """Wall seconds of ref_tree_run over the batch `a` (modified in place) on `threads`
+        host threads (the extension configs' CPU baseline)."""
+        a = np.ascontiguousarray(a, dtype=np.uint64)
+        bp = np.ascontiguousarray(b, dtype=np.uint64) if b is not None else None
+        ns = C.c_uint64()
+        self._check(self.lib.ref_time_tree(p, N, n_bits, tree, layers, kind, direction, a,
+                                           bp.ctypes.data if bp is not None else None,
+                                           a.size // N, threads, C.byref(ns)))
+        return ns.value * 1e-9
 
     def sweep_checksum(self, variant, p, n, ell, A, B) -> int:
         """Wrapping u64 sum of the reference's checked reduction over the grid A x B,
@@ -456,6 +472,16 @@ class RefParams:
         out = np.empty(self.N, dtype=np.uint64)
         self.r._check(self.r.lib.ref_observed(self.h, kind, dir, a, states, out))
         return states, out
+
+    def time_convolution(self, kind, x, y, threads=1):
+        """Wall seconds of cyclic_convolution_via_ntt (transform.hpp:372-379) over a batch."""
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        y = np.ascontiguousarray(y, dtype=np.uint64)
+        out = np.empty_like(x)
+        ns = C.c_uint64()
+        self.r._check(self.r.lib.ref_time_convolution(self.h, kind, x, y, out, x.size // self.N,
+                                                      threads, C.byref(ns)))
+        return ns.value * 1e-9
 
     def time_batch(self, kind, mode, a, threads):
         a = np.ascontiguousarray(a, dtype=np.uint64)

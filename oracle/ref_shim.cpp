@@ -247,7 +247,8 @@ void ref_naive_dft(const uint64_t* f, size_t N, uint64_t omega, uint64_t p, uint
 
 // ---- CPU baseline: the reference's own batch loop, sharded over host threads ----
 // mode 0: forward only (ntt_forward_inplace, the reference bench path,
-// bench.hpp:198-230); mode 1: forward then intt_inverse (round trip).
+// bench.hpp:198-230); mode 1: forward then intt_inverse (round trip); mode 2: intt_inverse
+// only (`a` holds spectra in butterfly order).
 // `a` holds batch canonical polys; each thread works on its own contiguous shard.
 // Returns elapsed wall nanoseconds in *ns.
 int ref_time_batch(void* hv, int kind, int mode, uint64_t* a, size_t batch, int threads,
@@ -263,6 +264,11 @@ int ref_time_batch(void* hv, int kind, int mode, uint64_t* a, size_t batch, int 
         for (size_t i = lo; i < hi; ++i) {
           uint64_t* poly = a + i * P.size;
           std::memcpy(buf.data(), poly, P.size * 8);
+          if (mode == 2) {
+            const Polynomial f = intt_inverse(Spectrum{buf, Ordering::bit_reversed}, P, k);
+            std::memcpy(poly, f.data(), P.size * 8);
+            continue;
+          }
           ntt_forward_inplace(buf, P, k);
           if (mode == 1) {
             const Polynomial f = intt_inverse(Spectrum{buf, Ordering::bit_reversed}, P, k);
@@ -518,6 +524,52 @@ int ref_tree_run(uint64_t p, uint32_t N, unsigned n_bits, int nega, uint32_t lay
         std::memcpy(x, prod.data(), N * 8);
       }
     }
+  });
+}
+
+// CPU baselines of the extension configs: ref_tree_run over `batch` polys split across
+// `threads` host threads (each shard independent); elapsed wall ns in *ns
+int ref_time_tree(uint64_t p, uint32_t N, unsigned n_bits, int nega, uint32_t layers, int kind,
+                  int dir, uint64_t* a, const uint64_t* b, size_t batch, int threads, uint64_t* ns) {
+  return guarded([&] {
+    if (threads < 1) threads = 1;
+    std::atomic<int> failed{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+      const size_t lo = batch * t / threads, hi = batch * (t + 1) / threads;
+      pool.emplace_back([&, lo, hi] {
+        if (ref_tree_run(p, N, n_bits, nega, layers, kind, dir, a + lo * N, b ? b + lo * N : nullptr,
+                         hi - lo) != 0)
+          failed = 1;
+      });
+    }
+    for (auto& th : pool) th.join();
+    const auto t1 = std::chrono::steady_clock::now();
+    *ns = static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+    if (failed) throw contract_violation("ref_time_tree: a worker failed");
+  });
+}
+
+// cyclic_convolution_via_ntt (transform.hpp:372-379) over host threads, wall ns in *ns
+int ref_time_convolution(void* hv, int kind, const uint64_t* x, const uint64_t* y, uint64_t* out,
+                         size_t batch, int threads, uint64_t* ns) {
+  return guarded([&] {
+    if (threads < 1) threads = 1;
+    std::atomic<int> failed{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+      const size_t lo = batch * t / threads, hi = batch * (t + 1) / threads;
+      const size_t N = static_cast<Handle*>(hv)->P.size;
+      pool.emplace_back([&, lo, hi, N] {
+        if (ref_convolution(hv, kind, x + lo * N, y + lo * N, out + lo * N, hi - lo) != 0) failed = 1;
+      });
+    }
+    for (auto& th : pool) th.join();
+    const auto t1 = std::chrono::steady_clock::now();
+    *ns = static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+    if (failed) throw contract_violation("ref_time_convolution: a worker failed");
   });
 }
 

@@ -7,7 +7,9 @@ one loop iteration of a fast256 consumer warp transforms 2 polynomials, i.e. 64
 butterflies per thread (8 layers x 8) or 56 (7 layers).  The fmaheavy estimate uses the
 measured issue costs (profiles/r1a_imad_microbench.txt): IMAD 2 cycles, IMAD.HI /
 IMAD.WIDE 4 cycles per warp instruction on one SM sub-partition.
-Usage: python tools/sass_census.py [lib.so] [name-regex] [--ops]   (--ops: opcode breakdown)
+Usage: python tools/sass_census.py [lib.so] [name-regex] [--ops] [--json OUT]
+  --ops: opcode breakdown; --json OUT: also write the rows (+ the library's sha256) for
+  bench.py's executed-instruction IMAD roof
 """
 import re
 import subprocess
@@ -16,6 +18,12 @@ from collections import Counter
 
 OPS = "--ops" in sys.argv
 sys.argv = [a for a in sys.argv if a != "--ops"]
+JSON = None
+if "--json" in sys.argv:
+    i = sys.argv.index("--json")
+    JSON = sys.argv[i + 1]
+    del sys.argv[i:i + 2]
+rows = []
 
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2402_00675_b200/libnttk_gpu.so"
 pat = re.compile(sys.argv[2] if len(sys.argv) > 2 else r"tma_kernel.*(ImprovedN16ILb0EEEtLi8|ImprovedN32EjLi8|HarveyILi16ELb0EEEtLi8|HarveyILi32ELb0EEEjLi8|SmontILi16EEtLi8|SmontILi32EEjLi8)")
@@ -60,5 +68,20 @@ for part in re.split(r"\n\s+Function : ", txt)[1:]:
     short = re.sub(r"_ZN9nttk_b200\w*?_GLOBAL__N__\w+?\d+(fwd|inv)", r"\1", name)[:70]
     print(f"{short:70s} {n:5d} {imad:5d} {hi:4d} {wide:5d} {iadd:5d} {alu:4d} {lsu:4d} "
           f"{fcyc:12d} {fcyc / bfly:8.2f}")
+    rows.append({"kernel": name, "instr": n, "imad": imad, "imad_hi": hi, "imad_wide": wide,
+                 "iadd3": iadd, "alu": alu, "lsu": lsu, "fmaheavy_cycles_per_iter": fcyc,
+                 "polys_per_iter": 2, "ops": dict(c.most_common())})
     if OPS:
         print("    " + "  ".join(f"{k}:{v}" for k, v in c.most_common()))
+
+if JSON:
+    import hashlib
+    import json
+
+    with open(lib, "rb") as fh:
+        sha = hashlib.sha256(fh.read()).hexdigest()
+    with open(JSON, "w") as fh:
+        json.dump({"lib": lib, "lib_sha256": sha,
+                   "note": "hottest consumer loop per kernel; one iteration = 2 polynomials per "
+                           "warp; fmaheavy cycles = 2 x IMAD + 4 x (IMAD.HI + IMAD.WIDE) per "
+                           "warp on one SM sub-partition", "rows": rows}, fh, indent=1)
