@@ -191,9 +191,10 @@ int run_transform(const HostParams& P, int kind, int dir, const void* in, void* 
 int run_product(const HostParams& P, int kind, const void* l, const void* r, void* out,
                 size_t batch, int elem, cudaStream_t st) {
   cudaError_t e;
-  if (nttk_b200::product_supports(P, kind, elem, l, r, out)) {
-    e = nttk_b200::product_launch(P, kind, l, r, out, batch, elem, st);
-  } else if ((P.N >> P.layers) == 2) {
+  const bool basemul = (P.N >> P.layers) == 2;
+  if (nttk_b200::product_supports(P, kind, basemul, elem, l, r, out)) {
+    e = nttk_b200::product_launch(P, kind, basemul, l, r, out, batch, elem, st);
+  } else if (basemul) {
     std::string err;
     const nttk_b200::DeviceTables* T = P.device_tables(current_device(), err);
     if (!T) return fail(NTTK_CUDA, err);
@@ -436,8 +437,10 @@ int nttk_pointwise_multiply(nttk_params_t h, int kind, const void* d_l, const vo
   if (int s = check_kind(h->P, kind, "pointwise_multiply")) return s;
   if (int s = check_canonical_storage(h->P, elem, "pointwise_multiply")) return s;
   if (int s = need_device("pointwise_multiply")) return s;
-  cudaError_t e = nttk_b200::generic_pointwise(h->P, kind, d_l, d_r, d_out, batch, elem,
-                                               static_cast<cudaStream_t>(stream));
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = nttk_b200::product_supports(h->P, kind, false, elem, d_l, d_r, d_out)
+                      ? nttk_b200::product_launch(h->P, kind, false, d_l, d_r, d_out, batch, elem, st)
+                      : nttk_b200::generic_pointwise(h->P, kind, d_l, d_r, d_out, batch, elem, st);
   if (batch) ++g_launches;
   if (e != cudaSuccess) return cuda_fail(e, "pointwise_multiply");
   return NTTK_OK;
