@@ -96,7 +96,9 @@ int nttk_params_get_info(nttk_params_t P, nttk_params_info* out);
  * (dir 0 forward, 1 inverse): 1/2 fast canonicalisation (u16 Barrett / u32 shift), 4 fused
  * u16 first merge layer, 8 lazy merge, 16 forward twiddle-1 blocks, 32 inverse twiddle-1
  * blocks (TW1), 64 u16 inverse without canonicalisation (DEFER), 128 u32 inverse partial
- * canonicalisation.  Status 2 if the kind is not built into P. */
+ * canonicalisation, 256 (dir 1) the fused polymul runs the kind's lazy Montgomery twin
+ * (harvey / smont, n = 16), 512 the direction runs the n = 16 product on an n = 32 improved
+ * parameter set (narrow image).  Status 2 if the kind is not built into P. */
 int nttk_params_fast_flags(nttk_params_t P, int kind, int dir, uint32_t* flags);
 /* read back a host table (names: dif_w dif_wq dif_mont ct_plain ct_plantard ct_mont
  * ct_smont gs_plain gs_wq gs_mont gs_plantard gs_smont); returns its length */

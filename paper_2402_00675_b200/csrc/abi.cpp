@@ -160,7 +160,7 @@ int run_transform(const HostParams& P, int kind, int dir, const void* in, void* 
   cudaError_t e;
   if (P.N != 256 && use_fast(P, kind) && nttk_b200::fastn_supports(P, elem, in, out)) {
     std::string err;
-    const uint32_t* tab = P.fastn_table(current_device(), kind, dir, err);
+    const uint32_t* tab = P.fastn_table(current_device(), P.image(kind, dir), dir, err);
     if (!tab) return fail(NTTK_CUDA, err);
     e = nttk_b200::fastn_launch(P, kind, dir, in, out, batch, elem, tab, st);
     g_launches += batch ? 1 : 0;
@@ -380,7 +380,7 @@ int nttk_params_fast_flags(nttk_params_t h, int kind, int dir, uint32_t* flags) 
   if (!h || !flags) return fail(NTTK_CONTRACT, "params_fast_flags: null argument");
   if (dir != 0 && dir != 1) return fail(NTTK_CONTRACT, "params_fast_flags: dir must be 0 or 1");
   if (int s = check_kind(h->P, kind, "params_fast_flags")) return s;
-  *flags = h->P.fast[kind][dir].flags;
+  *flags = h->P.fast[kind][dir].flags | (h->P.image(kind, dir) == nttk_b200::kNarrow ? 512u : 0u);
   return NTTK_OK;
 }
 

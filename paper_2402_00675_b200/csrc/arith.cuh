@@ -144,6 +144,10 @@ struct ImprovedN16 {
   __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
     return mp_n16<PAPER_FORM>(v, A.scale_lo, A.p);
   }
+  // MP(1^, v): canonical residue of any v inside Prop. 4's range (narrow inverse)
+  __device__ static uint32_t canon1(uint32_t v, const FastArgs& A) {
+    return mp_n16<false>(v, A.one_lo, A.p);
+  }
   // (X, Y) -> (MP(n^, X + Y), MP((w n^{-1})^, X + off - Y)): both canonical, so the
   // result equals scale() applied after the last merge (canonical outputs are unique)
   __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
@@ -506,6 +510,107 @@ struct Smont {
   __device__ static uint32_t mulc(uint32_t y, Enc e, const FastArgs& A) {
     const int32_t r = smont_mul<N_BITS>(static_cast<int32_t>(y), static_cast<int32_t>(e.x), e.y, A);
     return static_cast<uint32_t>(r + (r < 0 ? static_cast<int32_t>(A.p) : 0));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Lazy twins of Harvey<16, true> and Smont<16> for the fused polymul (polymul_tma.cu).
+// Inside fused fwd(a), fwd(b), product, inverse only the canonical output is pinned (it is
+// unique), so -- exactly as the improved kernels carry lazy Plantard words -- the
+// Montgomery kinds drop every intermediate normalisation that exists only to keep the
+// standalone transform's words bit-exact:
+//   HarveyLazy16  no [0, 2p) min-subtractions in the CT forward or the GS inverse; the
+//                 inverse carries the improved kernel's offsets 2^{m-1} p, the last layer
+//                 folds N^{-1} and ends with one exact Barrett reduction (mod_cb)
+//   SmontLazy16   no signed Barrett on the GS sums; N^{-1} folded into the last layer,
+//                 which canonicalises with one lift + mod_cb
+// Host-validated bounds (params.cpp, ProdArgs::lazy; n = 16, u16):
+//   harvey: (1 + 2L) p < 2^16 (every forward/product operand < 2^16, so each Montgomery
+//           product r = d + p lies in (0, 2p)); (p - 1) 2^L p < 2^32 (inverse products);
+//           final r < (p - 1) 2^L p / 2^16 + p < 2^17 (mod_cb exact)
+//   smont:  (L + 1) p <= 2^16 (|r| < p in the forward and the product);
+//           (p/2 + 1) 2^L p + 2^15 p < 2^31 (no int32 overflow in the inverse products);
+//           final |r| + lzk < 2^17 with lzk = K p > max |r| (FastArgs::lzk)
+// Montgomery difference: d = (w t >> 16) - hi(q p) with q = (p^{-1} w t mod 2^16) << 16;
+// the Montgomery product is r = d + p (harvey_mul), so callers fold the + p into their adds.
+__device__ __forceinline__ uint32_t mont_diff16(uint32_t t, uint32_t w, const FastArgs& A) {
+  const uint32_t prod = w * t;
+  const uint32_t q16 = prod * A.pinv;
+  return (prod >> 16) - __umulhi(q16, A.p);
+}
+
+struct HarveyLazy16 {
+  using Tw = uint32_t;
+  static constexpr bool kSigned = false;
+  static constexpr bool kFold = true;
+  __device__ static Tw tw(const FastArgs& A, int k) { return A.lo[k]; }
+  // CT: X' = X + r, Y' = X + 2p - r with r = d + p in (0, 2p)
+  __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    const uint32_t d = mont_diff16(y, w, A);
+    y = x + A.p - d;
+    x = x + d + A.p;
+  }
+  // GS at merge depth m (off = 2^{m-1} p >= every Y input): X' = X + Y, Y' = r(X + off - Y)
+  __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    x = x + y + A.zero;
+    y = mont_diff16(t, w, A) + A.p;
+  }
+  __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t off, const FastArgs& A) {
+    const uint32_t t = x + off - y;
+    const uint32_t a = mont_diff16(x + y + A.zero, A.scale_lo, A) + A.p;
+    const uint32_t b = mont_diff16(t, A.fold_lo, A) + A.p;
+    x = mod_cb(a, A);
+    y = mod_cb(b, A);
+  }
+  __device__ static uint32_t scale(uint32_t v, const FastArgs& A) { return mod_cb(mont_diff16(v, A.scale_lo, A) + A.p, A); }
+  // product stage: canonical encoding x R mod p (one min), canonical product
+  using Enc = uint32_t;
+  __device__ static Enc enc(uint32_t x, const ProdArgs& Q, const FastArgs& A) {
+    const uint32_t r = mont_diff16(x, Q.enc_lo, A) + A.p;
+    return umin32(r, r - A.p);
+  }
+  __device__ static Enc genc(int k, const ProdArgs& Q) { return Q.g_lo[k]; }
+  __device__ static uint32_t mulc(uint32_t y, Enc e, const FastArgs& A) {
+    const uint32_t r = mont_diff16(y, e, A) + A.p;
+    return umin32(r, r - A.p);
+  }
+};
+
+struct SmontLazy16 {
+  using Tw = uint2;
+  static constexpr bool kSigned = true;
+  static constexpr bool kFold = true;
+  __device__ static Tw tw(const FastArgs& A, int k) { return make_uint2(A.lo[k], A.hi[k]); }
+  __device__ static void fwd(uint32_t& x, uint32_t& y, Tw w, const FastArgs& A) {
+    Smont<16>::fwd(x, y, w, A);
+  }
+  __device__ static void inv(uint32_t& x, uint32_t& y, Tw w, uint32_t, const FastArgs& A) {
+    const int32_t xs = static_cast<int32_t>(x), ys = static_cast<int32_t>(y);
+    x = static_cast<uint32_t>(xs + ys) + A.zero;
+    y = static_cast<uint32_t>(smont_mul<16>(xs - ys, static_cast<int32_t>(w.x), w.y, A));
+  }
+  // canonical residue of a signed |r| < lzk (lzk = K p): lift, then exact Barrett
+  __device__ static uint32_t canon(int32_t r, const FastArgs& A) {
+    return mod_cb(static_cast<uint32_t>(r) + A.lzk, A);
+  }
+  __device__ static void inv_last(uint32_t& x, uint32_t& y, uint32_t, const FastArgs& A) {
+    const int32_t xs = static_cast<int32_t>(x), ys = static_cast<int32_t>(y);
+    const int32_t a = smont_mul<16>(xs + ys, static_cast<int32_t>(A.scale_lo), A.scale_hi, A);
+    const int32_t b = smont_mul<16>(xs - ys, static_cast<int32_t>(A.fold_lo), A.fold_hi, A);
+    x = canon(a, A);
+    y = canon(b, A);
+  }
+  __device__ static uint32_t scale(uint32_t v, const FastArgs& A) {
+    return canon(smont_mul<16>(static_cast<int32_t>(v), static_cast<int32_t>(A.scale_lo), A.scale_hi, A), A);
+  }
+  using Enc = uint2;
+  __device__ static Enc enc(uint32_t x, const ProdArgs& Q, const FastArgs& A) {
+    return Smont<16>::enc(x, Q, A);
+  }
+  __device__ static Enc genc(int k, const ProdArgs& Q) { return Smont<16>::genc(k, Q); }
+  __device__ static uint32_t mulc(uint32_t y, Enc e, const FastArgs& A) {
+    return Smont<16>::mulc(y, e, A);
   }
 };
 

@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
 // improved n=16); 3: u32 partial canonicalisation to [0, 2p) with doubled merge offsets
 // (A.flags bit 7, lazy improved n=32).  MODE bit 2: lazy merge outputs (A.flags bit 3, improved).  Bit 3: TW1
 // multiply-free block-0 merges (A.flags bit 5); bit 4: DEFER, no input canonicalisation
-// (A.flags bit 6, u16 improved n=16) -- see inv_body_lazy.
+// (A.flags bit 6, u16 improved n=16) -- see inv_body_lazy.  Bit 5: narrow image
+// (A.flags bit 9, ImprovedN16 on n = 32 parameters) -- see inv_body_narrow.
 template <class K, class IO, int L, int MODE>
 __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
     inv256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
@@ -193,8 +194,11 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
       }
-      inv_body<K, L, CM == 2, (MODE & 4) != 0, (MODE & 8) != 0, (MODE & 16) != 0, kPacked, CM == 3 ? 1 : 0>(
-          v, twl, A, X);
+      if constexpr ((MODE & 32) != 0)
+        inv_body_narrow<K, L>(v, twl, A, X);
+      else
+        inv_body<K, L, CM == 2, (MODE & 4) != 0, (MODE & 8) != 0, (MODE & 16) != 0, kPacked, CM == 3 ? 1 : 0>(
+            v, twl, A, X);
       store_strided<IO>(optr, j, v, S, X, poly < nb);
       poly += pstep;
       optr += ostep;
@@ -272,6 +276,11 @@ cudaError_t inv_launch_canon(const void* in, void* out, size_t batch, const Fast
 
 template <class K, class IO, int L>
 cudaError_t inv_launch(const void* in, void* out, size_t batch, const FastArgs& A, cudaStream_t st) {
+  if constexpr (std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 4) {
+    if (A.flags & 512)  // narrow image (n = 32 parameters on the n = 16 product)
+      return (A.flags & 2) ? inv_launch_mode<K, IO, L, 32 | 1>(in, out, batch, A, st)
+                           : inv_launch_mode<K, IO, L, 32>(in, out, batch, A, st);
+  }
   if constexpr (lazy_of<K>::value) {
     if (A.flags & 8) {
       if constexpr (L == 8) {
@@ -348,6 +357,9 @@ cudaError_t fast256_tma_launch_one(const HostParams& P, int kind, int dir, const
   if (batch == 0) return cudaSuccess;
   switch (kind) {
     case NTTK_IMPROVED:
+      if (P.image(kind, dir) == kNarrow)  // n = 32 parameters on the n = 16 product
+        return by_io<ImprovedN16<false>, false>(dir, L, elem_bytes, in, out, batch,
+                                                P.fast[kNarrow][dir], st);
       return n16 ? by_io<ImprovedN16<false>, false>(dir, L, elem_bytes, in, out, batch, A, st)
                  : by_io<ImprovedN32, false>(dir, L, elem_bytes, in, out, batch, A, st);
     case NTTK_HARVEY:

@@ -460,6 +460,51 @@ __device__ __forceinline__ void inv_body_n_lazy(uint32_t (&v)[32], const uint2* 
   }
 }
 
+// narrow inverse (ImprovedN16 on an n = 32 improved parameter set; tma_common.cuh
+// inv_body_narrow): compile-time bound exponents e[], reduction by MP(1^, .) before a merge
+// that would leave n = 16's Prop. 4 range and before the transpose
+template <class K, int LOGN>
+__device__ __forceinline__ void inv_body_n_narrow(uint32_t (&v)[32], const uint2* tws, const FastArgs& A,
+                                                  const XposeN<(1 << LOGN) / 32>& X, int j) {
+  using Tw = typename K::Tw;
+  constexpr int G = (1 << LOGN) / 32;
+  int e[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) e[k] = 0;
+#pragma unroll
+  for (int s = LOGN; s >= 6; --s) {  // phase 1: contiguous, register half-span h = 2^{LOGN-s}
+    const int h = 1 << (LOGN - s);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      const Tw w = tw_smem<Tw>(tws, seg_base<LOGN, true>(s) + (k >> (LOGN - s + 1)) * G + j);
+      narrow_bf<K>(v[k], v[k + h], e[k], e[k + h], w, false, A);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (e[k]) v[k] = K::canon1(v[k], A);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    v[k] = X.get(k);
+    e[k] = 0;
+  }
+#pragma unroll
+  for (int s = 5; s >= 1; --s) {  // phase 2: strided, h = 2^{5-s}, N^{-1} folded into s = 1
+    const int h = 1 << (5 - s);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      const Tw w = s == 1 ? Tw{} : K::tw(A, 32 - (2 << (s - 1)) + (k >> (6 - s)));
+      narrow_bf<K>(v[k], v[k + h], e[k], e[k + h], w, s == 1, A);
+    }
+  }
+}
+
 template <int LOGN, bool TRANSPOSE, bool MERGE>
 __device__ __forceinline__ void stage_table(uint2* tws, const uint32_t* tab) {
   constexpr int N = 1 << LOGN, G = N / 32;
@@ -526,7 +571,8 @@ __global__ void __launch_bounds__(GeoN<LOGN, IO, kFwdConsN>::kThreadsN)
 }
 
 // MODE bits 0-1 -- 0: generic canonicalisation of the input words; 1: host-validated fast
-// form.  MODE bit 2: lazy merge (policy kLazy, A.flags bit 3); bit 3: TW1 (A.flags bit 5).
+// form.  MODE bit 2: lazy merge (policy kLazy, A.flags bit 3); bit 3: TW1 (A.flags bit 5);
+// bit 5: narrow image (A.flags bit 9, inv_body_n_narrow).
 template <class K, class IO, int LOGN, int MODE>
 __global__ void __launch_bounds__(kThreads)
     invn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
@@ -579,7 +625,8 @@ __global__ void __launch_bounds__(kThreads)
     release_stage(&empty[s], lane);
 #pragma unroll
     for (int k = 0; k < 32; ++k) v[k] = canon<IO, K::kSigned, (MODE & 3) == 1>(v[k], A);
-    if constexpr ((MODE & 4) != 0) inv_body_n_lazy<K, LOGN, (MODE & 8) != 0>(v, tws, A, X, j);
+    if constexpr ((MODE & 32) != 0) inv_body_n_narrow<K, LOGN>(v, tws, A, X, j);
+    else if constexpr ((MODE & 4) != 0) inv_body_n_lazy<K, LOGN, (MODE & 8) != 0>(v, tws, A, X, j);
     else inv_body_n<K, LOGN>(v, tws, A, X, j);
     store_strided_n<IO, G>(out + poly * GN::N, j, v, X, poly < batch);
   }
@@ -642,6 +689,9 @@ cudaError_t inv_n_canon(const void* in, void* out, size_t batch, const uint32_t*
 template <class K, class IO, int LOGN>
 cudaError_t inv_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
                   cudaStream_t st) {
+  if constexpr (std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 4) {
+    if (A.flags & 512) return inv_n_canon<K, IO, LOGN, 32>(in, out, batch, tab, A, st);  // narrow
+  }
   if constexpr (lazy_of<K>::value) {
     if (A.flags & 8) {
       if (A.flags & 32) return inv_n_canon<K, IO, LOGN, 4 | 8>(in, out, batch, tab, A, st);
@@ -686,6 +736,9 @@ cudaError_t fastn_launch(const HostParams& P, int kind, int dir, const void* in,
   if (batch == 0) return cudaSuccess;
   switch (kind) {
     case NTTK_IMPROVED:
+      if (P.image(kind, dir) == kNarrow)  // n = 32 parameters on the n = 16 product (tab: narrow)
+        return by_elem<ImprovedN16<false>, false>(dir, logn, elem_bytes, in, out, batch, tab,
+                                                  P.fast[kNarrow][dir], st);
       return n16 ? by_elem<ImprovedN16<false>, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st)
                  : by_elem<ImprovedN32, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st);
     case NTTK_HARVEY:

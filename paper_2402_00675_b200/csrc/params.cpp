@@ -251,6 +251,11 @@ void fill_fast(HostParams& P, int kind) {
       } else if (kind == NTTK_NTL) {
         A.fold_lo = static_cast<uint32_t>(wl);
         A.fold_hi = static_cast<uint32_t>((u128(wl) << P.n_bits) / p);
+      } else if (kind == NTTK_SMONT) {  // SmontLazy16::inv_last (fused polymul)
+        const int64_t ws = to_smont(wl, c);
+        const uint64_t fq = static_cast<uint64_t>(ws) * c.p_inv_beta & c.beta_mask;
+        A.fold_lo = static_cast<uint32_t>(ws);
+        A.fold_hi = n16 ? static_cast<uint32_t>(fq << 16) : static_cast<uint32_t>(fq);
       }
     }
     // full per-direction twiddle words (reference table order) in the kind's encoding
@@ -394,7 +399,81 @@ void fill_fast(HostParams& P, int kind) {
       break;
     }
   }
+  // lazy twins of the Montgomery kinds for the fused polymul (arith.cuh HarveyLazy16 /
+  // SmontLazy16): n = 16, CT forward (negacyclic tree), bounds stated there
+  {
+    const uint64_t L = P.layers, pL = p << L;
+    FastArgs& AI = P.fast[kind][1];
+    const bool cb = (AI.flags & 1) && (P.fast[kind][0].flags & 1);
+    if (n16 && cb && P.tree == NTTK_NEGACYCLIC && kind == NTTK_HARVEY) {
+      if ((1 + 2 * L) * p < (uint64_t(1) << 16) && u128(p - 1) * pL < (u128(1) << 32) &&
+          ((u128(p - 1) * pL) >> 16) + 2 * p < (u128(1) << 17))
+        Q.lazy = 1;
+    }
+    if (n16 && cb && kind == NTTK_SMONT) {
+      const u128 half = p / 2 + 1;
+      const uint64_t rmax = static_cast<uint64_t>((half * pL >> 16) + p / 2 + 1);  // final |r|
+      const uint64_t lzk = (rmax / p + 1) * p;
+      if ((L + 1) * p < (uint64_t(1) << 15) && half * pL + (u128(p) << 15) < (u128(1) << 31) &&
+          2 * lzk < (uint64_t(1) << 17)) {
+        AI.lzk = static_cast<uint32_t>(lzk);
+        Q.lazy = 1;
+      }
+    }
+    if (Q.lazy) AI.flags |= 256;  // introspection only (nttk_params_fast_flags)
+  }
   P.fast_mask |= 1u << kind;
+}
+
+// Narrow image of an n = 32 improved parameter set (HostParams::narrow).  The improved
+// butterflies' words do not depend on n: X' = X + r, Y' = X + p - r with r = w t mod p
+// canonical, and the n = 16 modified Plantard product is exact for
+// W T < 2^16 (2^16 - p) (Prop. 4).  The forward's operands are its lazy
+// words, below (L + 1) p; so for small p (the paper's Table 2 presets: 7681, 12289) the
+// whole forward runs on the cheaper n = 16 product, bit-exact with the reference's n = 32
+// run.  The image is fill_fast's own output for the same tree at n = 16.
+void fill_narrow(HostParams& P) {
+  if (P.n_bits != 32 || P.p >= (1u << 15)) return;
+  const uint64_t p = P.p;
+  const Ctx c16 = make_ctx(p, 16, P.log2N);
+  const u128 lim = u128(c16.beta) * (c16.beta - p);  // Prop. 4: W T < 2^16 (2^16 - p)
+  if (!(u128(p - 1) * ((P.layers + 1) * p) < lim)) return;
+  HostParams T;
+  T.desc = P.desc;
+  T.desc.n_bits = 16;
+  T.p = P.p;
+  T.N = P.N;
+  T.log2N = P.log2N;
+  T.n_bits = 16;
+  T.tree = P.tree;
+  T.layers = P.layers;
+  T.kinds = 1u << NTTK_IMPROVED;
+  T.ctx = c16;
+  T.omega = P.omega;
+  T.omega_inv = P.omega_inv;
+  T.n_inv = P.n_inv;
+  T.ct_plain = P.ct_plain;
+  T.gs_plain = P.gs_plain;
+  T.gamma = P.gamma;
+  for (uint64_t w : T.ct_plain) T.ct_plantard.push_back(to_plantard(w, c16));
+  for (uint64_t w : T.gs_plain) T.gs_plantard.push_back(to_plantard(w, c16));
+  T.n_inv_hat = to_plantard(T.n_inv, c16);
+  if (!fast_eligible(T, NTTK_IMPROVED)) return;
+  fill_fast(T, NTTK_IMPROVED);
+  P.fast[kNarrow][0] = T.fast[NTTK_IMPROVED][0];
+  P.fastn_tab[kNarrow][0] = T.fastn_tab[NTTK_IMPROVED][0];
+  P.narrow[0] = true;
+  // inverse (tma_common.cuh inv_body_narrow): every GS operand below 2^kNarrowEmax p, kept
+  // there by MP(1^, .) reductions; only the full trees of the fast kernels carry the body
+  const bool full = (P.N == 256 && P.layers == 8) || ((P.N == 512 || P.N == 1024) && P.layers == P.log2N);
+  if (full && u128(p - 1) * (p << kNarrowEmax) < lim) {
+    FastArgs I = T.fast[NTTK_IMPROVED][1];
+    I.flags = (I.flags & 3u) | 512u;  // canonicalisation bits only: no lazy / TW1 / DEFER
+    I.one_lo = static_cast<uint32_t>(to_plantard(1, c16) * c16.mu);
+    P.fast[kNarrow][1] = I;
+    P.fastn_tab[kNarrow][1] = T.fastn_tab[NTTK_IMPROVED][1];
+    P.narrow[1] = true;
+  }
 }
 
 }  // namespace
@@ -416,8 +495,8 @@ const uint32_t* HostParams::fastn_table(int device, int kind, int dir, std::stri
   std::lock_guard<std::mutex> lock(mu_dev);
   if (!fastn_dev[device]) {
     const size_t stride = 2 * size_t(N);
-    std::vector<uint32_t> host(10 * stride, 0);
-    for (int k = 0; k < 5; ++k)
+    std::vector<uint32_t> host(12 * stride, 0);
+    for (int k = 0; k < 6; ++k)
       for (int d = 0; d < 2; ++d)
         std::copy(fastn_tab[k][d].begin(), fastn_tab[k][d].end(), host.begin() + (2 * k + d) * stride);
     uint32_t* buf = nullptr;
@@ -643,6 +722,7 @@ int build_params(const nttk_params_desc& d, HostParams& P, std::string& err) {
 
   for (int k : {NTTK_NTL, NTTK_HARVEY, NTTK_SCOTT, NTTK_IMPROVED, NTTK_SMONT})
     if (has(k) && fast_eligible(P, k)) fill_fast(P, k);
+  if ((P.fast_mask >> NTTK_IMPROVED) & 1u) fill_narrow(P);
   return NTTK_OK;
 }
 

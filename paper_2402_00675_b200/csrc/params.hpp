@@ -71,6 +71,7 @@ struct FastArgs {
                            // bit7: u32 inverse with partial canonicalisation to [0, 2p)
   uint32_t fold_lo = 0, fold_hi = 0;  // last merge twiddle times N^{-1}, kind encoding
   uint32_t soff = 0;       // scott: butterfly offset (N/L) p (butterfly.hpp:172-184)
+  uint32_t lzk = 0;        // SmontLazy16: K p > every final |r| (lift before mod_cb)
   uint32_t lo[256] = {};   // twiddle words in reference table order
   uint32_t hi[256] = {};   // high words of 64-bit premultiplied Plantard twiddles
 };
@@ -83,6 +84,8 @@ struct ProdArgs {
   uint32_t enc_lo = 0, enc_hi = 0;  // improved: (2^{4n} mod p) mu; harvey: 2^{2n} mod p; smont: centered R^2 + quotient factor
   uint32_t mu_lo = 0, mu_hi = 0;    // improved: p^{-1} mod 2^{2n}
   uint32_t basemul = 0;             // 1: degree-2 leaves (x^2 - gamma), 0: slotwise
+  uint32_t lazy = 0;                // 1: the fused polymul may run the kind's lazy twin
+                                    // (HarveyLazy16 / SmontLazy16, bounds in params.cpp)
   uint32_t g_lo[128] = {}, g_hi[128] = {};  // gamma per pair, kind encoding (basemul)
 };
 
@@ -90,6 +93,10 @@ struct PolymulArgs {
   FastArgs fwd, inv;
   ProdArgs prod;
 };
+
+constexpr int kNarrow = 5;  // pseudo-kind index of the narrow improved image
+// narrow inverse: every GS operand below 2^kNarrowEmax p (tma_common.cuh inv_body_narrow)
+constexpr int kNarrowEmax = 4;
 
 struct HostParams {
   nttk_params_desc desc{};
@@ -108,11 +115,21 @@ struct HostParams {
   std::vector<uint64_t> gamma;
   // fast-path images, indexed [kind][dir] (dir 0 forward, 1 inverse)
   uint32_t fast_mask = 0;
-  FastArgs fast[5][2];
+  FastArgs fast[6][2];  // [5] = kNarrow
   ProdArgs prod[5];
+  // n = 16 evaluation of an n = 32 improved parameter set (params.cpp fill_narrow): the
+  // improved words do not depend on n, so when every operand of a
+  // direction lies inside the n = 16 Prop. 4 range the kernels run ImprovedN16 on the
+  // image fast[kNarrow][dir] (IMAD + IMAD.HI per product instead of IMAD.HI + IMAD +
+  // IMAD.WIDE)
+  bool narrow[2] = {};
+  // fast-image index of (kind, dir): kNarrow where the narrow image applies
+  int image(int kind, int dir) const {
+    return kind == NTTK_IMPROVED && n_bits == 32 && narrow[dir] ? kNarrow : kind;
+  }
   // N = 512 / 1024 fast kernels: whole per-direction tables, interleaved (lo, hi) words,
   // uploaded once per device on first use
-  std::vector<uint32_t> fastn_tab[5][2];
+  std::vector<uint32_t> fastn_tab[6][2];
   mutable uint32_t* fastn_dev[64] = {};
   const uint32_t* fastn_table(int device, int kind, int dir, std::string& err) const;
 

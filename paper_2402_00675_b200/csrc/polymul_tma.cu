@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "arith.cuh"
@@ -242,6 +243,16 @@ cudaError_t polymul256_launch(const HostParams& P, int kind, const void* a, cons
   return cudaSuccess;
 }
 
+// NTTK_POLYMUL_EAGER=1 runs the standalone-transform policies of harvey / smont inside the
+// fused kernel (the A/B of the lazy twins; tests check both against the oracle)
+bool eager_kinds() {
+  static const bool v = [] {
+    const char* e = std::getenv("NTTK_POLYMUL_EAGER");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 cudaError_t polymul256_launch_one(const HostParams& P, int kind, const void* a, const void* b,
                                   void* out, size_t batch, int elem_bytes, cudaStream_t st) {
   if (batch == 0) return cudaSuccess;
@@ -259,9 +270,13 @@ cudaError_t polymul256_launch_one(const HostParams& P, int kind, const void* a, 
       if (cyclic)
         return n16 ? by_io<Harvey<16, false>, true>(L, elem_bytes, a, b, out, batch, PA, st)
                    : by_io<Harvey<32, false>, true>(L, elem_bytes, a, b, out, batch, PA, st);
+      if (n16 && PA.prod.lazy && elem_bytes == 2 && !eager_kinds())
+        return by_io<HarveyLazy16, false>(L, elem_bytes, a, b, out, batch, PA, st);
       return n16 ? by_io<Harvey<16, true>, false>(L, elem_bytes, a, b, out, batch, PA, st)
                  : by_io<Harvey<32, true>, false>(L, elem_bytes, a, b, out, batch, PA, st);
     case NTTK_SMONT:
+      if (n16 && PA.prod.lazy && elem_bytes == 2 && !eager_kinds())
+        return by_io<SmontLazy16, false>(L, elem_bytes, a, b, out, batch, PA, st);
       return n16 ? by_io<Smont<16>, false>(L, elem_bytes, a, b, out, batch, PA, st)
                  : by_io<Smont<32>, false>(L, elem_bytes, a, b, out, batch, PA, st);
     default: return cudaErrorInvalidValue;

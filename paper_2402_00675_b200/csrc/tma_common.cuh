@@ -584,6 +584,77 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl
   }
 }
 
+// Narrow inverse (HostParams::narrow[1]: ImprovedN16 on an n = 32 improved parameter set,
+// e.g. the paper's Table 2 presets).  The inverse output is canonical, so its words are free,
+// but every GS operand must stay inside n = 16's Prop. 4 range W T < 2^16 (2^16 - p), i.e.
+// T < 2^EMAX p (host-validated, FastArgs::flags bit 9 with EMAX = kNarrowEmax).  e[]
+// (compile-time after the unroll) is the bound exponent of each register's word (word <
+// 2^e p): X' = X + Y < 2^{max e + 1} p, Y' = MP(w, T) is canonical; the GS offset is
+// 2^{max e} p >= Y.  A butterfly that would exceed 2^EMAX p first reduces its inputs with one
+// Plantard product by 1^ (canonical).  Words are reduced before the transpose, so phase 2
+// starts canonical and its e[] stays compile-time.
+
+template <class K>
+__device__ __forceinline__ void narrow_bf(uint32_t& x, uint32_t& y, int& ex, int& ey,
+                                          typename K::Tw w, bool last, const FastArgs& A) {
+  int em = ex > ey ? ex : ey;
+  if (em + 1 > kNarrowEmax) {
+    if (ex) x = K::canon1(x, A);
+    if (ey) y = K::canon1(y, A);
+    em = 0;
+  }
+  if (last) {
+    K::inv_last(x, y, A.off[em + 1], A);
+  } else {
+    K::inv(x, y, w, A.off[em + 1], A);
+  }
+  ex = em + 1;
+  ey = 0;
+}
+
+template <class K, int L, class TWL>
+__device__ __forceinline__ void inv_body_narrow(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                                const Xpose& X) {
+  using Tw = typename K::Tw;
+  constexpr int TL = 1 << L;
+  int e[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) e[r] = 0;
+#pragma unroll
+  for (int sl = 8; sl >= 5; --sl) {  // phase 1: merge layers s = L..5
+    if (sl > L) continue;
+    const int h = 1 << (8 - sl);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      const int base = sl == 5 ? 0 : sl == 6 ? 1 : sl == 7 ? 3 : 7;
+      narrow_bf<K>(v[r], v[r + h], e[r], e[r + h], twl[base + (r >> (9 - sl))], false, A);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    if (e[r]) v[r] = K::canon1(v[r], A);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    v[r] = X.get(r);
+    e[r] = 0;
+  }
+#pragma unroll
+  for (int sl = 4; sl >= 1; --sl) {  // phase 2: merge layers s = 4..1, N^{-1} folded into s = 1
+    const int h = 1 << (4 - sl);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      const Tw w = sl == 1 ? Tw{} : K::tw(A, TL - (2 << (sl - 1)) + (r >> (5 - sl)));
+      narrow_bf<K>(v[r], v[r + h], e[r], e[r + h], w, sl == 1, A);
+    }
+  }
+}
+
 // LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3); TW1 / DEFER: see there.
 template <class K, int L, bool FUSE, bool LAZY = false, bool TW1 = false, bool DEFER = false,
           bool PACKED = false, int OSH = 0, class TWL>

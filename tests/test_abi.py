@@ -189,3 +189,47 @@ def test_fast_flags_refused_where_bounds_fail(engine):
     assert P10.fast_flags(K.improved, 1) & TW1
     with pytest.raises(engine.ContractViolation):
         P10.fast_flags(K.harvey, 1)  # kind not built into these params
+
+
+PM_LAZY = 256
+
+
+def test_fast_flags_polymul_lazy_montgomery(engine):
+    """params.cpp: the fused polymul's lazy Montgomery twins (arith.cuh HarveyLazy16 /
+    SmontLazy16) are admitted for Kyber n = 16 (config 2) and refused where their bounds or
+    their n = 16 / CT-forward preconditions fail."""
+    K = engine.ButterflyKind
+    nega = engine.Tree.negacyclic
+    Pk = engine.build_params(3329, 256, 16, [K.harvey, K.smont, K.improved], tree=nega, layers=7,
+                             exact_bound=True)
+    assert Pk.fast_flags(K.harvey, 1) & PM_LAZY and Pk.fast_flags(K.smont, 1) & PM_LAZY
+    assert not Pk.fast_flags(K.improved, 1) & PM_LAZY
+    # cyclic harvey runs the DIF forward (no lazy twin); cyclic smont (CT) keeps it
+    Pc = engine.build_params(3329, 256, 16, [K.harvey, K.smont], exact_bound=True)
+    assert not Pc.fast_flags(K.harvey, 1) & PM_LAZY and Pc.fast_flags(K.smont, 1) & PM_LAZY
+    # n = 32 (Dilithium): eager policies
+    Pd = engine.build_params(8380417, 256, 32, [K.harvey, K.smont], tree=nega, layers=8,
+                             exact_bound=True)
+    assert not Pd.fast_flags(K.harvey, 1) & PM_LAZY and not Pd.fast_flags(K.smont, 1) & PM_LAZY
+    # (1 + 2L) p >= 2^16: a forward operand could reach 2^16, refused
+    Pb = engine.build_params(7681, 256, 16, [K.harvey, K.smont], tree=nega, layers=7,
+                             exact_bound=True)
+    assert not Pb.fast_flags(K.harvey, 1) & PM_LAZY and not Pb.fast_flags(K.smont, 1) & PM_LAZY
+
+
+NARROW = 512
+
+
+def test_fast_flags_narrow_image(engine):
+    """params.cpp fill_narrow: an n = 32 improved parameter set whose forward operands stay
+    inside the n = 16 Prop. 4 range runs on the n = 16 product (the paper's Table 2 presets);
+    Dilithium (p > 2^15) and n = 16 sets do not."""
+    K = engine.ButterflyKind
+    for name in ("kyber256", "newhope512", "falcon1024"):
+        P = engine.preset(name)
+        assert P.fast_flags(K.improved, 0) & NARROW, name
+        assert not P.fast_flags(K.harvey, 0) & NARROW
+    Pd = engine.build_params(8380417, 256, 32, [K.improved], exact_bound=True)
+    assert not Pd.fast_flags(K.improved, 0) & NARROW
+    Pk = engine.build_params(3329, 256, 16, [K.improved], exact_bound=True)
+    assert not Pk.fast_flags(K.improved, 0) & NARROW

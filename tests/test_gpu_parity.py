@@ -326,6 +326,25 @@ def test_polymul_vs_schoolbook(oracle, kind, n, tree, layers):
         assert (bm == Q.basemul(kind, Q.forward(kind, a), Q.forward(kind, b))).all()
 
 
+@pytest.mark.parametrize("kind,tree,layers", [(HARVEY, NEGA, 7), (SMONT, NEGA, 7), (SMONT, CYCLIC, 8)])
+def test_polymul_lazy_montgomery_extremes(oracle, kind, tree, layers):
+    """The fused polymul's lazy Montgomery twins (arith.cuh HarveyLazy16 / SmontLazy16, no
+    intermediate normalisation) on the operands that drive every bound to its maximum:
+    all p - 1, all zero, alternating extremes, one hot coefficient -- bit-exact with the
+    oracle's eager reference loop."""
+    p = KYBER
+    P = engine_params(p, 256, 16, [kind], tree=tree, layers=layers, exact=True)
+    assert P.fast_flags(kind, 1) & 256  # the lazy twin is the one that runs
+    Q = oracle.params(p, 256, 16, (kind,), tree=tree, layers=layers, exact=True)
+    rows = [np.full(256, p - 1), np.zeros(256, dtype=np.int64),
+            np.where(np.arange(256) % 2 == 0, p - 1, 0), np.eye(256, dtype=np.int64)[0] * (p - 1),
+            np.where(np.arange(256) < 128, p - 1, 0), np.arange(256) % p]
+    a = np.stack(rows + [oracle.rng(71, p, 256)]).astype(np.int64)
+    for b in (a, a[::-1].copy(), np.full_like(a, p - 1)):
+        got = from_dev(nttk.polymul(P, kind, to_dev(a, 2), to_dev(b, 2)))
+        assert (got == Q.polymul(kind, a, b)).all()
+
+
 def test_all_reference_kinds_at_presets_via_host_api(oracle):
     """Every ButterflyKind at the reference presets (generic kernel for N != 256 and n=32)."""
     for name, p, N, n in (("kyber256", 7681, 256, 32), ("falcon512", 12289, 512, 32),
