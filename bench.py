@@ -230,20 +230,32 @@ def ncu_traffic(kernel: str, nk: int, nd: int):
     return None
 
 
-def sass_census():
-    """Executed fmaheavy cycles per polynomial of the bench kernels from the committed SASS
-    census (tools/sass_census.py --json), flagged stale when the library changed since."""
+def kernel_source_sha():
+    """sha256 over the sources the library is compiled from (csrc/, include/, Makefile):
+    the SASS of a rebuild from the same sources with the same nvcc is the same."""
+    import glob
     import hashlib
 
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2402_00675_b200", "csrc", "*")))
+    files += [os.path.join(ROOT, "include", "nttk_gpu.h"), os.path.join(ROOT, "Makefile")]
+    for f in files:
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode() + b"\0" + fh.read())
+    return h.hexdigest()
+
+
+def sass_census():
+    """Executed fmaheavy cycles per polynomial of the bench kernels from the committed SASS
+    census (tools/sass_census.py --json), flagged stale when the kernel sources changed
+    since (the census records their sha256; a rebuild of the same sources is the same SASS)."""
     path = latest_profile("r*_sass_census.json")
     if not path:
         return None, None
     with open(path) as fh:
         d = json.load(fh)
-    lib = os.path.join(ROOT, "paper_2402_00675_b200", "libnttk_gpu.so")
     try:
-        with open(lib, "rb") as fh:
-            stale = hashlib.sha256(fh.read()).hexdigest() != d["lib_sha256"]
+        stale = kernel_source_sha() != d.get("src_sha256")
     except OSError:
         stale = True
     out = {}

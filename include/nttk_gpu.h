@@ -127,6 +127,21 @@ int nttk_basemul(nttk_params_t P, int kind, const void* d_lhs, const void* d_rhs
 int nttk_polymul(nttk_params_t P, int kind, const void* d_a, const void* d_b, void* d_out,
                  size_t batch, int elem_bytes, void* stream);
 
+/* ---- captured plans (small batches) ------------------------------------------
+ * Engine extension, no reference counterpart: the reference transforms one polynomial per
+ * call (transform.hpp:207-379); a batch of a few thousand polynomials finishes on the B200
+ * in microseconds, where the per-call host work (argument checks, launch) dominates.  A plan
+ * fixes one operation on fixed device buffers, runs it once (table uploads, checks), and
+ * records `repeat` back-to-back copies into a CUDA graph; nttk_plan_launch replays the graph
+ * on `stream` (one host call per `repeat` operations).  op: NTTK_PLAN_FORWARD / _INVERSE
+ * (d_b unused) or NTTK_PLAN_POLYMUL; same contracts as the device entry points above. */
+typedef struct nttk_plan* nttk_plan_t;
+enum { NTTK_PLAN_FORWARD = 0, NTTK_PLAN_INVERSE = 1, NTTK_PLAN_POLYMUL = 2 };
+int nttk_plan_create(nttk_params_t P, int kind, int op, const void* d_a, const void* d_b,
+                     void* d_out, size_t batch, int elem_bytes, int repeat, nttk_plan_t* plan);
+int nttk_plan_launch(nttk_plan_t plan, void* stream);
+void nttk_plan_destroy(nttk_plan_t plan);
+
 /* ---- host entry points (checked, synchronous) ------------------------------ */
 
 /* ntt_forward (transform.hpp:207-224) on host buffers: rejects non-canonical

@@ -955,3 +955,79 @@ int nttk_reduce_host(int op, const nttk_reduction_ctx* ctx, const int64_t* h_x, 
 }
 
 }  // extern "C"
+
+// ---- captured plans (include/nttk_gpu.h) ----------------------------------------
+struct nttk_plan {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t kernels = 0;  // kernel launches per replay (launch count diagnostics)
+};
+
+extern "C" {
+
+int nttk_plan_create(nttk_params_t h, int kind, int op, const void* d_a, const void* d_b,
+                     void* d_out, size_t batch, int elem, int repeat, nttk_plan_t* plan) {
+  if (!h || !plan) return fail(NTTK_CONTRACT, "plan_create: null argument");
+  if (op < NTTK_PLAN_FORWARD || op > NTTK_PLAN_POLYMUL)
+    return fail(NTTK_CONTRACT, "plan_create: unknown op");
+  if (repeat < 1) return fail(NTTK_CONTRACT, "plan_create: repeat must be >= 1");
+  *plan = nullptr;
+  if (int s = check_kind(h->P, kind, "plan_create")) return s;
+  if (int s = need_device("plan_create")) return s;
+  // the synchronous first-use uploads happen here, outside the capture (nothing runs: the
+  // buffers are untouched until the first nttk_plan_launch)
+  const HostParams& P = h->P;
+  std::string err;
+  const int dev = current_device();
+  if (!P.device_tables(dev, err)) return fail(NTTK_CUDA, "plan_create: " + err);
+  if (P.N != 256 && use_fast(P, kind))
+    for (int dir = 0; dir < 2; ++dir)
+      if (!P.fastn_table(dev, P.image(kind, dir), dir, err)) return fail(NTTK_CUDA, "plan_create: " + err);
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e, "plan_create");
+  nttk_plan* p = new nttk_plan;
+  int rc = NTTK_OK;
+  const uint64_t before = g_launches.load();
+  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed);
+  for (int i = 0; e == cudaSuccess && rc == NTTK_OK && i < repeat; ++i) {
+    switch (op) {
+      case NTTK_PLAN_FORWARD: rc = nttk_ntt_forward(h, kind, d_a, d_out, batch, elem, st); break;
+      case NTTK_PLAN_INVERSE: rc = nttk_intt_inverse(h, kind, d_a, d_out, batch, elem, st); break;
+      default: rc = nttk_polymul(h, kind, d_a, d_b, d_out, batch, elem, st);
+    }
+  }
+  p->kernels = (g_launches.load() - before) / uint64_t(repeat);
+  const std::string keep = g_err;
+  const cudaError_t ec = e == cudaSuccess ? cudaStreamEndCapture(st, &p->graph) : e;
+  if (e == cudaSuccess) e = ec;
+  if (e == cudaSuccess && rc == NTTK_OK) e = cudaGraphInstantiate(&p->exec, p->graph, 0);
+  cudaStreamDestroy(st);
+  if (rc != NTTK_OK) {
+    g_err = keep;  // the failing call's message, not the capture teardown's
+  } else if (e != cudaSuccess) {
+    rc = cuda_fail(e, "plan_create");
+  }
+  if (rc != NTTK_OK) {
+    nttk_plan_destroy(p);
+    return rc;
+  }
+  *plan = p;
+  return NTTK_OK;
+}
+
+int nttk_plan_launch(nttk_plan_t plan, void* stream) {
+  if (!plan || !plan->exec) return fail(NTTK_CONTRACT, "plan_launch: null plan");
+  const cudaError_t e = cudaGraphLaunch(plan->exec, static_cast<cudaStream_t>(stream));
+  g_launches += plan->kernels;
+  return e == cudaSuccess ? int(NTTK_OK) : cuda_fail(e, "plan_launch");
+}
+
+void nttk_plan_destroy(nttk_plan_t plan) {
+  if (!plan) return;
+  if (plan->exec) cudaGraphExecDestroy(plan->exec);
+  if (plan->graph) cudaGraphDestroy(plan->graph);
+  delete plan;
+}
+
+}  // extern "C"

@@ -276,10 +276,10 @@ cudaError_t inv_launch_canon(const void* in, void* out, size_t batch, const Fast
 
 template <class K, class IO, int L>
 cudaError_t inv_launch(const void* in, void* out, size_t batch, const FastArgs& A, cudaStream_t st) {
-  if constexpr (std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 4) {
+  if constexpr (std::is_same<K, ImprovedN16<false>>::value) {
     if (A.flags & 512)  // narrow image (n = 32 parameters on the n = 16 product)
-      return (A.flags & 2) ? inv_launch_mode<K, IO, L, 32 | 1>(in, out, batch, A, st)
-                           : inv_launch_mode<K, IO, L, 32>(in, out, batch, A, st);
+      return (A.flags & (sizeof(IO) == 2 ? 1u : 2u)) ? inv_launch_mode<K, IO, L, 32 | 1>(in, out, batch, A, st)
+                                                     : inv_launch_mode<K, IO, L, 32>(in, out, batch, A, st);
   }
   if constexpr (lazy_of<K>::value) {
     if (A.flags & 8) {

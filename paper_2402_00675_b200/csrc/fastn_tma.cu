@@ -689,7 +689,7 @@ cudaError_t inv_n_canon(const void* in, void* out, size_t batch, const uint32_t*
 template <class K, class IO, int LOGN>
 cudaError_t inv_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
                   cudaStream_t st) {
-  if constexpr (std::is_same<K, ImprovedN16<false>>::value && sizeof(IO) == 4) {
+  if constexpr (std::is_same<K, ImprovedN16<false>>::value) {
     if (A.flags & 512) return inv_n_canon<K, IO, LOGN, 32>(in, out, batch, tab, A, st);  // narrow
   }
   if constexpr (lazy_of<K>::value) {

@@ -135,7 +135,7 @@ EXPORTS = (
     "nttk_butterfly", "nttk_butterfly_host", "nttk_ntt_forward_observed",
     "nttk_intt_inverse_observed",
     "nttk_last_error", "nttk_launch_count", "nttk_device_available", "nttk_version",
-    "nttk_plantard_correction_fires",
+    "nttk_plantard_correction_fires", "nttk_plan_create", "nttk_plan_launch", "nttk_plan_destroy",
 )
 
 _lib_handle = None
@@ -185,6 +185,11 @@ def lib() -> C.CDLL:
         L.nttk_launch_count.restype = C.c_uint64
         L.nttk_plantard_correction_fires.restype = C.c_uint64
         L.nttk_version.restype = C.c_char_p
+        L.nttk_plan_create.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, sz, C.c_int, C.c_int,
+                                       C.POINTER(vp)]
+        L.nttk_plan_launch.argtypes = [vp, vp]
+        L.nttk_plan_destroy.argtypes = [vp]
+        L.nttk_plan_destroy.restype = None
         _lib_handle = L
     return _lib_handle
 
@@ -512,6 +517,39 @@ def inverse(P: NttParams, kind, x, out=None, stream=None):
         P.handle, int(kind), x.data_ptr(), out.data_ptr(), _batch_of(x, P.size), e,
         _stream_ptr(stream, x))))
     return out
+
+
+class Plan:
+    """A captured operation on fixed device tensors (nttk_plan_create, include/nttk_gpu.h):
+    `repeat` back-to-back forward / inverse / polymul calls recorded into one CUDA graph;
+    launch() replays it (small batches: one host call instead of `repeat`).  Creating a plan
+    runs nothing; the tensors must stay alive while the plan is used."""
+
+    FORWARD, INVERSE, POLYMUL = 0, 1, 2
+
+    def __init__(self, P: NttParams, kind, op: int, a, out, b=None, repeat: int = 1):
+        e = _torch_elem(a)
+        _match(a, out, "out")
+        if b is not None:
+            _match(a, b, "b")
+        self._keep = (P, a, b, out)  # the graph holds raw pointers
+        h = C.c_void_p()
+        _on_device(a, lambda: _check(lib().nttk_plan_create(
+            P.handle, int(kind), int(op), a.data_ptr(), b.data_ptr() if b is not None else None,
+            out.data_ptr(), _batch_of(a, P.size), e, int(repeat), C.byref(h))))
+        self.handle = h.value
+        self.device = a.device
+
+    def launch(self, stream=None) -> None:
+        import torch
+
+        with torch.cuda.device(self.device):
+            _check(lib().nttk_plan_launch(self.handle, _stream_ptr(stream, self._keep[1])))
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib_handle is not None:
+            _lib_handle.nttk_plan_destroy(self.handle)
+            self.handle = None
 
 
 def _binary(fn, P: NttParams, kind, a, b, out, stream):

@@ -228,6 +228,7 @@ def test_fast_flags_narrow_image(engine):
     for name in ("kyber256", "newhope512", "falcon1024"):
         P = engine.preset(name)
         assert P.fast_flags(K.improved, 0) & NARROW, name
+        assert P.fast_flags(K.improved, 1) & NARROW, name  # inverse: bounded merge operands
         assert not P.fast_flags(K.harvey, 0) & NARROW
     Pd = engine.build_params(8380417, 256, 32, [K.improved], exact_bound=True)
     assert not Pd.fast_flags(K.improved, 0) & NARROW

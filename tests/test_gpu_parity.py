@@ -855,3 +855,44 @@ def test_plantard_correction_fires_counter():
     assert want > 0
     nttk.modmul_sweep(2, q, n, 0, torch.from_numpy(W).cuda(), torch.from_numpy(T).cuda())
     assert nttk.plantard_correction_fires() - before == want
+
+
+def test_captured_plans_match_eager_calls(oracle):
+    """nttk_plan_create / nttk_plan_launch (include/nttk_gpu.h): a captured forward, inverse
+    and fused polymul (config 1 / config 2 shapes, small batch) give the eager calls' words;
+    creating a plan runs nothing; repeat > 1 replays the operation in place."""
+    Pn = engine_params(KYBER, 256, 16, [IMPROVED, HARVEY], tree=NEGA, layers=7, exact=True)
+    Q = oracle.params(KYBER, 256, 16, (IMPROVED, HARVEY), tree=NEGA, layers=7, exact=True)
+    B = 4096
+    f = oracle.rng(81, KYBER, B * 256).reshape(B, 256)
+    g = oracle.rng(82, KYBER, B * 256).reshape(B, 256)
+    x, y = to_dev(f, 2), to_dev(g, 2)
+    out = torch.zeros_like(x)
+    plan = nttk.Plan(Pn, IMPROVED, nttk.Plan.FORWARD, x, out)
+    torch.cuda.synchronize()
+    assert not out.any()  # nothing ran at creation
+    plan.launch()
+    torch.cuda.synchronize()
+    assert (from_dev(out) == Q.forward(IMPROVED, f)).all()
+    inv = torch.empty_like(x)
+    nttk.Plan(Pn, IMPROVED, nttk.Plan.INVERSE, out, inv).launch()
+    torch.cuda.synchronize()
+    assert torch.equal(inv, x)
+    for k in (IMPROVED, HARVEY):
+        pm = torch.empty_like(x)
+        nttk.Plan(Pn, k, nttk.Plan.POLYMUL, x, pm, b=y).launch()
+        torch.cuda.synchronize()
+        assert (from_dev(pm) == Q.polymul(k, f, g)).all()
+    # repeat: 3 in-place forwards of the N = 1024 preset (fastn kernel, narrow image)
+    P = nttk.preset("newhope1024")
+    Qn = oracle.params(12289, 1024, 32, (IMPROVED,))
+    h = oracle.rng(83, 12289, 8 * 1024).reshape(8, 1024)
+    z = to_dev(h, 4)
+    nttk.Plan(P, IMPROVED, nttk.Plan.INVERSE, z, z, repeat=3).launch()
+    torch.cuda.synchronize()
+    want = h
+    for _ in range(3):
+        want = Qn.inverse(IMPROVED, want)
+    assert (from_dev(z) == want).all()
+    with pytest.raises(nttk.ContractViolation):
+        nttk.Plan(Pn, SCOTT, nttk.Plan.FORWARD, x, out)  # kind not built into Pn

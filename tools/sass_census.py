@@ -78,10 +78,16 @@ if JSON:
     import hashlib
     import json
 
+    import os
+
     with open(lib, "rb") as fh:
         sha = hashlib.sha256(fh.read()).hexdigest()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from bench import kernel_source_sha
+
     with open(JSON, "w") as fh:
-        json.dump({"lib": lib, "lib_sha256": sha,
+        json.dump({"lib": lib, "lib_sha256": sha, "src_sha256": kernel_source_sha(),
                    "note": "hottest consumer loop per kernel; one iteration = 2 polynomials per "
                            "warp; fmaheavy cycles = 2 x IMAD + 4 x (IMAD.HI + IMAD.WIDE) per "
                            "warp on one SM sub-partition", "rows": rows}, fh, indent=1)
