@@ -473,22 +473,15 @@ def run_extras(dev):
     x = torch.randint(0, KYBER_Q, (4096, 256), generator=g, device=dev, dtype=torch.int32).to(torch.int16)
     y = torch.empty_like(x)
     ms = _time_ms(torch, lambda: nttk.forward(P1, K.improved, x, y), 200, 10)
-    # the same call captured 50x into one CUDA graph: device time per call without the
-    # host's per-call launch overhead (the ABI launches are capture-safe after warm-up)
+    # the same call through a captured plan (nttk_plan_create: 50 forwards in one CUDA graph):
+    # device time per call without the host's per-call work
     gms = None
     try:
-        cs = torch.cuda.Stream()
-        cs.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(cs):
-            nttk.forward(P1, K.improved, x, y)
-        torch.cuda.current_stream().wait_stream(cs)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for _ in range(50):
-                nttk.forward(P1, K.improved, x, y)
-        gms = _time_ms(torch, graph.replay, 20, 3) / 50
+        plan = nttk.Plan(P1, K.improved, nttk.Plan.FORWARD, x, y, repeat=50)
+        gms = _time_ms(torch, plan.launch, 20, 3) / 50
+        del plan
     except Exception as e:  # report, do not fail the bench line
-        gms = f"graph capture failed: {e}"
+        gms = f"plan capture failed: {e}"
     ex["config1_kyber7_fwd_4096"] = {
         "us_per_call": ms * 1e3, "polys_per_s": 4096 / (ms / 1e3),
         "graph_us_per_call": gms * 1e3 if isinstance(gms, float) else gms,

@@ -54,8 +54,10 @@ struct GeoN {
   // inverse with 128B-swizzled tensor-map stages (tma_common.cuh inv_swz): one box of
   // kTileN polynomials, 1024-byte aligned, no pad
   static constexpr int kRowsPerPoly = kPolyBytes / 128;
-  static constexpr int kBoxRows = kTileN * kRowsPerPoly;  // <= 256
-  static constexpr int kSwzStageBytes = kBoxRows * 128;
+  static constexpr int kTileRows = kTileN * kRowsPerPoly;
+  static constexpr int kBoxRows = kTileRows < 256 ? kTileRows : 256;  // TMA box limit
+  static constexpr int kBoxes = kTileRows / kBoxRows;                  // boxes per stage
+  static constexpr int kSwzStageBytes = kTileRows * 128;
   static constexpr int kSwzSmem = 1024 + kStages * kSwzStageBytes + kConsumers * kScratchWords * 4 +
                                   N * 8 + 2 * kStages * 8;
 };
@@ -573,12 +575,13 @@ __global__ void __launch_bounds__(GeoN<LOGN, IO, kFwdConsN>::kThreadsN)
 // MODE bits 0-1 -- 0: generic canonicalisation of the input words; 1: host-validated fast
 // form.  MODE bit 2: lazy merge (policy kLazy, A.flags bit 3); bit 3: TW1 (A.flags bit 5);
 // bit 5: narrow image (A.flags bit 9, inv_body_n_narrow).
-template <class K, class IO, int LOGN, int MODE>
-__global__ void __launch_bounds__(kThreads)
+template <class K, class IO, int LOGN, int MODE, int C = kConsumers>
+__global__ void __launch_bounds__((C + 1) * 32)
     invn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                     const uint32_t* __restrict__ tab, const __grid_constant__ FastArgs A,
                     const __grid_constant__ CUtensorMap tmap) {
-  using GN = GeoN<LOGN, IO>;
+  using GN = GeoN<LOGN, IO, C>;
+  constexpr int kConsumers = C;
   constexpr bool SWZ = inv_swz<IO>();
   constexpr int kStageBytes = SWZ ? GN::kSwzStageBytes : GN::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -589,15 +592,15 @@ __global__ void __launch_bounds__(kThreads)
   uint64_t* full = reinterpret_cast<uint64_t*>(tws + GN::N);
   uint64_t* empty = full + GN::kStages;
   stage_table<LOGN, true, true>(tws, tab);
-  init_barriers(full, empty, GN::kStages);
+  init_barriers(full, empty, GN::kStages, kConsumers);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kConsumers) {
     if (lane == 0) {
       if constexpr (SWZ)
-        produce_rows<GN::kBoxRows, GN::kStages>(
+        produce_rows<GN::kBoxRows, GN::kStages, GN::kBoxes>(
             &tmap, static_cast<uint32_t>((batch + GN::kTileN - 1) / GN::kTileN), stages, full, empty);
       else
-        produce_n<LOGN, IO>(in, batch, stages, full, empty);
+        produce_n<LOGN, IO, kConsumers>(in, batch, stages, full, empty);
     }
     return;
   }
@@ -650,12 +653,18 @@ cudaError_t fwd_n(const void* in, void* out, size_t batch, const uint32_t* tab, 
   return cudaGetLastError();
 }
 
+// consumer warps of the N = 512 / 1024 inverse (two 256-row tensor boxes per stage at 16)
+constexpr int inv_cons_n() {
+  return 16;
+}
+
 template <class K, class IO, int LOGN, int MODE>
 cudaError_t inv_n_mode(const void* in, void* out, size_t batch, const uint32_t* tab,
                        const FastArgs& A, cudaStream_t st) {
-  using GN = GeoN<LOGN, IO>;
+  constexpr int C = inv_cons_n();
+  using GN = GeoN<LOGN, IO, C>;
   static OccCache occ;
-  auto kern = invn_tma_kernel<K, IO, LOGN, MODE>;
+  auto kern = invn_tma_kernel<K, IO, LOGN, MODE, C>;
   constexpr bool SWZ = inv_swz<IO>();
   constexpr int smem = SWZ ? GN::kSwzSmem : GN::kSmem;
   // the swizzled input is addressed through a tensor map of <= kMaxMapRows rows
@@ -668,8 +677,8 @@ cudaError_t inv_n_mode(const void* in, void* out, size_t batch, const uint32_t* 
       const cudaError_t e = make_rows128_map(&map, src, uint64_t(n) * GN::kRowsPerPoly, GN::kBoxRows);
       if (e != cudaSuccess) return e;
     }
-    const int blocks = grid_n(kern, smem, occ, (n + GN::kTileN - 1) / GN::kTileN);
-    kern<<<blocks, kThreads, smem, st>>>(src, static_cast<IO*>(out) + done * GN::N, n, tab, A, map);
+    const int blocks = grid_n(kern, smem, occ, (n + GN::kTileN - 1) / GN::kTileN, GN::kThreadsN);
+    kern<<<blocks, GN::kThreadsN, smem, st>>>(src, static_cast<IO*>(out) + done * GN::N, n, tab, A, map);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     done += n;

@@ -122,8 +122,9 @@ __host__ __device__ constexpr uint32_t swz128(uint32_t L) {
   return (L & ~127u) | ((((L >> 4) & 7u) ^ ((L >> 7) & 7u)) << 4);
 }
 
-// producer over 128-byte-row tensor boxes: tile t = rows [t BOX_ROWS, (t+1) BOX_ROWS)
-template <int BOX_ROWS, int STAGES>
+// producer over 128-byte-row tensor boxes: tile t = rows [t NBOX BOX_ROWS, (t+1) NBOX BOX_ROWS),
+// NBOX boxes per stage (a box is at most 256 rows)
+template <int BOX_ROWS, int STAGES, int NBOX = 1>
 __device__ __forceinline__ void produce_rows(const CUtensorMap* map, uint32_t ntiles, uint8_t* stages,
                                              uint64_t* full, uint64_t* empty) {
   constexpr uint32_t kBytes = BOX_ROWS * 128;
@@ -131,8 +132,10 @@ __device__ __forceinline__ void produce_rows(const CUtensorMap* map, uint32_t nt
   uint32_t s = 0, phase = 0, k = 0;
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
     if (k >= uint32_t(STAGES)) mbar_wait(&empty[s], phase ^ 1);
-    mbar_expect_tx(&full[s], kBytes);
-    bulk_tensor_g2s(stages + s * kBytes, map, 0, int(t * BOX_ROWS), &full[s]);
+    mbar_expect_tx(&full[s], NBOX * kBytes);
+#pragma unroll
+    for (int b = 0; b < NBOX; ++b)
+      bulk_tensor_g2s(stages + (s * NBOX + b) * kBytes, map, 0, int((t * NBOX + b) * BOX_ROWS), &full[s]);
     if (++s == uint32_t(STAGES)) {
       s = 0;
       phase ^= 1;
