@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "arith.cuh"
@@ -61,7 +62,7 @@ template <class K, class IO, int DIR>
 using GeoSwzK = GeoSwz<IO, DIR, cons_of<K, IO, DIR>::value>;
 
 // ---------------------------------------------------------------------------
-template <class K, class IO, int L, bool PER_INDEX, bool W1>
+template <class K, class IO, int L, bool PER_INDEX, bool W1, bool F1 = false>
 __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
                                   GeoK<K, IO, 0, L, W1>::kC >= 16 ? 1 : fwd_minb<IO>())
     fwd256_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
@@ -83,6 +84,13 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
   const int j = lane & 15, half = lane >> 4;
   Xpose X;
   X.init(scratch + warp * kScratchWords + half * 272, j);
+  // F1: per-lane surplus corrections E[m] = (m - cj) p of the last layer (fwd_body_f1)
+  uint32_t E[5];
+  if constexpr (F1) {
+    const int cj = int(kF1Surplus) - ((j >> 3) & (j >> 2) & 1) - ((j >> 1) & 1) - (j & 1);
+#pragma unroll
+    for (int m = 0; m < 5; ++m) E[m] = pin(uint32_t(m - cj) * A.p);
+  }
   auto run = [&](const auto& twl) {
     // 32-bit tile/poly counters (the launcher splits batches >= 2^31), a stride pointer for
     // the output and incremental stage/phase: loop bookkeeping off the 64-bit datapath
@@ -97,7 +105,10 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
       load_strided<IO, K::kSigned>(
           v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
       release_stage(&empty[s], lane);
-      fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
+      if constexpr (F1)
+        fwd_body_f1<K>(v, twl, A, X, E);
+      else
+        fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
       if constexpr (sizeof(IO) == 4)
         store_contiguous_coalesced(reinterpret_cast<uint32_t*>(optr), j, v, X,
                                    scratch + warp * kScratchWords + half * 272, poly < nb);
@@ -214,6 +225,15 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
 }
 
 // ---------------------------------------------------------------------------
+// A/B switch while the F1 forward is measured (NTTK_FWD_F1=0 runs the umulhi form)
+bool f1_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("NTTK_FWD_F1");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 template <class Kern>
 int grid_for(Kern kern, int threads, int tile, int smem, OccCache& occ, size_t batch) {
   const int o = occupancy_current(kern, threads, smem, occ);
@@ -223,11 +243,11 @@ int grid_for(Kern kern, int threads, int tile, int smem, OccCache& occ, size_t b
   return static_cast<int>(tiles < full ? tiles : full);
 }
 
-template <class K, class IO, int L, bool PER_INDEX, bool W1>
+template <class K, class IO, int L, bool PER_INDEX, bool W1, bool F1 = false>
 cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs& A,
                          cudaStream_t st) {
   static OccCache occ;
-  auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1>;
+  auto kern = fwd256_tma_kernel<K, IO, L, PER_INDEX, W1, F1>;
   constexpr int smem = GeoK<K, IO, 0, L, W1>::kSmem;
   using G = GeoK<K, IO, 0, L, W1>;
   const int blocks = grid_for(kern, G::kThreadsP, G::kTileP, smem, occ, batch);
@@ -238,6 +258,10 @@ cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs
 template <class K, class IO, int L, bool PER_INDEX>
 cudaError_t fwd_launch(const void* in, void* out, size_t batch, const FastArgs& A, cudaStream_t st) {
   if constexpr (w1_of<K>::value && !PER_INDEX) {
+    if constexpr (std::is_same<K, ImprovedN16<false>>::value && L == 8) {
+      if ((A.flags & 1024) && f1_enabled())
+        return fwd_launch_w<K, IO, L, PER_INDEX, true, true>(in, out, batch, A, st);
+    }
     if (A.flags & 16) return fwd_launch_w<K, IO, L, PER_INDEX, true>(in, out, batch, A, st);
   }
   return fwd_launch_w<K, IO, L, PER_INDEX, false>(in, out, batch, A, st);

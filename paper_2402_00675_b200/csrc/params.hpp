@@ -68,10 +68,12 @@ struct FastArgs {
                            // bit4: forward block-0 twiddles are 1 (cyclic, improved);
                            // bit5: inverse phase-2 block-0 twiddles are 1 (TW1, L = 8);
                            // bit6: u16 inverse without canonicalisation (DEFER);
-                           // bit7: u32 inverse with partial canonicalisation to [0, 2p)
+                           // bit7: u32 inverse with partial canonicalisation to [0, 2p);
+                           // bit10: F1 forward (paper-form products, fwd_body_f1)
   uint32_t fold_lo = 0, fold_hi = 0;  // last merge twiddle times N^{-1}, kind encoding
   uint32_t soff = 0;       // scott: butterfly offset (N/L) p (butterfly.hpp:172-184)
   uint32_t lzk = 0;        // SmontLazy16: K p > every final |r| (lift before mod_cb)
+  uint32_t f1_sp = 0, f1_sp1 = 0;  // F1 forward surplus S p and (S + 1) p (fwd_body_f1)
   uint32_t lo[256] = {};   // twiddle words in reference table order
   uint32_t hi[256] = {};   // high words of 64-bit premultiplied Plantard twiddles
 };
@@ -97,6 +99,8 @@ struct PolymulArgs {
 constexpr int kNarrow = 5;  // pseudo-kind index of the narrow improved image
 // narrow inverse: every GS operand below 2^kNarrowEmax p (tma_common.cuh inv_body_narrow)
 constexpr int kNarrowEmax = 4;
+// F1 forward: surplus multiples of p injected by layer 1 (tma_common.cuh fwd_body_f1)
+constexpr uint32_t kF1Surplus = 6;
 
 struct HostParams {
   nttk_params_desc desc{};

@@ -373,6 +373,82 @@ __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const TWL& twl, cons
   }
 }
 
+// F1 forward (ImprovedN16, cyclic L = 8 with the W1 blocks, A.flags bit 10).  Layers 2..7
+// use the paper-form product with the final shift fused into the add:
+//   g = (y w_hat mu) >> 16;  R = g p + p;  X' = X + (R >> 16)  (LEA.HI);  Y' = 2X - X'
+// i.e. IMAD + SHF + IMAD + LEA.HI + IADD3 (2 fmaheavy + 3 ALU issue slots instead of IMAD +
+// IMAD.HI + 2 IADD3: 7.1 vs 7.7 cycles per warp-butterfly in registers,
+// profiles/r2_bf_forms_microbench.txt).  Y' = X - r is the reference's X + p - r minus p, so
+// every word carries a surplus sigma p (exact mod p, so the products are unchanged): layer 1
+// (twiddle 1 everywhere) injects S = kF1Surplus into both outputs for free, each F1 Y-step
+// spends one, and an X input always keeps sigma >= 1 (S = 6 covers the 5 F1 layers before
+// the last).  Layer 8 runs the umulhi form and subtracts the surplus in its IADD3s: for the
+// X position i = 16 j + r of the contiguous phase sigma = S - [i7 & i6] - popcount(i5..i1)
+// (block 0 of layer 2 is a W1 block, which spends none) -- a lane part cj and a register
+// part; E[m] = (m - cj) p are per-lane registers.  Largest word (9 + S) p, host-validated
+// against Prop. 4.  A CPU model of this schedule is checked against the reference loop in
+// tests/test_oracle.py.
+__device__ __forceinline__ void f1_bf(uint32_t& x, uint32_t& y, uint32_t w, const FastArgs& A) {
+  const uint32_t R = ((y * w) >> 16) * A.p + A.p;
+  const uint32_t s = x + (R >> 16);
+  y = x + x - s;
+  x = s;
+}
+
+template <class K, class TWL>
+__device__ __forceinline__ void fwd_body_f1(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                            const Xpose& X, const uint32_t (&E)[5]) {
+  static_assert(kW1Layers == 2, "the surplus schedule assumes W1 blocks on layers 1-2");
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // layer 1: one block, twiddle 1, r = Y (canonical input)
+    const uint32_t x = v[r], y = v[r + 8];
+    v[r] = x + y + A.f1_sp;
+    v[r + 8] = x + A.f1_sp1 - y;
+  }
+#pragma unroll
+  for (int sl = 2; sl <= 4; ++sl) {  // layers 2..4 (strided phase)
+    const int h = 8 >> (sl - 1);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      const int blk = r >> (5 - sl);
+      if (sl == 2 && blk == 0) {  // W1 block: canonical residue of Y = y_ref + S p (< (2 + S) p)
+        uint32_t c = v[r + h] - A.f1_sp;
+        c = umin32(c, c - A.p);
+        const uint32_t x = v[r];
+        v[r + h] = x + A.p - c;
+        v[r] = x + c + A.zero;
+        continue;
+      }
+      f1_bf(v[r], v[r + h], K::tw(A, (1 << (sl - 1)) - 1 + blk), A);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) X.put(r, v[r]);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) X.get4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+#pragma unroll
+  for (int sl = 5; sl <= 7; ++sl) {  // layers 5..7 (contiguous phase)
+    const int h = 1 << (8 - sl);
+    const int base = sl == 5 ? 0 : sl == 6 ? 1 : 3;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      f1_bf(v[r], v[r + h], twl[base + (r >> (9 - sl))], A);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 16; r += 2) {  // layer 8: umulhi form, surplus removed
+    const int k = ((r >> 1) & 1) + ((r >> 2) & 1) + ((r >> 3) & 1);
+    const uint32_t rr = mp_n16<false>(v[r + 1], twl[7 + (r >> 1)], A.p);
+    const uint32_t x = v[r];
+    v[r + 1] = x - rr + E[k + 1];
+    v[r] = x + rr + E[k];
+  }
+}
+
 template <class K, class = void>
 struct lazy_of {
   static constexpr bool value = false;

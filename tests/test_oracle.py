@@ -336,3 +336,51 @@ def test_sweep_full_grid_checksums_match_reference(oracle):
         ctx = oracle.ctx(row["q"], row["n_bits"], 0, row["ell"])
         _, s = oracle.sweep(row["variant"], ctx, A, B, want_results=False, threads=threads)
         assert "%016x" % s == row["checksum"], row
+
+
+def _f1_schedule_model(a, ct, p, S):
+    """Integer model of tma_common.cuh fwd_body_f1 (cyclic N = 256, L = 8): surplus S p
+    injected by layer 1, paper-form Y' = X - r on the multiply blocks of layers 2..7, the
+    last layer subtracts sigma p; asserts every F1 X input keeps a surplus >= 1 and every
+    product operand lies inside Prop. 4's n = 16 range."""
+    a = [int(v) for v in a]
+    lim = (1 << 16) * ((1 << 16) - p)
+    for s in range(1, 9):
+        span = 256 >> s
+        for i in range(256):
+            if i & span:
+                continue
+            x, y, blk = a[i], a[i + span], i >> (9 - s)
+            if s == 1:
+                a[i], a[i + span] = x + y + S * p, x + (S + 1) * p - y
+                continue
+            if s == 2 and blk == 0:
+                c = y - S * p
+                c = c - p if c >= p else c
+                a[i], a[i + span] = x + c, x + p - c
+                continue
+            w = int(ct[(1 << (s - 1)) - 1 + blk])
+            assert w * y < lim
+            r = w * y % p
+            if s < 8:
+                assert x - r >= 0
+                a[i], a[i + span] = x + r, x - r
+            else:
+                b = lambda k: (i >> k) & 1  # noqa: E731
+                sig = S - (b(7) & b(6)) - sum(b(k) for k in range(1, 6))
+                a[i], a[i + span] = x + r - sig * p, x + p - r - sig * p
+    return a
+
+
+@pytest.mark.parametrize("p", [3329, 7681])
+def test_f1_forward_schedule_matches_reference_loop(oracle, p):
+    """The surplus bookkeeping of the F1 forward (kF1Surplus = 6) reproduces the reference's
+    lazy forward words (butterfly.hpp:224-230 driven by transform.hpp:77-96) on extreme and
+    random inputs -- the CPU proof of the schedule the GPU kernel runs."""
+    Q = oracle.params(p, 256, 16 if p == 3329 else 32, (IMPROVED,), exact=p == 3329)
+    ct = Q.table("ct_plain")
+    rows = [np.full(256, p - 1), np.zeros(256, dtype=np.int64), oracle.rng(5, p, 256),
+            oracle.rng(6, p, 256), np.where(np.arange(256) % 3 == 0, p - 1, 0)]
+    want = Q.forward(IMPROVED, np.stack(rows))
+    for k, row in enumerate(rows):
+        assert _f1_schedule_model(row, ct, p, 6) == [int(v) for v in want[k]]
