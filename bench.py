@@ -551,12 +551,14 @@ def run_extras(dev):
         del xk, sk, ok
     ex["kinds_2^20"] = kt
     # the paper's Table 2 parameter sets (params.hpp:273-306 presets, n = 32, u32 storage):
-    # every kind, forward and inverse, 2^16 polys
-    t2 = {}
+    # every kind, forward and inverse, a steady-state batch of 2^27 coefficients (512 MiB in
+    # + 512 MiB out: 2^19 / 2^18 / 2^17 polys), with each kernel's HBM roof per polynomial
+    peak, _ = measured_peaks()
+    t2 = {"batch": "2^27 coefficients (u32) per call", "hbm_peak_GBps": peak}
     for name in ("kyber256", "newhope512", "newhope1024"):
         Pp = nttk.preset(name)
         Np, qp = Pp.size, Pp.p
-        Bp = 1 << 16
+        Bp = (1 << 27) // Np
         xp = torch.randint(0, qp, (Bp, Np), generator=g, device=dev, dtype=torch.int32)
         sp, op = torch.empty_like(xp), torch.empty_like(xp)
         row = {}
@@ -564,15 +566,20 @@ def run_extras(dev):
             fms = _time_ms(torch, lambda: nttk.forward(Pp, kind, xp, sp), 10)
             ims = _time_ms(torch, lambda: nttk.inverse(Pp, kind, sp, op), 10)
             assert torch.equal(op, xp), (name, kind)
+            roof = 2 * Np * 4 / (peak * 1e9) * 1e9  # ns per polynomial at the HBM peak
             row[kind.name] = {"fwd_ns_per_poly": fms * 1e6 / Bp, "inv_ns_per_poly": ims * 1e6 / Bp,
-                              "fast_path": kind in Pp.fast_path}
+                              "hbm_roof_ns_per_poly": roof,
+                              "fwd_frac_of_hbm": roof / (fms * 1e6 / Bp),
+                              "inv_frac_of_hbm": roof / (ims * 1e6 / Bp),
+                              "fast_path": kind in Pp.fast_path,
+                              "n16_product": bool(kind == K.improved and Pp.fast_flags(kind, 0) & 512)}
         cpu = table2_cpu_reference(qp, Np)
         if cpu:
             for kname, v in cpu.items():
                 row[kname].update(v)
         t2[name] = row
         del xp, sp, op
-    ex["table2_presets_2^16"] = t2
+    ex["table2_presets"] = t2
     # config 5: reduction sweep, 2^30 operand pairs (2^15 x 2^15 grid) per (q, variant) from
     # tests/golden/sweep_inputs.py; every checksum must equal the unmodified reference's over
     # the same full grid (tests/golden/sweep_2p30.json) or the bench line fails.  "mults" are

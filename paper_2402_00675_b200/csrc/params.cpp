@@ -429,6 +429,11 @@ void fill_fast(HostParams& P, int kind) {
         Q.lazy = 1;
       }
     }
+    // improved: the free F1 forwards (tma_common.cuh fwd_body_f1_free) carry up to (L - 1) p
+    // of surplus; every product operand stays below (2 L) p, inside Prop. 4's n = 16 range
+    if (n16 && kind == NTTK_IMPROVED && (L == 7 || L == 8) &&
+        u128(p - 1) * (2 * L * p) < u128(c.beta) * (c.beta - p))
+      Q.lazy = 1;
     if (Q.lazy) AI.flags |= 256;  // introspection only (nttk_params_fast_flags)
   }
   P.fast_mask |= 1u << kind;

@@ -90,7 +90,7 @@ constexpr int pm_minb() {
   return sizeof(IO) == 4 ? 2 : 1;
 }
 
-template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
+template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1, bool F1 = false>
 __global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, pm_minb<IO>())
     polymul256_tma_kernel(const IO* __restrict__ a, const IO* __restrict__ b, IO* __restrict__ out,
                           size_t batch, const __grid_constant__ PolymulArgs PA) {
@@ -133,6 +133,8 @@ __global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, pm_minb<IO>())
     for (int q = 0; q < 8; ++q) gam[q] = pin(K::genc(8 * j + q, PA.prod));
   }
 
+  // F1 forwards: surplus (L - 1) p (fwd_body_f1_free)
+  const uint32_t sp = pin(uint32_t(L - 1) * AF.p), sp1 = sp + AF.p;
   // 32-bit counters, stride pointer, incremental stage/phase (launcher splits >= 2^30)
   const uint32_t ntiles = static_cast<uint32_t>((batch + kTile - 1) / kTile);
   const uint32_t nb = static_cast<uint32_t>(batch), pstep = gridDim.x * kTile;
@@ -146,8 +148,13 @@ __global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, pm_minb<IO>())
     load_strided<IO, K::kSigned>(va, reinterpret_cast<const IO*>(base + G::poly_offset(warp, half, 0)), j);
     load_strided<IO, K::kSigned>(vb, reinterpret_cast<const IO*>(base + G::poly_offset(warp, half, 1)), j);
     release_stage(&empty[s], lane);
-    fwd_body<K, L, PER_INDEX, W1>(va, twf, AF, X);
-    fwd_body<K, L, PER_INDEX, W1>(vb, twf, AF, X);
+    if constexpr (F1) {
+      fwd_body_f1_free<K, L, W1>(va, twf, AF, X, sp, sp1);
+      fwd_body_f1_free<K, L, W1>(vb, twf, AF, X, sp, sp1);
+    } else {
+      fwd_body<K, L, PER_INDEX, W1>(va, twf, AF, X);
+      fwd_body<K, L, PER_INDEX, W1>(vb, twf, AF, X);
+    }
     // product stage (contiguous ownership, canonical results in va)
     if (PA.prod.basemul) {
 #pragma unroll
@@ -176,11 +183,21 @@ __global__ void __launch_bounds__((pm_cons<IO>() + 1) * 32, pm_minb<IO>())
 }
 
 
-template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
-cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
-                      cudaStream_t st) {
+// NTTK_POLYMUL_EAGER=1 runs the standalone-transform policies of harvey / smont inside the
+// fused kernel (the A/B of the lazy twins; tests check both against the oracle)
+bool eager_kinds() {
+  static const bool v = [] {
+    const char* e = std::getenv("NTTK_POLYMUL_EAGER");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+template <auto KERN, class K, class IO>
+cudaError_t launch_k(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
+                     cudaStream_t st) {
   static OccCache occ;
-  auto kern = polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY, W1>;
+  auto kern = KERN;
   constexpr int smem = Geo2<IO>::kSmem + 480 * int(sizeof(typename K::Tw));
   constexpr int kThreads = (Geo2<IO>::kConsumers + 1) * 32, kTile = 2 * Geo2<IO>::kConsumers;
   const int g_sms2 = sm_count_current();
@@ -191,6 +208,16 @@ cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, con
   kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(a), static_cast<const IO*>(b),
                                       static_cast<IO*>(out), batch, PA);
   return cudaGetLastError();
+}
+
+template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>
+cudaError_t launch_lz(const void* a, const void* b, void* out, size_t batch, const PolymulArgs& PA,
+                      cudaStream_t st) {
+  if constexpr (std::is_same<K, ImprovedN16<false>>::value && !PER_INDEX) {
+    if (PA.prod.lazy && !eager_kinds())
+      return launch_k<polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY, W1, true>, K, IO>(a, b, out, batch, PA, st);
+  }
+  return launch_k<polymul256_tma_kernel<K, IO, L, PER_INDEX, LAZY, W1, false>, K, IO>(a, b, out, batch, PA, st);
 }
 
 template <class K, class IO, int L, bool PER_INDEX>
@@ -241,16 +268,6 @@ cudaError_t polymul256_launch(const HostParams& P, int kind, const void* a, cons
     done += n;
   }
   return cudaSuccess;
-}
-
-// NTTK_POLYMUL_EAGER=1 runs the standalone-transform policies of harvey / smont inside the
-// fused kernel (the A/B of the lazy twins; tests check both against the oracle)
-bool eager_kinds() {
-  static const bool v = [] {
-    const char* e = std::getenv("NTTK_POLYMUL_EAGER");
-    return e && e[0] == '1';
-  }();
-  return v;
 }
 
 cudaError_t polymul256_launch_one(const HostParams& P, int kind, const void* a, const void* b,

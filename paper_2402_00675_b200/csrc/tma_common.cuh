@@ -449,6 +449,57 @@ __device__ __forceinline__ void fwd_body_f1(uint32_t (&v)[16], const TWL& twl, c
   }
 }
 
+// F1 forward whose words are free (the fused polymul: only its canonical product is pinned):
+// the same paper-form layers as fwd_body_f1 on every layer after the first, no final
+// correction -- outputs are exact mod p, below (L + 1 + S) p with S = L - 1 (host-validated,
+// ProdArgs::lazy).  Layer 1 injects the surplus (W1 block on the cyclic tree, umulhi product
+// on the negacyclic one); block 0 of layer 2 keeps its W1 form on the cyclic tree.
+template <class K, int L, bool W1, class TWL>
+__device__ __forceinline__ void fwd_body_f1_free(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                                 const Xpose& X, uint32_t sp, uint32_t sp1) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // layer 1: one block
+    const uint32_t x = v[r], y = v[r + 8];
+    const uint32_t c = W1 ? y : mp_n16<false>(y, K::tw(A, 0), A.p);
+    v[r] = x + c + sp;
+    v[r + 8] = x + sp1 - c;
+  }
+#pragma unroll
+  for (int sl = 2; sl <= 4; ++sl) {
+    const int h = 8 >> (sl - 1);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      const int blk = r >> (5 - sl);
+      if (W1 && sl == 2 && blk == 0) {
+        uint32_t c = v[r + h] - sp;
+        c = umin32(c, c - A.p);
+        const uint32_t x = v[r];
+        v[r + h] = x + A.p - c;
+        v[r] = x + c + A.zero;
+        continue;
+      }
+      f1_bf(v[r], v[r + h], K::tw(A, (1 << (sl - 1)) - 1 + blk), A);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) X.put(r, v[r]);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) X.get4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+#pragma unroll
+  for (int sl = 5; sl <= L; ++sl) {
+    const int h = 1 << (8 - sl);
+    const int base = sl == 5 ? 0 : sl == 6 ? 1 : sl == 7 ? 3 : 7;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      f1_bf(v[r], v[r + h], twl[base + (r >> (9 - sl))], A);
+    }
+  }
+}
+
 template <class K, class = void>
 struct lazy_of {
   static constexpr bool value = false;

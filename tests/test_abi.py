@@ -195,15 +195,16 @@ PM_LAZY = 256
 
 
 def test_fast_flags_polymul_lazy_montgomery(engine):
-    """params.cpp: the fused polymul's lazy Montgomery twins (arith.cuh HarveyLazy16 /
-    SmontLazy16) are admitted for Kyber n = 16 (config 2) and refused where their bounds or
+    """params.cpp: the fused polymul's lazy twins (arith.cuh HarveyLazy16 / SmontLazy16, the
+    improved kind's free F1 forwards) are admitted for Kyber n = 16 (config 2) and refused where their bounds or
     their n = 16 / CT-forward preconditions fail."""
     K = engine.ButterflyKind
     nega = engine.Tree.negacyclic
     Pk = engine.build_params(3329, 256, 16, [K.harvey, K.smont, K.improved], tree=nega, layers=7,
                              exact_bound=True)
     assert Pk.fast_flags(K.harvey, 1) & PM_LAZY and Pk.fast_flags(K.smont, 1) & PM_LAZY
-    assert not Pk.fast_flags(K.improved, 1) & PM_LAZY
+    # improved: the free F1 forwards (tma_common.cuh fwd_body_f1_free)
+    assert Pk.fast_flags(K.improved, 1) & PM_LAZY
     # cyclic harvey runs the DIF forward (no lazy twin); cyclic smont (CT) keeps it
     Pc = engine.build_params(3329, 256, 16, [K.harvey, K.smont], exact_bound=True)
     assert not Pc.fast_flags(K.harvey, 1) & PM_LAZY and Pc.fast_flags(K.smont, 1) & PM_LAZY
