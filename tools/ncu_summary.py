@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarise an ncu --set full report into profiles/ (JSON + markdown).
 
-usage: python tools/ncu_summary.py <report.ncu-rep> <out-prefix>
+usage: python tools/ncu_summary.py <report.ncu-rep | raw-page.csv> <out-prefix>
 Writes <out-prefix>.json (per-kernel metrics, consumed by bench.py for roofline.traffic)
 and <out-prefix>.md (human-readable table + top stall reasons).
 """
@@ -12,8 +12,11 @@ import subprocess
 import sys
 
 rep, prefix = sys.argv[1], sys.argv[2]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True).stdout
+if rep.endswith(".csv"):  # a raw page exported on the GPU box (ncu -i rep --page raw --csv)
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 idx = {h: i for i, h in enumerate(hdr)}
