@@ -46,7 +46,10 @@ def val(r, key):
     i = idx.get(key)
     if i is None or r[i] in ("", "n/a"):
         return None
-    v = float(r[i].replace(",", ""))
+    try:
+        v = float(r[i].replace(",", ""))
+    except ValueError:  # "no data" etc.
+        return None
     u = units[i]
     if key.startswith("dram__bytes"):
         v *= SCALE.get(u, 1.0)
