@@ -341,6 +341,57 @@ __device__ __forceinline__ void fwd_body_n(uint32_t (&v)[32], const uint2* tws, 
   }
 }
 
+// F1 forward for N = 512 / 1024 (ImprovedN16 -- the narrow image of the Table 2 presets --
+// A.flags bit 10; tma_common.cuh fwd_body_f1 has the derivation): layer 1 (twiddle 1) injects
+// the surplus S = L - 2 (A.f1_sp), layers 2..L-1 run the F1 form (Y' = X - r spends one), the
+// last layer runs the umulhi form and removes sigma = S - popcount(i bits L-2..1) of the X
+// position i = 32 j + k with the per-lane registers E[m] = (m - cj) p.
+template <class K, int LOGN>
+__device__ __forceinline__ void fwd_body_n_f1(uint32_t (&v)[32], const uint2* tws, const FastArgs& A,
+                                              const XposeN<(1 << LOGN) / 32>& X, int j,
+                                              const uint32_t (&E)[6]) {
+  using Tw = typename K::Tw;
+  constexpr int N = 1 << LOGN, G = N / 32;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {  // layer 1: one block, twiddle 1, r = Y (canonical input)
+    const uint32_t x = v[k], y = v[k + 16];
+    v[k] = x + y + A.f1_sp;
+    v[k + 16] = x + A.f1_sp1 - y;
+  }
+#pragma unroll
+  for (int s = 2; s <= 5; ++s) {  // phase 1 (strided), uniform twiddles
+    const int h = 16 >> (s - 1);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      f1_bf(v[k], v[k + h], K::tw(A, (1 << (s - 1)) - 1 + (k >> (6 - s))), A);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) X.put(k, v[k]);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X.get4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+#pragma unroll
+  for (int s = 6; s < LOGN; ++s) {  // phase 2 (contiguous), lane twiddles from shared memory
+    const int h = 1 << (LOGN - s);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      f1_bf(v[k], v[k + h], tw_smem<Tw>(tws, seg_base<LOGN, false>(s) + (k >> (LOGN - s + 1)) * G + j), A);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {  // layer L: umulhi form, surplus removed
+    const int kk = ((k >> 1) & 1) + ((k >> 2) & 1) + ((k >> 3) & 1) + ((k >> 4) & 1);
+    const uint32_t r = mp_n16<false>(v[k + 1], tw_smem<Tw>(tws, seg_base<LOGN, false>(LOGN) + (k >> 1) * G + j), A.p);
+    const uint32_t x = v[k];
+    v[k + 1] = x - r + E[kk + 1];
+    v[k] = x + r + E[kk];
+  }
+}
+
 // inverse: run_merge_layers + N^{-1} (transform.hpp:99-116, 323-335), contiguous
 // canonical in -> strided canonical out
 template <class K, int LOGN>
@@ -531,7 +582,7 @@ __device__ __forceinline__ void stage_table(uint2* tws, const uint32_t* tab) {
 // harvey -12 %, improved +0.7 % vs 8, profiles/r1b_fastn_store.txt)
 constexpr int kFwdConsN = 16;
 
-template <class K, class IO, int LOGN, bool PER_INDEX>
+template <class K, class IO, int LOGN, bool PER_INDEX, bool F1 = false>
 __global__ void __launch_bounds__(GeoN<LOGN, IO, kFwdConsN>::kThreadsN)
     fwdn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
                     const uint32_t* __restrict__ tab, const __grid_constant__ FastArgs A) {
@@ -554,6 +605,12 @@ __global__ void __launch_bounds__(GeoN<LOGN, IO, kFwdConsN>::kThreadsN)
   const int j = lane & (G - 1), half = GN::PPW == 2 ? lane >> 4 : 0;
   XposeN<G> X;
   X.init(scratch + warp * GN::kScratchWords + half * GN::kRegionWords, j);
+  uint32_t E[6];  // F1: last-layer surplus corrections (fwd_body_n_f1)
+  if constexpr (F1) {
+    const int cj = LOGN - 2 - __popc(uint32_t(j) & ((1u << (LOGN - 6)) - 1u));
+#pragma unroll
+    for (int m = 0; m < 6; ++m) E[m] = pin(uint32_t(m - cj) * A.p);
+  }
   const size_t ntiles = (batch + GN::kTileN - 1) / GN::kTileN;
   int it = 0;
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -564,7 +621,10 @@ __global__ void __launch_bounds__(GeoN<LOGN, IO, kFwdConsN>::kThreadsN)
     load_strided_n<IO, G, K::kSigned>(
         v, reinterpret_cast<const IO*>(stages + s * GN::kStageBytes + GN::poly_offset(warp, half)), j);
     release_stage(&empty[s], lane);
-    fwd_body_n<K, LOGN, PER_INDEX>(v, tws, A, X, j);
+    if constexpr (F1)
+      fwd_body_n_f1<K, LOGN>(v, tws, A, X, j, E);
+    else
+      fwd_body_n<K, LOGN, PER_INDEX>(v, tws, A, X, j);
     if constexpr (sizeof(IO) == 4)
       store_contiguous_n_coalesced<IO, G>(out + poly * GN::N, j, v, X, poly < batch);
     else if (poly < batch)
@@ -641,12 +701,12 @@ int grid_n(Kern kern, int smem, OccCache& occ, size_t tiles, int threads = kThre
   return static_cast<int>(tiles < full ? tiles : full);
 }
 
-template <class K, class IO, int LOGN, bool PER_INDEX>
-cudaError_t fwd_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
-                  cudaStream_t st) {
+template <class K, class IO, int LOGN, bool PER_INDEX, bool F1>
+cudaError_t fwd_n_f(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
+                    cudaStream_t st) {
   using GN = GeoN<LOGN, IO, kFwdConsN>;
   static OccCache occ;
-  auto kern = fwdn_tma_kernel<K, IO, LOGN, PER_INDEX>;
+  auto kern = fwdn_tma_kernel<K, IO, LOGN, PER_INDEX, F1>;
   const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN, GN::kThreadsN);
   kern<<<blocks, GN::kThreadsN, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,
                                             tab, A);
@@ -656,6 +716,15 @@ cudaError_t fwd_n(const void* in, void* out, size_t batch, const uint32_t* tab, 
 // consumer warps of the N = 512 / 1024 inverse (two 256-row tensor boxes per stage at 16)
 constexpr int inv_cons_n() {
   return 16;
+}
+
+template <class K, class IO, int LOGN, bool PER_INDEX>
+cudaError_t fwd_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
+                  cudaStream_t st) {
+  if constexpr (std::is_same<K, ImprovedN16<false>>::value && !PER_INDEX) {
+    if (A.flags & 1024) return fwd_n_f<K, IO, LOGN, PER_INDEX, true>(in, out, batch, tab, A, st);
+  }
+  return fwd_n_f<K, IO, LOGN, PER_INDEX, false>(in, out, batch, tab, A, st);
 }
 
 template <class K, class IO, int LOGN, int MODE>

@@ -239,14 +239,19 @@ void fill_fast(HostParams& P, int kind) {
         P.ct_plain[0] == 1 && P.ct_plain[1] == 1 && P.ct_plain[3] == 1 && P.ct_plain[7] == 1 &&
         uint64_t(4) * P.p < (uint64_t(1) << 32))
       A.flags |= 16;
-    // F1 forward (tma_common.cuh fwd_body_f1, improved n = 16, cyclic L = 8 with the W1
-    // blocks): every word carries up to kF1Surplus extra multiples of p, so the largest
-    // operand is (L + 1 + S) p; Prop. 4 must hold for it
-    if (kind == NTTK_IMPROVED && n16 && dir == 0 && P.layers == 8 && (A.flags & 16) &&
-        u128(p - 1) * ((9 + kF1Surplus) * p) < u128(c.beta) * (c.beta - p)) {
-      A.f1_sp = static_cast<uint32_t>(kF1Surplus * p);
-      A.f1_sp1 = static_cast<uint32_t>((kF1Surplus + 1) * p);
-      A.flags |= 1024;
+    // F1 forward (tma_common.cuh fwd_body_f1 at N = 256, fastn_tma.cu fwd_body_n_f1 at N =
+    // 512 / 1024; improved n = 16, cyclic full trees whose layer 1 has twiddle 1): every word
+    // carries up to S = L - 2 extra multiples of p, so the largest operand is (2 L - 1) p;
+    // Prop. 4 must hold for it
+    {
+      const uint64_t L = P.layers, S = L - 2;
+      const bool full = (P.N == 256 && L == 8) || ((P.N == 512 || P.N == 1024) && L == P.log2N);
+      if (kind == NTTK_IMPROVED && n16 && dir == 0 && full && (A.flags & 16) &&
+          u128(p - 1) * ((2 * L - 1) * p) < u128(c.beta) * (c.beta - p)) {
+        A.f1_sp = static_cast<uint32_t>(S * p);
+        A.f1_sp1 = static_cast<uint32_t>((S + 1) * p);
+        A.flags |= 1024;
+      }
     }
     // last merge twiddle times N^{-1} (the final scaling folded into the last layer)
     {

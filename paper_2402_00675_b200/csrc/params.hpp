@@ -99,7 +99,7 @@ struct PolymulArgs {
 constexpr int kNarrow = 5;  // pseudo-kind index of the narrow improved image
 // narrow inverse: every GS operand below 2^kNarrowEmax p (tma_common.cuh inv_body_narrow)
 constexpr int kNarrowEmax = 4;
-// F1 forward: surplus multiples of p injected by layer 1 (tma_common.cuh fwd_body_f1)
+// F1 forward at N = 256: surplus multiples of p injected by layer 1 (= L - 2, fwd_body_f1)
 constexpr uint32_t kF1Surplus = 6;
 
 struct HostParams {

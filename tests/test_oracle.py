@@ -338,23 +338,26 @@ def test_sweep_full_grid_checksums_match_reference(oracle):
         assert "%016x" % s == row["checksum"], row
 
 
-def _f1_schedule_model(a, ct, p, S):
-    """Integer model of tma_common.cuh fwd_body_f1 (cyclic N = 256, L = 8): surplus S p
-    injected by layer 1, paper-form Y' = X - r on the multiply blocks of layers 2..7, the
-    last layer subtracts sigma p; asserts every F1 X input keeps a surplus >= 1 and every
-    product operand lies inside Prop. 4's n = 16 range."""
+def _f1_schedule_model(a, ct, p, S, w1_layer2=True):
+    """Integer model of the F1 forwards (tma_common.cuh fwd_body_f1 at N = 256 with the layer-2
+    W1 block, fastn_tma.cu fwd_body_n_f1 at N = 512 / 1024 without it): surplus S p injected
+    by layer 1 (twiddle 1), paper-form Y' = X - r on layers 2..L-1, the last layer subtracts
+    sigma p; asserts every F1 X input keeps a surplus >= 1 and every product operand lies
+    inside Prop. 4's n = 16 range."""
     a = [int(v) for v in a]
+    N = len(a)
+    L = N.bit_length() - 1
     lim = (1 << 16) * ((1 << 16) - p)
-    for s in range(1, 9):
-        span = 256 >> s
-        for i in range(256):
+    for s in range(1, L + 1):
+        span = N >> s
+        for i in range(N):
             if i & span:
                 continue
-            x, y, blk = a[i], a[i + span], i >> (9 - s)
+            x, y, blk = a[i], a[i + span], i >> (L + 1 - s)
             if s == 1:
                 a[i], a[i + span] = x + y + S * p, x + (S + 1) * p - y
                 continue
-            if s == 2 and blk == 0:
+            if w1_layer2 and s == 2 and blk == 0:
                 c = y - S * p
                 c = c - p if c >= p else c
                 a[i], a[i + span] = x + c, x + p - c
@@ -362,12 +365,15 @@ def _f1_schedule_model(a, ct, p, S):
             w = int(ct[(1 << (s - 1)) - 1 + blk])
             assert w * y < lim
             r = w * y % p
-            if s < 8:
+            if s < L:
                 assert x - r >= 0
                 a[i], a[i + span] = x + r, x - r
             else:
                 b = lambda k: (i >> k) & 1  # noqa: E731
-                sig = S - (b(7) & b(6)) - sum(b(k) for k in range(1, 6))
+                spent = sum(b(k) for k in range(1, L - 1))
+                if w1_layer2:  # the layer-2 W1 block (bit L-1 = 0) spends nothing
+                    spent -= b(L - 2) * (1 - b(L - 1))
+                sig = S - spent
                 a[i], a[i + span] = x + r - sig * p, x + p - r - sig * p
     return a
 
@@ -384,3 +390,17 @@ def test_f1_forward_schedule_matches_reference_loop(oracle, p):
     want = Q.forward(IMPROVED, np.stack(rows))
     for k, row in enumerate(rows):
         assert _f1_schedule_model(row, ct, p, 6) == [int(v) for v in want[k]]
+
+
+@pytest.mark.parametrize("N", [512, 1024])
+def test_f1_forward_schedule_n512_1024(oracle, N):
+    """The N = 512 / 1024 F1 forward (fastn_tma.cu fwd_body_n_f1, surplus L - 2) reproduces the
+    reference's lazy forward words at the paper's Table 2 modulus."""
+    p = 12289
+    Q = oracle.params(p, N, 32, (IMPROVED,))
+    ct = Q.table("ct_plain")
+    L = N.bit_length() - 1
+    rows = [np.full(N, p - 1), oracle.rng(7, p, N), np.where(np.arange(N) % 2 == 0, p - 1, 0)]
+    want = Q.forward(IMPROVED, np.stack(rows))
+    for k, row in enumerate(rows):
+        assert _f1_schedule_model(row, ct, p, L - 2, w1_layer2=False) == [int(v) for v in want[k]]
