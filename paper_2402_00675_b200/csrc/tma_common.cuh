@@ -388,10 +388,23 @@ __device__ __forceinline__ void fwd_body(uint32_t (&v)[16], const TWL& twl, cons
 // part; E[m] = (m - cj) p are per-lane registers.  Largest word (9 + S) p, host-validated
 // against Prop. 4.  A CPU model of this schedule is checked against the reference loop in
 // tests/test_oracle.py.
+// IMAD_Y: Y' = 2 X - X' as one IMAD by the opaque constant A.two, so 3 IMAD (fmaheavy) +
+// SHF + LEA.HI (ALU) balance the two pipes -- 6.1 cycles per warp-butterfly in registers
+// against 7.1 with Y' = X + X - X' as an IADD3 and 7.7 for the umulhi form
+// (profiles/r2_bf_forms_microbench.txt).  In the kernels it pays where the ALU pipe is the
+// busier one: the N = 256 Kyber forward 0.911 -> 0.879 ms; the N = 512/1024 forwards and the
+// fused polymul measured 1.5-3 % slower with it and keep the IADD3 (profiles/r2_f3_ab.txt).
+template <bool IMAD_Y = false>
 __device__ __forceinline__ void f1_bf(uint32_t& x, uint32_t& y, uint32_t w, const FastArgs& A) {
   const uint32_t R = ((y * w) >> 16) * A.p + A.p;
   const uint32_t s = x + (R >> 16);
-  y = x + x - s;
+  if constexpr (IMAD_Y) {
+    uint32_t t;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(x), "r"(A.two), "r"(0u - s));
+    y = t;
+  } else {
+    y = x + x - s;
+  }
   x = s;
 }
 
@@ -420,7 +433,7 @@ __device__ __forceinline__ void fwd_body_f1(uint32_t (&v)[16], const TWL& twl, c
         v[r] = x + c + A.zero;
         continue;
       }
-      f1_bf(v[r], v[r + h], K::tw(A, (1 << (sl - 1)) - 1 + blk), A);
+      f1_bf<true>(v[r], v[r + h], K::tw(A, (1 << (sl - 1)) - 1 + blk), A);
     }
   }
   __syncwarp();
@@ -436,7 +449,7 @@ __device__ __forceinline__ void fwd_body_f1(uint32_t (&v)[16], const TWL& twl, c
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
-      f1_bf(v[r], v[r + h], twl[base + (r >> (9 - sl))], A);
+      f1_bf<true>(v[r], v[r + h], twl[base + (r >> (9 - sl))], A);
     }
   }
 #pragma unroll

@@ -18,6 +18,7 @@
 __constant__ uint32_t c_w[16];
 __constant__ uint32_t c_p, c_zero;
 
+__constant__ uint32_t c_two;
 template <int FORM>
 __device__ __forceinline__ void bf32(uint32_t& x, uint32_t& y, uint32_t w, uint32_t p, uint32_t z) {
   const uint32_t hh = y * w;
@@ -25,10 +26,17 @@ __device__ __forceinline__ void bf32(uint32_t& x, uint32_t& y, uint32_t w, uint3
     const uint32_t rr = __umulhi(hh, p);
     y = x + p - rr;
     x = x + rr + z;
-  } else {  // FORM 1
+  } else if (FORM == 1) {
     const uint32_t R = (hh >> 16) * p + p;
     const uint32_t s = x + (R >> 16);
     y = x + x - s;
+    x = s;
+  } else {  // FORM 3: F1 with Y' = 2X - X' on the FMA pipe (IMAD by an opaque 2)
+    const uint32_t R = (hh >> 16) * p + p;
+    const uint32_t s = x + (R >> 16);
+    uint32_t t;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(x), "r"(c_two), "r"(0u - s));
+    y = t;
     x = s;
   }
 }
@@ -112,6 +120,51 @@ __global__ void bf64_kernel(uint32_t* out) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// GS (inverse) forms: (x, y, w) -> (x + y, MP(w, x + off - y)), off a constant-bank word
+//   G0 umulhi   IADD3 t; IADD3 x + y; IMAD h; IMAD.HI r; XOR fence (the eager kernel form)
+//   G1 paper    IADD3 t; IADD3 x + y; IMAD h; SHF; IMAD (h>>16) p + p; SHF
+__constant__ uint32_t c_off;
+//   G2 balanced IADD3 t; IMAD x + y (opaque 1); IMAD h; SHF; IMAD; SHF  (3 IMAD + 3 ALU)
+__constant__ uint32_t c_one;
+template <int FORM>
+__device__ __forceinline__ void gs32(uint32_t& x, uint32_t& y, uint32_t w, uint32_t p, uint32_t z) {
+  const uint32_t t = x + c_off - y;
+  if (FORM == 2) {
+    uint32_t s;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(x), "r"(c_one), "r"(y));
+    x = s;
+  } else {
+    x = x + y + z;
+  }
+  const uint32_t h = t * w;
+  if (FORM == 0) y = __umulhi(h, p) ^ z;
+  else y = (((h >> 16) + 1u) * p) >> 16;
+}
+template <int ITERS, int FORM>
+__global__ void gs_kernel(uint32_t* out) {
+  uint32_t v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = threadIdx.x * 16 + r;
+  const uint32_t p = c_p, z = c_zero;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int sl = 1; sl <= 4; ++sl) {
+      const int h = 1 << (sl - 1);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r & h) continue;
+        gs32<FORM>(v[r], v[r + h], c_w[(1 << (sl - 1)) - 1 + (r >> sl)], p, z);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] &= 0xffffu;
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc ^= v[r];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 int main() {
   uint32_t w[16];
   for (int i = 0; i < 16; ++i) w[i] = 0x9e3779b9u * (i + 1);
@@ -119,6 +172,8 @@ int main() {
   cudaMemcpyToSymbol(c_w, w, sizeof w);
   cudaMemcpyToSymbol(c_p, &p, 4);
   cudaMemcpyToSymbol(c_zero, &z, 4);
+  const uint32_t two = 2;
+  cudaMemcpyToSymbol(c_two, &two, 4);
   int sms = 0, clk = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
@@ -153,5 +208,13 @@ int main() {
   run(bf32_kernel<ITERS, 0, 1, 0xe>, "F0, F1 on layers 1-3");
   run(bf64_kernel<ITERS, 0x2, true>, "F2, F0 on layer 1");
   run(bf64_kernel<ITERS, 0x6, true>, "F2, F0 on layers 1-2");
+  const uint32_t off = 2 * p;
+  cudaMemcpyToSymbol(c_off, &off, 4);
+  run(bf32_kernel<ITERS, 3, 3, 0>, "F3 F1 with IMAD 2X - X' (all layers)");
+  run(gs_kernel<ITERS, 0>, "G0 GS umulhi + fence");
+  run(gs_kernel<ITERS, 1>, "G1 GS paper form");
+  const uint32_t one = 1;
+  cudaMemcpyToSymbol(c_one, &one, 4);
+  run(gs_kernel<ITERS, 2>, "G2 GS paper form, X + Y as IMAD");
   return 0;
 }
