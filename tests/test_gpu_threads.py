@@ -64,3 +64,43 @@ def test_concurrent_threads_fresh_process(tmp_path):
     r = subprocess.run([sys.executable, str(script), ROOT], capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "threads ok" in r.stdout, r.stdout + r.stderr
+
+
+AB_SCRIPT = r'''
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+from oracle.oracle import Oracle, IMPROVED, HARVEY, SMONT, NEGA
+import paper_2402_00675_b200.nttk as nttk
+o = Oracle()
+K = nttk.ButterflyKind
+# Kyber forward (F1 off: umulhi form everywhere)
+P = nttk.build_params(3329, 256, 16, [K.improved], exact_bound=True)
+Q = o.params(3329, 256, 16, (IMPROVED,), exact=True)
+f = o.rng(31, 3329, 257 * 256).reshape(257, 256)
+y = nttk.forward(P, K.improved, torch.from_numpy(f.astype(np.int16)).cuda())
+assert (y.cpu().numpy().astype(np.int64) & 0xffff == Q.forward(IMPROVED, f)).all()
+# fused polymul with the eager policies of every kind
+for kind, k in ((K.improved, IMPROVED), (K.harvey, HARVEY), (K.smont, SMONT)):
+    P = nttk.build_params(3329, 256, 16, [kind], tree=nttk.Tree.negacyclic, layers=7, exact_bound=True)
+    Q = o.params(3329, 256, 16, (k,), tree=NEGA, layers=7, exact=True)
+    a = o.rng(32, 3329, 65 * 256).reshape(65, 256)
+    b = o.rng(33, 3329, 65 * 256).reshape(65, 256)
+    c = nttk.polymul(P, kind, torch.from_numpy(a.astype(np.int16)).cuda(),
+                     torch.from_numpy(b.astype(np.int16)).cuda())
+    assert (c.cpu().numpy().astype(np.int64) == Q.polymul(k, a, b)).all(), kind
+print("ok")
+'''
+
+
+def test_ab_switches_keep_parity(tmp_path):
+    """The two runtime A/B switches (NTTK_FWD_F1=0: umulhi-form Kyber forward;
+    NTTK_POLYMUL_EAGER=1: the standalone policies inside the fused polymul) select other
+    exact arithmetic; in a fresh process their words must equal the oracle's too."""
+    script = tmp_path / "ab.py"
+    script.write_text(AB_SCRIPT)
+    env = dict(os.environ, NTTK_FWD_F1="0", NTTK_POLYMUL_EAGER="1")
+    r = subprocess.run([sys.executable, str(script), ROOT], capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
