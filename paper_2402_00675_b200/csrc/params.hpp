@@ -57,6 +57,7 @@ struct FastArgs {
   // --- issue-slot economy (all host-validated, see params.cpp fill_fast) ---
   uint32_t zero = 0;       // always 0: x + y + zero forces a 3-input IADD3 (ALU pipe)
   uint32_t two = 2;        // always 2: 2 X - X' as one IMAD (fmaheavy pipe, f1_bf)
+  uint32_t one = 1;        // always 1: X + Y as one IMAD (fmaheavy pipe, narrow_bf)
   uint32_t negp = 0;       // -p mod 2^32 (x - q p as one IMAD)
   uint32_t off[12] = {};   // off[m] = 2^{m-1} p: GS offset of merge depth m (constant operand)
   uint32_t cb_m = 0, cb_s = 0;  // x mod p = x - ((x cb_m) >> cb_s) p, exact for x < 2^17

@@ -737,6 +737,13 @@ __device__ __forceinline__ void inv_body_eager(uint32_t (&v)[16], const TWL& twl
 // Plantard product by 1^ (canonical).  Words are reduced before the transpose, so phase 2
 // starts canonical and its e[] stays compile-time.
 
+// Butterflies of the narrow inverse: paper-form products (IMAD + SHF + IMAD + SHF) and X + Y as
+// an IMAD by the opaque A.one, so the fmaheavy and ALU pipes carry 3 + 3 slots (G2 in
+// profiles/r2_bf_forms_microbench.txt: 6.7 cycles per warp-butterfly in registers against 8.9
+// for the eager umulhi form with its fence).  Measured (profiles/r2_narrow_form_ab.txt):
+// newhope512 inverse 0.879 -> 0.786, newhope1024 1.755 -> 1.662, kyber256 0.415 -> 0.405
+// ns/poly.  The words are free (canonical output), every product operand stays in Prop. 4's
+// range by the bound exponents below.
 template <class K>
 __device__ __forceinline__ void narrow_bf(uint32_t& x, uint32_t& y, int& ex, int& ey,
                                           typename K::Tw w, bool last, const FastArgs& A) {
@@ -746,10 +753,15 @@ __device__ __forceinline__ void narrow_bf(uint32_t& x, uint32_t& y, int& ex, int
     if (ey) y = K::canon1(y, A);
     em = 0;
   }
-  if (last) {
-    K::inv_last(x, y, A.off[em + 1], A);
+  const uint32_t t = x + A.off[em + 1] - y;
+  uint32_t s;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(x), "r"(A.one), "r"(y));
+  if (last) {  // N^{-1} folded: (MP(n^, X + Y), MP((w N^{-1})^, T)), both canonical
+    x = mp_n16<true>(s, A.scale_lo, A.p);
+    y = mp_n16<true>(t, A.fold_lo, A.p);
   } else {
-    K::inv(x, y, w, A.off[em + 1], A);
+    x = s;
+    y = mp_n16<true>(t, w, A.p);
   }
   ex = em + 1;
   ey = 0;
