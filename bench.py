@@ -204,7 +204,11 @@ NCU_KERNELS = {"kyber_fwd": "fwd256_tma_kernel<ImprovedN16", "kyber_inv": "inv25
 CENSUS_KERNELS = {"kyber_fwd": "fwd256_tma_kernelINS_11ImprovedN16ILb0EEEtLi8ELb0ELb1E",
                   "kyber_inv": "inv256_tma_kernelINS_11ImprovedN16ILb0EEEtLi8ELi30E",
                   "dil_fwd": "fwd256_tma_kernelINS_11ImprovedN32EjLi8ELb0ELb1E",
-                  "dil_inv": "inv256_tma_kernelINS_11ImprovedN32EjLi8ELi15E"}
+                  "dil_inv": "inv256_tma_kernelINS_11ImprovedN32EjLi8ELi15E",
+                  # config 2 (fused polymul, 7-layer negacyclic, u16): the kernels that run
+                  "pm_modified_plantard": "polymul256_tma_kernelINS_11ImprovedN16ILb0EEEtLi7ELb0ELb1ELb0ELb1E",
+                  "pm_montgomery_R2^16": "polymul256_tma_kernelINS_12HarveyLazy16EtLi7E",
+                  "pm_signed_montgomery": "polymul256_tma_kernelINS_11SmontLazy16EtLi7E"}
 
 
 def latest_profile(pattern: str):
@@ -492,11 +496,21 @@ def run_extras(dev):
     xb = torch.randint(0, KYBER_Q, (B, 256), generator=g, device=dev, dtype=torch.int32).to(torch.int16)
     xc = torch.empty_like(xa)
     c2 = {}
+    census, _ = sass_census()
+    n_smsp = 4 * torch.cuda.get_device_properties(dev).multi_processor_count
+    clk_hz = 1.965e9  # the pool's SM clock under load (bench clocks record)
     for name, kind in (("modified_plantard", K.improved), ("montgomery_R2^16", K.harvey),
                        ("signed_montgomery", K.smont)):
         P2 = nttk.build_params(KYBER_Q, 256, 16, [kind], tree=NEG, layers=7, exact_bound=True)
         ms = _time_ms(torch, lambda: nttk.polymul(P2, kind, xa, xb, xc), 20)
         c2[name] = {"ms": ms, "products_per_s": B / (ms / 1e3)}
+        # executed-instruction roof: fmaheavy cycles per product of the kernel's SASS loop
+        cyc = (census or {}).get("pm_" + name)
+        if cyc:
+            roof = n_smsp * clk_hz / cyc
+            c2[name].update({"imad_executed_roof_products_per_s": roof,
+                             "frac_of_imad_executed_roof": B / (ms / 1e3) / roof,
+                             "fmaheavy_cycles_per_product": cyc})
     # the standalone basemul kernel (product.cu) on the same 65536 pairs of forward spectra:
     # HBM-bound, 3 x 512 B per polynomial pair (two spectra in, one product out)
     peak, _ = measured_peaks()

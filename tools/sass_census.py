@@ -26,7 +26,9 @@ if "--json" in sys.argv:
 rows = []
 
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2402_00675_b200/libnttk_gpu.so"
-pat = re.compile(sys.argv[2] if len(sys.argv) > 2 else r"tma_kernel.*(ImprovedN16ILb0EEEtLi8|ImprovedN32EjLi8|HarveyILi16ELb0EEEtLi8|HarveyILi32ELb0EEEjLi8|SmontILi16EEtLi8|SmontILi32EEjLi8)")
+pat = re.compile(sys.argv[2] if len(sys.argv) > 2 else
+                 r"tma_kernel.*(ImprovedN16ILb0EEEtLi8|ImprovedN32EjLi8|HarveyILi16ELb0EEEtLi8|HarveyILi32ELb0EEEjLi8|SmontILi16EEtLi8|SmontILi32EEjLi8)"
+                 r"|polymul256_tma_kernel.*(ImprovedN16ILb0EEEtLi7|HarveyLazy16EtLi7|SmontLazy16EtLi7)")
 txt = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 FMA2 = ("IMAD", "IMAD.IADD", "IMAD.MOV", "IMAD.MOV.U32", "IMAD.SHL.U32", "IMAD.X", "IMAD.U32")
 FMA4 = ("IMAD.HI.U32", "IMAD.WIDE.U32", "IMAD.WIDE", "IMAD.HI")
