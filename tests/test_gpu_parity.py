@@ -896,3 +896,21 @@ def test_captured_plans_match_eager_calls(oracle):
     assert (from_dev(z) == want).all()
     with pytest.raises(nttk.ContractViolation):
         nttk.Plan(Pn, SCOTT, nttk.Plan.FORWARD, x, out)  # kind not built into Pn
+
+
+@pytest.mark.parametrize("name", ["kyber256", "newhope512", "newhope1024"])
+def test_narrow_image_extremes(oracle, name):
+    """The paper's Table 2 presets run on the narrow image (n = 16 product on the n = 32 set;
+    F1/F3 forward, bound-exponent inverse with paper-form products): extreme canonical inputs
+    through the forward and extreme storage words through the inverse, bit-exact with the
+    oracle's n = 32 reference loop."""
+    P = nttk.preset(name)
+    assert P.fast_flags(IMPROVED, 0) & 512 and P.fast_flags(IMPROVED, 1) & 512
+    p, N = P.p, P.size
+    Q = oracle.params(p, N, 32, (IMPROVED,))
+    rows = [np.full(N, p - 1), np.zeros(N, dtype=np.int64), np.where(np.arange(N) % 2 == 0, p - 1, 0),
+            np.where(np.arange(N) < N // 2, p - 1, 0), np.arange(N) % p, oracle.rng(91, p, N)]
+    f = np.stack(rows).astype(np.int64)
+    assert (from_dev(nttk.forward(P, IMPROVED, to_dev(f, 4))) == Q.forward(IMPROVED, f)).all()
+    w = _extreme_words(p, 32, 67, 5 + N, N)
+    assert (from_dev(nttk.inverse(P, IMPROVED, to_dev(w, 4))) == Q.inverse(IMPROVED, w)).all()
