@@ -205,7 +205,9 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
       }
-      if constexpr ((MODE & 32) != 0)
+      if constexpr ((MODE & 64) != 0)
+        inv_body_ct(v, twl, A, X);
+      else if constexpr ((MODE & 32) != 0)
         inv_body_narrow<K, L>(v, twl, A, X);
       else
         inv_body<K, L, CM == 2, (MODE & 4) != 0, (MODE & 8) != 0, (MODE & 16) != 0, kPacked, CM == 3 ? 1 : 0>(
@@ -220,11 +222,23 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
     }
   };
   Tw twl[15];
-  inv_twiddles<K, L>(twl, A, j);
+  if constexpr ((MODE & 64) != 0)
+    ct_twiddles<K>(twl, A, j);
+  else
+    inv_twiddles<K, L>(twl, A, j);
   run(twl);
 }
 
 // ---------------------------------------------------------------------------
+// A/B switch while the CT-form inverse is measured (NTTK_INV_CT=0 runs the GS lazy merge)
+bool ct_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("NTTK_INV_CT");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // A/B switch while the F1 forward is measured (NTTK_FWD_F1=0 runs the umulhi form)
 bool f1_enabled() {
   static const bool v = [] {
@@ -381,6 +395,8 @@ cudaError_t fast256_tma_launch_one(const HostParams& P, int kind, int dir, const
   if (batch == 0) return cudaSuccess;
   switch (kind) {
     case NTTK_IMPROVED:
+      if (dir == 1 && elem_bytes == 2 && P.ct_inv && ct_enabled())  // CT-form Kyber inverse
+        return inv_launch_mode<ImprovedN16<false>, uint16_t, 8, 64 | 16 | 2>(in, out, batch, P.fast_ctinv, st);
       if (P.image(kind, dir) == kNarrow)  // n = 32 parameters on the n = 16 product
         return by_io<ImprovedN16<false>, false>(dir, L, elem_bytes, in, out, batch,
                                                 P.fast[kNarrow][dir], st);

@@ -451,6 +451,93 @@ void fill_fast(HostParams& P, int kind) {
 // words, below (L + 1) p; so for small p (the paper's Table 2 presets: 7681, 12289) the
 // whole forward runs on the cheaper n = 16 product, bit-exact with the reference's n = 32
 // run.  The image is fill_fast's own output for the same tree at n = 16.
+// CT-form inverse for the Kyber tree (improved n = 16, N = 256, cyclic L = 8, u16 input).  The
+// inverse output is canonical, hence unique, so any exact algorithm gives the reference's bits
+// (intt_inverse, transform.hpp:233-343).  inv_body_ct runs a radix-2 DIT on the bit-reversed
+// spectrum with omega^{-1}: a[i+j] = u + w v, a[i+j+len] = u - w v, w = omega^{-(N/2len) j}.
+// Those are CT butterflies, so the balanced F3 form applies (tma_common.cuh f1_bf), and the
+// j = 0 butterfly of every block in the register-local layers len = 1..8 is multiply-free.
+// Raw u16 words enter unreduced.  The host tracks the value interval of every register through
+// the kernel's exact schedule and picks, per layer, the multiples of p that the multiply-free
+// butterflies add to keep every F3 X input >= p (so X - r never underflows); the last layer
+// folds N^{-1} into two Plantard products per butterfly.  Every product operand must stay
+// inside Prop. 4's range, else the image is refused (the GS inverse stays).
+void fill_ct_inverse(HostParams& P) {
+  if (P.n_bits != 16 || P.N != 256 || P.layers != 8 || P.tree != NTTK_CYCLIC) return;
+  if (!((P.fast_mask >> NTTK_IMPROVED) & 1u)) return;
+  const Ctx& c = P.ctx;
+  const uint64_t p = P.p;
+  const u128 lim = u128(c.beta) * (c.beta - p);
+  auto rup = [&](int64_t x) -> int64_t { return x <= 0 ? 0 : (x + int64_t(p) - 1) / int64_t(p) * int64_t(p); };
+  auto prod_ok = [&](int64_t v) { return v >= 0 && u128(p - 1) * uint64_t(v) < lim; };
+  int64_t lo[16], hi[16];
+  for (int r = 0; r < 16; ++r) lo[r] = 0, hi[r] = 65535;
+  const int64_t P_ = int64_t(p);
+  uint32_t consts[8];
+  const int64_t floor_of[4] = {6 * P_, 5 * P_, 4 * P_, 3 * P_};  // remaining F3 layers + 3p
+  for (int li = 0; li < 4; ++li) {  // register-local layers len = 1, 2, 4, 8
+    const int len = 1 << li;
+    int64_t c1 = 0, c2 = 0;
+    for (int r = 0; r < 16; ++r)
+      if (!(r & len) && (r & (len - 1)) == 0) {
+        c1 = std::max(c1, rup(floor_of[li] - lo[r] - lo[r + len]));
+        c2 = std::max(c2, rup(floor_of[li] - lo[r] + hi[r + len]));
+      }
+    consts[2 * li] = static_cast<uint32_t>(c1);
+    consts[2 * li + 1] = static_cast<uint32_t>(c2);
+    int64_t nlo[16], nhi[16];
+    std::copy(lo, lo + 16, nlo);
+    std::copy(hi, hi + 16, nhi);
+    for (int r = 0; r < 16; ++r) {
+      if (r & len) continue;
+      const int u = r, v = r + len;
+      if ((r & (len - 1)) == 0) {
+        nlo[u] = lo[u] + lo[v] + c1, nhi[u] = hi[u] + hi[v] + c1;
+        nlo[v] = lo[u] - hi[v] + c2, nhi[v] = hi[u] - lo[v] + c2;
+      } else {
+        if (lo[u] < P_ || !prod_ok(hi[v])) return;
+        nlo[u] = lo[u], nhi[u] = hi[u] + P_ - 1;
+        nlo[v] = lo[u] - P_ + 1, nhi[v] = hi[u];
+      }
+    }
+    std::copy(nlo, nlo + 16, lo);
+    std::copy(nhi, nhi + 16, hi);
+  }
+  int64_t L0 = lo[0], H0 = hi[0];  // after the transpose a register may hold any position
+  for (int r = 1; r < 16; ++r) L0 = std::min(L0, lo[r]), H0 = std::max(H0, hi[r]);
+  if (L0 < 0 || H0 >= (int64_t(1) << 32)) return;
+  for (int r = 0; r < 16; ++r) lo[r] = L0, hi[r] = H0;
+  for (int h = 1; h <= 4; h *= 2) {  // strided layers len = 16, 32, 64 (all F3)
+    int64_t nlo[16], nhi[16];
+    std::copy(lo, lo + 16, nlo);
+    std::copy(hi, hi + 16, nhi);
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      if (lo[r] < P_ || !prod_ok(hi[r + h])) return;
+      nlo[r] = lo[r], nhi[r] = hi[r] + P_ - 1;
+      nlo[r + h] = lo[r] - P_ + 1, nhi[r + h] = hi[r];
+    }
+    std::copy(nlo, nlo + 16, lo);
+    std::copy(nhi, nhi + 16, hi);
+  }
+  for (int r = 0; r < 16; ++r)  // last layer: both operands are Plantard products
+    if (!prod_ok(hi[r])) return;
+  FastArgs A = P.fast[NTTK_IMPROVED][1];
+  A.flags = (A.flags & 3u) | 2048u;
+  std::copy(consts, consts + 8, A.ct_c);
+  const uint64_t oi = static_cast<uint64_t>(inverse(P.omega, p));
+  uint64_t w = 1;
+  for (int e = 0; e < 128; ++e) {  // lo[e] = (omega^{-e})^ mu, lo[128 + e] = (N^{-1} omega^{-e})^ mu
+    A.lo[e] = static_cast<uint32_t>(to_plantard(w, c) * c.mu & c.r2n_mask);
+    A.lo[128 + e] = static_cast<uint32_t>(
+        to_plantard(static_cast<uint64_t>(u128(w) * P.n_inv % p), c) * c.mu & c.r2n_mask);
+    w = static_cast<uint64_t>(u128(w) * oi % p);
+  }
+  A.scale_lo = static_cast<uint32_t>(to_plantard(P.n_inv, c) * c.mu & c.r2n_mask);
+  P.fast_ctinv = A;
+  P.ct_inv = true;
+}
+
 void fill_narrow(HostParams& P) {
   if (P.n_bits != 32 || P.p >= (1u << 15)) return;
   const uint64_t p = P.p;
@@ -741,7 +828,10 @@ int build_params(const nttk_params_desc& d, HostParams& P, std::string& err) {
 
   for (int k : {NTTK_NTL, NTTK_HARVEY, NTTK_SCOTT, NTTK_IMPROVED, NTTK_SMONT})
     if (has(k) && fast_eligible(P, k)) fill_fast(P, k);
-  if ((P.fast_mask >> NTTK_IMPROVED) & 1u) fill_narrow(P);
+  if ((P.fast_mask >> NTTK_IMPROVED) & 1u) {
+    fill_narrow(P);
+    fill_ct_inverse(P);
+  }
   return NTTK_OK;
 }
 

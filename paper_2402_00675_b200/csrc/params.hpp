@@ -71,11 +71,13 @@ struct FastArgs {
                            // bit5: inverse phase-2 block-0 twiddles are 1 (TW1, L = 8);
                            // bit6: u16 inverse without canonicalisation (DEFER);
                            // bit7: u32 inverse with partial canonicalisation to [0, 2p);
-                           // bit10: F1 forward (paper-form products, fwd_body_f1)
+                           // bit10: F1 forward (paper-form products, fwd_body_f1);
+                           // bit11: CT-form inverse image (HostParams::fast_ctinv)
   uint32_t fold_lo = 0, fold_hi = 0;  // last merge twiddle times N^{-1}, kind encoding
   uint32_t soff = 0;       // scott: butterfly offset (N/L) p (butterfly.hpp:172-184)
   uint32_t lzk = 0;        // SmontLazy16: K p > every final |r| (lift before mod_cb)
   uint32_t f1_sp = 0, f1_sp1 = 0;  // F1 forward surplus S p and (S + 1) p (fwd_body_f1)
+  uint32_t ct_c[8] = {};   // CT-form inverse: (X, Y) offsets of the twiddle-1 butterflies per layer
   uint32_t lo[256] = {};   // twiddle words in reference table order
   uint32_t hi[256] = {};   // high words of 64-bit premultiplied Plantard twiddles
 };
@@ -129,6 +131,10 @@ struct HostParams {
   // image fast[kNarrow][dir] (IMAD + IMAD.HI per product instead of IMAD.HI + IMAD +
   // IMAD.WIDE)
   bool narrow[2] = {};
+  // CT-form inverse of the Kyber u16 tree (params.cpp fill_ct_inverse, tma_common.cuh
+  // inv_body_ct): DIT butterflies on the bit-reversed spectrum with per-index twiddles
+  bool ct_inv = false;
+  FastArgs fast_ctinv;
   // fast-image index of (kind, dir): kNarrow where the narrow image applies
   int image(int kind, int dir) const {
     return kind == NTTK_IMPROVED && n_bits == 32 && narrow[dir] ? kNarrow : kind;

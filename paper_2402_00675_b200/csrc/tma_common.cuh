@@ -810,6 +810,79 @@ __device__ __forceinline__ void inv_body_narrow(uint32_t (&v)[16], const TWL& tw
   }
 }
 
+// CT-form inverse (HostParams::fast_ctinv, A.flags bit 11; params.cpp fill_ct_inverse has the
+// derivation and the bound checks).  Radix-2 DIT on the bit-reversed spectrum with omega^{-1}:
+// contiguous phase len = 1, 2, 4, 8 (uniform twiddles A.lo[(128 / len) jb], the jb = 0
+// butterfly of every block multiply-free with the host's offsets A.ct_c), transpose, strided
+// phase len = 16, 32, 64 (lane twiddles), then len = 128 with N^{-1} folded into two Plantard
+// products per butterfly and a min to the canonical residue.  Raw packed u16 words in v[8..15]
+// (the first layer pairs the halves of one word: dp2a); every product is the balanced F3 form.
+template <class K>
+__device__ __forceinline__ void ct_twiddles(uint32_t (&twl)[15], const FastArgs& A, int j) {
+  twl[0] = pin(A.lo[8 * j]);  // len 16: omega^{-8 j}
+#pragma unroll
+  for (int b = 0; b < 2; ++b) twl[1 + b] = pin(A.lo[4 * (j + 16 * b)]);  // len 32
+#pragma unroll
+  for (int b = 0; b < 4; ++b) twl[3 + b] = pin(A.lo[2 * (j + 16 * b)]);  // len 64
+#pragma unroll
+  for (int b = 0; b < 8; ++b) twl[7 + b] = pin(A.lo[128 + j + 16 * b]);  // len 128, N^{-1} folded
+}
+
+template <class TWL>
+__device__ __forceinline__ void inv_body_ct(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                            const Xpose& X) {
+  {
+    uint32_t t[16];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {  // len 1: positions 2m, 2m + 1 = the halves of word m
+      const uint32_t pw = v[8 + m];
+      asm("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(t[2 * m]) : "r"(pw), "r"(0x0101u), "r"(A.ct_c[0]));
+      asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(t[2 * m + 1]) : "r"(pw), "r"(0xff01u), "r"(A.ct_c[1]));
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = t[r];
+  }
+#pragma unroll
+  for (int li = 1; li <= 3; ++li) {  // len 2, 4, 8
+    const int len = 1 << li;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & len) continue;
+      const int jb = r & (len - 1);
+      if (jb == 0) {
+        const uint32_t u = v[r], w = v[r + len];
+        v[r] = u + w + A.ct_c[2 * li];
+        v[r + len] = u - w + A.ct_c[2 * li + 1];
+      } else {
+        f1_bf<true>(v[r], v[r + len], A.lo[(128 >> li) * jb], A);
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = X.get(r);
+#pragma unroll
+  for (int h = 1; h <= 4; h *= 2) {  // len 16, 32, 64
+    const int base = h == 1 ? 0 : h == 2 ? 1 : 3;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      f1_bf<true>(v[r], v[r + h], twl[base + (r & (h - 1))], A);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // len 128: (u + w v) N^{-1}, (u - w v) N^{-1}, canonical
+    const uint32_t a = mp_n16<true>(v[r], A.scale_lo, A.p);
+    const uint32_t b = mp_n16<true>(v[r + 8], twl[7 + r], A.p);
+    const uint32_t s = a + b, d = a + A.p - b;
+    v[r] = umin32(s, s - A.p);
+    v[r + 8] = umin32(d, d - A.p);
+  }
+}
+
 // LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3); TW1 / DEFER: see there.
 template <class K, int L, bool FUSE, bool LAZY = false, bool TW1 = false, bool DEFER = false,
           bool PACKED = false, int OSH = 0, class TWL>

@@ -235,3 +235,21 @@ def test_fast_flags_narrow_image(engine):
     assert not Pd.fast_flags(K.improved, 0) & NARROW
     Pk = engine.build_params(3329, 256, 16, [K.improved], exact_bound=True)
     assert not Pk.fast_flags(K.improved, 0) & NARROW
+
+
+CT_INV = 2048
+
+
+def test_fast_flags_ct_inverse(engine):
+    """params.cpp fill_ct_inverse: the Kyber u16 tree (improved n = 16, cyclic N = 256) admits
+    the CT-form inverse (every product operand inside Prop. 4's range under the host's interval
+    propagation); other trees and word sizes keep the GS inverse."""
+    K = engine.ButterflyKind
+    Pk = engine.build_params(3329, 256, 16, [K.improved], exact_bound=True)
+    assert Pk.fast_flags(K.improved, 1) & CT_INV
+    assert not Pk.fast_flags(K.improved, 0) & CT_INV
+    Pn = engine.build_params(3329, 256, 16, [K.improved], tree=engine.Tree.negacyclic, layers=7,
+                             exact_bound=True)
+    assert not Pn.fast_flags(K.improved, 1) & CT_INV
+    Pd = engine.build_params(8380417, 256, 32, [K.improved], exact_bound=True)
+    assert not Pd.fast_flags(K.improved, 1) & CT_INV

@@ -81,6 +81,10 @@ Q = o.params(3329, 256, 16, (IMPROVED,), exact=True)
 f = o.rng(31, 3329, 257 * 256).reshape(257, 256)
 y = nttk.forward(P, K.improved, torch.from_numpy(f.astype(np.int16)).cuda())
 assert (y.cpu().numpy().astype(np.int64) & 0xffff == Q.forward(IMPROVED, f)).all()
+# Kyber u16 inverse on arbitrary words (CT off: the GS lazy-merge body)
+w = np.random.RandomState(3).randint(0, 1 << 16, size=(129, 256)).astype(np.uint16)
+z = nttk.inverse(P, K.improved, torch.from_numpy(w.view(np.int16)).cuda())
+assert (z.cpu().numpy().astype(np.int64) == Q.inverse(IMPROVED, w.astype(np.uint64))).all()
 # fused polymul with the eager policies of every kind
 for kind, k in ((K.improved, IMPROVED), (K.harvey, HARVEY), (K.smont, SMONT)):
     P = nttk.build_params(3329, 256, 16, [kind], tree=nttk.Tree.negacyclic, layers=7, exact_bound=True)
@@ -95,12 +99,13 @@ print("ok")
 
 
 def test_ab_switches_keep_parity(tmp_path):
-    """The two runtime A/B switches (NTTK_FWD_F1=0: umulhi-form Kyber forward;
-    NTTK_POLYMUL_EAGER=1: the standalone policies inside the fused polymul) select other
-    exact arithmetic; in a fresh process their words must equal the oracle's too."""
+    """The runtime A/B switches (NTTK_FWD_F1=0: umulhi-form Kyber forward; NTTK_INV_CT=0: the
+    GS lazy-merge Kyber inverse; NTTK_POLYMUL_EAGER=1: the standalone policies inside the fused
+    polymul) select other exact arithmetic; in a fresh process their words must equal the
+    oracle's too."""
     script = tmp_path / "ab.py"
     script.write_text(AB_SCRIPT)
-    env = dict(os.environ, NTTK_FWD_F1="0", NTTK_POLYMUL_EAGER="1")
+    env = dict(os.environ, NTTK_FWD_F1="0", NTTK_POLYMUL_EAGER="1", NTTK_INV_CT="0")
     r = subprocess.run([sys.executable, str(script), ROOT], capture_output=True, text=True,
                        timeout=600, env=env)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

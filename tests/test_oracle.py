@@ -404,3 +404,85 @@ def test_f1_forward_schedule_n512_1024(oracle, N):
     want = Q.forward(IMPROVED, np.stack(rows))
     for k, row in enumerate(rows):
         assert _f1_schedule_model(row, ct, p, L - 2, w1_layer2=False) == [int(v) for v in want[k]]
+
+
+def _ct_inverse_model(F, p, omega):
+    """Integer model of tma_common.cuh inv_body_ct (Kyber N = 256): radix-2 DIT on the
+    bit-reversed spectrum with omega^{-1}, raw words in, the multiply-free jb = 0 butterflies of
+    len 1..8 adding per-layer offsets chosen as params.cpp fill_ct_inverse chooses them (interval
+    propagation, worst case merged at the transpose), F3 products elsewhere, N^{-1} folded into
+    the last layer.  Asserts the bounds the host validates."""
+    N = 256
+    lim = (1 << 16) * ((1 << 16) - p)
+    rup = lambda x: 0 if x <= 0 else (x + p - 1) // p * p  # noqa: E731
+    oi = pow(omega, p - 2, p)
+    ninv = pow(N, p - 2, p)
+    lo, hi = [0] * 16, [65535] * 16
+    consts = []
+    for li, fl in enumerate((6 * p, 5 * p, 4 * p, 3 * p)):
+        ln = 1 << li
+        free = [r for r in range(16) if not r & ln and r & (ln - 1) == 0]
+        c1 = max(rup(fl - lo[r] - lo[r + ln]) for r in free)
+        c2 = max(rup(fl - lo[r] + hi[r + ln]) for r in free)
+        consts.append((c1, c2))
+        nlo, nhi = lo[:], hi[:]
+        for r in range(16):
+            if r & ln:
+                continue
+            if r & (ln - 1) == 0:
+                nlo[r], nhi[r] = lo[r] + lo[r + ln] + c1, hi[r] + hi[r + ln] + c1
+                nlo[r + ln], nhi[r + ln] = lo[r] - hi[r + ln] + c2, hi[r] - lo[r + ln] + c2
+            else:
+                nlo[r], nhi[r] = lo[r], hi[r] + p - 1
+                nlo[r + ln], nhi[r + ln] = lo[r] - p + 1, hi[r]
+        lo, hi = nlo, nhi
+    v = [[int(F[16 * j + r]) for r in range(16)] for j in range(16)]
+    for a in v:  # contiguous phase: position 16 j + r
+        for li in range(4):
+            ln = 1 << li
+            c1, c2 = consts[li]
+            for r in range(16):
+                if r & ln:
+                    continue
+                jb = r & (ln - 1)
+                u, x = a[r], a[r + ln]
+                if jb == 0:
+                    a[r], a[r + ln] = u + x + c1, u - x + c2
+                else:
+                    assert x * (p - 1) < lim
+                    rr = x * pow(oi, (128 // ln) * jb, p) % p
+                    assert u - rr >= 0
+                    a[r], a[r + ln] = u + rr, u - rr
+    pos = {16 * j + r: v[j][r] for j in range(16) for r in range(16)}
+    out = [0] * N
+    for j in range(16):  # strided phase: position j + 16 r
+        a = [pos[j + 16 * r] for r in range(16)]
+        for h in (1, 2, 4):
+            for r in range(16):
+                if r & h:
+                    continue
+                u, x = a[r], a[r + h]
+                assert x * (p - 1) < lim
+                rr = x * pow(oi, (8 // h) * (j + 16 * (r % h)), p) % p
+                assert u - rr >= 0
+                a[r], a[r + h] = u + rr, u - rr
+        for r in range(8):
+            assert a[r] * (p - 1) < lim and a[r + 8] * (p - 1) < lim
+            A = a[r] * ninv % p
+            B = a[r + 8] * (ninv * pow(oi, j + 16 * r, p) % p) % p
+            out[j + 16 * r], out[j + 16 * (r + 8)] = (A + B) % p, (A - B) % p
+    return out
+
+
+def test_ct_inverse_schedule_matches_reference(oracle):
+    """The CT-form Kyber inverse (tma_common.cuh inv_body_ct) gives the reference's canonical
+    inverse (transform.hpp:233-343) on raw u16 words: all-max, all-zero, alternating, random."""
+    p = 3329
+    Q = oracle.params(p, 256, 16, (IMPROVED,), exact=True)
+    rs = np.random.RandomState(5)
+    rows = [np.full(256, 65535), np.zeros(256, dtype=np.int64),
+            np.where(np.arange(256) % 2 == 0, 65535, 0), rs.randint(0, 65536, 256),
+            rs.randint(0, p, 256)]
+    want = Q.inverse(IMPROVED, np.stack(rows).astype(np.uint64))
+    for k, row in enumerate(rows):
+        assert _ct_inverse_model(row, p, Q.omega) == [int(v) for v in want[k]]
