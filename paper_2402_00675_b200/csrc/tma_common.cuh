@@ -816,7 +816,9 @@ __device__ __forceinline__ void inv_body_narrow(uint32_t (&v)[16], const TWL& tw
 // butterfly of every block multiply-free with the host's offsets A.ct_c), transpose, strided
 // phase len = 16, 32, 64 (lane twiddles), then len = 128 with N^{-1} folded into two Plantard
 // products per butterfly and a min to the canonical residue.  Raw packed u16 words in v[8..15]
-// (the first layer pairs the halves of one word: dp2a); every product is the balanced F3 form.
+// (the first layer pairs the halves of one word: dp2a).  Products: F1 with the IADD3 Y in the
+// contiguous phase, F3 (IMAD Y) in the strided one -- the best of the per-layer masks measured
+// (0.939 vs 0.942 ms all-F3, 0.958 all-F1; profiles/r2_ct_inverse_ab.txt).
 template <class K>
 __device__ __forceinline__ void ct_twiddles(uint32_t (&twl)[15], const FastArgs& A, int j) {
   twl[0] = pin(A.lo[8 * j]);  // len 16: omega^{-8 j}
@@ -854,7 +856,7 @@ __device__ __forceinline__ void inv_body_ct(uint32_t (&v)[16], const TWL& twl, c
         v[r] = u + w + A.ct_c[2 * li];
         v[r + len] = u - w + A.ct_c[2 * li + 1];
       } else {
-        f1_bf<true>(v[r], v[r + len], A.lo[(128 >> li) * jb], A);
+        f1_bf<false>(v[r], v[r + len], A.lo[(128 >> li) * jb], A);  // IADD3 Y (ALU)
       }
     }
   }
@@ -870,7 +872,7 @@ __device__ __forceinline__ void inv_body_ct(uint32_t (&v)[16], const TWL& twl, c
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
-      f1_bf<true>(v[r], v[r + h], twl[base + (r & (h - 1))], A);
+      f1_bf<true>(v[r], v[r + h], twl[base + (r & (h - 1))], A);  // IMAD Y (fmaheavy)
     }
   }
 #pragma unroll
