@@ -205,8 +205,10 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
       }
-      if constexpr ((MODE & 64) != 0)
-        inv_body_ct(v, twl, A, X);
+      if constexpr ((MODE & 64) != 0) {
+        if constexpr (sizeof(IO) == 2) inv_body_ct(v, twl, A, X);
+        else inv_body_ct32(v, twl, A, X);
+      }
       else if constexpr ((MODE & 32) != 0)
         inv_body_narrow<K, L>(v, twl, A, X);
       else
@@ -222,8 +224,10 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
     }
   };
   Tw twl[15];
-  if constexpr ((MODE & 64) != 0)
+  if constexpr ((MODE & 64) != 0 && sizeof(IO) == 2)
     ct_twiddles<K>(twl, A, j);
+  else if constexpr ((MODE & 64) != 0)
+    ct_twiddles32(twl, A, j);
   else
     inv_twiddles<K, L>(twl, A, j);
   run(twl);
@@ -395,8 +399,12 @@ cudaError_t fast256_tma_launch_one(const HostParams& P, int kind, int dir, const
   if (batch == 0) return cudaSuccess;
   switch (kind) {
     case NTTK_IMPROVED:
-      if (dir == 1 && elem_bytes == 2 && P.ct_inv && ct_enabled())  // CT-form Kyber inverse
-        return inv_launch_mode<ImprovedN16<false>, uint16_t, 8, 64 | 16 | 2>(in, out, batch, P.fast_ctinv, st);
+      if (dir == 1 && P.ct_inv && ct_enabled()) {  // CT-form inverses (Kyber u16, Dilithium u32)
+        if (n16 && elem_bytes == 2)
+          return inv_launch_mode<ImprovedN16<false>, uint16_t, 8, 64 | 16 | 2>(in, out, batch, P.fast_ctinv, st);
+        if (!n16 && elem_bytes == 4)
+          return inv_launch_mode<ImprovedN32, uint32_t, 8, 64 | 3>(in, out, batch, P.fast_ctinv, st);
+      }
       if (P.image(kind, dir) == kNarrow)  // n = 32 parameters on the n = 16 product
         return by_io<ImprovedN16<false>, false>(dir, L, elem_bytes, in, out, batch,
                                                 P.fast[kNarrow][dir], st);

@@ -462,9 +462,67 @@ void fill_fast(HostParams& P, int kind) {
 // butterflies add to keep every F3 X input >= p (so X - r never underflows); the last layer
 // folds N^{-1} into two Plantard products per butterfly.  Every product operand must stay
 // inside Prop. 4's range, else the image is refused (the GS inverse stays).
+// n = 32 (Dilithium, u32): the same DIT schedule with the umulhi-form Plantard products of
+// ImprovedN32 (X' = X + r, Y' = X + p - r: never negative), inputs partially reduced to [0, 2p)
+// on load (shift reduction, A.flags bit 1); the multiply-free butterflies add the multiple of p
+// that covers their Y input.  Every word stays below 2^32 (host-checked); Prop. 4's n = 32 range
+// holds for any 32-bit operand.
+void fill_ct_inverse32(HostParams& P) {
+  const Ctx& c = P.ctx;
+  const uint64_t p = P.p;
+  const FastArgs& G = P.fast[NTTK_IMPROVED][1];
+  if (!(G.flags & 2) || (uint64_t(1) << G.cs_s) < p) return;  // the shift reduction of the load
+  auto rup = [&](uint64_t x) { return (x + p - 1) / p * p; };
+  uint64_t hi[16];
+  for (int r = 0; r < 16; ++r) hi[r] = 2 * p - 1;  // after v + (v >> s) (-p): below 2p
+  uint32_t consts[8] = {};
+  for (int li = 0; li < 4; ++li) {
+    const int len = 1 << li;
+    uint64_t c2 = 0;
+    for (int r = 0; r < 16; ++r)
+      if (!(r & len) && (r & (len - 1)) == 0) c2 = std::max(c2, rup(hi[r + len]));
+    consts[2 * li + 1] = static_cast<uint32_t>(c2);
+    uint64_t nhi[16];
+    std::copy(hi, hi + 16, nhi);
+    for (int r = 0; r < 16; ++r) {
+      if (r & len) continue;
+      if ((r & (len - 1)) == 0) {
+        nhi[r] = hi[r] + hi[r + len];
+        nhi[r + len] = hi[r] + c2;
+      } else {
+        nhi[r] = hi[r] + p - 1;
+        nhi[r + len] = hi[r] + p;
+      }
+    }
+    std::copy(nhi, nhi + 16, hi);
+  }
+  uint64_t H = 0;
+  for (int r = 0; r < 16; ++r) H = std::max(H, hi[r]);
+  H += 3 * p;  // strided layers len 16, 32, 64: X' < X + p, Y' <= X + p
+  if (H >= (uint64_t(1) << 32) || 2 * p >= (uint64_t(1) << 31)) return;
+  FastArgs A = G;
+  A.flags = (A.flags & 3u) | 2048u;
+  std::copy(consts, consts + 8, A.ct_c);
+  const uint64_t oi = static_cast<uint64_t>(inverse(P.omega, p));
+  uint64_t w = 1;
+  for (int e = 0; e < 128; ++e) {
+    const uint64_t a = to_plantard(w, c) * c.mu & c.r2n_mask;
+    const uint64_t b = to_plantard(static_cast<uint64_t>(u128(w) * P.n_inv % p), c) * c.mu & c.r2n_mask;
+    A.lo[e] = static_cast<uint32_t>(a), A.hi[e] = static_cast<uint32_t>(a >> 32);
+    A.lo[128 + e] = static_cast<uint32_t>(b), A.hi[128 + e] = static_cast<uint32_t>(b >> 32);
+    w = static_cast<uint64_t>(u128(w) * oi % p);
+  }
+  const uint64_t sm = to_plantard(P.n_inv, c) * c.mu & c.r2n_mask;
+  A.scale_lo = static_cast<uint32_t>(sm), A.scale_hi = static_cast<uint32_t>(sm >> 32);
+  P.fast_ctinv = A;
+  P.ct_inv = true;
+}
+
 void fill_ct_inverse(HostParams& P) {
-  if (P.n_bits != 16 || P.N != 256 || P.layers != 8 || P.tree != NTTK_CYCLIC) return;
+  if (P.N != 256 || P.layers != 8 || P.tree != NTTK_CYCLIC) return;
   if (!((P.fast_mask >> NTTK_IMPROVED) & 1u)) return;
+  if (P.n_bits == 32) return fill_ct_inverse32(P);
+  if (P.n_bits != 16) return;
   const Ctx& c = P.ctx;
   const uint64_t p = P.p;
   const u128 lim = u128(c.beta) * (c.beta - p);

@@ -885,6 +885,65 @@ __device__ __forceinline__ void inv_body_ct(uint32_t (&v)[16], const TWL& twl, c
   }
 }
 
+// n = 32 twin (Dilithium, u32; params.cpp fill_ct_inverse32): inputs partially reduced to
+// [0, 2p), ImprovedN32's umulhi-form products in the CT butterfly (X + r, X + p - r), the
+// multiply-free jb = 0 butterflies add A.ct_c[2 li + 1] >= their Y input, N^{-1} folded.
+__device__ __forceinline__ void ct_twiddles32(uint2 (&twl)[15], const FastArgs& A, int j) {
+  auto tw = [&](int e) { return make_uint2(A.lo[e], A.hi[e]); };
+  twl[0] = pin(tw(8 * j));
+#pragma unroll
+  for (int b = 0; b < 2; ++b) twl[1 + b] = pin(tw(4 * (j + 16 * b)));
+#pragma unroll
+  for (int b = 0; b < 4; ++b) twl[3 + b] = pin(tw(2 * (j + 16 * b)));
+#pragma unroll
+  for (int b = 0; b < 8; ++b) twl[7 + b] = pin(tw(128 + j + 16 * b));
+}
+
+template <class TWL>
+__device__ __forceinline__ void inv_body_ct32(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                              const Xpose& X) {
+#pragma unroll
+  for (int li = 0; li <= 3; ++li) {  // len 1, 2, 4, 8 (contiguous)
+    const int len = 1 << li;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & len) continue;
+      const int jb = r & (len - 1);
+      if (jb == 0) {
+        const uint32_t u = v[r], w = v[r + len];
+        v[r] = u + w + A.zero;
+        v[r + len] = u + A.ct_c[2 * li + 1] - w;
+      } else {
+        const int e = (128 >> li) * jb;
+        ImprovedN32::fwd(v[r], v[r + len], make_uint2(A.lo[e], A.hi[e]), A);
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = X.get(r);
+#pragma unroll
+  for (int h = 1; h <= 4; h *= 2) {  // len 16, 32, 64 (strided)
+    const int base = h == 1 ? 0 : h == 2 ? 1 : 3;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      ImprovedN32::fwd(v[r], v[r + h], twl[base + (r & (h - 1))], A);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // len 128, N^{-1} folded
+    const uint32_t a = mp_n32(v[r], A.scale_lo, A.scale_hi, A.p);
+    const uint32_t b = mp_n32(v[r + 8], twl[7 + r].x, twl[7 + r].y, A.p);
+    const uint32_t s = a + b, d = a + A.p - b;
+    v[r] = umin32(s, s - A.p);
+    v[r + 8] = umin32(d, d - A.p);
+  }
+}
+
 // LAZY: inv_body_lazy (policy kLazy, host-validated A.flags bit 3); TW1 / DEFER: see there.
 template <class K, int L, bool FUSE, bool LAZY = false, bool TW1 = false, bool DEFER = false,
           bool PACKED = false, int OSH = 0, class TWL>

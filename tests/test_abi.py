@@ -241,9 +241,10 @@ CT_INV = 2048
 
 
 def test_fast_flags_ct_inverse(engine):
-    """params.cpp fill_ct_inverse: the Kyber u16 tree (improved n = 16, cyclic N = 256) admits
-    the CT-form inverse (every product operand inside Prop. 4's range under the host's interval
-    propagation); other trees and word sizes keep the GS inverse."""
+    """params.cpp fill_ct_inverse: the Kyber tree (improved n = 16, cyclic N = 256) and the
+    Dilithium tree (n = 32) admit the CT-form inverse (every product operand inside Prop. 4's
+    range, every word below 2^32, under the host's interval propagation); negacyclic trees and
+    N != 256 keep the GS inverse."""
     K = engine.ButterflyKind
     Pk = engine.build_params(3329, 256, 16, [K.improved], exact_bound=True)
     assert Pk.fast_flags(K.improved, 1) & CT_INV
@@ -252,4 +253,6 @@ def test_fast_flags_ct_inverse(engine):
                              exact_bound=True)
     assert not Pn.fast_flags(K.improved, 1) & CT_INV
     Pd = engine.build_params(8380417, 256, 32, [K.improved], exact_bound=True)
-    assert not Pd.fast_flags(K.improved, 1) & CT_INV
+    assert Pd.fast_flags(K.improved, 1) & CT_INV
+    Pb = engine.build_params(12289, 1024, 32, [K.improved])
+    assert not Pb.fast_flags(K.improved, 1) & CT_INV

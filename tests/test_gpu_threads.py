@@ -85,6 +85,12 @@ assert (y.cpu().numpy().astype(np.int64) & 0xffff == Q.forward(IMPROVED, f)).all
 w = np.random.RandomState(3).randint(0, 1 << 16, size=(129, 256)).astype(np.uint16)
 z = nttk.inverse(P, K.improved, torch.from_numpy(w.view(np.int16)).cuda())
 assert (z.cpu().numpy().astype(np.int64) == Q.inverse(IMPROVED, w.astype(np.uint64))).all()
+# Dilithium u32 inverse on arbitrary words (CT off: the GS lazy merge with partial canonicalisation)
+Pd = nttk.build_params(8380417, 256, 32, [K.improved], exact_bound=True)
+Qd = o.params(8380417, 256, 32, (IMPROVED,), exact=True)
+wd = np.random.RandomState(4).randint(0, 1 << 32, size=(65, 256), dtype=np.uint64)
+zd = nttk.inverse(Pd, K.improved, torch.from_numpy(wd.astype(np.uint32).view(np.int32)).cuda())
+assert (zd.cpu().numpy().view(np.uint32).astype(np.int64) == Qd.inverse(IMPROVED, wd)).all()
 # fused polymul with the eager policies of every kind
 for kind, k in ((K.improved, IMPROVED), (K.harvey, HARVEY), (K.smont, SMONT)):
     P = nttk.build_params(3329, 256, 16, [kind], tree=nttk.Tree.negacyclic, layers=7, exact_bound=True)
