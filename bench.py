@@ -199,12 +199,12 @@ class ClockSampler:
 
 NCU_KERNELS = {"kyber_fwd": "fwd256_tma_kernel<ImprovedN16", "kyber_inv": "inv256_tma_kernel<ImprovedN16",
                "dil_fwd": "fwd256_tma_kernel<ImprovedN32", "dil_inv": "inv256_tma_kernel<ImprovedN32"}
-# the SASS-census instantiations of the bench kernels (MODE 30 = DEFER+dp2a Kyber inverse,
-# 15 = partial-canonicalisation lazy Dilithium inverse; W1 forwards)
+# the SASS-census instantiations of the bench kernels (MODE 82 / 67 = the CT-form Kyber /
+# Dilithium inverses; F1 + W1 forwards -- the last matching census row wins)
 CENSUS_KERNELS = {"kyber_fwd": "fwd256_tma_kernelINS_11ImprovedN16ILb0EEEtLi8ELb0ELb1E",
-                  "kyber_inv": "inv256_tma_kernelINS_11ImprovedN16ILb0EEEtLi8ELi30E",
+                  "kyber_inv": "inv256_tma_kernelINS_11ImprovedN16ILb0EEEtLi8ELi82E",
                   "dil_fwd": "fwd256_tma_kernelINS_11ImprovedN32EjLi8ELb0ELb1E",
-                  "dil_inv": "inv256_tma_kernelINS_11ImprovedN32EjLi8ELi15E",
+                  "dil_inv": "inv256_tma_kernelINS_11ImprovedN32EjLi8ELi67E",
                   # config 2 (fused polymul, 7-layer negacyclic, u16): the kernels that run
                   "pm_modified_plantard": "polymul256_tma_kernelINS_11ImprovedN16ILb0EEEtLi7ELb0ELb1ELb0ELb1E",
                   "pm_montgomery_R2^16": "polymul256_tma_kernelINS_12HarveyLazy16EtLi7E",
