@@ -380,7 +380,9 @@ int nttk_params_fast_flags(nttk_params_t h, int kind, int dir, uint32_t* flags) 
   if (!h || !flags) return fail(NTTK_CONTRACT, "params_fast_flags: null argument");
   if (dir != 0 && dir != 1) return fail(NTTK_CONTRACT, "params_fast_flags: dir must be 0 or 1");
   if (int s = check_kind(h->P, kind, "params_fast_flags")) return s;
-  *flags = h->P.fast[kind][dir].flags | (h->P.image(kind, dir) == nttk_b200::kNarrow ? 512u : 0u) |
+  const int img = h->P.image(kind, dir);
+  *flags = h->P.fast[kind][dir].flags | (img == nttk_b200::kNarrow ? 512u : 0u) |
+           (img == nttk_b200::kCtN ? 512u | 2048u : 0u) |
            (kind == NTTK_IMPROVED && dir == 1 && h->P.ct_inv ? 2048u : 0u);
   return NTTK_OK;
 }

@@ -234,15 +234,6 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
 }
 
 // ---------------------------------------------------------------------------
-// A/B switch while the CT-form inverse is measured (NTTK_INV_CT=0 runs the GS lazy merge)
-bool ct_enabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("NTTK_INV_CT");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
 // A/B switch while the F1 forward is measured (NTTK_FWD_F1=0 runs the umulhi form)
 bool f1_enabled() {
   static const bool v = [] {
@@ -399,7 +390,7 @@ cudaError_t fast256_tma_launch_one(const HostParams& P, int kind, int dir, const
   if (batch == 0) return cudaSuccess;
   switch (kind) {
     case NTTK_IMPROVED:
-      if (dir == 1 && P.ct_inv && ct_enabled()) {  // CT-form inverses (Kyber u16, Dilithium u32)
+      if (dir == 1 && P.ct_inv && ct_inverse_enabled()) {  // CT-form inverses (Kyber u16, Dilithium u32)
         if (n16 && elem_bytes == 2)
           return inv_launch_mode<ImprovedN16<false>, uint16_t, 8, 64 | 16 | 2>(in, out, batch, P.fast_ctinv, st);
         if (!n16 && elem_bytes == 4)

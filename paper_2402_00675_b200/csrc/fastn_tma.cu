@@ -558,6 +558,97 @@ __device__ __forceinline__ void inv_body_n_narrow(uint32_t (&v)[32], const uint2
   }
 }
 
+// CT-form inverse of the narrow image at N = 512 / 1024 (A.flags bit 11; params.cpp
+// fill_ct_inverse_n, tma_common.cuh inv_body_ct has the N = 256 derivation).  Radix-2 DIT on the
+// bit-reversed spectrum with omega^{-1}.  Contiguous phase (position 32 j + k, len = 1..16): the
+// jb = 0 butterfly of every block is multiply-free, the others run the F1 form with the uniform
+// twiddles A.lo[(16 / len) jb].  Strided phase (position j + G k, len = G h): F-form butterflies
+// with the lane twiddles of the shared-memory table (segment (h - 1) G, entry kk G + j), then
+// h = 16 with N^{-1} folded into two Plantard products per butterfly and a min to the canonical
+// residue.  The value interval [lo p, hi p) of every register is tracked at compile time (the
+// arrays below fold away in the full unroll): an F butterfly's X input needs lo >= 1 + the floor
+// its Y output must keep for the F layers still ahead (rq[]), the multiply-free butterflies set
+// their outputs' floors with the offsets A.pm[m] = m p, and an input wider than kT[li] p is first
+// reduced by one product by 1^ (four per lane in all).  Every product operand stays below
+// kCtLimN p, host-checked against Prop. 4's n = 16 range.
+template <class K, int LOGN, bool F3C, bool F3S>
+__device__ __forceinline__ void inv_body_n_ct(uint32_t (&v)[32], const uint32_t* tws, const FastArgs& A,
+                                              const XposeN<(1 << LOGN) / 32>& X, int j) {
+  constexpr int G = (1 << LOGN) / 32;
+  constexpr int H0 = LOGN == 10 ? 1 : 2;   // first strided register distance
+  constexpr int FS = LOGN == 10 ? 4 : 3;   // strided F layers (h = H0 .. 8)
+  constexpr int kT[5] = {1, 2, 4, 1, 2};   // widest multiply-free input per layer
+  int rq[6][32];  // rq[li][k]: floor register k needs before contiguous layer li
+#pragma unroll
+  for (int k = 0; k < 32; ++k) rq[5][k] = FS;
+#pragma unroll
+  for (int li = 4; li >= 0; --li) {
+    const int len = 1 << li;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & len) continue;
+      if ((k & (len - 1)) == 0) {
+        rq[li][k] = rq[li][k + len] = 0;
+      } else {
+        const int a = rq[li + 1][k], b = rq[li + 1][k + len] + 1;
+        rq[li][k] = a > b ? a : b;
+        rq[li][k + len] = 0;
+      }
+    }
+  }
+  int lo[32], hi[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) lo[k] = 0, hi[k] = 1;  // canonical input
+#pragma unroll
+  for (int li = 0; li < 5; ++li) {  // contiguous phase: len = 1, 2, 4, 8, 16
+    const int len = 1 << li;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & len) continue;
+      const int jb = k & (len - 1), m = k + len;
+      if (jb == 0) {
+        if (hi[k] - lo[k] > kT[li]) v[k] = K::canon1(v[k], A), lo[k] = 0, hi[k] = 1;
+        if (hi[m] - lo[m] > kT[li]) v[m] = K::canon1(v[m], A), lo[m] = 0, hi[m] = 1;
+        const int c1 = rq[li + 1][k] - (lo[k] + lo[m]), c2 = rq[li + 1][m] - (lo[k] - hi[m]);
+        const uint32_t u = v[k], w = v[m];
+        v[k] = u + w + A.pm[c1 < 0 ? 0 : c1];
+        v[m] = u - w + A.pm[c2 < 0 ? 0 : c2];
+        const int xl = lo[k] + lo[m] + (c1 < 0 ? 0 : c1), xh = hi[k] + hi[m] + (c1 < 0 ? 0 : c1);
+        const int yl = lo[k] - hi[m] + (c2 < 0 ? 0 : c2), yh = hi[k] - lo[m] + (c2 < 0 ? 0 : c2);
+        lo[k] = xl, hi[k] = xh, lo[m] = yl, hi[m] = yh;
+      } else {
+        f1_bf<F3C>(v[k], v[m], A.lo[(16 >> li) * jb], A);
+        lo[m] = lo[k] - 1, hi[m] = hi[k];
+        hi[k] = hi[k] + 1;
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X.put4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = X.get(k);
+#pragma unroll
+  for (int h = H0; h <= 8; h *= 2) {  // strided phase: len = G h
+    const uint32_t* seg = tws + (h - 1) * G + j;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & h) continue;
+      f1_bf<F3S>(v[k], v[k + h], seg[(k & (h - 1)) * G], A);
+    }
+  }
+  const uint32_t* seg = tws + 15 * G + j;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {  // len = N / 2: (u + w v) N^{-1}, (u - w v) N^{-1}, canonical
+    const uint32_t a = mp_n16<true>(v[k], A.scale_lo, A.p);
+    const uint32_t b = mp_n16<true>(v[k + 16], seg[k * G], A.p);
+    const uint32_t s = a + b, d = a + A.p - b;
+    v[k] = umin32(s, s - A.p);
+    v[k + 16] = umin32(d, d - A.p);
+  }
+}
+
 template <int LOGN, bool TRANSPOSE, bool MERGE>
 __device__ __forceinline__ void stage_table(uint2* tws, const uint32_t* tab) {
   constexpr int N = 1 << LOGN, G = N / 32;
@@ -634,7 +725,17 @@ __global__ void __launch_bounds__(GeoN<LOGN, IO, kFwdConsN>::kThreadsN)
 
 // MODE bits 0-1 -- 0: generic canonicalisation of the input words; 1: host-validated fast
 // form.  MODE bit 2: lazy merge (policy kLazy, A.flags bit 3); bit 3: TW1 (A.flags bit 5);
-// bit 5: narrow image (A.flags bit 9, inv_body_n_narrow).
+// bit 5: narrow image (A.flags bit 9, inv_body_n_narrow); bit 6: CT-form narrow inverse (A.flags
+// bit 11, inv_body_n_ct; the table is staged verbatim).
+// Product forms of the CT-form inverse (f1_bf: Y' = 2 X - X' as an IADD3 or as an IMAD) in the
+// contiguous / strided phase.  Measured (profiles/r2_ctn_inverse_ab.txt, ns/poly at 2^17):
+// N = 512 IADD3 / IMAD 0.705 (IMAD / IADD3 0.722, all-IMAD 0.721, all-IADD3 0.722);
+// N = 1024 IMAD / IADD3 1.405 (IADD3 / IMAD 1.426, all-IMAD 1.411, all-IADD3 1.439).
+template <int LOGN>
+constexpr bool ct_f3_contiguous() {
+  return LOGN == 10;
+}
+
 template <class K, class IO, int LOGN, int MODE, int C = kConsumers>
 __global__ void __launch_bounds__((C + 1) * 32)
     invn_tma_kernel(const IO* __restrict__ in, IO* __restrict__ out, size_t batch,
@@ -651,7 +752,7 @@ __global__ void __launch_bounds__((C + 1) * 32)
   uint2* tws = reinterpret_cast<uint2*>(scratch + kConsumers * GN::kScratchWords);
   uint64_t* full = reinterpret_cast<uint64_t*>(tws + GN::N);
   uint64_t* empty = full + GN::kStages;
-  stage_table<LOGN, true, true>(tws, tab);
+  stage_table<LOGN, (MODE & 64) == 0, true>(tws, tab);
   init_barriers(full, empty, GN::kStages, kConsumers);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kConsumers) {
@@ -688,7 +789,9 @@ __global__ void __launch_bounds__((C + 1) * 32)
     release_stage(&empty[s], lane);
 #pragma unroll
     for (int k = 0; k < 32; ++k) v[k] = canon<IO, K::kSigned, (MODE & 3) == 1>(v[k], A);
-    if constexpr ((MODE & 32) != 0) inv_body_n_narrow<K, LOGN>(v, tws, A, X, j);
+    if constexpr ((MODE & 64) != 0)
+      inv_body_n_ct<K, LOGN, ct_f3_contiguous<LOGN>(), !ct_f3_contiguous<LOGN>()>(v, reinterpret_cast<const uint32_t*>(tws), A, X, j);
+    else if constexpr ((MODE & 32) != 0) inv_body_n_narrow<K, LOGN>(v, tws, A, X, j);
     else if constexpr ((MODE & 4) != 0) inv_body_n_lazy<K, LOGN, (MODE & 8) != 0>(v, tws, A, X, j);
     else inv_body_n<K, LOGN>(v, tws, A, X, j);
     store_strided_n<IO, G>(out + poly * GN::N, j, v, X, poly < batch);
@@ -768,6 +871,7 @@ template <class K, class IO, int LOGN>
 cudaError_t inv_n(const void* in, void* out, size_t batch, const uint32_t* tab, const FastArgs& A,
                   cudaStream_t st) {
   if constexpr (std::is_same<K, ImprovedN16<false>>::value) {
+    if (A.flags & 2048) return inv_n_canon<K, IO, LOGN, 64>(in, out, batch, tab, A, st);  // CT form
     if (A.flags & 512) return inv_n_canon<K, IO, LOGN, 32>(in, out, batch, tab, A, st);  // narrow
   }
   if constexpr (lazy_of<K>::value) {
@@ -814,9 +918,9 @@ cudaError_t fastn_launch(const HostParams& P, int kind, int dir, const void* in,
   if (batch == 0) return cudaSuccess;
   switch (kind) {
     case NTTK_IMPROVED:
-      if (P.image(kind, dir) == kNarrow)  // n = 32 parameters on the n = 16 product (tab: narrow)
-        return by_elem<ImprovedN16<false>, false>(dir, logn, elem_bytes, in, out, batch, tab,
-                                                  P.fast[kNarrow][dir], st);
+      if (P.image(kind, dir) == kNarrow || P.image(kind, dir) == kCtN)  // n = 32 parameters on the
+        return by_elem<ImprovedN16<false>, false>(dir, logn, elem_bytes, in, out, batch, tab,  // n = 16 product
+                                                  P.fast[P.image(kind, dir)][dir], st);
       return n16 ? by_elem<ImprovedN16<false>, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st)
                  : by_elem<ImprovedN32, false>(dir, logn, elem_bytes, in, out, batch, tab, A, st);
     case NTTK_HARVEY:

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace nttk_b200 {
@@ -596,6 +597,42 @@ void fill_ct_inverse(HostParams& P) {
   P.ct_inv = true;
 }
 
+// CT-form inverse of the narrow image at N = 512 / 1024 (fastn_tma.cu inv_body_n_ct; the N = 256
+// derivation above applies).  Lane j owns positions 32 j + k in the contiguous phase (len = 1..16,
+// uniform twiddles omega^{-(N/32) e} in A.lo[e], e < 16, the jb = 0 butterflies multiply-free) and
+// j + G k in the strided phase (len = G h; lane twiddles from the shared-memory table, segment
+// (h - 1) G holds omega^{-(16/h)(j + G kk)} at kk G + j; the h = 16 segment carries N^{-1}).
+// The kernel's schedule is fixed at compile time in units of p: canonical inputs, offsets
+// A.pm[m] = m p, four canon1 reductions, every product operand below kCtLimN p -- so the image
+// is valid exactly when kCtLimN p lies inside Prop. 4's n = 16 range.  The schedule itself is
+// proven on the CPU against the reference inverse (tests/test_oracle.py).
+void fill_ct_inverse_n(HostParams& P, const Ctx& c16) {
+  const uint64_t p = P.p, N = P.N, G = N / 32;
+  const u128 lim = u128(c16.beta) * (c16.beta - p);
+  if (!(u128(p - 1) * (uint64_t(kCtLimN) * p - 1) < lim)) return;
+  FastArgs A = P.fast[kNarrow][1];
+  A.flags = (A.flags & 3u) | 2048u;
+  for (uint32_t m = 0; m < 12; ++m) A.pm[m] = m * static_cast<uint32_t>(p);
+  auto enc = [&](uint64_t w) { return static_cast<uint32_t>(to_plantard(w, c16) * c16.mu & c16.r2n_mask); };
+  const uint64_t oi = static_cast<uint64_t>(inverse(P.omega, p));
+  std::vector<uint64_t> pw(N / 2);  // omega^{-e}
+  pw[0] = 1;
+  for (size_t e = 1; e < pw.size(); ++e) pw[e] = static_cast<uint64_t>(u128(pw[e - 1]) * oi % p);
+  for (int e = 0; e < 16; ++e) A.lo[e] = enc(pw[(N / 32) * e]);
+  std::vector<uint32_t> tab(2 * N, 0);
+  for (uint64_t h = 1; h <= 16; h *= 2)
+    for (uint64_t kk = 0; kk < h; ++kk)
+      for (uint64_t j = 0; j < G; ++j) {
+        uint64_t w = pw[(16 / h) * (j + G * kk)];
+        if (h == 16) w = static_cast<uint64_t>(u128(w) * P.n_inv % p);
+        tab[(h - 1) * G + kk * G + j] = enc(w);
+      }
+  A.scale_lo = enc(P.n_inv);
+  P.fast[kCtN][1] = A;
+  P.fastn_tab[kCtN][1] = tab;
+  P.ct_inv_n = true;
+}
+
 void fill_narrow(HostParams& P) {
   if (P.n_bits != 32 || P.p >= (1u << 15)) return;
   const uint64_t p = P.p;
@@ -637,10 +674,19 @@ void fill_narrow(HostParams& P) {
     P.fast[kNarrow][1] = I;
     P.fastn_tab[kNarrow][1] = T.fastn_tab[NTTK_IMPROVED][1];
     P.narrow[1] = true;
+    if ((P.N == 512 || P.N == 1024) && P.tree == NTTK_CYCLIC) fill_ct_inverse_n(P, c16);
   }
 }
 
 }  // namespace
+
+bool ct_inverse_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("NTTK_INV_CT");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 
 HostParams::~HostParams() {
   for (auto& d : dev)
@@ -659,8 +705,8 @@ const uint32_t* HostParams::fastn_table(int device, int kind, int dir, std::stri
   std::lock_guard<std::mutex> lock(mu_dev);
   if (!fastn_dev[device]) {
     const size_t stride = 2 * size_t(N);
-    std::vector<uint32_t> host(12 * stride, 0);
-    for (int k = 0; k < 6; ++k)
+    std::vector<uint32_t> host(14 * stride, 0);
+    for (int k = 0; k < 7; ++k)
       for (int d = 0; d < 2; ++d)
         std::copy(fastn_tab[k][d].begin(), fastn_tab[k][d].end(), host.begin() + (2 * k + d) * stride);
     uint32_t* buf = nullptr;

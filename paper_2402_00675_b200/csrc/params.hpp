@@ -78,6 +78,7 @@ struct FastArgs {
   uint32_t lzk = 0;        // SmontLazy16: K p > every final |r| (lift before mod_cb)
   uint32_t f1_sp = 0, f1_sp1 = 0;  // F1 forward surplus S p and (S + 1) p (fwd_body_f1)
   uint32_t ct_c[8] = {};   // CT-form inverse: (X, Y) offsets of the twiddle-1 butterflies per layer
+  uint32_t pm[12] = {};    // pm[m] = m p: offsets of the N = 512 / 1024 CT-form inverse (inv_body_n_ct)
   uint32_t lo[256] = {};   // twiddle words in reference table order
   uint32_t hi[256] = {};   // high words of 64-bit premultiplied Plantard twiddles
 };
@@ -101,6 +102,12 @@ struct PolymulArgs {
 };
 
 constexpr int kNarrow = 5;  // pseudo-kind index of the narrow improved image
+constexpr int kCtN = 6;     // pseudo-kind index of the N = 512 / 1024 CT-form inverse image
+// CT-form inverse at N = 512 / 1024 (fastn_tma.cu inv_body_n_ct): every product operand stays
+// below kCtLimN p, which must lie inside the n = 16 Prop. 4 range (params.cpp fill_ct_inverse_n)
+constexpr int kCtLimN = 20;
+// NTTK_INV_CT=0 keeps the GS-form inverses (the A/B of the CT-form ones)
+bool ct_inverse_enabled();
 // narrow inverse: every GS operand below 2^kNarrowEmax p (tma_common.cuh inv_body_narrow)
 constexpr int kNarrowEmax = 4;
 // F1 forward at N = 256: surplus multiples of p injected by layer 1 (= L - 2, fwd_body_f1)
@@ -123,7 +130,7 @@ struct HostParams {
   std::vector<uint64_t> gamma;
   // fast-path images, indexed [kind][dir] (dir 0 forward, 1 inverse)
   uint32_t fast_mask = 0;
-  FastArgs fast[6][2];  // [5] = kNarrow
+  FastArgs fast[7][2];  // [5] = kNarrow, [6] = kCtN
   ProdArgs prod[5];
   // n = 16 evaluation of an n = 32 improved parameter set (params.cpp fill_narrow): the
   // improved words do not depend on n, so when every operand of a
@@ -135,13 +142,17 @@ struct HostParams {
   // inv_body_ct): DIT butterflies on the bit-reversed spectrum with per-index twiddles
   bool ct_inv = false;
   FastArgs fast_ctinv;
-  // fast-image index of (kind, dir): kNarrow where the narrow image applies
+  // CT-form inverse of the narrow image at N = 512 / 1024 (params.cpp fill_ct_inverse_n)
+  bool ct_inv_n = false;
+  // fast-image index of (kind, dir): kNarrow where the narrow image applies, kCtN where its
+  // inverse runs in CT form
   int image(int kind, int dir) const {
-    return kind == NTTK_IMPROVED && n_bits == 32 && narrow[dir] ? kNarrow : kind;
+    if (!(kind == NTTK_IMPROVED && n_bits == 32 && narrow[dir])) return kind;
+    return dir == 1 && ct_inv_n && ct_inverse_enabled() ? kCtN : kNarrow;
   }
   // N = 512 / 1024 fast kernels: whole per-direction tables, interleaved (lo, hi) words,
   // uploaded once per device on first use
-  std::vector<uint32_t> fastn_tab[6][2];
+  std::vector<uint32_t> fastn_tab[7][2];
   mutable uint32_t* fastn_dev[64] = {};
   const uint32_t* fastn_table(int device, int kind, int dir, std::string& err) const;
 

@@ -243,8 +243,10 @@ CT_INV = 2048
 def test_fast_flags_ct_inverse(engine):
     """params.cpp fill_ct_inverse: the Kyber tree (improved n = 16, cyclic N = 256) and the
     Dilithium tree (n = 32) admit the CT-form inverse (every product operand inside Prop. 4's
-    range, every word below 2^32, under the host's interval propagation); negacyclic trees and
-    N != 256 keep the GS inverse."""
+    range, every word below 2^32, under the host's interval propagation); negacyclic trees keep
+    the GS inverse.  fill_ct_inverse_n: the narrow image at N = 512 / 1024 runs in CT form when
+    kCtLimN p = 20 p lies inside the n = 16 range (the Table 2 modulus 12289), else the GS narrow
+    body stays (p = 13313: 16 p fits, 20 p does not)."""
     K = engine.ButterflyKind
     Pk = engine.build_params(3329, 256, 16, [K.improved], exact_bound=True)
     assert Pk.fast_flags(K.improved, 1) & CT_INV
@@ -254,5 +256,14 @@ def test_fast_flags_ct_inverse(engine):
     assert not Pn.fast_flags(K.improved, 1) & CT_INV
     Pd = engine.build_params(8380417, 256, 32, [K.improved], exact_bound=True)
     assert Pd.fast_flags(K.improved, 1) & CT_INV
-    Pb = engine.build_params(12289, 1024, 32, [K.improved])
-    assert not Pb.fast_flags(K.improved, 1) & CT_INV
+    for N in (512, 1024):
+        Pb = engine.build_params(12289, N, 32, [K.improved])
+        assert Pb.fast_flags(K.improved, 1) & (CT_INV | NARROW) == CT_INV | NARROW
+        assert not Pb.fast_flags(K.improved, 0) & CT_INV
+    lim = lambda p: (1 << 16) * ((1 << 16) - p)  # noqa: E731
+    p = 13313
+    assert (p - 1) * (16 * p) < lim(p) <= (p - 1) * (20 * p - 1)
+    Pc = engine.build_params(p, 512, 32, [K.improved])
+    assert Pc.fast_flags(K.improved, 1) & (CT_INV | NARROW) == NARROW
+    P7 = engine.build_params(7681, 256, 32, [K.improved])  # N = 256 narrow image: GS narrow body
+    assert P7.fast_flags(K.improved, 1) & (CT_INV | NARROW) == NARROW

@@ -914,3 +914,24 @@ def test_narrow_image_extremes(oracle, name):
     assert (from_dev(nttk.forward(P, IMPROVED, to_dev(f, 4))) == Q.forward(IMPROVED, f)).all()
     w = _extreme_words(p, 32, 67, 5 + N, N)
     assert (from_dev(nttk.inverse(P, IMPROVED, to_dev(w, 4))) == Q.inverse(IMPROVED, w)).all()
+
+
+@pytest.mark.parametrize("N", [512, 1024])
+def test_ct_narrow_inverse_and_its_fallback(oracle, N):
+    """N = 512 / 1024 improved inverses: the Table 2 modulus 12289 runs the CT-form narrow inverse
+    (fastn_tma.cu inv_body_n_ct, flags bit 11); p = 13313 fits the narrow image but not
+    kCtLimN p, so it keeps the GS narrow body.  Extreme and random storage words, ragged batches, bit-exact with the oracle's n = 32 reference inverse
+    (transform.hpp:233-343)."""
+    for p, ct in ((12289, True), (13313, False)):
+        P = nttk.build_params(p, N, 32, [IMPROVED])
+        fl = P.fast_flags(IMPROVED, 1)
+        assert bool(fl & 2048) == ct and fl & 512
+        Q = oracle.params(p, N, 32, (IMPROVED,))
+        for batch in (15, 33, 67):
+            w = _extreme_words(p, 32, batch, 7 + N + batch, N)
+            assert (from_dev(nttk.inverse(P, IMPROVED, to_dev(w, 4))) == Q.inverse(IMPROVED, w)).all()
+            assert (from_dev(nttk.inverse(P, IMPROVED, to_dev(w[:1], 4))) == Q.inverse(IMPROVED, w[:1])).all()
+        f = oracle.rng(17, p, 70 * N).reshape(70, N).astype(np.int64)
+        s = nttk.forward(P, IMPROVED, to_dev(f, 4))
+        assert (from_dev(s) == Q.forward(IMPROVED, f)).all()
+        assert (from_dev(nttk.inverse(P, IMPROVED, s)) == f).all()

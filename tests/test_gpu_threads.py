@@ -91,6 +91,13 @@ Qd = o.params(8380417, 256, 32, (IMPROVED,), exact=True)
 wd = np.random.RandomState(4).randint(0, 1 << 32, size=(65, 256), dtype=np.uint64)
 zd = nttk.inverse(Pd, K.improved, torch.from_numpy(wd.astype(np.uint32).view(np.int32)).cuda())
 assert (zd.cpu().numpy().view(np.uint32).astype(np.int64) == Qd.inverse(IMPROVED, wd)).all()
+# Table 2 presets, inverse on arbitrary words (CT off: the GS narrow body of fastn_tma.cu)
+for name in ("newhope512", "newhope1024"):
+    Pn = nttk.preset(name)
+    Qn = o.params(Pn.p, Pn.size, 32, (IMPROVED,))
+    wn = np.random.RandomState(5).randint(0, 1 << 32, size=(35, Pn.size), dtype=np.uint64)
+    zn = nttk.inverse(Pn, K.improved, torch.from_numpy(wn.astype(np.uint32).view(np.int32)).cuda())
+    assert (zn.cpu().numpy().view(np.uint32).astype(np.int64) == Qn.inverse(IMPROVED, wn)).all(), name
 # fused polymul with the eager policies of every kind
 for kind, k in ((K.improved, IMPROVED), (K.harvey, HARVEY), (K.smont, SMONT)):
     P = nttk.build_params(3329, 256, 16, [kind], tree=nttk.Tree.negacyclic, layers=7, exact_bound=True)
@@ -106,7 +113,7 @@ print("ok")
 
 def test_ab_switches_keep_parity(tmp_path):
     """The runtime A/B switches (NTTK_FWD_F1=0: umulhi-form Kyber forward; NTTK_INV_CT=0: the
-    GS lazy-merge Kyber inverse; NTTK_POLYMUL_EAGER=1: the standalone policies inside the fused
+    GS lazy-merge Kyber / Dilithium inverses and the GS narrow inverse at N = 512 / 1024; NTTK_POLYMUL_EAGER=1: the standalone policies inside the fused
     polymul) select other exact arithmetic; in a fresh process their words must equal the
     oracle's too."""
     script = tmp_path / "ab.py"

@@ -474,6 +474,96 @@ def _ct_inverse_model(F, p, omega):
     return out
 
 
+def _ct_inverse_model_n(F, p, omega, N):
+    """Integer model of fastn_tma.cu inv_body_n_ct (N = 512 / 1024, narrow image): canonical
+    input, compile-time interval schedule in units of p (floors rq, offsets m p, canon1 when a
+    multiply-free input is wider than kT p), F-form products, N^{-1} folded.  Asserts every bound
+    the schedule promises with the actual values, and Prop. 4's n = 16 range below kCtLimN p."""
+    G, FS = N // 32, (4 if N == 1024 else 3)
+    H0 = 1 if N == 1024 else 2
+    kT, LIM = (1, 2, 4, 1, 2), 20
+    lim = (1 << 16) * ((1 << 16) - p)
+    assert (p - 1) * (LIM * p - 1) < lim
+    oi, ninv = pow(omega, p - 2, p), pow(N, p - 2, p)
+    rq = [[0] * 32 for _ in range(6)]
+    rq[5] = [FS] * 32
+    for li in range(4, -1, -1):
+        ln = 1 << li
+        for k in range(32):
+            if k & ln or k & (ln - 1) == 0:
+                continue
+            rq[li][k] = max(rq[li + 1][k], rq[li + 1][k + ln] + 1)
+    ncanon = 0
+    pos = {}
+    for j in range(N // 32):  # contiguous phase: position 32 j + k
+        v = [int(F[32 * j + k]) % p for k in range(32)]
+        lo, hi = [0] * 32, [1] * 32
+        for li in range(5):
+            ln = 1 << li
+            for k in range(32):
+                if k & ln:
+                    continue
+                m, jb = k + ln, k & (ln - 1)
+                if jb == 0:
+                    for r in (k, m):
+                        if hi[r] - lo[r] > kT[li]:
+                            assert v[r] < LIM * p
+                            v[r], lo[r], hi[r] = v[r] % p, 0, 1
+                            ncanon += j == 0
+                    c1 = max(0, rq[li + 1][k] - (lo[k] + lo[m]))
+                    c2 = max(0, rq[li + 1][m] - (lo[k] - hi[m]))
+                    assert c1 < 12 and c2 < 12
+                    u, w = v[k], v[m]
+                    v[k], v[m] = u + w + c1 * p, u - w + c2 * p
+                    lo[k], hi[k], lo[m], hi[m] = (lo[k] + lo[m] + c1, hi[k] + hi[m] + c1,
+                                                  lo[k] - hi[m] + c2, hi[k] - lo[m] + c2)
+                else:
+                    assert v[m] < LIM * p and lo[k] >= rq[li][k] >= 1
+                    rr = v[m] * pow(oi, (N // (2 * ln)) * jb, p) % p
+                    v[k], v[m] = v[k] + rr, v[k] - rr
+                    lo[m], hi[m], hi[k] = lo[k] - 1, hi[k], hi[k] + 1
+                for r in (k, m):
+                    assert lo[r] * p <= v[r] < hi[r] * p and lo[r] >= rq[li + 1][r]
+        assert min(lo) >= FS and max(hi) + FS <= LIM
+        for k in range(32):
+            pos[32 * j + k] = v[k]
+    assert ncanon == 4
+    out = [0] * N
+    for j in range(G):  # strided phase: position j + G k
+        a = [pos[j + G * k] for k in range(32)]
+        h = H0
+        while h <= 8:
+            for k in range(32):
+                if k & h:
+                    continue
+                assert a[k + h] * (p - 1) < lim
+                rr = a[k + h] * pow(oi, (16 // h) * (j + G * (k % h)), p) % p
+                assert a[k] - rr >= 0
+                a[k], a[k + h] = a[k] + rr, a[k] - rr
+            h *= 2
+        for k in range(16):
+            assert a[k] < LIM * p and a[k + 16] < LIM * p
+            A = a[k] * ninv % p
+            B = a[k + 16] * (ninv * pow(oi, j + G * k, p) % p) % p
+            out[j + G * k], out[j + G * (k + 16)] = (A + B) % p, (A - B) % p
+    return out
+
+
+@pytest.mark.parametrize("N", [512, 1024])
+def test_ct_inverse_schedule_n_matches_reference(oracle, N):
+    """The CT-form narrow inverse at N = 512 / 1024 (fastn_tma.cu inv_body_n_ct) gives the
+    reference's canonical inverse (transform.hpp:233-343) for the Table 2 modulus: extreme,
+    alternating and random canonical spectra (the kernel canonicalises raw words first)."""
+    p = 12289
+    Q = oracle.params(p, N, 32, (IMPROVED,))
+    rs = np.random.RandomState(11)
+    rows = [np.full(N, p - 1), np.zeros(N, dtype=np.int64), np.where(np.arange(N) % 2 == 0, p - 1, 0),
+            np.where(np.arange(N) % 2 == 1, p - 1, 0), rs.randint(0, p, N), rs.randint(0, 1 << 32, N)]
+    want = Q.inverse(IMPROVED, np.stack(rows).astype(np.uint64))
+    for k, row in enumerate(rows):
+        assert _ct_inverse_model_n(row, p, Q.omega, N) == [int(v) for v in want[k]]
+
+
 def test_ct_inverse_schedule_matches_reference(oracle):
     """The CT-form Kyber inverse (tma_common.cuh inv_body_ct) gives the reference's canonical
     inverse (transform.hpp:233-343) on raw u16 words: all-max, all-zero, alternating, random."""
