@@ -98,8 +98,12 @@ int nttk_params_get_info(nttk_params_t P, nttk_params_info* out);
  * blocks (TW1), 64 u16 inverse without canonicalisation (DEFER), 128 u32 inverse partial
  * canonicalisation, 256 (dir 1) the fused polymul runs the kind's lazy Montgomery twin
  * (harvey / smont, n = 16), 512 the direction runs the n = 16 product on an n = 32 improved
- * parameter set (narrow image), 1024 (dir 0) the F1 forward, 2048 (dir 1) the u16 inverse runs
- * the CT-form body.  Status 2 if the kind is not built into P. */
+ * parameter set (narrow image), 1024 (dir 0) the F1 forward, 2048 (dir 1) the inverse runs the
+ * CT-form body (N = 256: Kyber u16 / Dilithium u32 trees; N = 512 / 1024: the narrow image when
+ * 20 p lies inside the n = 16 Prop. 4 range).  Status 2 if the kind is not built into P.
+ * Process-wide A/B switches read once from the environment (results never change):
+ * NTTK_INV_CT=0 keeps the GS-form inverses, NTTK_FWD_F1=0 the umulhi-form Kyber forward,
+ * NTTK_POLYMUL_EAGER=1 the standalone policies inside the fused polymul. */
 int nttk_params_fast_flags(nttk_params_t P, int kind, int dir, uint32_t* flags);
 /* read back a host table (names: dif_w dif_wq dif_mont ct_plain ct_plantard ct_mont
  * ct_smont gs_plain gs_wq gs_mont gs_plantard gs_smont); returns its length */
