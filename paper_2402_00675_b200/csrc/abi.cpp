@@ -383,7 +383,7 @@ int nttk_params_fast_flags(nttk_params_t h, int kind, int dir, uint32_t* flags) 
   const int img = h->P.image(kind, dir);
   *flags = h->P.fast[kind][dir].flags | (img == nttk_b200::kNarrow ? 512u : 0u) |
            (img == nttk_b200::kCtN ? 512u | 2048u : 0u) |
-           (kind == NTTK_IMPROVED && dir == 1 && h->P.ct_inv ? 2048u : 0u);
+           (kind == NTTK_IMPROVED && dir == 1 && (h->P.ct_inv || h->P.ct_inv_c) ? 2048u : 0u);
   return NTTK_OK;
 }
 

@@ -206,8 +206,8 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
         for (int r = 0; r < 16; ++r) v[r] = canon<IO, K::kSigned, CM == 1>(v[r], A);
       }
       if constexpr ((MODE & 64) != 0) {
-        if constexpr (sizeof(IO) == 2) inv_body_ct(v, twl, A, X);
-        else inv_body_ct32(v, twl, A, X);
+        if constexpr (std::is_same<K, ImprovedN32>::value) inv_body_ct32(v, twl, A, X);
+        else inv_body_ct<kPacked>(v, twl, A, X);
       }
       else if constexpr ((MODE & 32) != 0)
         inv_body_narrow<K, L>(v, twl, A, X);
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(GeoK<K, IO, 1>::kThreadsP, 1)
     }
   };
   Tw twl[15];
-  if constexpr ((MODE & 64) != 0 && sizeof(IO) == 2)
+  if constexpr ((MODE & 64) != 0 && !std::is_same<K, ImprovedN32>::value)
     ct_twiddles<K>(twl, A, j);
   else if constexpr ((MODE & 64) != 0)
     ct_twiddles32(twl, A, j);
@@ -396,6 +396,13 @@ cudaError_t fast256_tma_launch_one(const HostParams& P, int kind, int dir, const
         if (!n16 && elem_bytes == 4)
           return inv_launch_mode<ImprovedN32, uint32_t, 8, 64 | 3>(in, out, batch, P.fast_ctinv, st);
       }
+      // canonicalised u32 words through the n = 16 CT body (n = 16 sets in u32 storage, and the
+      // narrow image of an n = 32 set: the kyber256 preset)
+      if (dir == 1 && P.ct_inv_c && elem_bytes == 4 && ct_inverse_enabled() &&
+          (n16 || P.image(kind, dir) == kNarrow))
+        return (P.fast_ctinv_c.flags & 2u)
+                   ? inv_launch_mode<ImprovedN16<false>, uint32_t, 8, 64 | 1>(in, out, batch, P.fast_ctinv_c, st)
+                   : inv_launch_mode<ImprovedN16<false>, uint32_t, 8, 64>(in, out, batch, P.fast_ctinv_c, st);
       if (P.image(kind, dir) == kNarrow)  // n = 32 parameters on the n = 16 product
         return by_io<ImprovedN16<false>, false>(dir, L, elem_bytes, in, out, batch,
                                                 P.fast[kNarrow][dir], st);

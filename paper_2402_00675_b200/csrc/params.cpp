@@ -519,24 +519,26 @@ void fill_ct_inverse32(HostParams& P) {
   P.ct_inv = true;
 }
 
-void fill_ct_inverse(HostParams& P) {
-  if (P.N != 256 || P.layers != 8 || P.tree != NTTK_CYCLIC) return;
-  if (!((P.fast_mask >> NTTK_IMPROVED) & 1u)) return;
-  if (P.n_bits == 32) return fill_ct_inverse32(P);
-  if (P.n_bits != 16) return;
-  const Ctx& c = P.ctx;
+// n = 16 image for input words in [0, in_hi] (65535: raw u16 words; p - 1: canonicalised words)
+bool ct_image16(const HostParams& P, const Ctx& c, int64_t in_hi, const FastArgs& base, FastArgs& out) {
   const uint64_t p = P.p;
   const u128 lim = u128(c.beta) * (c.beta - p);
-  auto rup = [&](int64_t x) -> int64_t { return x <= 0 ? 0 : (x + int64_t(p) - 1) / int64_t(p) * int64_t(p); };
+  // offsets are multiples of p, rounded up; the canonical-input image may also subtract (its
+  // sums would otherwise outgrow Prop. 4's range for p = 7681), the raw-u16 image never needs to
+  const bool neg = in_hi != 65535;
+  auto rup = [&](int64_t x) -> int64_t {
+    if (x <= 0) return neg ? -((-x) / int64_t(p)) * int64_t(p) : 0;
+    return (x + int64_t(p) - 1) / int64_t(p) * int64_t(p);
+  };
   auto prod_ok = [&](int64_t v) { return v >= 0 && u128(p - 1) * uint64_t(v) < lim; };
   int64_t lo[16], hi[16];
-  for (int r = 0; r < 16; ++r) lo[r] = 0, hi[r] = 65535;
+  for (int r = 0; r < 16; ++r) lo[r] = 0, hi[r] = in_hi;
   const int64_t P_ = int64_t(p);
   uint32_t consts[8];
   const int64_t floor_of[4] = {6 * P_, 5 * P_, 4 * P_, 3 * P_};  // remaining F3 layers + 3p
   for (int li = 0; li < 4; ++li) {  // register-local layers len = 1, 2, 4, 8
     const int len = 1 << li;
-    int64_t c1 = 0, c2 = 0;
+    int64_t c1 = neg ? INT64_MIN : 0, c2 = neg ? INT64_MIN : 0;
     for (int r = 0; r < 16; ++r)
       if (!(r & len) && (r & (len - 1)) == 0) {
         c1 = std::max(c1, rup(floor_of[li] - lo[r] - lo[r + len]));
@@ -554,7 +556,7 @@ void fill_ct_inverse(HostParams& P) {
         nlo[u] = lo[u] + lo[v] + c1, nhi[u] = hi[u] + hi[v] + c1;
         nlo[v] = lo[u] - hi[v] + c2, nhi[v] = hi[u] - lo[v] + c2;
       } else {
-        if (lo[u] < P_ || !prod_ok(hi[v])) return;
+        if (lo[u] < P_ || !prod_ok(hi[v])) return false;
         nlo[u] = lo[u], nhi[u] = hi[u] + P_ - 1;
         nlo[v] = lo[u] - P_ + 1, nhi[v] = hi[u];
       }
@@ -564,7 +566,7 @@ void fill_ct_inverse(HostParams& P) {
   }
   int64_t L0 = lo[0], H0 = hi[0];  // after the transpose a register may hold any position
   for (int r = 1; r < 16; ++r) L0 = std::min(L0, lo[r]), H0 = std::max(H0, hi[r]);
-  if (L0 < 0 || H0 >= (int64_t(1) << 32)) return;
+  if (L0 < 0 || H0 >= (int64_t(1) << 32)) return false;
   for (int r = 0; r < 16; ++r) lo[r] = L0, hi[r] = H0;
   for (int h = 1; h <= 4; h *= 2) {  // strided layers len = 16, 32, 64 (all F3)
     int64_t nlo[16], nhi[16];
@@ -572,7 +574,7 @@ void fill_ct_inverse(HostParams& P) {
     std::copy(hi, hi + 16, nhi);
     for (int r = 0; r < 16; ++r) {
       if (r & h) continue;
-      if (lo[r] < P_ || !prod_ok(hi[r + h])) return;
+      if (lo[r] < P_ || !prod_ok(hi[r + h])) return false;
       nlo[r] = lo[r], nhi[r] = hi[r] + P_ - 1;
       nlo[r + h] = lo[r] - P_ + 1, nhi[r + h] = hi[r];
     }
@@ -580,8 +582,8 @@ void fill_ct_inverse(HostParams& P) {
     std::copy(nhi, nhi + 16, hi);
   }
   for (int r = 0; r < 16; ++r)  // last layer: both operands are Plantard products
-    if (!prod_ok(hi[r])) return;
-  FastArgs A = P.fast[NTTK_IMPROVED][1];
+    if (!prod_ok(hi[r])) return false;
+  FastArgs A = base;
   A.flags = (A.flags & 3u) | 2048u;
   std::copy(consts, consts + 8, A.ct_c);
   const uint64_t oi = static_cast<uint64_t>(inverse(P.omega, p));
@@ -593,8 +595,23 @@ void fill_ct_inverse(HostParams& P) {
     w = static_cast<uint64_t>(u128(w) * oi % p);
   }
   A.scale_lo = static_cast<uint32_t>(to_plantard(P.n_inv, c) * c.mu & c.r2n_mask);
-  P.fast_ctinv = A;
-  P.ct_inv = true;
+  out = A;
+  return true;
+}
+
+void fill_ct_inverse(HostParams& P) {
+  if (P.N != 256 || P.layers != 8 || P.tree != NTTK_CYCLIC) return;
+  if (!((P.fast_mask >> NTTK_IMPROVED) & 1u)) return;
+  if (P.n_bits == 32) {
+    fill_ct_inverse32(P);
+    // the narrow image (kyber256 preset): canonicalised u32 words through the n = 16 body
+    if (P.narrow[1])
+      P.ct_inv_c = ct_image16(P, make_ctx(P.p, 16, P.log2N), int64_t(P.p) - 1, P.fast[kNarrow][1], P.fast_ctinv_c);
+    return;
+  }
+  if (P.n_bits != 16) return;
+  P.ct_inv = ct_image16(P, P.ctx, 65535, P.fast[NTTK_IMPROVED][1], P.fast_ctinv);
+  P.ct_inv_c = ct_image16(P, P.ctx, int64_t(P.p) - 1, P.fast[NTTK_IMPROVED][1], P.fast_ctinv_c);
 }
 
 // CT-form inverse of the narrow image at N = 512 / 1024 (fastn_tma.cu inv_body_n_ct; the N = 256

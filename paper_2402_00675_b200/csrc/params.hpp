@@ -142,6 +142,10 @@ struct HostParams {
   // inv_body_ct): DIT butterflies on the bit-reversed spectrum with per-index twiddles
   bool ct_inv = false;
   FastArgs fast_ctinv;
+  // the same CT-form inverse for canonicalised (unpacked) input words: u32 storage of an n = 16
+  // improved set, or the narrow image of an n = 32 set (the kyber256 preset)
+  bool ct_inv_c = false;
+  FastArgs fast_ctinv_c;
   // CT-form inverse of the narrow image at N = 512 / 1024 (params.cpp fill_ct_inverse_n)
   bool ct_inv_n = false;
   // fast-image index of (kind, dir): kNarrow where the narrow image applies, kCtN where its

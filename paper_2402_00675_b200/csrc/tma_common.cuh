@@ -830,10 +830,12 @@ __device__ __forceinline__ void ct_twiddles(uint32_t (&twl)[15], const FastArgs&
   for (int b = 0; b < 8; ++b) twl[7 + b] = pin(A.lo[128 + j + 16 * b]);  // len 128, N^{-1} folded
 }
 
-template <class TWL>
+// PACKED: raw u16 words, two per register in v[8..15]; else canonicalised words in v[0..15] (u32
+// storage of an n = 16 set, or the narrow image of an n = 32 set: HostParams::fast_ctinv_c).
+template <bool PACKED = true, class TWL>
 __device__ __forceinline__ void inv_body_ct(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
                                             const Xpose& X) {
-  {
+  if constexpr (PACKED) {
     uint32_t t[16];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {  // len 1: positions 2m, 2m + 1 = the halves of word m
@@ -843,6 +845,13 @@ __device__ __forceinline__ void inv_body_ct(uint32_t (&v)[16], const TWL& twl, c
     }
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = t[r];
+  } else {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {  // len 1
+      const uint32_t u = v[2 * m], w = v[2 * m + 1];
+      v[2 * m] = u + w + A.ct_c[0];
+      v[2 * m + 1] = u - w + A.ct_c[1];
+    }
   }
 #pragma unroll
   for (int li = 1; li <= 3; ++li) {  // len 2, 4, 8

@@ -265,5 +265,5 @@ def test_fast_flags_ct_inverse(engine):
     assert (p - 1) * (16 * p) < lim(p) <= (p - 1) * (20 * p - 1)
     Pc = engine.build_params(p, 512, 32, [K.improved])
     assert Pc.fast_flags(K.improved, 1) & (CT_INV | NARROW) == NARROW
-    P7 = engine.build_params(7681, 256, 32, [K.improved])  # N = 256 narrow image: GS narrow body
-    assert P7.fast_flags(K.improved, 1) & (CT_INV | NARROW) == NARROW
+    P7 = engine.build_params(7681, 256, 32, [K.improved])  # N = 256 narrow image: CT body on
+    assert P7.fast_flags(K.improved, 1) & (CT_INV | NARROW) == CT_INV | NARROW  # canonicalised words

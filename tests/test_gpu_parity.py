@@ -935,3 +935,20 @@ def test_ct_narrow_inverse_and_its_fallback(oracle, N):
         s = nttk.forward(P, IMPROVED, to_dev(f, 4))
         assert (from_dev(s) == Q.forward(IMPROVED, f)).all()
         assert (from_dev(nttk.inverse(P, IMPROVED, s)) == f).all()
+
+
+def test_ct_inverse_canonical_input_images(oracle):
+    """N = 256 CT-form inverse on canonicalised (unpacked) words (HostParams::fast_ctinv_c): the
+    Kyber n = 16 set in u32 storage and the narrow image of the kyber256 preset (q = 7681,
+    n = 32).  Extreme, raw 32-bit and random words, ragged batches, bit-exact with the oracle."""
+    for p, n, exact in ((3329, 16, True), (7681, 32, False)):
+        P = nttk.build_params(p, 256, n, [IMPROVED], exact_bound=exact)
+        assert P.fast_flags(IMPROVED, 1) & 2048
+        Q = oracle.params(p, 256, n, (IMPROVED,), exact=exact)
+        for batch in (13, 35, 130):
+            w = _extreme_words(p, 32, batch, 11 + batch + p)
+            assert (from_dev(nttk.inverse(P, IMPROVED, to_dev(w, 4))) == Q.inverse(IMPROVED, w)).all()
+        f = oracle.rng(23, p, 77 * 256).reshape(77, 256).astype(np.int64)
+        s = nttk.forward(P, IMPROVED, to_dev(f, 4))
+        assert (from_dev(s) == Q.forward(IMPROVED, f)).all()
+        assert (from_dev(nttk.inverse(P, IMPROVED, s)) == f).all()

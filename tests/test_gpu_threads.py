@@ -91,8 +91,8 @@ Qd = o.params(8380417, 256, 32, (IMPROVED,), exact=True)
 wd = np.random.RandomState(4).randint(0, 1 << 32, size=(65, 256), dtype=np.uint64)
 zd = nttk.inverse(Pd, K.improved, torch.from_numpy(wd.astype(np.uint32).view(np.int32)).cuda())
 assert (zd.cpu().numpy().view(np.uint32).astype(np.int64) == Qd.inverse(IMPROVED, wd)).all()
-# Table 2 presets, inverse on arbitrary words (CT off: the GS narrow body of fastn_tma.cu)
-for name in ("newhope512", "newhope1024"):
+# Table 2 presets, inverse on arbitrary words (CT off: the GS narrow bodies)
+for name in ("kyber256", "newhope512", "newhope1024"):
     Pn = nttk.preset(name)
     Qn = o.params(Pn.p, Pn.size, 32, (IMPROVED,))
     wn = np.random.RandomState(5).randint(0, 1 << 32, size=(35, Pn.size), dtype=np.uint64)

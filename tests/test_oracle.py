@@ -406,7 +406,7 @@ def test_f1_forward_schedule_n512_1024(oracle, N):
         assert _f1_schedule_model(row, ct, p, L - 2, w1_layer2=False) == [int(v) for v in want[k]]
 
 
-def _ct_inverse_model(F, p, omega):
+def _ct_inverse_model(F, p, omega, in_hi=65535):
     """Integer model of tma_common.cuh inv_body_ct (Kyber N = 256): radix-2 DIT on the
     bit-reversed spectrum with omega^{-1}, raw words in, the multiply-free jb = 0 butterflies of
     len 1..8 adding per-layer offsets chosen as params.cpp fill_ct_inverse chooses them (interval
@@ -414,10 +414,11 @@ def _ct_inverse_model(F, p, omega):
     the last layer.  Asserts the bounds the host validates."""
     N = 256
     lim = (1 << 16) * ((1 << 16) - p)
-    rup = lambda x: 0 if x <= 0 else (x + p - 1) // p * p  # noqa: E731
+    neg = in_hi != 65535  # the canonical-input image may subtract multiples of p as well
+    rup = lambda x: (-((-x) // p) * p if neg else 0) if x <= 0 else (x + p - 1) // p * p  # noqa: E731
     oi = pow(omega, p - 2, p)
     ninv = pow(N, p - 2, p)
-    lo, hi = [0] * 16, [65535] * 16
+    lo, hi = [0] * 16, [in_hi] * 16
     consts = []
     for li, fl in enumerate((6 * p, 5 * p, 4 * p, 3 * p)):
         ln = 1 << li
@@ -436,6 +437,8 @@ def _ct_inverse_model(F, p, omega):
                 nlo[r], nhi[r] = lo[r], hi[r] + p - 1
                 nlo[r + ln], nhi[r + ln] = lo[r] - p + 1, hi[r]
         lo, hi = nlo, nhi
+    if in_hi == p - 1:  # the unpacked variant canonicalises its input words first
+        F = [int(x) % p for x in F]
     v = [[int(F[16 * j + r]) for r in range(16)] for j in range(16)]
     for a in v:  # contiguous phase: position 16 j + r
         for li in range(4):
