@@ -1,5 +1,7 @@
 # CT-form narrow inverse at N = 512 / 1024: parity of the fastn / narrow tests, then the A/B
-# against the GS narrow body (NTTK_INV_CT=0) and the F-form masks (variants/ctnCS.so)
+# against the GS narrow body (NTTK_INV_CT=0) and the F-form masks (variants/ctnCS.so, built with
+# tools/build_variant.sh from temporary -D switches of ct_f3_contiguous; the switches were removed
+# once the per-N choice was made, so only the GS / CT rows can be re-run as is)
 cd $GRAFT_REPO_ROOT
 O=gpurun_out/${1:-ctn}
 mkdir -p $O

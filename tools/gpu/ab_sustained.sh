@@ -1,4 +1,6 @@
-# F1 (IADD3) vs F3 (IMAD) forms of Y' = 2X - X' under SUSTAINED load (the bench step, power-capped)
+# F1 (IADD3) vs F3 (IMAD) forms of Y' = 2X - X' under SUSTAINED load (the bench step, power-capped).
+# The variants were built with tools/build_variant.sh from temporary -D switches in tma_common.cuh
+# (removed after the measurement: F3 stayed); the base rows and tools/step_probe.py re-run as is.
 cd $GRAFT_REPO_ROOT
 O=gpurun_out/${1:-sus}
 mkdir -p $O

@@ -1,7 +1,7 @@
 # round-2 closing measurement after the CT-form inverses: parity, smoke, bench line, reference
 # arm, ncu launch list and one full capture of the four config-4 kernels -- outputs under gpurun_out/$1
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/${1:-final2}
+O=gpurun_out/${1:-measure}
 mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -q > $O/gputest.log 2>&1; echo "pytest rc=$?" >> $O/gputest.log
 tail -2 $O/gputest.log

@@ -1,7 +1,7 @@
 # after the CT-form narrow inverse (N = 512 / 1024): full parity, stress, bench line, reference
 # arm, ncu captures of the fastn inverses -- outputs under gpurun_out/$1
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/${1:-final3}
+O=gpurun_out/${1:-measure_fastn}
 mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -q > $O/gputest.log 2>&1; echo "pytest rc=$?" >> $O/gputest.log
 tail -2 $O/gputest.log
