@@ -477,6 +477,82 @@ def _ct_inverse_model(F, p, omega, in_hi=65535):
     return out
 
 
+def _ct_inverse_model32(F, p, omega):
+    """Integer model of tma_common.cuh inv_body_ct32 (Dilithium, n = 32): inputs partially reduced
+    to [0, 2p) by the shift reduction, umulhi-form CT butterflies (X + r, X + p - r) on the DIT
+    schedule of _ct_inverse_model, the multiply-free jb = 0 butterflies adding the multiple of p
+    that params.cpp fill_ct_inverse32 picks (>= their Y input), N^{-1} folded.  Asserts that
+    every word stays below 2^32 and non-negative."""
+    N = 256
+    s = p.bit_length()  # 2^s >= p: v - (v >> s) p lies in [0, 2p) for every 32-bit v
+    oi, ninv = pow(omega, p - 2, p), pow(N, p - 2, p)
+    rup = lambda x: (x + p - 1) // p * p  # noqa: E731
+    hi = [2 * p - 1] * 16
+    consts = []
+    for li in range(4):
+        ln = 1 << li
+        c2 = max(rup(hi[r + ln]) for r in range(16) if not r & ln and r & (ln - 1) == 0)
+        consts.append(c2)
+        nhi = hi[:]
+        for r in range(16):
+            if r & ln:
+                continue
+            if r & (ln - 1) == 0:
+                nhi[r], nhi[r + ln] = hi[r] + hi[r + ln], hi[r] + c2
+            else:
+                nhi[r], nhi[r + ln] = hi[r] + p - 1, hi[r] + p
+        hi = nhi
+    assert max(hi) + 3 * p < 1 << 32
+    red = [int(x) - (int(x) >> s) * p for x in F]
+    assert all(0 <= x < 2 * p for x in red)
+    v = [[red[16 * j + r] for r in range(16)] for j in range(16)]
+    for a in v:
+        for li in range(4):
+            ln = 1 << li
+            for r in range(16):
+                if r & ln:
+                    continue
+                jb = r & (ln - 1)
+                u, x = a[r], a[r + ln]
+                if jb == 0:
+                    assert consts[li] >= x
+                    a[r], a[r + ln] = u + x, u + consts[li] - x
+                else:
+                    rr = x * pow(oi, (128 // ln) * jb, p) % p
+                    a[r], a[r + ln] = u + rr, u + p - rr
+                assert 0 <= a[r] < 1 << 32 and 0 <= a[r + ln] < 1 << 32
+    pos = {16 * j + r: v[j][r] for j in range(16) for r in range(16)}
+    out = [0] * N
+    for j in range(16):
+        a = [pos[j + 16 * r] for r in range(16)]
+        for h in (1, 2, 4):
+            for r in range(16):
+                if r & h:
+                    continue
+                rr = a[r + h] * pow(oi, (8 // h) * (j + 16 * (r % h)), p) % p
+                a[r], a[r + h] = a[r] + rr, a[r] + p - rr
+                assert a[r] < 1 << 32 and a[r + h] < 1 << 32
+        for r in range(8):
+            A = a[r] * ninv % p
+            B = a[r + 8] * (ninv * pow(oi, j + 16 * r, p) % p) % p
+            out[j + 16 * r], out[j + 16 * (r + 8)] = (A + B) % p, (A - B) % p
+    return out
+
+
+def test_ct_inverse_schedule32_matches_reference(oracle):
+    """The CT-form Dilithium inverse (tma_common.cuh inv_body_ct32) gives the reference's
+    canonical inverse (transform.hpp:233-343) on arbitrary 32-bit words."""
+    p = 8380417
+    Q = oracle.params(p, 256, 32, (IMPROVED,), exact=True)
+    rs = np.random.RandomState(9)
+    rows = [np.full(256, (1 << 32) - 1), np.zeros(256, dtype=np.int64),
+            np.where(np.arange(256) % 2 == 0, (1 << 32) - 1, 0), rs.randint(0, 1 << 32, 256),
+            rs.randint(0, p, 256)]
+    want = Q.inverse(IMPROVED, np.stack(rows).astype(np.uint64))
+    for k, row in enumerate(rows):
+        assert _ct_inverse_model32(row, p, Q.omega) == [int(v) for v in want[k]]
+
+
 def _ct_inverse_model_n(F, p, omega, N):
     """Integer model of fastn_tma.cu inv_body_n_ct (N = 512 / 1024, narrow image): canonical
     input, compile-time interval schedule in units of p (floors rq, offsets m p, canon1 when a
