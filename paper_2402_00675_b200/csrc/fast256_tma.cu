@@ -260,8 +260,8 @@ cudaError_t fwd_launch_w(const void* in, void* out, size_t batch, const FastArgs
   constexpr int smem = GeoK<K, IO, 0, L, W1>::kSmem;
   using G = GeoK<K, IO, 0, L, W1>;
   const int blocks = grid_for(kern, G::kThreadsP, G::kTileP, smem, occ, batch);
-  kern<<<blocks, G::kThreadsP, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A);
-  return cudaGetLastError();
+  return launch_pdl(kern, blocks, G::kThreadsP, smem, st, static_cast<const IO*>(in), static_cast<IO*>(out),
+                    batch, A);
 }
 
 template <class K, class IO, int L, bool PER_INDEX>
@@ -290,8 +290,8 @@ cudaError_t inv_launch_mode(const void* in, void* out, size_t batch, const FastA
   }
   using G = GeoK<K, IO, 1>;
   const int blocks = grid_for(kern, G::kThreadsP, G::kTileP, smem, occ, batch);
-  kern<<<blocks, G::kThreadsP, smem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch, A, map);
-  return cudaGetLastError();
+  return launch_pdl(kern, blocks, G::kThreadsP, smem, st, static_cast<const IO*>(in), static_cast<IO*>(out),
+                    batch, A, map);
 }
 
 template <class K, class IO, int L, int LZ>

@@ -132,6 +132,7 @@ __device__ __forceinline__ void produce_n(const IO* in, size_t batch, uint8_t* s
   constexpr int kConsumers = C;
   const size_t ntiles = (batch + GN::kTileN - 1) / GN::kTileN;
   int k = 0;
+  pdl_wait();
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
     const int s = k % GN::kStages;
     if (k >= GN::kStages) mbar_wait(&empty[s], ((k / GN::kStages) & 1) ^ 1);
@@ -811,9 +812,8 @@ cudaError_t fwd_n_f(const void* in, void* out, size_t batch, const uint32_t* tab
   static OccCache occ;
   auto kern = fwdn_tma_kernel<K, IO, LOGN, PER_INDEX, F1>;
   const int blocks = grid_n(kern, GN::kSmem, occ, (batch + GN::kTileN - 1) / GN::kTileN, GN::kThreadsN);
-  kern<<<blocks, GN::kThreadsN, GN::kSmem, st>>>(static_cast<const IO*>(in), static_cast<IO*>(out), batch,
-                                            tab, A);
-  return cudaGetLastError();
+  return launch_pdl(kern, blocks, GN::kThreadsN, GN::kSmem, st, static_cast<const IO*>(in), static_cast<IO*>(out),
+                    batch, tab, A);
 }
 
 // consumer warps of the N = 512 / 1024 inverse (two 256-row tensor boxes per stage at 16)
@@ -850,8 +850,8 @@ cudaError_t inv_n_mode(const void* in, void* out, size_t batch, const uint32_t* 
       if (e != cudaSuccess) return e;
     }
     const int blocks = grid_n(kern, smem, occ, (n + GN::kTileN - 1) / GN::kTileN, GN::kThreadsN);
-    kern<<<blocks, GN::kThreadsN, smem, st>>>(src, static_cast<IO*>(out) + done * GN::N, n, tab, A, map);
-    const cudaError_t e = cudaGetLastError();
+    const cudaError_t e = launch_pdl(kern, blocks, GN::kThreadsN, smem, st, src,
+                                     static_cast<IO*>(out) + done * GN::N, n, tab, A, map);
     if (e != cudaSuccess) return e;
     done += n;
   }

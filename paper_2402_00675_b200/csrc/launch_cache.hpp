@@ -48,4 +48,28 @@ int occupancy_current(Kern kern, int threads, int smem, OccCache& cache) {
   return v;
 }
 
+// Launch with programmatic dependent launch (PDL) allowed: when the previous launch on the stream
+// is one of the TMA kernels (which signal griddepcontrol.launch_dependents as they start), this
+// grid's CTAs become resident as that grid's CTAs exit and run their prologue (barrier init,
+// twiddle pins, table staging) under its tail; the producer warps block in griddepcontrol.wait
+// until the previous grid has completed and its writes are visible before they touch global
+// memory, and every consumer store depends on data the producer loaded after that wait.  After
+// any other kernel, a copy or an event the launch is ordered as usual.  It removes the
+// launch latency between back-to-back small launches (BASELINE configs 1 and 2).
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, int smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace nttk_b200

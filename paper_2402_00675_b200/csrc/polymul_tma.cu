@@ -61,6 +61,7 @@ __device__ __forceinline__ void produce2(const IO* a, const IO* b, size_t batch,
   constexpr int kConsumers = G::kConsumers, kTile = 2 * kConsumers;
   const size_t ntiles = (batch + kTile - 1) / kTile;
   int k = 0;
+  pdl_wait();
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
     const int s = k % G::kStages;
     if (k >= G::kStages) mbar_wait(&empty[s], ((k / G::kStages) & 1) ^ 1);
@@ -205,9 +206,8 @@ cudaError_t launch_k(const void* a, const void* b, void* out, size_t batch, cons
   const size_t tiles = (batch + kTile - 1) / kTile;
   const size_t full = size_t(g_sms2) * o;
   const int blocks = static_cast<int>(tiles < full ? tiles : full);
-  kern<<<blocks, kThreads, smem, st>>>(static_cast<const IO*>(a), static_cast<const IO*>(b),
-                                      static_cast<IO*>(out), batch, PA);
-  return cudaGetLastError();
+  return launch_pdl(kern, blocks, kThreads, smem, st, static_cast<const IO*>(a), static_cast<const IO*>(b),
+                    static_cast<IO*>(out), batch, PA);
 }
 
 template <class K, class IO, int L, bool PER_INDEX, bool LAZY, bool W1>

@@ -96,6 +96,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Programmatic dependent launch (launch_cache.hpp launch_pdl): the producer calls pdl_wait()
+// before its first global read; init_barriers() signals launch_dependents.  Both are no-ops for
+// a launch without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -129,6 +137,7 @@ __device__ __forceinline__ void produce_rows(const CUtensorMap* map, uint32_t nt
                                              uint64_t* full, uint64_t* empty) {
   constexpr uint32_t kBytes = BOX_ROWS * 128;
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+  pdl_wait();
   uint32_t s = 0, phase = 0, k = 0;
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
     if (k >= uint32_t(STAGES)) mbar_wait(&empty[s], phase ^ 1);
@@ -250,6 +259,7 @@ __device__ __forceinline__ void produce(const IO* in, size_t batch, uint8_t* sta
   constexpr int kTile = G::kTileP, kConsumers = G::kC;
   const size_t ntiles = (batch + kTile - 1) / kTile;
   int k = 0;
+  pdl_wait();
   for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
     const int s = k % G::kStages;
     if (k >= G::kStages) mbar_wait(&empty[s], ((k / G::kStages) & 1) ^ 1);
@@ -1147,6 +1157,7 @@ __device__ __forceinline__ void load_contiguous_swz(uint32_t (&v)[16], uint32_t 
 __device__ __forceinline__ void init_barriers(uint64_t* full, uint64_t* empty, int stages,
                                               int consumers = kConsumers) {
   if (threadIdx.x == 0) {
+    pdl_launch_dependents();
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], consumers);

@@ -952,3 +952,57 @@ def test_ct_inverse_canonical_input_images(oracle):
         s = nttk.forward(P, IMPROVED, to_dev(f, 4))
         assert (from_dev(s) == Q.forward(IMPROVED, f)).all()
         assert (from_dev(nttk.inverse(P, IMPROVED, s)) == f).all()
+
+
+def test_pdl_dependent_chains(oracle):
+    """The TMA kernels are launched with programmatic dependent launch allowed
+    (launch_cache.hpp launch_pdl): a small launch becomes resident while the previous one still
+    runs and must not read its input before that grid has completed.  Chains of dependent small
+    launches -- in place, each reading what the previous wrote, on idle SMs so the next grid
+    starts early -- end in the oracle's words."""
+    p = 3329
+    P = engine_params(p, 256, 16, [IMPROVED], exact=True)
+    Q = oracle.params(p, 256, 16, (IMPROVED,), exact=True)
+    for batch in (1, 37, 300):
+        f = oracle.rng(41 + batch, p, batch * 256).reshape(batch, 256).astype(np.int64)
+        buf = to_dev(f, 2)
+        for _ in range(25):
+            nttk.forward(P, IMPROVED, buf, buf)
+            nttk.inverse(P, IMPROVED, buf, buf)
+        assert (from_dev(buf) == f).all()
+        nttk.forward(P, IMPROVED, buf, buf)
+        assert (from_dev(buf) == Q.forward(IMPROVED, f)).all()
+    # Dilithium u32 (tensor-map producer) and the N = 1024 kernel in the same kind of chain
+    for pp, N, n, exact in ((8380417, 256, 32, True), (12289, 1024, 32, False)):
+        Pd = engine_params(pp, N, n, [IMPROVED], exact=exact)
+        f = oracle.rng(5, pp, 19 * N).reshape(19, N).astype(np.int64)
+        buf = to_dev(f, 4)
+        for _ in range(15):
+            nttk.forward(Pd, IMPROVED, buf, buf)
+            nttk.inverse(Pd, IMPROVED, buf, buf)
+        assert (from_dev(buf) == f).all()
+    # inside a captured plan the launches are back to back on the device, so the next grid really
+    # starts while the previous one runs (the kernels signal launch_dependents as they start):
+    # the in-place inverse of arbitrary words, 16 times per replay, against the oracle's iterate
+    for pp, n, elem in ((3329, 16, 2), (8380417, 32, 4)):
+        Pi = engine_params(pp, 256, n, [IMPROVED], exact=True)
+        Qi = oracle.params(pp, 256, n, (IMPROVED,), exact=True)
+        w = _extreme_words(pp, 8 * elem, 37, 77 + elem)
+        buf = to_dev(w, elem)
+        plan = nttk.Plan(Pi, IMPROVED, nttk.Plan.INVERSE, buf, buf, repeat=16)
+        plan.launch()
+        want = w
+        for _ in range(16):
+            want = np.asarray(Qi.inverse(IMPROVED, want)).astype(np.uint64)
+        assert (from_dev(buf) == want).all()
+        del plan
+    # fused polymul chain: c <- c * b, ten times (negacyclic Kyber tree, basemul)
+    Pn = engine_params(p, 256, 16, [IMPROVED], tree=NEGA, layers=7, exact=True)
+    Qn = oracle.params(p, 256, 16, (IMPROVED,), tree=NEGA, layers=7, exact=True)
+    a = oracle.rng(7, p, 21 * 256).reshape(21, 256).astype(np.int64)
+    b = oracle.rng(8, p, 21 * 256).reshape(21, 256).astype(np.int64)
+    c, db, want = to_dev(a, 2), to_dev(b, 2), a
+    for _ in range(10):
+        nttk.polymul(Pn, IMPROVED, c, db, c)
+        want = np.asarray(Qn.polymul(IMPROVED, want, b)).astype(np.int64)
+    assert (from_dev(c) == want).all()
