@@ -586,7 +586,8 @@ def run_extras(dev):
                               "fwd_frac_of_hbm": roof / (fms * 1e6 / Bp),
                               "inv_frac_of_hbm": roof / (ims * 1e6 / Bp),
                               "fast_path": kind in Pp.fast_path,
-                              "n16_product": bool(kind == K.improved and Pp.fast_flags(kind, 0) & 512)}
+                              "n16_product": bool(kind == K.improved and Pp.fast_flags(kind, 0) & 512),
+                              "ct_form_inverse": bool(kind == K.improved and Pp.fast_flags(kind, 1) & 2048)}
         cpu = table2_cpu_reference(qp, Np)
         if cpu:
             for kname, v in cpu.items():
