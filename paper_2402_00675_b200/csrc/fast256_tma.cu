@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
   // F1: per-lane surplus corrections E[m] = (m - cj) p of the last layer (fwd_body_f1)
   uint32_t E[5];
   if constexpr (F1) {
-    const int cj = int(kF1Surplus) - ((j >> 3) & (j >> 2) & 1) - ((j >> 1) & 1) - (j & 1);
+    const int cj = L == 8 ? int(kF1Surplus) - ((j >> 3) & (j >> 2) & 1) - ((j >> 1) & 1) - (j & 1)
+                          : int(kF1SurplusNega7) - __popc(uint32_t(j) & 7u);  // fwd_body_f1_nega7
 #pragma unroll
     for (int m = 0; m < 5; ++m) E[m] = pin(uint32_t(m - cj) * A.p);
   }
@@ -105,8 +106,10 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
       load_strided<IO, K::kSigned>(
           v, reinterpret_cast<const IO*>(stages + s * G::kStageBytes + G::poly_offset(warp, half)), j);
       release_stage(&empty[s], lane);
-      if constexpr (F1)
+      if constexpr (F1 && L == 8)
         fwd_body_f1<K>(v, twl, A, X, E);
+      else if constexpr (F1)
+        fwd_body_f1_nega7<K>(v, twl, A, X, E);
       else
         fwd_body<K, L, PER_INDEX, W1>(v, twl, A, X);
       if constexpr (sizeof(IO) == 4)
@@ -270,6 +273,10 @@ cudaError_t fwd_launch(const void* in, void* out, size_t batch, const FastArgs& 
     if constexpr (std::is_same<K, ImprovedN16<false>>::value && L == 8) {
       if ((A.flags & 1024) && f1_enabled())
         return fwd_launch_w<K, IO, L, PER_INDEX, true, true>(in, out, batch, A, st);
+    }
+    if constexpr (std::is_same<K, ImprovedN16<false>>::value && L == 7) {  // negacyclic: no W1
+      if ((A.flags & 1024) && !(A.flags & 16) && f1_enabled())
+        return fwd_launch_w<K, IO, L, PER_INDEX, false, true>(in, out, batch, A, st);
     }
     if (A.flags & 16) return fwd_launch_w<K, IO, L, PER_INDEX, true>(in, out, batch, A, st);
   }

@@ -247,7 +247,9 @@ void fill_fast(HostParams& P, int kind) {
     {
       const uint64_t L = P.layers, S = L - 2;
       const bool full = (P.N == 256 && L == 8) || ((P.N == 512 || P.N == 1024) && L == P.log2N);
-      if (kind == NTTK_IMPROVED && n16 && dir == 0 && full && (A.flags & 16) &&
+      // ... and the 7-layer negacyclic tree at N = 256 (fwd_body_f1_nega7: layer 1 multiplies)
+      const bool nega7 = P.N == 256 && L == 7 && P.tree == NTTK_NEGACYCLIC && !(A.flags & 16);
+      if (kind == NTTK_IMPROVED && n16 && dir == 0 && ((full && (A.flags & 16)) || nega7) &&
           u128(p - 1) * ((2 * L - 1) * p) < u128(c.beta) * (c.beta - p)) {
         A.f1_sp = static_cast<uint32_t>(S * p);
         A.f1_sp1 = static_cast<uint32_t>((S + 1) * p);

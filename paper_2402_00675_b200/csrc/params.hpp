@@ -112,6 +112,8 @@ bool ct_inverse_enabled();
 constexpr int kNarrowEmax = 4;
 // F1 forward at N = 256: surplus multiples of p injected by layer 1 (= L - 2, fwd_body_f1)
 constexpr uint32_t kF1Surplus = 6;
+// F1 forward of the 7-layer negacyclic tree: surplus L - 2 (tma_common.cuh fwd_body_f1_nega7)
+constexpr uint32_t kF1SurplusNega7 = 5;
 
 struct HostParams {
   nttk_params_desc desc{};

@@ -472,6 +472,57 @@ __device__ __forceinline__ void fwd_body_f1(uint32_t (&v)[16], const TWL& twl, c
   }
 }
 
+// F1 forward of the 7-layer negacyclic tree (the Kyber NTT, row a22; A.flags bit 10 at L = 7).
+// No layer has twiddle 1, so layer 1 runs the umulhi product and injects the surplus S = L - 2 = 5
+// inside its two IADD3s, layers 2..6 run the F3 form (each Y-step spends one), and layer 7
+// (register distance 2: the tree ends in degree-2 factors) runs the umulhi form and removes
+// sigma = S - popcount(i6..i2) of its X position i = 16 j + r: lane part cj = S - popcount(j & 7),
+// register part k = r3 + r2, E[m] = (m - cj) p.  Largest word (2 L - 1) p, host-validated.
+template <class K, class TWL>
+__device__ __forceinline__ void fwd_body_f1_nega7(uint32_t (&v)[16], const TWL& twl, const FastArgs& A,
+                                                  const Xpose& X, const uint32_t (&E)[5]) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // layer 1: one block, umulhi product, surplus injected
+    const uint32_t x = v[r], c = mp_n16<false>(v[r + 8], K::tw(A, 0), A.p);
+    v[r] = x + c + A.f1_sp;
+    v[r + 8] = x + A.f1_sp1 - c;
+  }
+#pragma unroll
+  for (int sl = 2; sl <= 4; ++sl) {  // layers 2..4 (strided phase)
+    const int h = 8 >> (sl - 1);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      f1_bf<true>(v[r], v[r + h], K::tw(A, (1 << (sl - 1)) - 1 + (r >> (5 - sl))), A);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) X.put(r, v[r]);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) X.get4(c, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+#pragma unroll
+  for (int sl = 5; sl <= 6; ++sl) {  // layers 5, 6 (contiguous phase)
+    const int h = 1 << (8 - sl);
+    const int base = sl == 5 ? 0 : 1;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & h) continue;
+      f1_bf<true>(v[r], v[r + h], twl[base + (r >> (9 - sl))], A);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {  // layer 7: umulhi form, surplus removed
+    if (r & 2) continue;
+    const int k = ((r >> 2) & 1) + ((r >> 3) & 1);
+    const uint32_t rr = mp_n16<false>(v[r + 2], twl[3 + (r >> 2)], A.p);
+    const uint32_t x = v[r];
+    v[r + 2] = x - rr + E[k + 1];
+    v[r] = x + rr + E[k];
+  }
+}
+
 // F1 forward whose words are free (the fused polymul: only its canonical product is pinned):
 // the same paper-form layers as fwd_body_f1 on every layer after the first, no final
 // correction -- outputs are exact mod p, below (L + 1 + S) p with S = L - 1 (host-validated,

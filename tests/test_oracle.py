@@ -378,6 +378,51 @@ def _f1_schedule_model(a, ct, p, S, w1_layer2=True):
     return a
 
 
+def _f1_nega7_model(a, ct, p):
+    """Integer model of tma_common.cuh fwd_body_f1_nega7 (Kyber, 7-layer negacyclic tree, N = 256):
+    layer 1 multiplies and injects the surplus S = 5, layers 2..6 run Y' = X - r, layer 7 removes
+    sigma = S - popcount(i6..i2); asserts every F-layer X input keeps a surplus >= 1 (no
+    underflow) and every product operand lies inside Prop. 4's n = 16 range."""
+    a = [int(v) for v in a]
+    N, L, S = 256, 7, 5
+    lim = (1 << 16) * ((1 << 16) - p)
+    for s in range(1, L + 1):
+        span = N >> s
+        for i in range(N):
+            if i & span:
+                continue
+            x, y, blk = a[i], a[i + span], i >> (9 - s)
+            w = int(ct[(1 << (s - 1)) - 1 + blk])
+            assert w * y < lim
+            r = w * y % p
+            if s == 1:
+                a[i], a[i + span] = x + r + S * p, x + (S + 1) * p - r
+            elif s < L:
+                assert x - r >= 0
+                a[i], a[i + span] = x + r, x - r
+            else:
+                sig = S - sum((i >> k) & 1 for k in range(2, 7))
+                assert sig >= 0
+                a[i], a[i + span] = x + r - sig * p, x + p - r - sig * p
+    return a
+
+
+def test_f1_forward_schedule_nega7(oracle):
+    """The F1 forward of the 7-layer negacyclic Kyber tree (fwd_body_f1_nega7) reproduces the
+    words of the reference's cores driven on that schedule (row a22: the oracle's tree forward is
+    pinned to reference-run words), on extreme and random canonical inputs."""
+    p = 3329
+    Q = oracle.params(p, 256, 16, (IMPROVED,), tree=NEGA, layers=7, exact=True)
+    ct = Q.table("ct_plain")
+    rs = np.random.RandomState(21)
+    rows = [np.full(256, p - 1), np.zeros(256, dtype=np.int64), np.where(np.arange(256) % 2 == 0, p - 1, 0),
+            np.where(np.arange(256) < 128, p - 1, 0), np.where(np.arange(256) < 128, 0, p - 1),
+            rs.randint(0, p, 256), rs.randint(0, p, 256)]
+    want = Q.forward(IMPROVED, np.stack(rows).astype(np.uint64))
+    for k, row in enumerate(rows):
+        assert _f1_nega7_model(row, ct, p) == [int(v) for v in want[k]]
+
+
 @pytest.mark.parametrize("p", [3329, 7681])
 def test_f1_forward_schedule_matches_reference_loop(oracle, p):
     """The surplus bookkeeping of the F1 forward (kF1Surplus = 6) reproduces the reference's
