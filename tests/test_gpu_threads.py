@@ -81,6 +81,11 @@ Q = o.params(3329, 256, 16, (IMPROVED,), exact=True)
 f = o.rng(31, 3329, 257 * 256).reshape(257, 256)
 y = nttk.forward(P, K.improved, torch.from_numpy(f.astype(np.int16)).cuda())
 assert (y.cpu().numpy().astype(np.int64) & 0xffff == Q.forward(IMPROVED, f)).all()
+# the 7-layer negacyclic Kyber forward (F1 off: umulhi form)
+P7 = nttk.build_params(3329, 256, 16, [K.improved], tree=nttk.Tree.negacyclic, layers=7, exact_bound=True)
+Q7 = o.params(3329, 256, 16, (IMPROVED,), tree=NEGA, layers=7, exact=True)
+y7 = nttk.forward(P7, K.improved, torch.from_numpy(f.astype(np.int16)).cuda())
+assert (y7.cpu().numpy().astype(np.int64) & 0xffff == Q7.forward(IMPROVED, f)).all()
 # Kyber u16 inverse on arbitrary words (CT off: the GS lazy-merge body)
 w = np.random.RandomState(3).randint(0, 1 << 16, size=(129, 256)).astype(np.uint16)
 z = nttk.inverse(P, K.improved, torch.from_numpy(w.view(np.int16)).cuda())
