@@ -84,6 +84,9 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
   const int j = lane & 15, half = lane >> 4;
   Xpose X;
   X.init(scratch + warp * kScratchWords + half * 272, j);
+  // u16 output 32-byte aligned: one 256-bit store per lane (store_contiguous; Kyber forward
+  // 0.888 -> 0.878 ms, profiles/r2_stg256_ab.txt); a 16-byte aligned buffer keeps the two 128-bit stores
+  const bool al32 = (reinterpret_cast<uintptr_t>(out) & 31) == 0;
   // F1: per-lane surplus corrections E[m] = (m - cj) p of the last layer (fwd_body_f1)
   uint32_t E[5];
   if constexpr (F1) {
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(GeoK<K, IO, 0, L, W1>::kThreadsP,
         store_contiguous_coalesced(reinterpret_cast<uint32_t*>(optr), j, v, X,
                                    scratch + warp * kScratchWords + half * 272, poly < nb);
       else if (poly < nb)
-        store_contiguous<IO>(optr, j, v);
+        store_contiguous<IO>(optr, j, v, al32);
       poly += pstep;
       optr += ostep;
       if (++s == G::kStages) {

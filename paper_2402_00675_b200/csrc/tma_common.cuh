@@ -1029,9 +1029,21 @@ __device__ __forceinline__ void inv_body(uint32_t (&v)[16], const TWL& twl, cons
 }
 
 // stores
+// AL32 (u16): the output is 32-byte aligned, so a lane's 16 coefficients leave in one 256-bit
+// store (STG.256, one full sector per lane) instead of two 128-bit stores of half a sector each
 template <class IO>
-__device__ __forceinline__ void store_contiguous(IO* out_poly, int j, const uint32_t (&v)[16]) {
+__device__ __forceinline__ void store_contiguous(IO* out_poly, int j, const uint32_t (&v)[16],
+                                                 bool al32 = false) {
   if constexpr (sizeof(IO) == 2) {
+    if (al32) {
+      asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(out_poly + 16 * j),
+                   "r"(__byte_perm(v[0], v[1], 0x5410)), "r"(__byte_perm(v[2], v[3], 0x5410)),
+                   "r"(__byte_perm(v[4], v[5], 0x5410)), "r"(__byte_perm(v[6], v[7], 0x5410)),
+                   "r"(__byte_perm(v[8], v[9], 0x5410)), "r"(__byte_perm(v[10], v[11], 0x5410)),
+                   "r"(__byte_perm(v[12], v[13], 0x5410)), "r"(__byte_perm(v[14], v[15], 0x5410))
+                   : "memory");
+      return;
+    }
     uint4* dst = reinterpret_cast<uint4*>(out_poly) + 2 * j;
     uint4 a, b;  // PRMT packs two low halves in one ALU op
     a.x = __byte_perm(v[0], v[1], 0x5410);
